@@ -1,0 +1,253 @@
+/*
+ * mpm_b200.h -- C ABI of the B200-native MLS-MPM substep core (libmpm_b200.so).
+ *
+ * This is the drop-in boundary for the substep loop of the reference package `mpmbench`
+ * (arxiv/paper_2111_00699).  The reference is Python + numba: its "kernels" are plain
+ * functions that borrow contiguous numpy buffers plus scalars and report problems through
+ * a counters array.  Every entry point below replaces one of those functions and keeps
+ * that contract, with device pointers instead of numpy views:
+ *
+ *   - the caller owns every buffer (the host layer grows them with the reference's
+ *     4x GrowBuffer rule, memory.py:18-22); the library borrows pointers for the
+ *     duration of the call, never retains them, and never allocates device memory;
+ *   - kernels never raise: they count into `counters[6]` (pipeline.py:57-63) and
+ *     `stats` and the host maps those onto the reference's exception classes;
+ *   - every call is asynchronous on `stream` and returns an mpm_status immediately;
+ *   - different worker handles may be driven from different host threads.
+ *
+ * Reference paths are relative to /root/reference/pkg/src/mpmbench/.
+ *
+ * Device data layout (fp32; the reference is fp64 with the same index structure):
+ *   particles  pdata[group][channel][32]   channel map of particles.py:24-31:
+ *              pos 0-2, vel 3-5, C 6-14 (row-major), mass 15, F 16-24 | J 16,
+ *              plastic scalar 25 (snow Jp / sand volume correction; not in the reference)
+ *   lane_meta  u16[group][32]   bits 0-9 lane key (pipeline.py:261-263), bit 15 quarantined
+ *   grid       float4 node[pblock][64] = (mass, mom_x, mom_y, mom_z) in raw buffers,
+ *              (mass, v_x, v_y, v_z) in vel; slot = Morton of the low two bits per axis
+ *              (pipeline.py:144-147).  The reference stores the same values channel-major
+ *              as [pblock][4][64] (grid.py:427-429).
+ */
+#ifndef MPM_B200_H
+#define MPM_B200_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define MPM_LANES 32          /* lane_width of a particle group (SimParams.lane_width default) */
+#define MPM_CELL_BIAS 64      /* grid.py CELL_BIAS */
+#define MPM_N_COUNTERS 6      /* pipeline.py:57-63 */
+#define MPM_LANE_QUARANTINED 0x8000u
+
+enum mpm_status {
+    MPM_OK = 0,
+    MPM_ERR_REJECTED_INPUT = -1,     /* RejectedInputError   */
+    MPM_ERR_SPATIAL_DOMAIN = -2,     /* SpatialDomainError   */
+    MPM_ERR_RESOURCE = -3,           /* ResourceError (CUDA runtime failure, capacity)    */
+    MPM_ERR_CONTRACT = -4,           /* ContractViolationError */
+    MPM_ERR_MODE_CONFLICT = -5,      /* ModeConflictError    */
+    MPM_ERR_DEGENERATE = -6,         /* DegenerateStateError */
+    MPM_ERR_CONFIG = -7,             /* ConfigError          */
+    MPM_ERR_BARRIER_TIMEOUT = -8     /* BarrierTimeoutError  */
+};
+
+enum mpm_material_kind {             /* domain.py:26-28 (+ two plastic kinds) */
+    MPM_MAT_FLUID = 0,
+    MPM_MAT_FIXED_COROTATED = 1,
+    MPM_MAT_SNOW = 2,
+    MPM_MAT_SAND = 3
+};
+
+enum mpm_counter {                   /* pipeline.py:57-63 */
+    MPM_C_ACCUM = 0, MPM_C_QUARANTINE = 1, MPM_C_DEGENERATE = 2,
+    MPM_C_SVD_CLAMP = 3, MPM_C_ADDRESS_ERR = 4, MPM_C_SUBGROUPS = 5
+};
+
+/* Material + step scalars of the transfer kernels: the scalar tail of
+ * _p2g_kernel / _gather_advect / _g2p2g_kernel (pipeline.py:316-320, 400-403, 604-610). */
+typedef struct mpm_transfer_params {
+    int32_t mat_kind;        /* enum mpm_material_kind */
+    int32_t nch;             /* channels per particle: 17 fluid, 25 corotated, 26 snow/sand */
+    double mu, lam;          /* Lame parameters */
+    double kappa, gamma;     /* fluid bulk modulus / exponent */
+    int32_t clamp_tension;   /* fluid: clamp negative pressure (pipeline.py:151-156) */
+    int32_t count_stats;     /* also maintain C_ACCUM / C_SUBGROUPS (costs atomics) */
+    double density;
+    double dx;
+    double dt;               /* scatter dt (this step) */
+    double dt_gather;        /* gather dt = dt of the grid update that produced vel (pipeline.py:1230) */
+    double flip_blend;       /* 0 = APIC only (pipeline.py:489-517) */
+    double margin_lo, margin_hi; /* free zone in cells: [origin-margin_lo, origin+4+margin_hi) */
+    double theta_c, theta_s, hardening;   /* snow */
+    double sand_alpha;       /* sand: sqrt(2/3) 2 sin(phi) / (3 - sin(phi)) */
+} mpm_transfer_params;
+
+/* Particle store view: ParticleStore (particles.py:268-287). */
+typedef struct mpm_store_view {
+    float *data;             /* [n_groups][nch][32] */
+    int64_t *orig_id;        /* [n_groups][32] */
+    uint16_t *lane_meta;     /* [n_groups][32] */
+    int32_t *group_len;      /* [n_groups] */
+    int32_t *group_block;    /* [n_groups] */
+    int32_t *group_start;    /* [n_groups] sorted position of lane 0 (exclusive scan of group_len) */
+    int32_t n_groups;
+    int32_t nch;
+} mpm_store_view;
+
+/* Block table view: BlockTable (grid.py:325-386). */
+typedef struct mpm_table_view {
+    int64_t *codes;          /* [count] Morton block codes, gblocks first */
+    int32_t *origin;         /* [count][4] biased cell coords of node 0 of the block (x,y,z,0) */
+    int32_t *neighbor;       /* [n_gblocks][27], index (rz*3+ry)*3+rx, centre 13 */
+    uint8_t *touched[2];     /* [count] per parity */
+    int32_t count;
+    int32_t n_gblocks;
+} mpm_table_view;
+
+/* Step status block written by the transfer kernels (device memory, 64 bytes):
+ *   out_stats[0] (free-zone violation) and out_stats[1] (max speed^2) of
+ *   _gather_advect (pipeline.py:408-409), plus counters[6] (pipeline.py:57-63). */
+typedef struct mpm_step_status {
+    int32_t zone_violation;
+    uint32_t vmax2_bits;             /* float bits of max |v|^2 (nonnegative, so uint order = float order) */
+    unsigned long long counters[MPM_N_COUNTERS];
+} mpm_step_status;
+
+/* ---- library ---------------------------------------------------------------------- */
+const char *mpm_version(void);
+const char *mpm_last_error(void);       /* text of the last CUDA error seen by this thread */
+int mpm_device_arch(void);              /* 100 for sm_100 */
+
+/* ---- rebuild-mapping: Worker._rebuild (pipeline.py:958-1015) ------------------------ */
+
+/* Compaction of the live lanes of the old store into rebuild input order
+ * (ParticleStore.gather_flat, particles.py:336-358; _gather_live, particles.py:177-188):
+ * group-major, lane-minor, quarantined lanes dropped (drop_quarantined=1) or kept.
+ * src_slot[i] = group*32+lane of input particle i; *n_live (device int32) = count. */
+int mpm_compact_live(const mpm_store_view *store, int drop_quarantined, int32_t *group_live_scratch,
+                     int32_t *src_slot, int32_t *n_live, int32_t *scan_scratch, void *stream);
+
+/* particle_code_batch (particles.py:52-58) + encode_batch (grid.py:92-107):
+ * code = Morton(floor(pos/dx - 0.5) + 64) evaluated in float64 with a DIVISION.
+ * Input particle i < n_live comes from the old store slot src_slot[i]; i >= n_live comes
+ * from the staged flat array staged[(i-n_live)*nch + ch].  *n_total (device) = n_live + n_staged.
+ * bad_index (device int32, reset to INT32_MAX by this call) receives the smallest i whose
+ * cell leaves [0, 2^21). */
+int mpm_particle_codes(const mpm_store_view *store, const int32_t *src_slot, const int32_t *n_live_dev,
+                       const float *staged, int32_t n_staged, int32_t n_upper, double dx,
+                       int64_t *codes, int32_t *n_total, int32_t *bad_index, void *stream);
+
+/* BlockHashTable.insert_batch in first-occurrence order (grid.py:136-157, 354-357):
+ * gidx[i] = dense index of block codes[i]>>6, indices issued in order of first occurrence
+ * over i.  Hash = multiply-shift of grid.py:130-133 on a table of hash_cap (power of two)
+ * entries that this call clears first.  *n_gblocks (device) receives the block count,
+ * gcodes[0..n_gblocks) the unique codes in index order.  overflow (device int32) is set
+ * when the table is too small. */
+int mpm_hash_insert_blocks(const int64_t *codes, const int32_t *n_dev, int32_t n_upper,
+                           int64_t *hkeys, int32_t *hvals, int32_t *hfirst, int32_t hash_cap,
+                           int32_t *pslot, int32_t *flag_scratch, int32_t *scan_scratch,
+                           int32_t *gidx, int64_t *gcodes, int32_t *n_gblocks, int32_t *overflow,
+                           void *stream);
+
+/* _dilate_and_link (grid.py:282-322) + the tail of BlockTable.rebuild (grid.py:362-386):
+ * 27-neighbourhood of every gblock inserted in (gblock, dz, dy, dx) order, new blocks
+ * numbered from n_gblocks in order of first appearance; fills codes, origin, neighbor.
+ * *count (device) = pblock count; bad_block (device, preset INT32_MAX) = smallest gblock
+ * index with a neighbour outside [0, 2^19). */
+int mpm_dilate_and_link(const int64_t *gcodes, int32_t n_gblocks, int64_t *hkeys, int32_t *hvals,
+                        int32_t *hfirst, int32_t hash_cap, int32_t *qslot, int32_t *flag_scratch,
+                        int32_t *scan_scratch, int64_t *codes, int32_t *origin, int32_t *neighbor,
+                        int32_t pblock_cap, int32_t *count, int32_t *bad_block, int32_t *overflow,
+                        void *stream);
+
+/* ParticleStore.histogram_sort part 1 (particles.py:360-399; _counting_sort_perm :66-80,
+ * _build_groups :152-173): stable counting sort by key=(gidx<<6)|(code&63) and the lane
+ * group structure.  perm[j] = input index of sorted position j.  bin_start has
+ * n_gblocks*64+1 entries.  *n_groups (device) = group count. */
+int mpm_sort_and_group(const int64_t *codes, const int32_t *gidx, const int32_t *n_dev, int32_t n_upper,
+                       int32_t n_gblocks, int32_t *bin_start, int32_t *tmp_perm, int32_t *perm,
+                       int32_t *block_group_first, int32_t *scan_scratch, int32_t *n_groups,
+                       void *stream);
+
+/* ParticleStore.histogram_sort part 2 (_scatter_sorted particles.py:192-199) fused with
+ * set_group_origins + _recompute_lane_keys (particles.py:235-261, 453): permutes all
+ * channels and ids from the old store / staged arrays into the new store, zero-fills
+ * padding lanes, writes group_len/group_block/group_start and the 10-bit lane keys
+ * (float64, MULTIPLICATION by 1/dx as in the reference). */
+int mpm_scatter_sorted(const mpm_store_view *old_store, const int32_t *src_slot, const int32_t *n_live_dev,
+                       const float *staged, const int64_t *staged_ids, const int32_t *perm,
+                       const int32_t *bin_start, const int32_t *block_group_first, int32_t n_gblocks,
+                       const int32_t *table_origin, double dx, const mpm_store_view *new_store,
+                       void *stream);
+
+/* ---- substep: Worker.run_step (pipeline.py:905-940) ---------------------------------
+ *
+ * Every substep entry point takes `guard`: NULL, or a device int32.  A kernel launched with a
+ * non-NULL guard returns without touching memory when *guard != 0, and the gather kernels
+ * set *guard = 1 together with status->zone_violation.  This lets the host enqueue step s+1
+ * before it has read step s's rebuild flag: if step s asked for a rebuild, step s+1's
+ * kernels are no-ops and the host re-issues the step after rebuilding (and clearing the
+ * guard).  Results are identical to the reference's "check flag, then step" order. */
+
+/* Worker._clear (pipeline.py:1022-1037): zero the rows of raw flagged in touched and reset
+ * the flags; full=1 clears every row (first use of a parity after a rebuild). */
+int mpm_clear(float *raw, uint8_t *touched, int32_t count, int full, int32_t *guard, void *stream);
+
+/* _p2g_kernel (pipeline.py:316-356): scatter_prep + subgroup scatter of every group into
+ * raw (float4 nodes), touched flags set for every addressed block. */
+int mpm_p2g(const mpm_store_view *store, const mpm_table_view *table, float *raw, uint8_t *touched,
+            const mpm_transfer_params *params, mpm_step_status *status, int32_t *guard, void *stream);
+
+/* _reduce_and_update + _grid_finalize (pipeline.py:1166-1231, 660-722): for every block
+ * flagged in touched: vel = raw (+ peer raw rows through peer_map where the peer touched
+ * the block) ; zero-mass nodes -> 0 ; v = mom/m ; vel_old saved before gravity when
+ * vel_old != NULL ; v += dt*g ; box boundary (inclusive comparisons on node world
+ * position).  n_peers may be 0.  peer_map[p][b] = peer p's index of local block b or -1. */
+int mpm_grid_update(const float *raw, const uint8_t *touched, float *vel, float *vel_old,
+                    const mpm_table_view *table, int32_t n_peers, const float *const *peer_raw,
+                    const uint8_t *const *peer_touched, const int32_t *const *peer_map,
+                    double dt, const double gravity[3], int apply_bc, int bc_sticky,
+                    const double box_lo[3], const double box_hi[3], double dx, int fuse_clear,
+                    float *raw_mut, uint8_t *touched_mut, int32_t *guard, void *stream);
+
+/* _gather_advect (pipeline.py:400-600). */
+int mpm_g2p(const mpm_store_view *store, const mpm_table_view *table, const float *vel,
+            const float *vel_old, const mpm_transfer_params *params, mpm_step_status *status,
+            int32_t *guard, void *stream);
+
+/* _g2p2g_kernel (pipeline.py:604-653): previous step's gather (dt_gather) fused with this
+ * step's scatter (dt). */
+int mpm_g2p2g(const mpm_store_view *store, const mpm_table_view *table, const float *vel,
+              const float *vel_old, float *raw, uint8_t *touched, const mpm_transfer_params *params,
+              mpm_step_status *status, int32_t *guard, void *stream);
+
+/* Reset zone_violation and vmax2_bits of a status block before a gather (the reference
+ * passes a fresh out_stats = zeros(2) per call, pipeline.py:1090). */
+int mpm_status_reset(mpm_step_status *status, int32_t *guard, void *stream);
+
+/* ---- readback / aggregates ---------------------------------------------------------- */
+
+/* ParticleStore.positions_with_ids / state readback (particles.py:466-475): all stored
+ * lanes (quarantined included) in (group, lane) order as flat[n][nch] + ids[n]. */
+int mpm_gather_state(const mpm_store_view *store, float *flat, int64_t *ids, void *stream);
+
+/* total_mass / total_momentum (particles.py:477-487) and kinetic energy, accumulated in
+ * float64: out[0]=mass, out[1..3]=momentum, out[4]=kinetic energy. */
+int mpm_particle_aggregates(const mpm_store_view *store, double *out5, void *stream);
+
+/* grid mass / momentum over touched blocks of raw (pipeline.py:1189-1203): out[0..3]. */
+int mpm_grid_aggregates(const float *raw, const uint8_t *touched, int32_t count, double *out4,
+                        void *stream);
+
+/* Shared-block tagging (Worker._post_barrier, pipeline.py:1147-1164; _hash_lookup_batch,
+ * grid.py:161-173): peer_map[local index of code] = position in peer_codes, -1 elsewhere. */
+int mpm_tag_shared(const int64_t *peer_codes, int32_t n_peer_codes, const int64_t *hkeys,
+                   const int32_t *hvals, int32_t hash_cap, int32_t *peer_map, int32_t local_count,
+                   void *stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* MPM_B200_H */

@@ -1,0 +1,138 @@
+"""ctypes binding of libmpm_b200.so (include/mpm_b200.h).
+
+The library is the product path: if it is missing, or the CUDA device is not a B200-class
+part when a compute call is made, this module raises -- there is no CPU fallback.
+Status codes map 1:1 onto the reference's exception classes
+(/root/reference/pkg/src/mpmbench/errors.py:4-37).
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+
+from . import errors as E
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "libmpm_b200.so")
+
+MPM_MAX_PEERS = 15
+N_COUNTERS = 6
+LANE_QUARANTINED = 0x8000
+
+p_void = C.c_void_p
+i32 = C.c_int32
+f64 = C.c_double
+
+
+class TransferParams(C.Structure):
+    _fields_ = [
+        ("mat_kind", i32), ("nch", i32),
+        ("mu", f64), ("lam", f64), ("kappa", f64), ("gamma", f64),
+        ("clamp_tension", i32), ("count_stats", i32),
+        ("density", f64), ("dx", f64), ("dt", f64), ("dt_gather", f64), ("flip_blend", f64),
+        ("margin_lo", f64), ("margin_hi", f64),
+        ("theta_c", f64), ("theta_s", f64), ("hardening", f64), ("sand_alpha", f64),
+    ]
+
+
+class StoreView(C.Structure):
+    _fields_ = [
+        ("data", p_void), ("orig_id", p_void), ("lane_meta", p_void), ("group_len", p_void),
+        ("group_block", p_void), ("group_start", p_void), ("n_groups", i32), ("nch", i32),
+    ]
+
+
+class TableView(C.Structure):
+    _fields_ = [
+        ("codes", p_void), ("origin", p_void), ("neighbor", p_void), ("touched", p_void * 2),
+        ("count", i32), ("n_gblocks", i32),
+    ]
+
+
+class StepStatus(C.Structure):
+    _fields_ = [("zone_violation", i32), ("vmax2_bits", C.c_uint32),
+                ("counters", C.c_ulonglong * N_COUNTERS)]
+
+
+STATUS_BYTES = C.sizeof(StepStatus)
+
+_STATUS_TO_ERROR = {
+    -1: E.RejectedInputError, -2: E.SpatialDomainError, -3: E.ResourceError,
+    -4: E.ContractViolationError, -5: E.ModeConflictError, -6: E.DegenerateStateError,
+    -7: E.ConfigError, -8: E.BarrierTimeoutError,
+}
+
+# name -> argtypes; every function returns int (mpm_status) unless listed in _RESTYPES
+_SIGNATURES = {
+    "mpm_compact_live": [C.POINTER(StoreView), i32, p_void, p_void, p_void, p_void, p_void],
+    "mpm_particle_codes": [C.POINTER(StoreView), p_void, p_void, p_void, i32, i32, f64, p_void,
+                           p_void, p_void, p_void],
+    "mpm_hash_insert_blocks": [p_void, p_void, i32, p_void, p_void, p_void, i32, p_void, p_void,
+                               p_void, p_void, p_void, p_void, p_void, p_void],
+    "mpm_dilate_and_link": [p_void, i32, p_void, p_void, p_void, i32, p_void, p_void, p_void,
+                            p_void, p_void, p_void, i32, p_void, p_void, p_void, p_void],
+    "mpm_sort_and_group": [p_void, p_void, p_void, i32, i32, p_void, p_void, p_void, p_void,
+                           p_void, p_void, p_void],
+    "mpm_scatter_sorted": [C.POINTER(StoreView), p_void, p_void, p_void, p_void, p_void, p_void,
+                           p_void, i32, p_void, f64, C.POINTER(StoreView), p_void],
+    "mpm_clear": [p_void, p_void, i32, i32, p_void, p_void],
+    "mpm_status_reset": [p_void, p_void, p_void],
+    "mpm_p2g": [C.POINTER(StoreView), C.POINTER(TableView), p_void, p_void,
+                C.POINTER(TransferParams), p_void, p_void, p_void],
+    "mpm_grid_update": [p_void, p_void, p_void, p_void, C.POINTER(TableView), i32,
+                        C.POINTER(p_void), C.POINTER(p_void), C.POINTER(p_void), f64,
+                        C.POINTER(f64), i32, i32, C.POINTER(f64), C.POINTER(f64), f64, i32,
+                        p_void, p_void, p_void, p_void],
+    "mpm_g2p": [C.POINTER(StoreView), C.POINTER(TableView), p_void, p_void,
+                C.POINTER(TransferParams), p_void, p_void, p_void],
+    "mpm_g2p2g": [C.POINTER(StoreView), C.POINTER(TableView), p_void, p_void, p_void, p_void,
+                  C.POINTER(TransferParams), p_void, p_void, p_void],
+    "mpm_gather_state": [C.POINTER(StoreView), p_void, p_void, p_void],
+    "mpm_particle_aggregates": [C.POINTER(StoreView), p_void, p_void],
+    "mpm_grid_aggregates": [p_void, p_void, i32, p_void, p_void],
+    "mpm_tag_shared": [p_void, i32, p_void, p_void, i32, p_void, i32, p_void],
+    "mpm_version": [],
+    "mpm_last_error": [],
+    "mpm_device_arch": [],
+}
+_RESTYPES = {"mpm_version": C.c_char_p, "mpm_last_error": C.c_char_p}
+
+EXPORTED_SYMBOLS = tuple(_SIGNATURES)
+
+_lib = None
+
+
+def lib() -> C.CDLL:
+    """Load libmpm_b200.so (built by paper_2111_00699_b200.build).  Raises ResourceError when
+    the library is missing: the CUDA core is the only implementation of the substep."""
+    global _lib
+    if _lib is None:
+        if not os.path.exists(LIB_PATH):
+            raise E.ResourceError(
+                f"{LIB_PATH} is missing: build it with `python -m paper_2111_00699_b200.build` "
+                "(there is no CPU fallback for the substep)")
+        handle = C.CDLL(LIB_PATH)
+        for name, argtypes in _SIGNATURES.items():
+            fn = getattr(handle, name)
+            fn.argtypes = argtypes
+            fn.restype = _RESTYPES.get(name, C.c_int)
+        _lib = handle
+    return _lib
+
+
+def check(status: int, what: str = "") -> None:
+    if status == 0:
+        return
+    cls = _STATUS_TO_ERROR.get(status, E.SimulationError)
+    detail = lib().mpm_last_error().decode() if status == -3 else ""
+    raise cls(f"{what or 'libmpm_b200'} failed with status {status} {detail}".strip())
+
+
+def require_device() -> None:
+    """Fail loudly unless a CUDA device of compute capability 10.x is current."""
+    import torch
+    if not torch.cuda.is_available():
+        raise E.ResourceError("no CUDA device: the MLS-MPM substep core is CUDA-only (sm_100a)")
+    arch = lib().mpm_device_arch()
+    if arch // 10 != 10:
+        raise E.ResourceError(f"libmpm_b200.so is built for sm_100a; current device is sm_{arch}")

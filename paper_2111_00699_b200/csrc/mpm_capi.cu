@@ -1,0 +1,44 @@
+// Library-level entry points and CUDA error plumbing of libmpm_b200.so.
+#include <stdio.h>
+#include <string.h>
+
+#include "mpm_common.cuh"
+
+namespace mpm {
+
+static thread_local char g_last_error[512] = "";
+
+void set_last_error(const char *what, cudaError_t e)
+{
+    snprintf(g_last_error, sizeof g_last_error, "%s: %s (%s)", what, cudaGetErrorString(e),
+             cudaGetErrorName(e));
+}
+
+// Launch-time errors only (bad configuration, no device, no kernel image): the call stays
+// asynchronous.  Execution errors surface at the host's next synchronisation.
+int check_launch(const char *what)
+{
+    cudaError_t e = cudaGetLastError();
+    if (e == cudaSuccess) return MPM_OK;
+    set_last_error(what, e);
+    return MPM_ERR_RESOURCE;
+}
+
+}  // namespace mpm
+
+extern "C" {
+
+const char *mpm_version(void) { return "mpm_b200 0.1 (sm_100a)"; }
+
+const char *mpm_last_error(void) { return mpm::g_last_error; }
+
+int mpm_device_arch(void)
+{
+    int dev = 0, major = 0, minor = 0;
+    if (cudaGetDevice(&dev) != cudaSuccess) { cudaGetLastError(); return 0; }
+    cudaDeviceGetAttribute(&major, cudaDevAttrComputeCapabilityMajor, dev);
+    cudaDeviceGetAttribute(&minor, cudaDevAttrComputeCapabilityMinor, dev);
+    return major * 10 + minor;
+}
+
+}  // extern "C"

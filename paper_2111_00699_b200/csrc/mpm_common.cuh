@@ -1,0 +1,92 @@
+// Shared device helpers of the B200 MLS-MPM core (sm_100a).
+// Reference paths are relative to /root/reference/pkg/src/mpmbench/.
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include "../../include/mpm_b200.h"
+
+#define MPM_SM_COUNT 148
+
+// particle channels (particles.py:24-31)
+#define CH_POS 0
+#define CH_VEL 3
+#define CH_C 6
+#define CH_MASS 15
+#define CH_DEF 16
+#define CH_PLASTIC 25
+
+#define MPM_EMPTY_KEY ((long long)-1)
+#define MPM_HASH_MULT 0x9E3779B97F4A7C15ull
+#define MPM_INT_MAX 0x7fffffff
+
+namespace mpm {
+
+// ---- error plumbing ---------------------------------------------------------------
+void set_last_error(const char *what, cudaError_t e);
+int check_launch(const char *what);
+
+// ---- Morton coding (grid.py:41-70), 21 bits per axis, x lowest ---------------------
+__host__ __device__ __forceinline__ unsigned long long part1by2(unsigned long long x)
+{
+    x &= 0x1FFFFFull;
+    x = (x | (x << 32)) & 0x1F00000000FFFFull;
+    x = (x | (x << 16)) & 0x1F0000FF0000FFull;
+    x = (x | (x << 8)) & 0x100F00F00F00F00Full;
+    x = (x | (x << 4)) & 0x10C30C30C30C30C3ull;
+    x = (x | (x << 2)) & 0x1249249249249249ull;
+    return x;
+}
+__host__ __device__ __forceinline__ unsigned long long compact1by2(unsigned long long x)
+{
+    x &= 0x1249249249249249ull;
+    x = (x ^ (x >> 2)) & 0x10C30C30C30C30C3ull;
+    x = (x ^ (x >> 4)) & 0x100F00F00F00F00Full;
+    x = (x ^ (x >> 8)) & 0x1F0000FF0000FFull;
+    x = (x ^ (x >> 16)) & 0x1F00000000FFFFull;
+    x = (x ^ (x >> 32)) & 0x1FFFFFull;
+    return x;
+}
+__host__ __device__ __forceinline__ long long encode_cell(long long x, long long y, long long z)
+{
+    return (long long)(part1by2((unsigned long long)x) | (part1by2((unsigned long long)y) << 1) |
+                       (part1by2((unsigned long long)z) << 2));
+}
+
+// multiply-shift hash of grid.py:130-133 (arithmetic shift of the wrapped signed product)
+__device__ __forceinline__ int hash_slot(long long key, int shift, int mask)
+{
+    long long prod = (long long)((unsigned long long)key * MPM_HASH_MULT);
+    return (int)((prod >> shift) & (long long)mask);
+}
+__host__ __device__ __forceinline__ int hash_shift_for(int cap)
+{
+    // grid.py: shift = 64 - log2(cap)
+    int bits = 0;
+    while ((1 << bits) < cap) ++bits;
+    return 64 - bits;
+}
+
+// node slot inside a 4^3 block: Morton of the low two bits per axis (pipeline.py:144-147)
+__device__ __forceinline__ int node_slot(int cx, int cy, int cz)
+{
+    return (cx & 1) | ((cy & 1) << 1) | ((cz & 1) << 2) | ((cx & 2) << 2) | ((cy & 2) << 3) |
+           ((cz & 2) << 4);
+}
+
+// Guard word of speculative launches: a step kernel launched with a non-null guard returns
+// without touching memory when *guard != 0 (set by the gather that found a particle outside
+// its free zone), so the host may enqueue step s+1 before it has read step s's flag.
+__device__ __forceinline__ bool guarded_out(const int *guard)
+{
+    return guard != nullptr && *((volatile const int *)guard) != 0;
+}
+
+// exclusive scan of int32 (three kernels, no library): out may alias in; total (device) optional
+void exclusive_scan_i32(const int32_t *in, int32_t *out, int32_t n, int32_t *block_sums,
+                        int32_t *total, cudaStream_t stream);
+// scratch entries needed by exclusive_scan_i32 for n elements
+inline int32_t scan_scratch_len(int64_t n) { return (int32_t)((n + 1023) / 1024 + 1); }
+
+}  // namespace mpm

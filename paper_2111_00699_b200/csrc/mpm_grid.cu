@@ -1,0 +1,245 @@
+// Grid kernels: buffer clear and the fused reduce + update + boundary kernel (sm_100a).
+//
+// Reference (paths relative to /root/reference/pkg/src/mpmbench/):
+//   Worker._clear             pipeline.py:1022-1037
+//   Worker._reduce_and_update pipeline.py:1166-1231
+//   _grid_finalize            pipeline.py:660-722
+//
+// One thread per grid node, four 4^3 blocks (256 nodes) per CTA; a node is one float4
+// (mass, momentum) so every access is a 16-byte vector and a warp covers 512 contiguous
+// bytes.  Untouched blocks exit after one flag read, so the launch covers the whole block
+// table and no compacted index list (the reference's flatnonzero) is needed.
+#include "mpm_common.cuh"
+
+#define MPM_MAX_PEERS 15
+
+namespace mpm {
+
+struct PeerSet {
+    const float4 *raw[MPM_MAX_PEERS];
+    const uint8_t *touched[MPM_MAX_PEERS];
+    const int *map[MPM_MAX_PEERS];
+    int n;
+};
+
+__global__ void __launch_bounds__(256) clear_kernel(float4 *raw, uint8_t *touched, int count, int full,
+                                                    const int *guard)
+{
+    if (guarded_out(guard)) return;
+    const int b = blockIdx.x * 4 + (threadIdx.x >> 6);
+    const int slot = threadIdx.x & 63;
+    const bool hit = b < count && (full || touched[b]);
+    __syncthreads();   // every thread has read the flag before it is reset
+    if (hit) {
+        raw[(size_t)b * 64 + slot] = make_float4(0.f, 0.f, 0.f, 0.f);
+        if (slot == 0) touched[b] = 0;
+    }
+}
+
+struct GridArgs {
+    const float4 *raw;
+    const uint8_t *touched;
+    float4 *vel;
+    float4 *vel_old;
+    const int4 *origin;
+    int count;
+    PeerSet peers;
+    float dt;
+    float gx, gy, gz;
+    int apply_bc, bc_sticky;
+    double blo[3], bhi[3];
+    double dx;
+    int fuse_clear;
+    float4 *raw_mut;
+    uint8_t *touched_mut;
+    const int *guard;
+};
+
+__global__ void __launch_bounds__(256) grid_update_kernel(const GridArgs a)
+{
+    if (guarded_out(a.guard)) return;
+    const int b = blockIdx.x * 4 + (threadIdx.x >> 6);
+    const int slot = threadIdx.x & 63;
+    const bool hit = b < a.count && a.touched[b];
+    if (a.fuse_clear) __syncthreads();
+    if (!hit) return;
+    const size_t idx = (size_t)b * 64 + slot;
+    float4 node = a.raw[idx];
+    // cross-worker reduction (pipeline.py:1172-1188): peers' raw rows are only read
+    for (int p = 0; p < a.peers.n; ++p) {
+        const int q = a.peers.map[p][b];
+        if (q < 0 || a.peers.touched[p][q] != 1) continue;
+        const float4 o = a.peers.raw[p][(size_t)q * 64 + slot];
+        node.x += o.x; node.y += o.y; node.z += o.z; node.w += o.w;
+    }
+    if (a.fuse_clear) {
+        a.raw_mut[idx] = make_float4(0.f, 0.f, 0.f, 0.f);
+        if (slot == 0) a.touched_mut[b] = 0;
+    }
+    const float m = node.x;
+    if (!(m > 0.0f)) {   // m <= 0 (pipeline.py:676-681)
+        a.vel[idx] = make_float4(0.f, 0.f, 0.f, 0.f);
+        return;
+    }
+    float vx = node.y / m, vy = node.z / m, vz = node.w / m;
+    if (a.vel_old) a.vel_old[idx] = make_float4(0.f, vx, vy, vz);   // saved before gravity (:692-698)
+    vx += a.dt * a.gx; vy += a.dt * a.gy; vz += a.dt * a.gz;
+    if (a.apply_bc) {
+        // node world position in float64 so that the inclusive comparisons of
+        // pipeline.py:707-718 classify nodes exactly like the reference
+        const int4 org = a.origin[b];
+        const int sx = (slot & 1) | ((slot >> 2) & 2);
+        const int sy = ((slot >> 1) & 1) | ((slot >> 3) & 2);
+        const int sz = ((slot >> 2) & 1) | ((slot >> 4) & 2);
+        const double px = (double)(org.x - MPM_CELL_BIAS + sx) * a.dx;
+        const double py = (double)(org.y - MPM_CELL_BIAS + sy) * a.dx;
+        const double pz = (double)(org.z - MPM_CELL_BIAS + sz) * a.dx;
+        if (a.bc_sticky) {
+            if (px <= a.blo[0] || px >= a.bhi[0] || py <= a.blo[1] || py >= a.bhi[1] ||
+                pz <= a.blo[2] || pz >= a.bhi[2]) { vx = 0.f; vy = 0.f; vz = 0.f; }
+        } else {
+            if ((px <= a.blo[0] && vx < 0.f) || (px >= a.bhi[0] && vx > 0.f)) vx = 0.f;
+            if ((py <= a.blo[1] && vy < 0.f) || (py >= a.bhi[1] && vy > 0.f)) vy = 0.f;
+            if ((pz <= a.blo[2] && vz < 0.f) || (pz >= a.bhi[2] && vz > 0.f)) vz = 0.f;
+        }
+    }
+    a.vel[idx] = make_float4(m, vx, vy, vz);
+}
+
+// ---- aggregates (float64 accumulation) ----------------------------------------------
+__device__ __forceinline__ double warp_sum(double v)
+{
+#pragma unroll
+    for (int d = 16; d > 0; d >>= 1) v += __shfl_down_sync(0xffffffffu, v, d);
+    return v;
+}
+
+__global__ void __launch_bounds__(256) particle_aggregates_kernel(const float *__restrict__ data, int nch,
+                                                                  const int *__restrict__ group_len,
+                                                                  int n_groups, double *out5)
+{
+    const int g = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    const int lane = threadIdx.x & 31;
+    double m = 0, mx = 0, my = 0, mz = 0, ke = 0;
+    if (g < n_groups && lane < group_len[g]) {
+        const float *gd = data + (size_t)g * nch * 32 + lane;
+        m = gd[CH_MASS * 32];
+        const double vx = gd[(CH_VEL + 0) * 32], vy = gd[(CH_VEL + 1) * 32], vz = gd[(CH_VEL + 2) * 32];
+        mx = m * vx; my = m * vy; mz = m * vz;
+        ke = 0.5 * m * (vx * vx + vy * vy + vz * vz);
+    }
+    m = warp_sum(m); mx = warp_sum(mx); my = warp_sum(my); mz = warp_sum(mz); ke = warp_sum(ke);
+    if (lane == 0 && g < n_groups) {
+        atomicAdd(&out5[0], m); atomicAdd(&out5[1], mx); atomicAdd(&out5[2], my);
+        atomicAdd(&out5[3], mz); atomicAdd(&out5[4], ke);
+    }
+}
+
+__global__ void __launch_bounds__(256) grid_aggregates_kernel(const float4 *__restrict__ raw,
+                                                              const uint8_t *__restrict__ touched,
+                                                              int count, double *out4)
+{
+    const int b = blockIdx.x * 4 + (threadIdx.x >> 6);
+    const int slot = threadIdx.x & 63;
+    const int lane = threadIdx.x & 31;
+    double m = 0, mx = 0, my = 0, mz = 0;
+    if (b < count && touched[b]) {
+        const float4 n = raw[(size_t)b * 64 + slot];
+        m = n.x; mx = n.y; my = n.z; mz = n.w;
+    }
+    m = warp_sum(m); mx = warp_sum(mx); my = warp_sum(my); mz = warp_sum(mz);
+    if (lane == 0 && m != 0.0) {
+        atomicAdd(&out4[0], m); atomicAdd(&out4[1], mx); atomicAdd(&out4[2], my); atomicAdd(&out4[3], mz);
+    }
+}
+
+__global__ void status_reset_kernel(mpm_step_status *status, const int *guard)
+{
+    if (guarded_out(guard)) return;
+    status->zone_violation = 0;
+    status->vmax2_bits = 0;
+}
+
+}  // namespace mpm
+
+using namespace mpm;
+
+extern "C" {
+
+int mpm_clear(float *raw, uint8_t *touched, int32_t count, int full, int32_t *guard, void *stream)
+{
+    if (count <= 0) return MPM_OK;
+    clear_kernel<<<(count + 3) / 4, 256, 0, (cudaStream_t)stream>>>((float4 *)raw, touched, count, full, guard);
+    return check_launch("mpm_clear");
+}
+
+int mpm_status_reset(mpm_step_status *status, int32_t *guard, void *stream)
+{
+    status_reset_kernel<<<1, 1, 0, (cudaStream_t)stream>>>(status, guard);
+    return check_launch("mpm_status_reset");
+}
+
+int mpm_grid_update(const float *raw, const uint8_t *touched, float *vel, float *vel_old,
+                    const mpm_table_view *table, int32_t n_peers, const float *const *peer_raw,
+                    const uint8_t *const *peer_touched, const int32_t *const *peer_map,
+                    double dt, const double gravity[3], int apply_bc, int bc_sticky,
+                    const double box_lo[3], const double box_hi[3], double dx, int fuse_clear,
+                    float *raw_mut, uint8_t *touched_mut, int32_t *guard, void *stream)
+{
+    if (!table || !gravity) return MPM_ERR_REJECTED_INPUT;
+    if (n_peers < 0 || n_peers > MPM_MAX_PEERS) return MPM_ERR_CONFIG;
+    if (apply_bc && (!box_lo || !box_hi)) return MPM_ERR_REJECTED_INPUT;
+    if (fuse_clear && (n_peers > 0 || !raw_mut || !touched_mut)) return MPM_ERR_MODE_CONFLICT;
+    if (table->count <= 0) return MPM_OK;
+    GridArgs a;
+    a.raw = (const float4 *)raw;
+    a.touched = touched;
+    a.vel = (float4 *)vel;
+    a.vel_old = (float4 *)vel_old;
+    a.origin = (const int4 *)table->origin;
+    a.count = table->count;
+    a.peers.n = n_peers;
+    for (int p = 0; p < n_peers; ++p) {
+        a.peers.raw[p] = (const float4 *)peer_raw[p];
+        a.peers.touched[p] = peer_touched[p];
+        a.peers.map[p] = peer_map[p];
+    }
+    a.dt = (float)dt;
+    a.gx = (float)gravity[0]; a.gy = (float)gravity[1]; a.gz = (float)gravity[2];
+    a.apply_bc = apply_bc;
+    a.bc_sticky = bc_sticky;
+    for (int k = 0; k < 3; ++k) {
+        a.blo[k] = apply_bc ? box_lo[k] : -1e30;
+        a.bhi[k] = apply_bc ? box_hi[k] : 1e30;
+    }
+    a.dx = dx;
+    a.fuse_clear = fuse_clear;
+    a.raw_mut = (float4 *)raw_mut;
+    a.touched_mut = touched_mut;
+    a.guard = guard;
+    grid_update_kernel<<<(a.count + 3) / 4, 256, 0, (cudaStream_t)stream>>>(a);
+    return check_launch("mpm_grid_update");
+}
+
+int mpm_particle_aggregates(const mpm_store_view *store, double *out5, void *stream_)
+{
+    cudaStream_t stream = (cudaStream_t)stream_;
+    cudaMemsetAsync(out5, 0, 5 * sizeof(double), stream);
+    const int G = store->n_groups;
+    if (G > 0)
+        particle_aggregates_kernel<<<(int)(((int64_t)G * 32 + 255) / 256), 256, 0, stream>>>(
+            store->data, store->nch, store->group_len, G, out5);
+    return check_launch("mpm_particle_aggregates");
+}
+
+int mpm_grid_aggregates(const float *raw, const uint8_t *touched, int32_t count, double *out4,
+                        void *stream_)
+{
+    cudaStream_t stream = (cudaStream_t)stream_;
+    cudaMemsetAsync(out4, 0, 4 * sizeof(double), stream);
+    if (count > 0)
+        grid_aggregates_kernel<<<(count + 3) / 4, 256, 0, stream>>>((const float4 *)raw, touched, count, out4);
+    return check_launch("mpm_grid_aggregates");
+}
+
+}  // extern "C"

@@ -1,0 +1,163 @@
+// Constitutive math of the transfer kernels in fp32 (sm_100a).
+// Restates, in single precision, the scalar routines of the reference:
+//   _svd3_scalars   domain.py:195-379   (Jacobi on F^T F, descending order, det(V)=+1,
+//                                        Gram-Schmidt U, sign carried by the last value)
+//   _corotated_tau  domain.py:383-441   tau = 2 mu (F - R) F^T + lam (J-1) J I
+//   _fluid_tau      pipeline.py:151-156 tau = -kappa (J^-gamma - 1)
+// The convergence thresholds are the fp32 counterparts of the reference's fp64 ones.
+#pragma once
+
+#include "mpm_common.cuh"
+
+namespace mpm {
+
+__device__ __forceinline__ float det3(const float *f)
+{
+    return f[0] * (f[4] * f[8] - f[5] * f[7]) - f[1] * (f[3] * f[8] - f[5] * f[6]) +
+           f[2] * (f[3] * f[7] - f[4] * f[6]);
+}
+
+// One Jacobi rotation zeroing a_pq (domain.py:232-303).  vp/vq: columns p,q of V (stride 3).
+__device__ __forceinline__ void jacobi_rotate(float &app, float &aqq, float &apq, float &arp,
+                                              float &arq, float *vp, float *vq)
+{
+    const float a_pq = apq;
+    const float theta = 0.5f * (aqq - app) / a_pq;
+    const float r = sqrtf(1.0f + theta * theta);
+    const float t = theta >= 0.0f ? 1.0f / (theta + r) : -1.0f / (r - theta);
+    const float c = rsqrtf(1.0f + t * t);
+    const float s = t * c;
+    const float pp = app, qq = aqq;
+    app = c * c * pp - 2.0f * s * c * a_pq + s * s * qq;
+    aqq = s * s * pp + 2.0f * s * c * a_pq + c * c * qq;
+    apq = 0.0f;
+    const float rp = arp, rq = arq;
+    arp = c * rp - s * rq;
+    arq = s * rp + c * rq;
+#pragma unroll
+    for (int k = 0; k < 3; ++k) {
+        const float tmp = vp[3 * k];
+        vp[3 * k] = c * tmp - s * vq[3 * k];
+        vq[3 * k] = s * tmp + c * vq[3 * k];
+    }
+}
+
+// f = u diag(s) v^T, row-major 3x3.  s[0] >= s[1] >= |s[2]|, det(u) = det(v) = +1.
+__device__ __forceinline__ void svd3(const float *f, float *u, float *s, float *v)
+{
+    float a00 = f[0] * f[0] + f[3] * f[3] + f[6] * f[6];
+    float a01 = f[0] * f[1] + f[3] * f[4] + f[6] * f[7];
+    float a02 = f[0] * f[2] + f[3] * f[5] + f[6] * f[8];
+    float a11 = f[1] * f[1] + f[4] * f[4] + f[7] * f[7];
+    float a12 = f[1] * f[2] + f[4] * f[5] + f[7] * f[8];
+    float a22 = f[2] * f[2] + f[5] * f[5] + f[8] * f[8];
+    v[0] = 1.f; v[1] = 0.f; v[2] = 0.f; v[3] = 0.f; v[4] = 1.f; v[5] = 0.f; v[6] = 0.f; v[7] = 0.f; v[8] = 1.f;
+    const float tol = 3e-8f * (fabsf(a00) + fabsf(a11) + fabsf(a22)) + 1e-37f;
+    for (int it = 0; it < 15; ++it) {
+        const float m01 = fabsf(a01), m02 = fabsf(a02), m12 = fabsf(a12);
+        float big = m01;
+        int pair = 0;
+        if (m02 > big) { big = m02; pair = 1; }
+        if (m12 > big) { big = m12; pair = 2; }
+        if (big <= tol) break;
+        if (pair == 0) jacobi_rotate(a00, a11, a01, a02, a12, v + 0, v + 1);
+        else if (pair == 1) jacobi_rotate(a00, a22, a02, a01, a12, v + 0, v + 2);
+        else jacobi_rotate(a11, a22, a12, a01, a02, v + 1, v + 2);
+    }
+    float w0 = a00, w1 = a11, w2 = a22, tmp;
+#define MPM_SWAPCOL(p, q)                                                                   \
+    {                                                                                       \
+        tmp = v[p]; v[p] = v[q]; v[q] = tmp;                                                \
+        tmp = v[3 + p]; v[3 + p] = v[3 + q]; v[3 + q] = tmp;                                \
+        tmp = v[6 + p]; v[6 + p] = v[6 + q]; v[6 + q] = tmp;                                \
+    }
+    if (w0 < w1) { tmp = w0; w0 = w1; w1 = tmp; MPM_SWAPCOL(0, 1) }
+    if (w1 < w2) { tmp = w1; w1 = w2; w2 = tmp; MPM_SWAPCOL(1, 2) }
+    if (w0 < w1) { tmp = w0; w0 = w1; w1 = tmp; MPM_SWAPCOL(0, 1) }
+#undef MPM_SWAPCOL
+    if (det3(v) < 0.0f) { v[2] = -v[2]; v[5] = -v[5]; v[8] = -v[8]; }
+    const float s0 = w0 > 0.0f ? sqrtf(w0) : 0.0f;
+    const float s1 = w1 > 0.0f ? sqrtf(w1) : 0.0f;
+    float s2 = w2 > 0.0f ? sqrtf(w2) : 0.0f;
+    float u00 = f[0] * v[0] + f[1] * v[3] + f[2] * v[6];
+    float u10 = f[3] * v[0] + f[4] * v[3] + f[5] * v[6];
+    float u20 = f[6] * v[0] + f[7] * v[3] + f[8] * v[6];
+    float n = sqrtf(u00 * u00 + u10 * u10 + u20 * u20);
+    if (n < 1e-30f) { u00 = 1.0f; u10 = 0.0f; u20 = 0.0f; }
+    else { const float inv = 1.0f / n; u00 *= inv; u10 *= inv; u20 *= inv; }
+    float u01 = f[0] * v[1] + f[1] * v[4] + f[2] * v[7];
+    float u11 = f[3] * v[1] + f[4] * v[4] + f[5] * v[7];
+    float u21 = f[6] * v[1] + f[7] * v[4] + f[8] * v[7];
+    const float d = u01 * u00 + u11 * u10 + u21 * u20;
+    u01 -= d * u00; u11 -= d * u10; u21 -= d * u20;
+    n = sqrtf(u01 * u01 + u11 * u11 + u21 * u21);
+    if (n < 1e-30f) {
+        u01 = -u10; u11 = u00; u21 = 0.0f;
+        const float n2 = sqrtf(u01 * u01 + u11 * u11);
+        if (n2 < 1e-30f) { u01 = 0.0f; u11 = 1.0f; u21 = 0.0f; }
+        else { u01 /= n2; u11 /= n2; }
+    } else { const float inv = 1.0f / n; u01 *= inv; u11 *= inv; u21 *= inv; }
+    const float u02 = u10 * u21 - u20 * u11;
+    const float u12 = u20 * u01 - u00 * u21;
+    const float u22 = u00 * u11 - u10 * u01;
+    const float fv0 = f[0] * v[2] + f[1] * v[5] + f[2] * v[8];
+    const float fv1 = f[3] * v[2] + f[4] * v[5] + f[5] * v[8];
+    const float fv2 = f[6] * v[2] + f[7] * v[5] + f[8] * v[8];
+    if (fv0 * u02 + fv1 * u12 + fv2 * u22 < 0.0f) s2 = -s2;
+    u[0] = u00; u[1] = u01; u[2] = u02; u[3] = u10; u[4] = u11; u[5] = u12;
+    u[6] = u20; u[7] = u21; u[8] = u22;
+    s[0] = s0; s[1] = s1; s[2] = s2;
+}
+
+// Fixed-corotated Kirchhoff stress (domain.py:383-441).  Returns 1 when the singular
+// values were floored (J <= 1e-10), as the reference's clamp flag.
+__device__ __forceinline__ int corotated_tau(const float *f, float mu, float lam, float *t)
+{
+    float J = det3(f);
+    float u[9], s[3], v[9];
+    svd3(f, u, s, v);
+    int clamped = 0;
+    float w[9];
+    if (J <= 1e-10f) {
+#pragma unroll
+        for (int k = 0; k < 3; ++k) if (s[k] < 1e-4f) s[k] = 1e-4f;
+        J = s[0] * s[1] * s[2];
+        clamped = 1;
+#pragma unroll
+        for (int a = 0; a < 3; ++a)
+#pragma unroll
+            for (int b = 0; b < 3; ++b)
+                w[3 * a + b] = s[0] * u[3 * a] * v[3 * b] + s[1] * u[3 * a + 1] * v[3 * b + 1] +
+                               s[2] * u[3 * a + 2] * v[3 * b + 2];
+    } else {
+#pragma unroll
+        for (int k = 0; k < 9; ++k) w[k] = f[k];   // U S V^T == F: skip the lossy reconstruction
+    }
+    float dm[9];
+#pragma unroll
+    for (int a = 0; a < 3; ++a)
+#pragma unroll
+        for (int b = 0; b < 3; ++b)
+            dm[3 * a + b] = w[3 * a + b] - (u[3 * a] * v[3 * b] + u[3 * a + 1] * v[3 * b + 1] +
+                                            u[3 * a + 2] * v[3 * b + 2]);
+    const float two_mu = 2.0f * mu;
+    const float diag = lam * (J - 1.0f) * J;
+#pragma unroll
+    for (int a = 0; a < 3; ++a)
+#pragma unroll
+        for (int b = 0; b < 3; ++b) {
+            const float acc = two_mu * (dm[3 * a] * w[3 * b] + dm[3 * a + 1] * w[3 * b + 1] +
+                                        dm[3 * a + 2] * w[3 * b + 2]);
+            t[3 * a + b] = (a == b) ? acc + diag : acc;
+        }
+    return clamped;
+}
+
+__device__ __forceinline__ float fluid_tau(float J, float kappa, float gamma, int clamp_tension)
+{
+    float p = kappa * (powf(J, -gamma) - 1.0f);
+    if (clamp_tension && p < 0.0f) p = 0.0f;
+    return -p;
+}
+
+}  // namespace mpm

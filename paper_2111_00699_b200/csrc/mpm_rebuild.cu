@@ -1,0 +1,705 @@
+// Rebuild-mapping on the device: particle codes, block hash with first-occurrence
+// numbering, 27-dilation, stable counting sort, lane-group packing.
+//
+// The reference builds these structures with SEQUENTIAL loops whose visiting order defines
+// the result (grid.py:136-157, 282-322; particles.py:66-80, 152-173).  The kernels here
+// are parallel but reproduce that order exactly:
+//   * "index = order of first occurrence" is computed as
+//         atomicMin(first[slot], sequence number)  ->  flag(sequence number == first)
+//         ->  exclusive scan of the flags  ->  index = scan[first]
+//   * the counting sort takes unordered tickets inside a (block, cell) bin and then ranks
+//     the members of each bin by input index, which is what a stable sort would produce.
+// Reference paths are relative to /root/reference/pkg/src/mpmbench/.
+#include "mpm_common.cuh"
+
+namespace mpm {
+
+// ===================================================================================
+// exclusive scan (int32): reduce / scan block sums / apply
+// ===================================================================================
+constexpr int SCAN_THREADS = 256;
+constexpr int SCAN_ITEMS = 4;
+constexpr int SCAN_TILE = SCAN_THREADS * SCAN_ITEMS;
+
+__device__ __forceinline__ int warp_inclusive_scan(int v, int lane)
+{
+#pragma unroll
+    for (int d = 1; d < 32; d <<= 1) {
+        int t = __shfl_up_sync(0xffffffffu, v, d);
+        if (lane >= d) v += t;
+    }
+    return v;
+}
+
+// exclusive scan of one value per thread across the CTA; returns the exclusive prefix, *total = CTA sum
+__device__ __forceinline__ int block_exclusive_scan(int v, int *total)
+{
+    __shared__ int warp_sums[33];
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const int nwarps = (blockDim.x + 31) >> 5;
+    const int inc = warp_inclusive_scan(v, lane);
+    if (lane == 31) warp_sums[warp] = inc;
+    __syncthreads();
+    if (warp == 0) {
+        const int w = lane < nwarps ? warp_sums[lane] : 0;
+        const int winc = warp_inclusive_scan(w, lane);
+        warp_sums[lane] = winc - w;
+        if (lane == 31) warp_sums[32] = winc;
+    }
+    __syncthreads();
+    const int excl = warp_sums[warp] + inc - v;
+    *total = warp_sums[32];
+    __syncthreads();   // warp_sums is reused by the next call
+    return excl;
+}
+
+__global__ void __launch_bounds__(SCAN_THREADS) scan_reduce_kernel(const int *in, int n, int *block_sums)
+{
+    const int base = blockIdx.x * SCAN_TILE + threadIdx.x * SCAN_ITEMS;
+    int s = 0;
+#pragma unroll
+    for (int k = 0; k < SCAN_ITEMS; ++k)
+        if (base + k < n) s += in[base + k];
+    int total;
+    block_exclusive_scan(s, &total);
+    if (threadIdx.x == 0) block_sums[blockIdx.x] = total;
+}
+
+__global__ void __launch_bounds__(1024) scan_blocksums_kernel(int *block_sums, int nb, int *total_out)
+{
+    __shared__ int carry;
+    if (threadIdx.x == 0) carry = 0;
+    __syncthreads();
+    for (int start = 0; start < nb; start += 1024) {
+        int i = start + threadIdx.x;
+        int v = i < nb ? block_sums[i] : 0;
+        int total;
+        int excl = block_exclusive_scan(v, &total);
+        int c = carry;
+        if (i < nb) block_sums[i] = excl + c;
+        __syncthreads();
+        if (threadIdx.x == 0) carry = c + total;
+        __syncthreads();
+    }
+    if (threadIdx.x == 0) {
+        block_sums[nb] = carry;
+        if (total_out) *total_out = carry;
+    }
+}
+
+__global__ void __launch_bounds__(SCAN_THREADS) scan_apply_kernel(const int *in, int *out, int n,
+                                                                  const int *block_sums)
+{
+    const int base = blockIdx.x * SCAN_TILE + threadIdx.x * SCAN_ITEMS;
+    int v[SCAN_ITEMS];
+    int s = 0;
+#pragma unroll
+    for (int k = 0; k < SCAN_ITEMS; ++k) {
+        v[k] = (base + k < n) ? in[base + k] : 0;
+        s += v[k];
+    }
+    int total;
+    int excl = block_exclusive_scan(s, &total) + block_sums[blockIdx.x];
+#pragma unroll
+    for (int k = 0; k < SCAN_ITEMS; ++k) {
+        if (base + k < n) out[base + k] = excl;
+        excl += v[k];
+    }
+}
+
+void exclusive_scan_i32(const int32_t *in, int32_t *out, int32_t n, int32_t *block_sums,
+                        int32_t *total, cudaStream_t stream)
+{
+    if (n <= 0) {
+        if (total) cudaMemsetAsync(total, 0, sizeof(int32_t), stream);
+        return;
+    }
+    const int nb = (n + SCAN_TILE - 1) / SCAN_TILE;
+    scan_reduce_kernel<<<nb, SCAN_THREADS, 0, stream>>>(in, n, block_sums);
+    scan_blocksums_kernel<<<1, 1024, 0, stream>>>(block_sums, nb, total);
+    scan_apply_kernel<<<nb, SCAN_THREADS, 0, stream>>>(in, out, n, block_sums);
+}
+
+// ===================================================================================
+// live-lane compaction (particles.py:177-188, 336-358)
+// ===================================================================================
+__global__ void __launch_bounds__(256) live_count_kernel(const uint16_t *__restrict__ lane_meta,
+                                                         const int *__restrict__ group_len,
+                                                         int n_groups, int drop_q,
+                                                         int *__restrict__ group_live)
+{
+    const int g = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    const int lane = threadIdx.x & 31;
+    if (g >= n_groups) return;
+    const int len = group_len[g];
+    bool live = lane < len;
+    if (live && drop_q) live = !(lane_meta[g * 32 + lane] & MPM_LANE_QUARANTINED);
+    unsigned m = __ballot_sync(0xffffffffu, live);
+    if (lane == 0) group_live[g] = __popc(m);
+}
+
+__global__ void __launch_bounds__(256) live_write_kernel(const uint16_t *__restrict__ lane_meta,
+                                                         const int *__restrict__ group_len,
+                                                         int n_groups, int drop_q,
+                                                         const int *__restrict__ group_base,
+                                                         int *__restrict__ src_slot)
+{
+    const int g = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    const int lane = threadIdx.x & 31;
+    if (g >= n_groups) return;
+    const int len = group_len[g];
+    bool live = lane < len;
+    if (live && drop_q) live = !(lane_meta[g * 32 + lane] & MPM_LANE_QUARANTINED);
+    unsigned m = __ballot_sync(0xffffffffu, live);
+    if (live) src_slot[group_base[g] + __popc(m & ((1u << lane) - 1u))] = g * 32 + lane;
+}
+
+// ===================================================================================
+// particle codes (particles.py:52-58, grid.py:92-107): float64, DIVISION by dx
+// ===================================================================================
+__device__ __forceinline__ float load_channel(const float *__restrict__ data, int nch, int slot, int ch)
+{
+    return data[((size_t)(slot >> 5) * nch + ch) * 32 + (slot & 31)];
+}
+
+__global__ void __launch_bounds__(256) particle_codes_kernel(
+    const float *__restrict__ data, int nch, const int *__restrict__ src_slot,
+    const int *__restrict__ n_live_dev, const float *__restrict__ staged, int n_staged, int n_upper,
+    double dx, long long *__restrict__ codes, int *__restrict__ bad_index)
+{
+    const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    const int n_live = n_live_dev ? *n_live_dev : 0;
+    const int n = n_live + n_staged;
+    if (i >= n_upper) return;
+    if (i >= n) { codes[i] = 0; return; }
+    float p[3];
+    if (i < n_live) {
+        const int slot = src_slot[i];
+#pragma unroll
+        for (int a = 0; a < 3; ++a) p[a] = load_channel(data, nch, slot, CH_POS + a);
+    } else {
+        const float *s = staged + (size_t)(i - n_live) * nch;
+#pragma unroll
+        for (int a = 0; a < 3; ++a) p[a] = s[CH_POS + a];
+    }
+    long long c[3];
+    bool bad = false;
+#pragma unroll
+    for (int a = 0; a < 3; ++a) {
+        double q = __dsub_rn(__ddiv_rn((double)p[a], dx), 0.5);
+        double fl = floor(q);
+        // non-finite positions fall outside the encodable range like any other stray particle
+        long long cell = (fl >= -4.0e18 && fl <= 4.0e18) ? (long long)fl + MPM_CELL_BIAS : -1;
+        if (cell < 0 || cell >= (1 << 21)) { bad = true; cell = 0; }
+        c[a] = cell;
+    }
+    if (bad) atomicMin(bad_index, i);
+    codes[i] = encode_cell(c[0], c[1], c[2]);
+}
+
+// ===================================================================================
+// hash insert in first-occurrence order (grid.py:136-157)
+// ===================================================================================
+__global__ void hash_clear_kernel(long long *hkeys, int *hvals, int *hfirst, int cap)
+{
+    const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i < cap) {
+        hkeys[i] = MPM_EMPTY_KEY;
+        hvals[i] = -1;
+        hfirst[i] = MPM_INT_MAX;
+    }
+}
+
+// returns the slot of `code` after inserting it if absent, or -1 on overflow
+__device__ __forceinline__ int hash_insert(long long *hkeys, int shift, int mask, long long code)
+{
+    int slot = hash_slot(code, shift, mask);
+    for (int probes = 0; probes <= mask; ++probes) {
+        long long prev = hkeys[slot];
+        if (prev == code) return slot;
+        if (prev == MPM_EMPTY_KEY) {
+            prev = (long long)atomicCAS((unsigned long long *)&hkeys[slot],
+                                        (unsigned long long)MPM_EMPTY_KEY, (unsigned long long)code);
+            if (prev == MPM_EMPTY_KEY || prev == code) return slot;
+        }
+        slot = (slot + 1) & mask;
+    }
+    return -1;
+}
+
+__device__ __forceinline__ int hash_find(const long long *hkeys, int shift, int mask, long long code)
+{
+    int slot = hash_slot(code, shift, mask);
+    for (int probes = 0; probes <= mask; ++probes) {
+        long long k = hkeys[slot];
+        if (k == code) return slot;
+        if (k == MPM_EMPTY_KEY) return -1;
+        slot = (slot + 1) & mask;
+    }
+    return -1;
+}
+
+__global__ void __launch_bounds__(256) block_insert_kernel(const long long *__restrict__ codes,
+                                                           const int *__restrict__ n_dev, int n_upper,
+                                                           long long *hkeys, int *hfirst, int shift,
+                                                           int mask, int *__restrict__ pslot,
+                                                           int *overflow)
+{
+    const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= n_upper) return;
+    if (i >= *n_dev) { pslot[i] = -1; return; }
+    const long long bcode = codes[i] >> 6;
+    const int slot = hash_insert(hkeys, shift, mask, bcode);
+    pslot[i] = slot;
+    if (slot < 0) { *overflow = 1; return; }
+    atomicMin(&hfirst[slot], i);
+}
+
+__global__ void __launch_bounds__(256) first_flag_kernel(const int *__restrict__ pslot,
+                                                         const int *__restrict__ hfirst,
+                                                         const int *__restrict__ hvals, int n_upper,
+                                                         int only_unassigned, int *__restrict__ flag)
+{
+    const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= n_upper) return;
+    const int slot = pslot[i];
+    int f = 0;
+    if (slot >= 0 && hfirst[slot] == i && (!only_unassigned || hvals[slot] < 0)) f = 1;
+    flag[i] = f;
+}
+
+__global__ void __launch_bounds__(256) block_assign_kernel(const long long *__restrict__ codes,
+                                                           const int *__restrict__ pslot,
+                                                           const int *__restrict__ hfirst,
+                                                           const int *__restrict__ rank, int n_upper,
+                                                           int *hvals, long long *__restrict__ gcodes)
+{
+    const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= n_upper) return;
+    const int slot = pslot[i];
+    if (slot >= 0 && hfirst[slot] == i) {
+        const int r = rank[i];
+        hvals[slot] = r;
+        gcodes[r] = codes[i] >> 6;
+    }
+}
+
+__global__ void __launch_bounds__(256) gidx_kernel(const int *__restrict__ pslot,
+                                                   const int *__restrict__ hvals, int n_upper,
+                                                   int *__restrict__ gidx)
+{
+    const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= n_upper) return;
+    const int slot = pslot[i];
+    gidx[i] = slot >= 0 ? hvals[slot] : -1;
+}
+
+// ===================================================================================
+// 27-dilation (grid.py:282-322)
+// ===================================================================================
+__global__ void __launch_bounds__(256) dilate_insert_kernel(const long long *__restrict__ gcodes,
+                                                            int n_g, long long *hkeys,
+                                                            const int *__restrict__ hvals, int *hfirst,
+                                                            int shift, int mask, int *__restrict__ qslot,
+                                                            int *bad_block, int *overflow)
+{
+    const int q = blockIdx.x * blockDim.x + threadIdx.x;
+    if (q >= n_g * 27) return;
+    const int g = q / 27, s = q - g * 27;
+    const int dz = s / 9 - 1, dy = (s / 3) % 3 - 1, dxx = s % 3 - 1;
+    const unsigned long long code = (unsigned long long)gcodes[g];
+    const long long nx = (long long)compact1by2(code) + dxx;
+    const long long ny = (long long)compact1by2(code >> 1) + dy;
+    const long long nz = (long long)compact1by2(code >> 2) + dz;
+    if (nx < 0 || ny < 0 || nz < 0 || nx >= (1 << 19) || ny >= (1 << 19) || nz >= (1 << 19)) {
+        atomicMin(bad_block, g);
+        qslot[q] = -1;
+        return;
+    }
+    const long long ncode = encode_cell(nx, ny, nz);
+    const int slot = hash_insert(hkeys, shift, mask, ncode);
+    qslot[q] = slot;
+    if (slot < 0) { *overflow = 1; return; }
+    if (hvals[slot] < 0) atomicMin(&hfirst[slot], q);   // gblock slots keep their index
+}
+
+__global__ void __launch_bounds__(256) dilate_assign_kernel(const int *__restrict__ qslot,
+                                                            const int *__restrict__ flag,
+                                                            const int *__restrict__ rank, int n_q,
+                                                            int n_g, int pblock_cap,
+                                                            const long long *__restrict__ hkeys,
+                                                            int *hvals, long long *__restrict__ codes,
+                                                            int *overflow)
+{
+    const int q = blockIdx.x * blockDim.x + threadIdx.x;
+    if (q >= n_q) return;
+    if (!flag[q]) return;
+    const int slot = qslot[q];
+    const int idx = n_g + rank[q];
+    if (idx >= pblock_cap) { *overflow = 2; return; }
+    hvals[slot] = idx;
+    codes[idx] = hkeys[slot];
+}
+
+__global__ void __launch_bounds__(256) dilate_link_kernel(const int *__restrict__ qslot,
+                                                          const int *__restrict__ hvals, int n_q,
+                                                          int *__restrict__ neighbor)
+{
+    const int q = blockIdx.x * blockDim.x + threadIdx.x;
+    if (q >= n_q) return;
+    const int slot = qslot[q];
+    neighbor[q] = slot >= 0 ? hvals[slot] : -1;
+}
+
+__global__ void __launch_bounds__(256) gblock_codes_kernel(const long long *__restrict__ gcodes,
+                                                           int n_g, long long *__restrict__ codes)
+{
+    const int g = blockIdx.x * blockDim.x + threadIdx.x;
+    if (g < n_g) codes[g] = gcodes[g];
+}
+
+__global__ void __launch_bounds__(256) block_origin_kernel(const long long *__restrict__ codes,
+                                                           const int *__restrict__ count_dev,
+                                                           int pblock_cap, int4 *__restrict__ origin)
+{
+    const int b = blockIdx.x * blockDim.x + threadIdx.x;
+    if (b >= pblock_cap || b >= *count_dev) return;
+    const unsigned long long code = (unsigned long long)codes[b];
+    origin[b] = make_int4(4 * (int)compact1by2(code), 4 * (int)compact1by2(code >> 1),
+                          4 * (int)compact1by2(code >> 2), 0);
+}
+
+__global__ void add_scalar_kernel(int *dst, const int *a, int b)
+{
+    *dst = *a + b;
+}
+
+// ===================================================================================
+// stable counting sort + lane groups (particles.py:66-80, 152-173)
+// ===================================================================================
+__global__ void __launch_bounds__(256) hist_kernel(const long long *__restrict__ codes,
+                                                   const int *__restrict__ gidx,
+                                                   const int *__restrict__ n_dev, int n_upper,
+                                                   int *bins, int *__restrict__ ticket)
+{
+    const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= n_upper || i >= *n_dev) return;
+    const int key = (gidx[i] << 6) | (int)(codes[i] & 63);
+    ticket[i] = atomicAdd(&bins[key], 1);
+}
+
+__global__ void __launch_bounds__(256) place_kernel(const long long *__restrict__ codes,
+                                                    const int *__restrict__ gidx,
+                                                    const int *__restrict__ n_dev, int n_upper,
+                                                    const int *__restrict__ bin_start,
+                                                    const int *__restrict__ ticket,
+                                                    int *__restrict__ tmp_perm)
+{
+    const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= n_upper || i >= *n_dev) return;
+    const int key = (gidx[i] << 6) | (int)(codes[i] & 63);
+    tmp_perm[bin_start[key] + ticket[i]] = i;
+}
+
+// rank the members of each bin by input index: the order a stable sort yields
+__global__ void __launch_bounds__(256) stable_rank_kernel(const long long *__restrict__ codes,
+                                                          const int *__restrict__ gidx,
+                                                          const int *__restrict__ n_dev, int n_upper,
+                                                          const int *__restrict__ bin_start,
+                                                          const int *__restrict__ tmp_perm,
+                                                          int *__restrict__ perm)
+{
+    const int j = blockIdx.x * blockDim.x + threadIdx.x;
+    if (j >= n_upper || j >= *n_dev) return;
+    const int i = tmp_perm[j];
+    const int key = (gidx[i] << 6) | (int)(codes[i] & 63);
+    const int s = bin_start[key], e = bin_start[key + 1];
+    int rank = 0;
+    for (int t = s; t < e; ++t) rank += tmp_perm[t] < i;
+    perm[s + rank] = i;
+}
+
+__global__ void __launch_bounds__(256) block_groups_kernel(const int *__restrict__ bin_start, int n_g,
+                                                           int *__restrict__ ngroups)
+{
+    const int b = blockIdx.x * blockDim.x + threadIdx.x;
+    if (b >= n_g) return;
+    const int c = bin_start[(b + 1) * 64] - bin_start[b * 64];
+    ngroups[b] = (c + 31) >> 5;
+}
+
+// ===================================================================================
+// scatter into the new AoSoA store (particles.py:192-199, 235-261, 453)
+// ===================================================================================
+__device__ __forceinline__ int clamp09(long long v) { return v < 0 ? 0 : (v > 9 ? 9 : (int)v); }
+
+__global__ void __launch_bounds__(256) scatter_sorted_kernel(
+    const float *__restrict__ old_data, const long long *__restrict__ old_ids, int nch,
+    const int *__restrict__ src_slot, const int *__restrict__ n_live_dev,
+    const float *__restrict__ staged, const long long *__restrict__ staged_ids,
+    const int *__restrict__ perm, const int *__restrict__ bin_start,
+    const int *__restrict__ block_group_first, int n_g, const int4 *__restrict__ table_origin,
+    double inv_dx, float *__restrict__ new_data, long long *__restrict__ new_ids,
+    uint16_t *__restrict__ new_meta, int *__restrict__ group_len, int *__restrict__ group_block,
+    int *__restrict__ group_start, int n_groups)
+{
+    const int g = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    const int lane = threadIdx.x & 31;
+    if (g >= n_groups) return;
+    // block of this group: last b with block_group_first[b] <= g
+    int lo = 0, hi = n_g;   // invariant: bgf[lo] <= g < bgf[hi]
+    while (hi - lo > 1) {
+        int mid = (lo + hi) >> 1;
+        if (block_group_first[mid] <= g) lo = mid; else hi = mid;
+    }
+    const int b = lo;
+    const int bstart = bin_start[b * 64], bend = bin_start[(b + 1) * 64];
+    const int first = bstart + (g - block_group_first[b]) * 32;
+    const int len = min(32, bend - first);
+    if (lane == 0) {
+        group_len[g] = len;
+        group_block[g] = b;
+        group_start[g] = first;
+    }
+    float *dst = new_data + (size_t)g * nch * 32 + lane;
+    if (lane >= len) {
+        for (int c = 0; c < nch; ++c) dst[c * 32] = 0.0f;
+        new_ids[g * 32 + lane] = 0;
+        new_meta[g * 32 + lane] = 0;
+        return;
+    }
+    const int i = perm[first + lane];
+    const int n_live = n_live_dev ? *n_live_dev : 0;
+    float px, py, pz;
+    if (i < n_live) {
+        const int slot = src_slot[i];
+        const float *src = old_data + (size_t)(slot >> 5) * nch * 32 + (slot & 31);
+        for (int c = 0; c < nch; ++c) dst[c * 32] = src[c * 32];
+        px = src[0]; py = src[32]; pz = src[64];
+        new_ids[g * 32 + lane] = old_ids[slot];
+    } else {
+        const float *src = staged + (size_t)(i - n_live) * nch;
+        for (int c = 0; c < nch; ++c) dst[c * 32] = src[c];
+        px = src[0]; py = src[1]; pz = src[2];
+        new_ids[g * 32 + lane] = staged_ids[i - n_live];
+    }
+    // lane key: float64 floor(p * inv_dx - 0.5) + bias - (origin - 4), clamped (particles.py:235-261)
+    const int4 org = table_origin[b];
+    const int kx = clamp09((long long)floor(__dsub_rn(__dmul_rn((double)px, inv_dx), 0.5)) + MPM_CELL_BIAS - (org.x - 4));
+    const int ky = clamp09((long long)floor(__dsub_rn(__dmul_rn((double)py, inv_dx), 0.5)) + MPM_CELL_BIAS - (org.y - 4));
+    const int kz = clamp09((long long)floor(__dsub_rn(__dmul_rn((double)pz, inv_dx), 0.5)) + MPM_CELL_BIAS - (org.z - 4));
+    new_meta[g * 32 + lane] = (uint16_t)(kx + 10 * (ky + 10 * kz));
+}
+
+// ===================================================================================
+// readback helpers
+// ===================================================================================
+__global__ void __launch_bounds__(256) gather_state_kernel(const float *__restrict__ data,
+                                                           const long long *__restrict__ ids, int nch,
+                                                           const int *__restrict__ group_len,
+                                                           const int *__restrict__ group_start,
+                                                           int n_groups, float *__restrict__ flat,
+                                                           long long *__restrict__ out_ids)
+{
+    const int g = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    const int lane = threadIdx.x & 31;
+    if (g >= n_groups || lane >= group_len[g]) return;
+    const size_t j = (size_t)group_start[g] + lane;
+    const float *src = data + (size_t)g * nch * 32 + lane;
+    for (int c = 0; c < nch; ++c) flat[j * nch + c] = src[c * 32];
+    out_ids[j] = ids[g * 32 + lane];
+}
+
+__global__ void __launch_bounds__(256) tag_shared_kernel(const long long *__restrict__ peer_codes,
+                                                         int n_peer, const long long *__restrict__ hkeys,
+                                                         const int *__restrict__ hvals, int shift,
+                                                         int mask, int *__restrict__ peer_map)
+{
+    const int q = blockIdx.x * blockDim.x + threadIdx.x;
+    if (q >= n_peer) return;
+    const int slot = hash_find(hkeys, shift, mask, peer_codes[q]);
+    if (slot >= 0 && hvals[slot] >= 0) peer_map[hvals[slot]] = q;
+}
+
+__global__ void fill_i32_kernel(int *p, int n, int v)
+{
+    const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i < n) p[i] = v;
+}
+
+}  // namespace mpm
+
+using namespace mpm;
+
+static inline int nblk(int64_t n, int t) { return (int)((n + t - 1) / t); }
+
+extern "C" {
+
+int mpm_compact_live(const mpm_store_view *store, int drop_quarantined, int32_t *group_live_scratch,
+                     int32_t *src_slot, int32_t *n_live, int32_t *scan_scratch, void *stream_)
+{
+    cudaStream_t stream = (cudaStream_t)stream_;
+    const int G = store->n_groups;
+    if (G <= 0) {
+        cudaMemsetAsync(n_live, 0, sizeof(int32_t), stream);
+        return check_launch("mpm_compact_live");
+    }
+    live_count_kernel<<<nblk((int64_t)G * 32, 256), 256, 0, stream>>>(
+        store->lane_meta, store->group_len, G, drop_quarantined, group_live_scratch);
+    exclusive_scan_i32(group_live_scratch, group_live_scratch, G, scan_scratch, n_live, stream);
+    live_write_kernel<<<nblk((int64_t)G * 32, 256), 256, 0, stream>>>(
+        store->lane_meta, store->group_len, G, drop_quarantined, group_live_scratch, src_slot);
+    return check_launch("mpm_compact_live");
+}
+
+int mpm_particle_codes(const mpm_store_view *store, const int32_t *src_slot, const int32_t *n_live_dev,
+                       const float *staged, int32_t n_staged, int32_t n_upper, double dx,
+                       int64_t *codes, int32_t *n_total, int32_t *bad_index, void *stream_)
+{
+    cudaStream_t stream = (cudaStream_t)stream_;
+    if (!(dx > 0.0)) return MPM_ERR_REJECTED_INPUT;
+    fill_i32_kernel<<<1, 32, 0, stream>>>(bad_index, 1, MPM_INT_MAX);
+    if (n_live_dev) add_scalar_kernel<<<1, 1, 0, stream>>>(n_total, n_live_dev, n_staged);
+    else fill_i32_kernel<<<1, 32, 0, stream>>>(n_total, 1, n_staged);
+    if (n_upper > 0)
+        particle_codes_kernel<<<nblk(n_upper, 256), 256, 0, stream>>>(
+            store->data, store->nch, src_slot, n_live_dev, staged, n_staged, n_upper, dx,
+            (long long *)codes, bad_index);
+    return check_launch("mpm_particle_codes");
+}
+
+int mpm_hash_insert_blocks(const int64_t *codes, const int32_t *n_dev, int32_t n_upper,
+                           int64_t *hkeys, int32_t *hvals, int32_t *hfirst, int32_t hash_cap,
+                           int32_t *pslot, int32_t *flag_scratch, int32_t *scan_scratch,
+                           int32_t *gidx, int64_t *gcodes, int32_t *n_gblocks, int32_t *overflow,
+                           void *stream_)
+{
+    cudaStream_t stream = (cudaStream_t)stream_;
+    if (hash_cap <= 0 || (hash_cap & (hash_cap - 1))) return MPM_ERR_REJECTED_INPUT;
+    const int shift = hash_shift_for(hash_cap), mask = hash_cap - 1;
+    hash_clear_kernel<<<nblk(hash_cap, 256), 256, 0, stream>>>((long long *)hkeys, hvals, hfirst, hash_cap);
+    cudaMemsetAsync(overflow, 0, sizeof(int32_t), stream);
+    if (n_upper <= 0) {
+        cudaMemsetAsync(n_gblocks, 0, sizeof(int32_t), stream);
+        return check_launch("mpm_hash_insert_blocks");
+    }
+    const int nb = nblk(n_upper, 256);
+    block_insert_kernel<<<nb, 256, 0, stream>>>((const long long *)codes, n_dev, n_upper,
+                                                (long long *)hkeys, hfirst, shift, mask, pslot, overflow);
+    first_flag_kernel<<<nb, 256, 0, stream>>>(pslot, hfirst, hvals, n_upper, 0, flag_scratch);
+    exclusive_scan_i32(flag_scratch, flag_scratch, n_upper, scan_scratch, n_gblocks, stream);
+    block_assign_kernel<<<nb, 256, 0, stream>>>((const long long *)codes, pslot, hfirst, flag_scratch,
+                                                n_upper, hvals, (long long *)gcodes);
+    gidx_kernel<<<nb, 256, 0, stream>>>(pslot, hvals, n_upper, gidx);
+    return check_launch("mpm_hash_insert_blocks");
+}
+
+int mpm_dilate_and_link(const int64_t *gcodes, int32_t n_g, int64_t *hkeys, int32_t *hvals,
+                        int32_t *hfirst, int32_t hash_cap, int32_t *qslot, int32_t *flag_scratch,
+                        int32_t *scan_scratch, int64_t *codes, int32_t *origin, int32_t *neighbor,
+                        int32_t pblock_cap, int32_t *count, int32_t *bad_block, int32_t *overflow,
+                        void *stream_)
+{
+    cudaStream_t stream = (cudaStream_t)stream_;
+    if (hash_cap <= 0 || (hash_cap & (hash_cap - 1))) return MPM_ERR_REJECTED_INPUT;
+    const int shift = hash_shift_for(hash_cap), mask = hash_cap - 1;
+    fill_i32_kernel<<<1, 32, 0, stream>>>(bad_block, 1, MPM_INT_MAX);
+    if (n_g <= 0) {
+        cudaMemsetAsync(count, 0, sizeof(int32_t), stream);
+        return check_launch("mpm_dilate_and_link");
+    }
+    if (n_g > pblock_cap) return MPM_ERR_RESOURCE;
+    const int n_q = n_g * 27;
+    const int nb = nblk(n_q, 256);
+    // hfirst of the halo slots must start at INT_MAX: gblock slots already hold particle indices,
+    // but those are never compared again (their hvals >= 0).
+    dilate_insert_kernel<<<nb, 256, 0, stream>>>((const long long *)gcodes, n_g, (long long *)hkeys,
+                                                 hvals, hfirst, shift, mask, qslot, bad_block, overflow);
+    first_flag_kernel<<<nb, 256, 0, stream>>>(qslot, hfirst, hvals, n_q, 1, flag_scratch);
+    // keep the flags: the scan result goes to a second array (flag_scratch + n_q)
+    int32_t *rank = flag_scratch + n_q;
+    exclusive_scan_i32(flag_scratch, rank, n_q, scan_scratch, count, stream);
+    gblock_codes_kernel<<<nblk(n_g, 256), 256, 0, stream>>>((const long long *)gcodes, n_g,
+                                                            (long long *)codes);
+    dilate_assign_kernel<<<nb, 256, 0, stream>>>(qslot, flag_scratch, rank, n_q, n_g, pblock_cap,
+                                                 (const long long *)hkeys, hvals, (long long *)codes,
+                                                 overflow);
+    dilate_link_kernel<<<nb, 256, 0, stream>>>(qslot, hvals, n_q, neighbor);
+    add_scalar_kernel<<<1, 1, 0, stream>>>(count, count, n_g);
+    block_origin_kernel<<<nblk(pblock_cap, 256), 256, 0, stream>>>((const long long *)codes, count,
+                                                                   pblock_cap, (int4 *)origin);
+    return check_launch("mpm_dilate_and_link");
+}
+
+int mpm_sort_and_group(const int64_t *codes, const int32_t *gidx, const int32_t *n_dev, int32_t n_upper,
+                       int32_t n_g, int32_t *bin_start, int32_t *tmp_perm, int32_t *perm,
+                       int32_t *block_group_first, int32_t *scan_scratch, int32_t *n_groups,
+                       void *stream_)
+{
+    cudaStream_t stream = (cudaStream_t)stream_;
+    if (n_g <= 0 || n_upper <= 0) {
+        cudaMemsetAsync(n_groups, 0, sizeof(int32_t), stream);
+        return check_launch("mpm_sort_and_group");
+    }
+    const int n_bins = n_g * 64;
+    const int nb = nblk(n_upper, 256);
+    // tickets live in `perm` until the final ranking overwrites it
+    cudaMemsetAsync(bin_start, 0, sizeof(int32_t) * (size_t)(n_bins + 1), stream);
+    hist_kernel<<<nb, 256, 0, stream>>>((const long long *)codes, gidx, n_dev, n_upper, bin_start, perm);
+    exclusive_scan_i32(bin_start, bin_start, n_bins + 1, scan_scratch, nullptr, stream);
+    place_kernel<<<nb, 256, 0, stream>>>((const long long *)codes, gidx, n_dev, n_upper, bin_start,
+                                         perm, tmp_perm);
+    stable_rank_kernel<<<nb, 256, 0, stream>>>((const long long *)codes, gidx, n_dev, n_upper,
+                                               bin_start, tmp_perm, perm);
+    block_groups_kernel<<<nblk(n_g, 256), 256, 0, stream>>>(bin_start, n_g, block_group_first);
+    // n_g+1 entries so that block_group_first[n_g] = n_groups
+    cudaMemsetAsync(block_group_first + n_g, 0, sizeof(int32_t), stream);
+    exclusive_scan_i32(block_group_first, block_group_first, n_g + 1, scan_scratch, n_groups, stream);
+    return check_launch("mpm_sort_and_group");
+}
+
+int mpm_scatter_sorted(const mpm_store_view *old_store, const int32_t *src_slot, const int32_t *n_live_dev,
+                       const float *staged, const int64_t *staged_ids, const int32_t *perm,
+                       const int32_t *bin_start, const int32_t *block_group_first, int32_t n_g,
+                       const int32_t *table_origin, double dx, const mpm_store_view *new_store,
+                       void *stream_)
+{
+    cudaStream_t stream = (cudaStream_t)stream_;
+    const int G = new_store->n_groups;
+    if (G <= 0) return MPM_OK;
+    const double inv_dx = 1.0 / dx;
+    scatter_sorted_kernel<<<nblk((int64_t)G * 32, 256), 256, 0, stream>>>(
+        old_store->data, (const long long *)old_store->orig_id, new_store->nch, src_slot, n_live_dev,
+        staged, (const long long *)staged_ids, perm, bin_start, block_group_first, n_g,
+        (const int4 *)table_origin, inv_dx, new_store->data, (long long *)new_store->orig_id,
+        new_store->lane_meta, new_store->group_len, new_store->group_block, new_store->group_start, G);
+    return check_launch("mpm_scatter_sorted");
+}
+
+int mpm_gather_state(const mpm_store_view *store, float *flat, int64_t *ids, void *stream_)
+{
+    cudaStream_t stream = (cudaStream_t)stream_;
+    const int G = store->n_groups;
+    if (G <= 0) return MPM_OK;
+    gather_state_kernel<<<nblk((int64_t)G * 32, 256), 256, 0, stream>>>(
+        store->data, (const long long *)store->orig_id, store->nch, store->group_len,
+        store->group_start, G, flat, (long long *)ids);
+    return check_launch("mpm_gather_state");
+}
+
+int mpm_tag_shared(const int64_t *peer_codes, int32_t n_peer_codes, const int64_t *hkeys,
+                   const int32_t *hvals, int32_t hash_cap, int32_t *peer_map, int32_t local_count,
+                   void *stream_)
+{
+    cudaStream_t stream = (cudaStream_t)stream_;
+    if (hash_cap <= 0 || (hash_cap & (hash_cap - 1))) return MPM_ERR_REJECTED_INPUT;
+    if (local_count > 0)
+        fill_i32_kernel<<<nblk(local_count, 256), 256, 0, stream>>>(peer_map, local_count, -1);
+    if (n_peer_codes > 0)
+        tag_shared_kernel<<<nblk(n_peer_codes, 256), 256, 0, stream>>>(
+            (const long long *)peer_codes, n_peer_codes, (const long long *)hkeys, hvals,
+            hash_shift_for(hash_cap), hash_cap - 1, peer_map);
+    return check_launch("mpm_tag_shared");
+}
+
+}  // extern "C"

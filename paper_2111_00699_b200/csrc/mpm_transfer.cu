@@ -1,0 +1,468 @@
+// Particle <-> grid transfers: P2G, G2P and the fused G2P2G kernel (sm_100a, fp32).
+//
+// Reference (paths relative to /root/reference/pkg/src/mpmbench/):
+//   _scatter_prep      pipeline.py:160-238     _subgroup_scatter  pipeline.py:242-312
+//   _p2g_kernel        pipeline.py:316-356     _gather_advect     pipeline.py:400-600
+//   _g2p2g_kernel      pipeline.py:604-653
+//
+// Mapping: one warp per particle group (<= 32 particles of one gblock, cell-sorted at the
+// last rebuild), lane = particle, one 128-byte row per channel.
+// Scatter: runs of consecutive lanes with the same 10-bit cell key are summed with a
+// segmented shuffle reduction and the run leader issues ONE vector reduction
+// (RED.E.ADD.F32x4) per grid node -- the reference's "one += per (subgroup, node)" contract
+// (pipeline.py:293-311) without sorting lanes first (its sort=none_between arm).
+#include "mpm_math.cuh"
+
+namespace mpm {
+
+struct TransferArgs {
+    float *data;
+    uint16_t *meta;
+    const int *group_len;
+    const int *group_block;
+    int n_groups;
+    int nch;
+    const int4 *origin;
+    const int *neighbor;
+    const float4 *vel;
+    const float4 *vel_old;
+    float4 *raw;
+    uint8_t *touched;
+    mpm_step_status *status;
+    float dx, inv_dx, dt, dt_gather, d_inv, coeff_base;
+    float mu, lam, kappa, gamma, flip;
+    float margin_lo, margin_hi;
+    float theta_c, theta_s, hardening, sand_alpha;
+    int clamp_tension, count_stats;
+    int *guard;
+};
+
+constexpr int TW = 8;   // warps (groups) per CTA
+
+__device__ __forceinline__ void red_add_v4(float4 *addr, float a, float b, float c, float d)
+{
+    atomicAdd(addr, make_float4(a, b, c, d));   // RED.E.ADD.F32x4 on sm_90+
+}
+
+__device__ __forceinline__ void quad_weights(float f, float *w)
+{
+    // pipeline.py:136-141
+    w[0] = 0.5f * ((1.5f - f) * (1.5f - f));
+    w[1] = 0.75f - (f - 1.0f) * (f - 1.0f);
+    w[2] = 0.5f * ((f - 0.5f) * (f - 0.5f));
+}
+
+// base cell (unbiased) of the quadratic stencil: floor(p * inv_dx - 0.5); one shared form so
+// the gather, the lane-key refresh and the scatter all see the same rounding.
+__device__ __forceinline__ float stencil_base(float p, float inv_dx, float *g)
+{
+    *g = p * inv_dx;
+    return floorf(*g - 0.5f);
+}
+
+// per-axis addressing of the three stencil cells: neighbour-row term and slot term
+struct AxisAddr {
+    int nterm[3];   // r * stride, r in 0..2, or -1000 when outside the 3x3x3 set
+    int sterm[3];
+};
+template <int AXIS>
+__device__ __forceinline__ void axis_addr(int cell, int block_coord, AxisAddr &a)
+{
+    constexpr int nstride = AXIS == 0 ? 1 : (AXIS == 1 ? 3 : 9);
+#pragma unroll
+    for (int i = 0; i < 3; ++i) {
+        const int c = cell + i;
+        const int r = (c >> 2) - block_coord + 1;
+        a.nterm[i] = (r < 0 || r > 2) ? -1000 : r * nstride;
+        a.sterm[i] = ((c & 1) << AXIS) | ((c & 2) << (AXIS + 2));
+    }
+}
+
+template <int MAT, bool GATHER, bool SCATTER>
+__global__ void __launch_bounds__(TW * 32) transfer_kernel(const TransferArgs a)
+{
+    if (guarded_out(a.guard)) return;
+    __shared__ int s_nrow[TW][28];
+    __shared__ unsigned s_vmax[TW];
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int g = blockIdx.x * TW + warp;
+    const unsigned FULL = 0xffffffffu;
+    unsigned vmax_bits = 0;
+
+    if (g < a.n_groups) {
+        const int len = a.group_len[g];
+        const int block = a.group_block[g];
+        const int4 org = a.origin[block];
+        if (lane < 27) s_nrow[warp][lane] = a.neighbor[block * 27 + lane];
+        __syncwarp();
+        const int *nrow = s_nrow[warp];
+        const int bcx = org.x >> 2, bcy = org.y >> 2, bcz = org.z >> 2;
+
+        float *gd = a.data + (size_t)g * a.nch * 32 + lane;
+        uint16_t meta = a.meta[g * 32 + lane];
+        bool active = lane < len && !(meta & MPM_LANE_QUARANTINED);
+        float m = active ? gd[CH_MASS * 32] : 0.0f;
+        active = active && (m > 0.0f);
+        int key = meta & 0x3ff;
+
+        float px = 0.f, py = 0.f, pz = 0.f, vx = 0.f, vy = 0.f, vz = 0.f;
+        float C[9];
+        float F[9];   // F (elastic kinds) or F[0] = J (fluid)
+        int addr_err = 0;
+        if (active) {
+            px = gd[(CH_POS + 0) * 32]; py = gd[(CH_POS + 1) * 32]; pz = gd[(CH_POS + 2) * 32];
+            if (MAT == MPM_MAT_FLUID) F[0] = gd[CH_DEF * 32];
+            else {
+#pragma unroll
+                for (int r = 0; r < 9; ++r) F[r] = gd[(CH_DEF + r) * 32];
+            }
+        }
+
+        // =========================== gather (pipeline.py:400-600) ===========================
+        if (GATHER) {
+            if (active) {
+                float gx, gy, gz;
+                const float bxf = stencil_base(px, a.inv_dx, &gx);
+                const float byf = stencil_base(py, a.inv_dx, &gy);
+                const float bzf = stencil_base(pz, a.inv_dx, &gz);
+                const float fx = gx - bxf, fy = gy - byf, fz = gz - bzf;
+                float wx[3], wy[3], wz[3];
+                quad_weights(fx, wx); quad_weights(fy, wy); quad_weights(fz, wz);
+                AxisAddr ax, ay, az;
+                axis_addr<0>((int)bxf + MPM_CELL_BIAS, bcx, ax);
+                axis_addr<1>((int)byf + MPM_CELL_BIAS, bcy, ay);
+                axis_addr<2>((int)bzf + MPM_CELL_BIAS, bcz, az);
+                float nvx = 0.f, nvy = 0.f, nvz = 0.f, dvx = 0.f, dvy = 0.f, dvz = 0.f;
+                float b[9];
+#pragma unroll
+                for (int r = 0; r < 9; ++r) b[r] = 0.f;
+                const bool use_flip = a.flip > 0.0f;
+#pragma unroll
+                for (int i = 0; i < 3; ++i) {
+                    const float dpx = ((float)i - fx) * a.dx;
+#pragma unroll
+                    for (int j = 0; j < 3; ++j) {
+                        const float dpy = ((float)j - fy) * a.dx;
+                        const float wxy = wx[i] * wy[j];
+#pragma unroll
+                        for (int k = 0; k < 3; ++k) {
+                            const int nidx = ax.nterm[i] + ay.nterm[j] + az.nterm[k];
+                            int nb = nidx >= 0 ? nrow[nidx] : -1;
+                            if (nb < 0) { ++addr_err; continue; }
+                            const int slot = ax.sterm[i] | ay.sterm[j] | az.sterm[k];
+                            const float4 vn = __ldg(&a.vel[(size_t)nb * 64 + slot]);
+                            const float w = wxy * wz[k];
+                            const float dpz = ((float)k - fz) * a.dx;
+                            nvx += w * vn.y; nvy += w * vn.z; nvz += w * vn.w;
+                            if (use_flip) {
+                                const float4 vo = __ldg(&a.vel_old[(size_t)nb * 64 + slot]);
+                                dvx += w * (vn.y - vo.y); dvy += w * (vn.z - vo.z); dvz += w * (vn.w - vo.w);
+                            }
+                            const float wvx = w * vn.y, wvy = w * vn.z, wvz = w * vn.w;
+                            b[0] += wvx * dpx; b[1] += wvx * dpy; b[2] += wvx * dpz;
+                            b[3] += wvy * dpx; b[4] += wvy * dpy; b[5] += wvy * dpz;
+                            b[6] += wvz * dpx; b[7] += wvz * dpy; b[8] += wvz * dpz;
+                        }
+                    }
+                }
+#pragma unroll
+                for (int r = 0; r < 9; ++r) C[r] = a.d_inv * b[r];
+                if (use_flip) {
+                    const float ovx = gd[(CH_VEL + 0) * 32], ovy = gd[(CH_VEL + 1) * 32],
+                                ovz = gd[(CH_VEL + 2) * 32];
+                    nvx = (1.0f - a.flip) * nvx + a.flip * (ovx + dvx);
+                    nvy = (1.0f - a.flip) * nvy + a.flip * (ovy + dvy);
+                    nvz = (1.0f - a.flip) * nvz + a.flip * (ovz + dvz);
+                }
+                const float dtg = a.dt_gather;
+                const float npx = px + dtg * nvx, npy = py + dtg * nvy, npz = pz + dtg * nvz;
+                if (!(isfinite(npx) && isfinite(npy) && isfinite(npz) && isfinite(nvx) &&
+                      isfinite(nvy) && isfinite(nvz))) {
+                    // quarantine (pipeline.py:525-531): state left as it was, mass zeroed
+                    meta |= MPM_LANE_QUARANTINED;
+                    a.meta[g * 32 + lane] = meta;
+                    gd[CH_MASS * 32] = 0.0f;
+                    atomicAdd(&a.status->counters[MPM_C_QUARANTINE], 1ull);
+                    active = false;
+                } else {
+                    px = npx; py = npy; pz = npz; vx = nvx; vy = nvy; vz = nvz;
+                    gd[(CH_POS + 0) * 32] = px; gd[(CH_POS + 1) * 32] = py; gd[(CH_POS + 2) * 32] = pz;
+                    gd[(CH_VEL + 0) * 32] = vx; gd[(CH_VEL + 1) * 32] = vy; gd[(CH_VEL + 2) * 32] = vz;
+                    if (!SCATTER) {
+                        // the fused kernel keeps C in registers; the split path stores it for P2G
+#pragma unroll
+                        for (int r = 0; r < 9; ++r) gd[(CH_C + r) * 32] = C[r];
+                    }
+                    if (MAT == MPM_MAT_FLUID) {
+                        F[0] *= 1.0f + dtg * (C[0] + C[4] + C[8]);
+                        gd[CH_DEF * 32] = F[0];
+                    } else {
+                        float A[9], Fn[9];
+#pragma unroll
+                        for (int r = 0; r < 9; ++r) A[r] = dtg * C[r];
+                        A[0] += 1.0f; A[4] += 1.0f; A[8] += 1.0f;
+#pragma unroll
+                        for (int r = 0; r < 3; ++r)
+#pragma unroll
+                            for (int c = 0; c < 3; ++c)
+                                Fn[3 * r + c] = A[3 * r] * F[c] + A[3 * r + 1] * F[3 + c] + A[3 * r + 2] * F[6 + c];
+#pragma unroll
+                        for (int r = 0; r < 9; ++r) { F[r] = Fn[r]; gd[(CH_DEF + r) * 32] = Fn[r]; }
+                    }
+                    // free zone [origin - margin_lo, origin + 4 + margin_hi) cells (pipeline.py:560-575)
+                    const float zx0 = ((float)(org.x - MPM_CELL_BIAS) - a.margin_lo) * a.dx;
+                    const float zy0 = ((float)(org.y - MPM_CELL_BIAS) - a.margin_lo) * a.dx;
+                    const float zz0 = ((float)(org.z - MPM_CELL_BIAS) - a.margin_lo) * a.dx;
+                    const float zx1 = ((float)(org.x - MPM_CELL_BIAS) + 4.0f + a.margin_hi) * a.dx;
+                    const float zy1 = ((float)(org.y - MPM_CELL_BIAS) + 4.0f + a.margin_hi) * a.dx;
+                    const float zz1 = ((float)(org.z - MPM_CELL_BIAS) + 4.0f + a.margin_hi) * a.dx;
+                    if (px < zx0 || px >= zx1 || py < zy0 || py >= zy1 || pz < zz0 || pz >= zz1) {
+                        a.status->zone_violation = 1;
+                        if (a.guard) *a.guard = 1;
+                    }
+                    vmax_bits = __float_as_uint(vx * vx + vy * vy + vz * vz);
+                    // lane key refresh (pipeline.py:585-599)
+                    float tmp;
+                    int kx = (int)stencil_base(px, a.inv_dx, &tmp) + MPM_CELL_BIAS - (org.x - 4);
+                    int ky = (int)stencil_base(py, a.inv_dx, &tmp) + MPM_CELL_BIAS - (org.y - 4);
+                    int kz = (int)stencil_base(pz, a.inv_dx, &tmp) + MPM_CELL_BIAS - (org.z - 4);
+                    kx = min(max(kx, 0), 9); ky = min(max(ky, 0), 9); kz = min(max(kz, 0), 9);
+                    key = kx + 10 * (ky + 10 * kz);
+                    a.meta[g * 32 + lane] = (uint16_t)key;
+                }
+            }
+        } else if (SCATTER) {
+            if (active) {
+                vx = gd[(CH_VEL + 0) * 32]; vy = gd[(CH_VEL + 1) * 32]; vz = gd[(CH_VEL + 2) * 32];
+#pragma unroll
+                for (int r = 0; r < 9; ++r) C[r] = gd[(CH_C + r) * 32];
+            }
+        }
+
+        // =========================== scatter (pipeline.py:160-312) ==========================
+        if (SCATTER) {
+            float Q[9];
+            if (active && !GATHER) {
+                if (!(isfinite(px) && isfinite(py) && isfinite(pz) && isfinite(vx) && isfinite(vy) &&
+                      isfinite(vz))) {
+                    meta |= MPM_LANE_QUARANTINED;
+                    a.meta[g * 32 + lane] = meta;
+                    gd[CH_MASS * 32] = 0.0f;
+                    atomicAdd(&a.status->counters[MPM_C_QUARANTINE], 1ull);
+                    active = false;
+                }
+            }
+            if (active) {
+                const float coeff = a.coeff_base * m;
+                if (MAT == MPM_MAT_FLUID) {
+                    float tau;
+                    if (F[0] <= 0.0f) {
+                        atomicAdd(&a.status->counters[MPM_C_DEGENERATE], 1ull);
+                        tau = 0.0f;
+                    } else tau = fluid_tau(F[0], a.kappa, a.gamma, a.clamp_tension);
+#pragma unroll
+                    for (int r = 0; r < 9; ++r) Q[r] = m * C[r];
+                    Q[0] += coeff * tau; Q[4] += coeff * tau; Q[8] += coeff * tau;
+                } else {
+                    float t[9];
+                    if (corotated_tau(F, a.mu, a.lam, t))
+                        atomicAdd(&a.status->counters[MPM_C_SVD_CLAMP], 1ull);
+#pragma unroll
+                    for (int r = 0; r < 9; ++r) Q[r] = m * C[r] + coeff * t[r];
+                }
+            }
+            // runs of consecutive active lanes with equal keys
+            const unsigned act = __ballot_sync(FULL, active);
+            const int prev_key = __shfl_up_sync(FULL, key, 1);
+            const bool head = !active || lane == 0 || prev_key != key || !((act >> (lane - 1)) & 1u);
+            const unsigned heads = __ballot_sync(FULL, head);
+            const unsigned above = lane == 31 ? 0u : (heads & ~((2u << lane) - 1u));
+            const int seg_last = above ? (__ffs(above) - 2) : 31;
+            const int maxd = __reduce_max_sync(FULL, seg_last - lane);
+            if (act) {
+                // addressing from the lane key (pipeline.py:261-272); weights relative to that base
+                const int kx = key % 10, ky = (key / 10) % 10, kz = key / 100;
+                const int basex = org.x - 4 + kx, basey = org.y - 4 + ky, basez = org.z - 4 + kz;
+                const float fx = px * a.inv_dx - (float)(basex - MPM_CELL_BIAS);
+                const float fy = py * a.inv_dx - (float)(basey - MPM_CELL_BIAS);
+                const float fz = pz * a.inv_dx - (float)(basez - MPM_CELL_BIAS);
+                float wx[3], wy[3], wz[3];
+                quad_weights(fx, wx); quad_weights(fy, wy); quad_weights(fz, wz);
+                AxisAddr ax, ay, az;
+                axis_addr<0>(basex, bcx, ax);
+                axis_addr<1>(basey, bcy, ay);
+                axis_addr<2>(basez, bcz, az);
+                const float mm = active ? m : 0.0f;
+                const float mvx = mm * vx, mvy = mm * vy, mvz = mm * vz;
+                if (!active) {
+#pragma unroll
+                    for (int r = 0; r < 9; ++r) Q[r] = 0.0f;
+                }
+                const bool leader = head && active;
+                unsigned nbmask = 0;
+#pragma unroll
+                for (int i = 0; i < 3; ++i) {
+                    const float dpx = ((float)i - fx) * a.dx;
+#pragma unroll
+                    for (int j = 0; j < 3; ++j) {
+                        const float dpy = ((float)j - fy) * a.dx;
+                        const float wxy = wx[i] * wy[j];
+#pragma unroll
+                        for (int k = 0; k < 3; ++k) {
+                            const float dpz = ((float)k - fz) * a.dx;
+                            const float w = active ? wxy * wz[k] : 0.0f;
+                            float c0 = w * mm;
+                            float c1 = w * (mvx + Q[0] * dpx + Q[1] * dpy + Q[2] * dpz);
+                            float c2 = w * (mvy + Q[3] * dpx + Q[4] * dpy + Q[5] * dpz);
+                            float c3 = w * (mvz + Q[6] * dpx + Q[7] * dpy + Q[8] * dpz);
+                            for (int d = 1; d <= maxd; d <<= 1) {
+                                const float t0 = __shfl_down_sync(FULL, c0, d);
+                                const float t1 = __shfl_down_sync(FULL, c1, d);
+                                const float t2 = __shfl_down_sync(FULL, c2, d);
+                                const float t3 = __shfl_down_sync(FULL, c3, d);
+                                if (lane + d <= seg_last) { c0 += t0; c1 += t1; c2 += t2; c3 += t3; }
+                            }
+                            if (leader) {
+                                const int nidx = ax.nterm[i] + ay.nterm[j] + az.nterm[k];
+                                const int nb = nidx >= 0 ? nrow[nidx] : -1;
+                                if (nb < 0) { ++addr_err; }
+                                else {
+                                    const int slot = ax.sterm[i] | ay.sterm[j] | az.sterm[k];
+                                    red_add_v4(&a.raw[(size_t)nb * 64 + slot], c0, c1, c2, c3);
+                                    nbmask |= 1u << nidx;
+                                }
+                            }
+                        }
+                    }
+                }
+                nbmask = __reduce_or_sync(FULL, nbmask);
+                if (lane < 27 && ((nbmask >> lane) & 1u)) a.touched[nrow[lane]] = 1;
+                if (a.count_stats && lane == 0) {
+                    const int runs = __popc(heads & act);
+                    atomicAdd(&a.status->counters[MPM_C_SUBGROUPS], (unsigned long long)runs);
+                    atomicAdd(&a.status->counters[MPM_C_ACCUM], (unsigned long long)runs * 27ull);
+                }
+            }
+        }
+        if (addr_err) atomicAdd(&a.status->counters[MPM_C_ADDRESS_ERR], (unsigned long long)addr_err);
+    }
+
+    if (GATHER) {
+        // max |v|^2 of the CTA -> one conditional atomicMax (pipeline.py:576-578)
+        vmax_bits = __reduce_max_sync(FULL, vmax_bits);
+        if (lane == 0) s_vmax[warp] = vmax_bits;
+        __syncthreads();
+        if (threadIdx.x == 0) {
+            unsigned mx = 0;
+#pragma unroll
+            for (int w = 0; w < TW; ++w) mx = max(mx, s_vmax[w]);
+            if (mx > *((volatile unsigned *)&a.status->vmax2_bits)) atomicMax(&a.status->vmax2_bits, mx);
+        }
+    }
+}
+
+static int fill_args(TransferArgs &a, const mpm_store_view *store, const mpm_table_view *table,
+                     const float *vel, const float *vel_old, float *raw, uint8_t *touched,
+                     const mpm_transfer_params *p, mpm_step_status *status, int32_t *guard)
+{
+    if (!store || !table || !p || !status) return MPM_ERR_REJECTED_INPUT;
+    if (!(p->dx > 0.0) || !(p->density > 0.0)) return MPM_ERR_REJECTED_INPUT;
+    if (p->mat_kind < 0 || p->mat_kind > MPM_MAT_SAND) return MPM_ERR_CONFIG;
+    a.data = store->data;
+    a.meta = store->lane_meta;
+    a.group_len = store->group_len;
+    a.group_block = store->group_block;
+    a.n_groups = store->n_groups;
+    a.nch = store->nch;
+    a.origin = (const int4 *)table->origin;
+    a.neighbor = table->neighbor;
+    a.vel = (const float4 *)vel;
+    a.vel_old = (const float4 *)vel_old;
+    a.raw = (float4 *)raw;
+    a.touched = touched;
+    a.status = status;
+    const double inv_dx = 1.0 / p->dx;
+    a.dx = (float)p->dx;
+    a.inv_dx = (float)inv_dx;
+    a.dt = (float)p->dt;
+    a.dt_gather = (float)p->dt_gather;
+    a.d_inv = (float)(4.0 * inv_dx * inv_dx);
+    a.coeff_base = (float)(-4.0 * p->dt * inv_dx * inv_dx / p->density);
+    a.mu = (float)p->mu; a.lam = (float)p->lam; a.kappa = (float)p->kappa; a.gamma = (float)p->gamma;
+    a.flip = (float)p->flip_blend;
+    a.margin_lo = (float)p->margin_lo; a.margin_hi = (float)p->margin_hi;
+    a.theta_c = (float)p->theta_c; a.theta_s = (float)p->theta_s;
+    a.hardening = (float)p->hardening; a.sand_alpha = (float)p->sand_alpha;
+    a.clamp_tension = p->clamp_tension;
+    a.count_stats = p->count_stats;
+    a.guard = guard;
+    if (a.flip > 0.0f && !vel_old) return MPM_ERR_REJECTED_INPUT;
+    return MPM_OK;
+}
+
+template <bool GATHER, bool SCATTER>
+static int launch_transfer(const TransferArgs &a, int mat, cudaStream_t stream)
+{
+    if (a.n_groups <= 0) return MPM_OK;
+    const int grid = (a.n_groups + TW - 1) / TW;
+    switch (mat) {
+    case MPM_MAT_FLUID:
+        transfer_kernel<MPM_MAT_FLUID, GATHER, SCATTER><<<grid, TW * 32, 0, stream>>>(a);
+        break;
+    case MPM_MAT_FIXED_COROTATED:
+        transfer_kernel<MPM_MAT_FIXED_COROTATED, GATHER, SCATTER><<<grid, TW * 32, 0, stream>>>(a);
+        break;
+    default:
+        return MPM_ERR_CONFIG;
+    }
+    return MPM_OK;
+}
+
+}  // namespace mpm
+
+using namespace mpm;
+
+extern "C" {
+
+int mpm_p2g(const mpm_store_view *store, const mpm_table_view *table, float *raw, uint8_t *touched,
+            const mpm_transfer_params *params, mpm_step_status *status, int32_t *guard, void *stream)
+{
+    TransferArgs a;
+    int rc = fill_args(a, store, table, nullptr, nullptr, raw, touched, params, status, guard);
+    if (rc == MPM_ERR_REJECTED_INPUT && params && params->flip_blend > 0.0) {
+        // P2G does not read vel_old
+        mpm_transfer_params q = *params;
+        q.flip_blend = 0.0;
+        rc = fill_args(a, store, table, nullptr, nullptr, raw, touched, &q, status, guard);
+    }
+    if (rc != MPM_OK) return rc;
+    rc = launch_transfer<false, true>(a, params->mat_kind, (cudaStream_t)stream);
+    if (rc != MPM_OK) return rc;
+    return check_launch("mpm_p2g");
+}
+
+int mpm_g2p(const mpm_store_view *store, const mpm_table_view *table, const float *vel,
+            const float *vel_old, const mpm_transfer_params *params, mpm_step_status *status,
+            int32_t *guard, void *stream)
+{
+    TransferArgs a;
+    int rc = fill_args(a, store, table, vel, vel_old, nullptr, nullptr, params, status, guard);
+    if (rc != MPM_OK) return rc;
+    rc = launch_transfer<true, false>(a, params->mat_kind, (cudaStream_t)stream);
+    if (rc != MPM_OK) return rc;
+    return check_launch("mpm_g2p");
+}
+
+int mpm_g2p2g(const mpm_store_view *store, const mpm_table_view *table, const float *vel,
+              const float *vel_old, float *raw, uint8_t *touched, const mpm_transfer_params *params,
+              mpm_step_status *status, int32_t *guard, void *stream)
+{
+    TransferArgs a;
+    int rc = fill_args(a, store, table, vel, vel_old, raw, touched, params, status, guard);
+    if (rc != MPM_OK) return rc;
+    rc = launch_transfer<true, true>(a, params->mat_kind, (cudaStream_t)stream);
+    if (rc != MPM_OK) return rc;
+    return check_launch("mpm_g2p2g");
+}
+
+}  // extern "C"

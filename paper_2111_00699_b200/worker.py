@@ -1,0 +1,828 @@
+"""CudaWorker: the reference's `Worker` surface over the B200 CUDA core.
+
+Mirrors /root/reference/pkg/src/mpmbench/pipeline.py:788-1238 (Worker), with
+ParticleStore (particles.py:268-487), BlockTable (grid.py:325-401) and GridStore
+(grid.py:415-454) re-hosted on device buffers.  Every phase is one call through the C ABI
+(include/mpm_b200.h); this module only sequences them, owns the buffers (4x growth rule) and
+maps counters / status codes onto the reference's exceptions.  There is no CPU path: without
+libmpm_b200.so or a CUDA device, construction raises ResourceError.
+
+Host/device protocol of one substep (pipeline.py:905-940):
+    [rebuild | clear(par)] -> [g2p2g | p2g] -> barrier -> grid update (+ peer rows) -> [g2p]
+    -> 56-byte status block D2H (free-zone flag, max speed^2, counters) -> host decides
+       whether the next step rebuilds (pipeline.py:1102-1104).
+"""
+from __future__ import annotations
+
+import ctypes as C
+import math
+
+import numpy as np
+import torch
+
+from . import _capi
+from ._capi import StepStatus, StoreView, TableView, TransferParams, check
+from .domain import Material, MaterialKind, SimParams, cfl_dt
+from .errors import (ConfigError, ContractViolationError, ModeConflictError, RejectedInputError,
+                     SpatialDomainError)
+from .memory import DeviceBuffer
+from .options import (C_ADDRESS_ERR, FREE_ZONE_HI_CELLS, FREE_ZONE_LO_CELLS, FUSED_MARGIN_CELLS,
+                      N_COUNTERS, BoundaryBox, PipelineOptions, StepFlags)
+
+CELL_BIAS = 64
+CH_POS, CH_VEL, CH_C, CH_MASS, CH_DEF, CH_PLASTIC = 0, 3, 6, 15, 16, 25
+LW = 32
+_INT_MAX = 0x7FFFFFFF
+_PHASES = ("rebuild", "sort", "p2g", "grid", "g2p")
+
+
+def channels_for(kind: int) -> int:
+    """particles.py:24-31: 17 channels for the fluid (J), 25 for F; +1 plastic scalar."""
+    kind = int(kind)
+    if kind == MaterialKind.WEAKLY_COMPRESSIBLE_FLUID:
+        return 17
+    if kind == MaterialKind.FIXED_COROTATED:
+        return 25
+    return 26
+
+
+def _pow2_at_least(n: int) -> int:
+    return 1 << max(int(n) - 1, 1).bit_length()
+
+
+# --------------------------------------------------------------------------------------
+# particle store (particles.py:268-487)
+# --------------------------------------------------------------------------------------
+class CudaParticleStore:
+    """AoSoA particle storage on the device: data[group][channel][32] fp32, double-buffered
+    so a rebuild permutes from the old copy into the new one."""
+
+    def __init__(self, kind, lane_width, device):
+        if int(lane_width) != LW:
+            raise ConfigError(f"the CUDA core maps one warp to one lane group: lane_width must be {LW}")
+        self.kind = int(kind)
+        self.lane_width = LW
+        self.nch = channels_for(kind)
+        self.device = device
+        mk = lambda dt, shape=(): [DeviceBuffer(dt, shape, device), DeviceBuffer(dt, shape, device)]
+        self._data = mk(torch.float32, (self.nch, LW))
+        self._orig_id = mk(torch.int64, (LW,))
+        self._lane_meta = mk(torch.int16, (LW,))
+        self._group_len = mk(torch.int32)
+        self._group_block = mk(torch.int32)
+        self._group_start = mk(torch.int32)
+        self.cur = 0
+        self.n_groups = 0
+        self.count = 0
+        self._staged = []
+        self.staged_count = 0
+        self._next_id = 0
+        self._table = None   # set by the worker: group_origin comes from the block table
+
+    # -- views for the C ABI --
+    def view(self, which=None) -> StoreView:
+        k = self.cur if which is None else which
+        return StoreView(self._data[k].ptr, self._orig_id[k].ptr, self._lane_meta[k].ptr,
+                         self._group_len[k].ptr, self._group_block[k].ptr,
+                         self._group_start[k].ptr, self.n_groups if k == self.cur else 0, self.nch)
+
+    @property
+    def realloc_count(self) -> int:
+        return sum(b.realloc_count for pair in (self._data, self._orig_id, self._lane_meta,
+                                                self._group_len, self._group_block,
+                                                self._group_start) for b in pair)
+
+    # -- population (particles.py:309-334) --
+    def default_deformation(self, n):
+        if self.kind == MaterialKind.WEAKLY_COMPRESSIBLE_FLUID:
+            return np.ones((n, 1), dtype=np.float32)
+        return np.tile(np.eye(3, dtype=np.float32).reshape(9), (n, 1))
+
+    def stage_append(self, positions, velocities, masses, deformation=None, affine=None, ids=None):
+        pos = np.atleast_2d(np.asarray(positions))
+        n = pos.shape[0]
+        if n == 0:
+            return 0
+        if pos.shape[1] != 3:
+            raise RejectedInputError(f"positions must have shape (n, 3), got {pos.shape}")
+        vel = np.atleast_2d(np.asarray(velocities))
+        if vel.shape != pos.shape:
+            raise RejectedInputError(f"velocities must have shape {pos.shape}, got {vel.shape}")
+        flat = np.zeros((n, self.nch), dtype=np.float32)
+        flat[:, CH_POS:CH_POS + 3] = pos
+        flat[:, CH_VEL:CH_VEL + 3] = vel
+        if affine is not None:
+            flat[:, CH_C:CH_C + 9] = np.asarray(affine).reshape(n, 9)
+        flat[:, CH_MASS] = np.broadcast_to(np.asarray(masses), (n,))
+        defo = self.default_deformation(n) if deformation is None \
+            else np.asarray(deformation, dtype=np.float32).reshape(n, -1)
+        flat[:, CH_DEF:CH_DEF + defo.shape[1]] = defo
+        if self.nch > CH_PLASTIC:
+            flat[:, CH_PLASTIC] = 1.0 if self.kind == MaterialKind.SNOW else 0.0
+        if ids is None:
+            ids = np.arange(self._next_id, self._next_id + n, dtype=np.int64)
+            self._next_id += n
+        else:
+            ids = np.asarray(ids, dtype=np.int64).reshape(n)
+            self._next_id = max(self._next_id, int(ids.max()) + 1)
+        self._staged.append((flat, ids))
+        self.staged_count += n
+        return n
+
+    def take_staged(self):
+        """Staged host arrays as pinned -> device tensors (flat fp32 [n, nch], ids int64 [n])."""
+        if not self._staged:
+            return None, None, 0
+        flat = np.concatenate([s[0] for s in self._staged], axis=0)
+        ids = np.concatenate([s[1] for s in self._staged], axis=0)
+        self._staged.clear()
+        n = self.staged_count
+        self.staged_count = 0
+        dflat = torch.from_numpy(flat).pin_memory().to(self.device, non_blocking=True)
+        dids = torch.from_numpy(ids).pin_memory().to(self.device, non_blocking=True)
+        return dflat, dids, n
+
+    # -- readback (lazy D2H views in the reference's layout / dtype) --
+    def _g(self, bufs):
+        return bufs[self.cur].data[:self.n_groups]
+
+    @property
+    def data(self):
+        return self._g(self._data).to(torch.float64).cpu().numpy()
+
+    @property
+    def orig_id(self):
+        return self._g(self._orig_id).cpu().numpy()
+
+    @property
+    def lane_key(self):
+        return (self._g(self._lane_meta).cpu().numpy().view(np.uint16) & 0x3FF).astype(np.int64)
+
+    @property
+    def quarantined(self):
+        return ((self._g(self._lane_meta).cpu().numpy().view(np.uint16) >> 15) & 1).astype(np.uint8)
+
+    @property
+    def group_len(self):
+        return self._g(self._group_len).cpu().numpy()
+
+    @property
+    def group_block(self):
+        return self._g(self._group_block).cpu().numpy()
+
+    @property
+    def group_origin(self):
+        origin = self._table._origin.data[:self._table.count, :3].cpu().numpy()
+        return origin[self.group_block.astype(np.int64)].astype(np.int32)
+
+    def state_with_ids(self):
+        """All stored lanes (quarantined included) in (group, lane) order: flat f64 [n, nch], ids."""
+        n = self.count
+        flat = torch.zeros((max(n, 1), self.nch), dtype=torch.float32, device=self.device)
+        ids = torch.zeros(max(n, 1), dtype=torch.int64, device=self.device)
+        if n:
+            v = self.view()
+            check(_capi.lib().mpm_gather_state(C.byref(v), flat.data_ptr(), ids.data_ptr(),
+                                               _stream_ptr()), "mpm_gather_state")
+        return flat[:n].to(torch.float64).cpu().numpy(), ids[:n].cpu().numpy()
+
+    def positions_with_ids(self):
+        """particles.py:466-475."""
+        flat, ids = self.state_with_ids()
+        return flat[:, CH_POS:CH_POS + 3].copy(), ids
+
+    def _aggregates(self):
+        out = torch.zeros(5, dtype=torch.float64, device=self.device)
+        v = self.view()
+        check(_capi.lib().mpm_particle_aggregates(C.byref(v), out.data_ptr(), _stream_ptr()),
+              "mpm_particle_aggregates")
+        return out.cpu().numpy()
+
+    def total_mass(self) -> float:
+        return float(self._aggregates()[0])
+
+    def total_momentum(self):
+        return self._aggregates()[1:4].copy()
+
+    def kinetic_energy(self) -> float:
+        return float(self._aggregates()[4])
+
+
+# --------------------------------------------------------------------------------------
+# block table (grid.py:325-401) and nodal buffers (grid.py:415-454)
+# --------------------------------------------------------------------------------------
+class CudaBlockTable:
+    def __init__(self, device):
+        self.device = device
+        self._codes = DeviceBuffer(torch.int64, (), device)
+        self._origin = DeviceBuffer(torch.int32, (4,), device)
+        self._neighbor = DeviceBuffer(torch.int32, (27,), device)
+        self._touched = [DeviceBuffer(torch.uint8, (), device), DeviceBuffer(torch.uint8, (), device)]
+        self._hkeys = DeviceBuffer(torch.int64, (), device)
+        self._hvals = DeviceBuffer(torch.int32, (), device)
+        self._hfirst = DeviceBuffer(torch.int32, (), device)
+        self.hash_cap = 0
+        self.count = 0
+        self.n_gblocks = 0
+
+    @property
+    def realloc_count(self) -> int:
+        return sum(b.realloc_count for b in (self._codes, self._origin, self._neighbor,
+                                             self._touched[0], self._touched[1], self._hkeys,
+                                             self._hvals, self._hfirst))
+
+    def ensure_hash(self, cap: int):
+        for b in (self._hkeys, self._hvals, self._hfirst):
+            if b.capacity < cap:
+                b.capacity = 0          # exact power-of-two sizing, contents are rebuilt anyway
+                b.len = 0
+                b.data = torch.empty(cap, dtype=b.dtype, device=self.device)
+                b.capacity = cap
+                b.realloc_count += 1
+        self.hash_cap = cap
+
+    def view(self) -> TableView:
+        t = TableView()
+        t.codes, t.origin, t.neighbor = self._codes.ptr, self._origin.ptr, self._neighbor.ptr
+        t.touched[0], t.touched[1] = self._touched[0].ptr, self._touched[1].ptr
+        t.count, t.n_gblocks = self.count, self.n_gblocks
+        return t
+
+    @property
+    def codes(self):
+        return self._codes.data[:self.count].cpu().numpy()
+
+    @property
+    def neighbor(self):
+        return self._neighbor.data[:self.n_gblocks].cpu().numpy()
+
+    @property
+    def touched(self):
+        return [self._touched[k].data[:self.count].cpu().numpy() for k in (0, 1)]
+
+    def touched_indices(self, buffer: int = 0):
+        return np.flatnonzero(self.touched[buffer])
+
+
+class CudaGrid:
+    """raw[0], raw[1], vel (+ vel_old): float4 nodes [pblock][64] on the device.  The numpy
+    properties return the reference's channel-major float64 layout [pblock, 4, 64]."""
+
+    def __init__(self, device):
+        self.device = device
+        self._raw = [DeviceBuffer(torch.float32, (64, 4), device), DeviceBuffer(torch.float32, (64, 4), device)]
+        self._vel = DeviceBuffer(torch.float32, (64, 4), device)
+        self._vel_old = None
+        self.count = 0
+
+    @property
+    def realloc_count(self) -> int:
+        n = self._raw[0].realloc_count + self._raw[1].realloc_count + self._vel.realloc_count
+        return n + (self._vel_old.realloc_count if self._vel_old is not None else 0)
+
+    def _ref_layout(self, buf):
+        return buf.data[:self.count].to(torch.float64).permute(0, 2, 1).contiguous().cpu().numpy()
+
+    @property
+    def raw(self):
+        return [self._ref_layout(self._raw[0]), self._ref_layout(self._raw[1])]
+
+    @property
+    def vel(self):
+        return self._ref_layout(self._vel)
+
+    @property
+    def vel_old(self):
+        if self._vel_old is None:
+            return None
+        return self._ref_layout(self._vel_old)[:, 1:4, :]
+
+
+def _stream_ptr() -> int:
+    return torch.cuda.current_stream().cuda_stream
+
+
+# --------------------------------------------------------------------------------------
+# worker (pipeline.py:788-1238)
+# --------------------------------------------------------------------------------------
+class CudaWorker:
+    """Drop-in for `mpmbench.pipeline.Worker` on one CUDA device."""
+
+    def __init__(self, wid, runtime, params: SimParams, material: Material,
+                 boundary: BoundaryBox | None, options: PipelineOptions | None = None,
+                 device=None, count_stats: bool = True, fuse_clear: bool = False):
+        _capi.require_device()
+        self.lib = _capi.lib()
+        self.device = torch.device(device if device is not None else "cuda:0")
+        self.wid = wid
+        self.runtime = runtime
+        self.params = params
+        self.material = material
+        self.boundary = boundary
+        self.options = options if options is not None else PipelineOptions()
+        if self.options.fusion != "merged" or self.options.sort == "full_every_step":
+            raise ConfigError("the CUDA core implements fusion=merged and sort=amortized|none_between "
+                              "(the other arms re-measure CPU ablations, SURVEY.md section 2 row 13)")
+        if self.options.deterministic:
+            raise ConfigError("deterministic fixed-point accumulation is not implemented on the CUDA core")
+        if int(material.kind) not in (0, 1):
+            raise ConfigError(f"material kind {material.kind!r} is not implemented on the CUDA core yet")
+        with torch.cuda.device(self.device):
+            self.store = CudaParticleStore(material.kind, params.lane_width, self.device)
+            self.table = CudaBlockTable(self.device)
+            self.grid = CudaGrid(self.device)
+            self.store._table = self.table
+            self._status = torch.zeros(_capi.STATUS_BYTES // 8, dtype=torch.int64, device=self.device)
+            self._status_host = torch.zeros(_capi.STATUS_BYTES // 8, dtype=torch.int64).pin_memory()
+            self._scalars = torch.zeros(16, dtype=torch.int32, device=self.device)
+            self._scalars_host = torch.zeros(16, dtype=torch.int32).pin_memory()
+        self.flags = StepFlags(deterministic_mode=False)
+        self.conservation = []
+        self.rebuild_steps = []
+        self.dt = params.dt
+        self._vel_dt = params.dt
+        self._global_step = 0
+        self._pending_gather = False
+        self._pending_full_clear_parity = -1
+        self._published_codes = (None, 0)
+        self._peer_map = [None] * runtime.n_workers
+        self._peer_states = None
+        self._fused_now = False
+        self._phase_ms = {k: 0.0 for k in _PHASES}
+        self._frame_steps = 0
+        self._frame_rebuilds = 0
+        self.cfl_mode = False
+        self.count_stats = bool(count_stats)
+        self.fuse_clear = bool(fuse_clear)
+        self.last_perm = None
+        self.last_gidx = None
+        self._scratch = {}
+        self._scratch_allocs = 0
+        self.kernel_calls = 0
+        m = material
+        self._tp = TransferParams(
+            mat_kind=int(m.kind), nch=self.store.nch, mu=float(m.mu), lam=float(m.lam),
+            kappa=float(m.bulk_modulus), gamma=float(m.gamma),
+            clamp_tension=int(bool(m.clamp_tension)), count_stats=int(self.count_stats),
+            density=float(m.density), dx=float(params.dx), dt=float(params.dt),
+            dt_gather=float(params.dt), flip_blend=float(params.flip_blend),
+            margin_lo=FREE_ZONE_LO_CELLS, margin_hi=FREE_ZONE_HI_CELLS - 4.0,
+            theta_c=float(m.theta_c), theta_s=float(m.theta_s), hardening=float(m.hardening),
+            sand_alpha=math.sqrt(2.0 / 3.0) * 2.0 * math.sin(math.radians(m.friction_angle))
+            / (3.0 - math.sin(math.radians(m.friction_angle))))
+
+    # -- small helpers ----------------------------------------------------------------
+    def _call(self, name, *args):
+        self.kernel_calls += 1
+        check(getattr(self.lib, name)(*args), name)
+
+    def _scratch_i32(self, tag, n):
+        """Tagged scratch (memory.py:72-114 ScratchPool): reused across rebuilds, 4x growth."""
+        buf = self._scratch.get(tag)
+        if buf is None:
+            buf = self._scratch[tag] = DeviceBuffer(torch.int32, (), self.device)
+        before = buf.realloc_count
+        buf.ensure_capacity(max(int(n), 1), keep=False)
+        self._scratch_allocs += buf.realloc_count - before
+        return buf
+
+    def _scratch_i64(self, tag, n):
+        buf = self._scratch.get(tag)
+        if buf is None:
+            buf = self._scratch[tag] = DeviceBuffer(torch.int64, (), self.device)
+        before = buf.realloc_count
+        buf.ensure_capacity(max(int(n), 1), keep=False)
+        self._scratch_allocs += buf.realloc_count - before
+        return buf
+
+    def _read_scalars(self):
+        self._scalars_host.copy_(self._scalars, non_blocking=True)
+        torch.cuda.current_stream().synchronize()
+        return self._scalars_host.numpy()
+
+    def _sptr(self, k):
+        return self._scalars.data_ptr() + 4 * k
+
+    @property
+    def counters(self):
+        self._status_host.copy_(self._status, non_blocking=True)
+        torch.cuda.current_stream().synchronize()
+        return self._status_host.numpy()[1:1 + N_COUNTERS].astype(np.int64)
+
+    @property
+    def frame_steps(self):
+        return self._frame_steps
+
+    @property
+    def frame_rebuilds(self):
+        return self._frame_rebuilds
+
+    @property
+    def phase_ms(self):
+        return dict(self._phase_ms)
+
+    @property
+    def realloc_count(self):
+        return (self.store.realloc_count + self.table.realloc_count + self.grid.realloc_count +
+                self._scratch_allocs)
+
+    # -- population (pipeline.py:831-850) -----------------------------------------------
+    def seed_particles(self, positions, velocities, masses, ids):
+        n = self.store.stage_append(positions, velocities, masses, ids=ids)
+        self.flags.rebuild_needed = True
+        return n
+
+    def append_particles(self, positions, velocities, masses, ids=None):
+        if len(np.atleast_2d(positions)) == 0:
+            return 0
+        if self.flags.fused_mode:
+            raise ModeConflictError("cannot add particles while the fused G2P2G transfer is active")
+        n = self.store.stage_append(positions, velocities, masses, ids=ids)
+        if n:
+            self.flags.rebuild_needed = True
+        return n
+
+    # -- per frame (pipeline.py:852-880) ------------------------------------------------
+    def begin_frame(self):
+        self._phase_ms = {k: 0.0 for k in _PHASES}
+        self._frame_steps = 0
+        self._frame_rebuilds = 0
+
+    def run_frame(self):
+        self.begin_frame()
+        with torch.cuda.device(self.device):
+            if self.cfl_mode:
+                c_sound = self.material.sound_speed()
+                t = 0.0
+                while t < self.params.frame_dt - 1e-12:
+                    vmax = self.runtime.global_vmax((self._global_step - 2) % 3)
+                    self.dt = cfl_dt(vmax + c_sound, self.params, self.params.frame_dt - t)
+                    self.run_step(self._global_step)
+                    t += self.dt
+                    self._frame_steps += 1
+            else:
+                self.dt = self.params.dt
+                for _ in range(self.params.steps_per_frame):
+                    self.run_step(self._global_step)
+                    self._frame_steps += 1
+            if self._pending_gather:
+                self._flush_gather()
+
+    # -- one step, split around the barrier (pipeline.py:905-940) --------------------------
+    def step_pre_barrier(self, step):
+        par = step & 1
+        if self.options.rebuild == "every_step":
+            self.flags.rebuild_needed = True
+        rebuilt = False
+        if self.flags.rebuild_needed:
+            if self._pending_gather:
+                self._flush_gather()
+            self._rebuild(step, par)
+            rebuilt = True
+        else:
+            self._clear(par)
+        fused_now = self._fused_active()
+        self.flags.fused_mode = fused_now
+        if fused_now and self._pending_gather:
+            self._run_g2p2g(step, par)
+        else:
+            if self._pending_gather:
+                self._flush_gather()
+            self._run_p2g(step, par)
+        self._publish(par, rebuilt)
+        self._fused_now = fused_now
+
+    def step_post_barrier(self, step):
+        par = step & 1
+        self._post_barrier(par)
+        self._reduce_and_update(par)
+        if self._fused_now:
+            self._pending_gather = True
+        else:
+            self._run_g2p(step)
+            self._pending_gather = False
+        self.flags.steps_since_rebuild += 1
+        self._global_step = step + 1
+
+    def run_step(self, step):
+        with torch.cuda.device(self.device):
+            self.step_pre_barrier(step)
+            self.runtime.barrier_wait(self.wid)
+            self.step_post_barrier(step)
+
+    # -- phases ---------------------------------------------------------------------------
+    def _fused_active(self):
+        if self.options.transfer != "g2p2g":
+            return False
+        if self.store.staged_count:
+            return False
+        if self.store.count >= self.options.fused_threshold:
+            return False
+        return True
+
+    def _rebuild(self, step, par):
+        """Worker._rebuild (pipeline.py:958-1015) on the device; two host syncs (block count,
+        then pblock + group counts) -- the paper's CPU-GPU sync points."""
+        lib, st, tb, gr = self.lib, self.store, self.table, self.grid
+        stream = _stream_ptr()
+        staged, staged_ids, n_staged = st.take_staged()
+        n_upper = st.count + n_staged
+        old = st.view()
+        S = self._scratch_i32
+        src_slot = S("src_slot", n_upper)
+        scan = S("scan", n_upper // 16 + 1024)   # block sums of the largest scan (n_g*64+1 bins)
+        codes = self._scratch_i64("codes", n_upper)
+        # scalars: 0 n_live, 1 n_total, 2 bad_index, 3 n_gblocks, 4 overflow, 5 count, 6 bad_block,
+        #          7 n_groups
+        glive = S("glive", st.n_groups + 1)
+        self._call("mpm_compact_live", C.byref(old), 1, glive.ptr, src_slot.ptr, self._sptr(0),
+                   scan.ptr, stream)
+        self._call("mpm_particle_codes", C.byref(old), src_slot.ptr, self._sptr(0),
+                   staged.data_ptr() if n_staged else None, n_staged, n_upper, float(self.params.dx),
+                   codes.ptr, self._sptr(1), self._sptr(2), stream)
+        pslot, flag, gidx = S("pslot", n_upper), S("flag", n_upper), S("gidx", n_upper)
+        gcodes = self._scratch_i64("gcodes", n_upper)
+        # hash capacity: load factor < 1/8 against the pblock count seen last time, or a
+        # conservative first guess; an overflow doubles it and retries
+        cap = max(tb.hash_cap, _pow2_at_least(8 * max(tb.count, 1)), 1 << 12)
+        if tb.count == 0:
+            cap = max(cap, _pow2_at_least(max(n_upper // 2, 1)))
+        while True:
+            tb.ensure_hash(cap)
+            self._call("mpm_hash_insert_blocks", codes.ptr, self._sptr(1), n_upper, tb._hkeys.ptr,
+                       tb._hvals.ptr, tb._hfirst.ptr, cap, pslot.ptr, flag.ptr, scan.ptr, gidx.ptr,
+                       gcodes.ptr, self._sptr(3), self._sptr(4), stream)
+            sc = self._read_scalars()
+            n, bad, n_g, overflow = int(sc[1]), int(sc[2]), int(sc[3]), int(sc[4])
+            if bad != _INT_MAX:
+                raise SpatialDomainError(
+                    f"worker {self.wid}: particle {bad} of the rebuild input lies outside the "
+                    f"encodable domain [0, 2^21) cells")
+            if not overflow and 8 * n_g <= cap:
+                break
+            cap *= 4
+        # 27-dilation; codes/origin/touched sized for the worst case 27 n_g (they are small)
+        pcap = max(27 * n_g, 1)
+        tb._codes.ensure_capacity(pcap, keep=False)
+        tb._origin.ensure_capacity(pcap, keep=False)
+        tb._neighbor.ensure_capacity(max(n_g, 1), keep=False)
+        for k in (0, 1):
+            tb._touched[k].len = min(tb._touched[k].len, tb.count)
+            tb._touched[k].ensure_capacity(pcap, keep=True)
+        qslot, qflag = S("qslot", 27 * n_g), S("qflag", 2 * 27 * n_g)
+        pcap_eff = min(tb._codes.capacity, tb._origin.capacity)
+        while True:
+            self._call("mpm_dilate_and_link", gcodes.ptr, n_g, tb._hkeys.ptr, tb._hvals.ptr,
+                       tb._hfirst.ptr, cap, qslot.ptr, qflag.ptr, scan.ptr, tb._codes.ptr,
+                       tb._origin.ptr, tb._neighbor.ptr, pcap_eff, self._sptr(5), self._sptr(6),
+                       self._sptr(4), stream)
+            bin_start = S("bin_start", n_g * 64 + 1)
+            tmp_perm, perm = S("tmp_perm", n_upper), S("perm", n_upper)
+            bgf = S("bgf", n_g + 1)
+            self._call("mpm_sort_and_group", codes.ptr, gidx.ptr, self._sptr(1), n_upper, n_g,
+                       bin_start.ptr, tmp_perm.ptr, perm.ptr, bgf.ptr, scan.ptr, self._sptr(7),
+                       stream)
+            sc = self._read_scalars()
+            overflow, count, bad_block, G = int(sc[4]), int(sc[5]), int(sc[6]), int(sc[7])
+            if bad_block != _INT_MAX:
+                code = int(gcodes.data[bad_block].item())
+                x, y, z = _decode(code)
+                raise SpatialDomainError(
+                    f"block ({x - CELL_BIAS // 4}, {y - CELL_BIAS // 4}, {z - CELL_BIAS // 4}) "
+                    f"touches the domain boundary; scenes must leave a one-block margin")
+            if overflow != 1:
+                break
+            # hash too small for the halo: rebuild the gblock part in a larger table
+            cap *= 4
+            tb.ensure_hash(cap)
+            self._call("mpm_hash_insert_blocks", codes.ptr, self._sptr(1), n_upper, tb._hkeys.ptr,
+                       tb._hvals.ptr, tb._hfirst.ptr, cap, pslot.ptr, flag.ptr, scan.ptr, gidx.ptr,
+                       gcodes.ptr, self._sptr(3), self._sptr(4), stream)
+        tb.n_gblocks, prev_count, tb.count = n_g, tb.count, count
+        tb._codes.len = tb._origin.len = count
+        tb._neighbor.len = n_g
+        # new particle store (other half of the double buffer)
+        nxt = 1 - st.cur
+        for bufs in (st._data, st._orig_id, st._lane_meta, st._group_len, st._group_block,
+                     st._group_start):
+            bufs[nxt].resize(G, keep=False)
+        new = StoreView(st._data[nxt].ptr, st._orig_id[nxt].ptr, st._lane_meta[nxt].ptr,
+                        st._group_len[nxt].ptr, st._group_block[nxt].ptr, st._group_start[nxt].ptr,
+                        G, st.nch)
+        self._call("mpm_scatter_sorted", C.byref(old), src_slot.ptr, self._sptr(0),
+                   staged.data_ptr() if n_staged else None,
+                   staged_ids.data_ptr() if n_staged else None, perm.ptr, bin_start.ptr, bgf.ptr,
+                   n_g, tb._origin.ptr, float(self.params.dx), C.byref(new), stream)
+        st.cur, st.n_groups, st.count = nxt, G, n
+        self.last_perm = perm.data[:n]
+        self.last_gidx = gidx.data[:n]
+        # nodal buffers (pipeline.py:996-1006): vel and raw[par] start from zero; the other
+        # parity keeps whatever it held and is cleared in full at its next use
+        gr._vel.resize(count, keep=False)
+        gr._raw[par].resize(count, keep=False)
+        gr._raw[1 - par].resize(count, keep=False)
+        if gr._vel_old is not None:
+            gr._vel_old.resize(count, keep=False)
+        gr.count = count
+        gr._vel.data[:count].zero_()
+        if count:
+            self._call("mpm_clear", gr._raw[par].ptr, tb._touched[par].ptr, count, 1, None, stream)
+        for k in (0, 1):
+            tb._touched[k].len = count
+        self._pending_full_clear_parity = 1 - par
+        self._published_codes = (tb._codes, count)
+        self.flags.rebuild_needed = False
+        self.flags.steps_since_rebuild = 0
+        self.rebuild_steps.append(step)
+        self._frame_rebuilds += 1
+
+    def _clear(self, par):
+        """Worker._clear (pipeline.py:1022-1037)."""
+        count = self.table.count
+        if not count:
+            return
+        full = int(self._pending_full_clear_parity == par)
+        if full:
+            self._pending_full_clear_parity = -1
+        elif self.fuse_clear and self.runtime.n_workers == 1:
+            return   # rows were zeroed by the grid update that consumed them
+        self._call("mpm_clear", self.grid._raw[par].ptr, self.table._touched[par].ptr, count, full,
+                   None, _stream_ptr())
+
+    def _params(self, margin_shrink=0.0):
+        tp = self._tp
+        tp.dt = float(self.dt)
+        tp.dt_gather = float(self._vel_dt)
+        tp.margin_lo = FREE_ZONE_LO_CELLS - margin_shrink
+        tp.margin_hi = FREE_ZONE_HI_CELLS - 4.0 - margin_shrink
+        return tp
+
+    def _vel_old_ptr(self):
+        if self.params.flip_blend > 0.0:
+            gr = self.grid
+            if gr._vel_old is None:
+                gr._vel_old = DeviceBuffer(torch.float32, (64, 4), self.device)
+            gr._vel_old.resize(self.table.count, keep=True)
+            return gr._vel_old.ptr
+        return None
+
+    def _run_p2g(self, step, par):
+        st = self.store
+        if not st.n_groups:
+            return
+        sv, tv = st.view(), self.table.view()
+        self._call("mpm_p2g", C.byref(sv), C.byref(tv), self.grid._raw[par].ptr,
+                   self.table._touched[par].ptr, C.byref(self._params()), self._status.data_ptr(),
+                   None, _stream_ptr())
+
+    def _run_g2p(self, step):
+        st = self.store
+        if not st.n_groups:
+            self.runtime.publish_vmax(step % 3, self.wid, 0.0)
+            return
+        sv, tv = st.view(), self.table.view()
+        stream = _stream_ptr()
+        self._call("mpm_status_reset", self._status.data_ptr(), None, stream)
+        self._call("mpm_g2p", C.byref(sv), C.byref(tv), self.grid._vel.ptr, self._vel_old_ptr(),
+                   C.byref(self._params()), self._status.data_ptr(), None, stream)
+        self._consume_status(step)
+
+    def _flush_gather(self):
+        self._run_g2p(self._global_step)
+        self._pending_gather = False
+
+    def _run_g2p2g(self, step, par):
+        st = self.store
+        if not st.n_groups:
+            return
+        sv, tv = st.view(), self.table.view()
+        stream = _stream_ptr()
+        self._call("mpm_status_reset", self._status.data_ptr(), None, stream)
+        self._call("mpm_g2p2g", C.byref(sv), C.byref(tv), self.grid._vel.ptr, self._vel_old_ptr(),
+                   self.grid._raw[par].ptr, self.table._touched[par].ptr,
+                   C.byref(self._params(FUSED_MARGIN_CELLS)), self._status.data_ptr(), None, stream)
+        self._consume_status(step)
+
+    def _consume_status(self, step):
+        """Read the status block written by a gather: free-zone flag -> rebuild_needed,
+        max speed -> vmax ring (pipeline.py:1102-1104), addressing counter -> exception
+        (pipeline.py:1233-1238)."""
+        self._status_host.copy_(self._status, non_blocking=True)
+        torch.cuda.current_stream().synchronize()
+        raw = self._status_host.numpy()
+        head = raw[:1].view(np.uint32)
+        if head[0]:
+            self.flags.rebuild_needed = True
+        vmax2 = float(head[1:2].view(np.float32)[0])
+        self.runtime.publish_vmax(step % 3, self.wid, math.sqrt(max(vmax2, 0.0)))
+        if raw[1 + C_ADDRESS_ERR]:
+            raise ContractViolationError(
+                f"worker {self.wid}: {int(raw[1 + C_ADDRESS_ERR])} stencil accesses left the "
+                f"27-neighbor pblock set")
+
+    def _check_addressing(self):
+        c = self.counters
+        if c[C_ADDRESS_ERR]:
+            raise ContractViolationError(
+                f"worker {self.wid}: {int(c[C_ADDRESS_ERR])} stencil accesses left the "
+                f"27-neighbor pblock set")
+
+    def _publish(self, par, rebuilt):
+        codes, count = self._published_codes
+        self.runtime.publish_step(par, self.wid, dict(
+            raw=self.grid._raw[par], touched=self.table._touched[par], codes=codes,
+            code_count=count, rebuilt=rebuilt))
+
+    def _post_barrier(self, par):
+        """Shared-block tagging on rebuild steps (pipeline.py:1147-1164)."""
+        n = self.runtime.n_workers
+        if n == 1:
+            return
+        states = [self.runtime.peer_step(par, q) for q in range(n)]
+        if any(s["rebuilt"] for s in states):
+            stream = _stream_ptr()
+            for q, s in enumerate(states):
+                if q == self.wid:
+                    continue
+                m = self._peer_map[q]
+                if m is None:
+                    m = self._peer_map[q] = DeviceBuffer(torch.int32, (), self.device)
+                m.resize(self.table.count, keep=False)
+                self._call("mpm_tag_shared", s["codes"].ptr, int(s["code_count"]),
+                           self.table._hkeys.ptr, self.table._hvals.ptr, self.table.hash_cap,
+                           m.ptr, self.table.count, stream)
+        self._peer_states = states
+
+    def _reduce_and_update(self, par):
+        """pipeline.py:1166-1231 in one kernel: reduce over peers, finalize, boundary."""
+        tb, gr = self.table, self.grid
+        count = tb.count
+        stream = _stream_ptr()
+        peers = []
+        if self.runtime.n_workers > 1 and self._peer_states is not None:
+            for q, s in enumerate(self._peer_states):
+                if q == self.wid or self._peer_map[q] is None:
+                    continue
+                peers.append((s["raw"].ptr, s["touched"].ptr, self._peer_map[q].ptr))
+        if self.options.collect_conservation:
+            self._collect_conservation(par)
+        n_p = len(peers)
+        arr = C.c_void_p * max(n_p, 1)
+        p_raw, p_touched, p_map = arr(), arr(), arr()
+        for k, (r, t, m) in enumerate(peers):
+            p_raw[k], p_touched[k], p_map[k] = r, t, m
+        grav = (C.c_double * 3)(*[float(g) for g in self.params.gravity])
+        bc = self.boundary
+        if bc is not None:
+            blo = (C.c_double * 3)(*[float(v) for v in bc.min_corner])
+            bhi = (C.c_double * 3)(*[float(v) for v in bc.max_corner])
+            sticky = int(bc.mode == "sticky")
+        else:
+            blo, bhi, sticky = (C.c_double * 3)(), (C.c_double * 3)(), 0
+        fuse = int(self.fuse_clear and self.runtime.n_workers == 1)
+        tv = tb.view()
+        if count:
+            self._call("mpm_grid_update", gr._raw[par].ptr, tb._touched[par].ptr, gr._vel.ptr,
+                       self._vel_old_ptr(), C.byref(tv), n_p, p_raw, p_touched, p_map,
+                       float(self.dt), grav, int(bc is not None), sticky, blo, bhi,
+                       float(self.params.dx), fuse, gr._raw[par].ptr if fuse else None,
+                       tb._touched[par].ptr if fuse else None, None, stream)
+        self._vel_dt = self.dt
+
+    def _collect_conservation(self, par):
+        """(pm, pmom x3, gm, gmom x3) rows of pipeline.py:1189-1203 (own raw rows only)."""
+        out = torch.zeros(4, dtype=torch.float64, device=self.device)
+        self._call("mpm_grid_aggregates", self.grid._raw[par].ptr, self.table._touched[par].ptr,
+                   self.table.count, out.data_ptr(), _stream_ptr())
+        p = self.store._aggregates()
+        g = out.cpu().numpy()
+        self.conservation.append((p[0], p[1], p[2], p[3], g[0], g[1], g[2], g[3]))
+
+
+def _decode(code: int):
+    def compact(v):
+        v &= 0x1249249249249249
+        v = (v ^ (v >> 2)) & 0x10C30C30C30C30C3
+        v = (v ^ (v >> 4)) & 0x100F00F00F00F00F
+        v = (v ^ (v >> 8)) & 0x1F0000FF0000FF
+        v = (v ^ (v >> 16)) & 0x1F00000000FFFF
+        v = (v ^ (v >> 32)) & 0x1FFFFF
+        return v
+    return compact(code), compact(code >> 1), compact(code >> 2)
+
+
+def make_single_worker(particles, velocities, material, params, boundary, mass, device=None,
+                       **options):
+    """The reference tests' harness (tests/conftest.py:18-38 of the reference) for the CUDA
+    worker: a solo runtime + worker, seeded and ready for `w.run_step(s)`."""
+    from .multiworker import SharedRuntime
+    particles = np.asarray(particles)
+    velocities = np.asarray(velocities)
+    worker_kw = {k: options.pop(k) for k in ("count_stats", "fuse_clear") if k in options}
+    vmax = float(np.linalg.norm(velocities, axis=1).max()) if len(velocities) else 0.0
+    runtime = SharedRuntime(1, initial_vmax=vmax)
+    w = CudaWorker(0, runtime, params, material, boundary, PipelineOptions(**options),
+                   device=device, **worker_kw)
+    w.seed_particles(particles, velocities, mass, ids=np.arange(len(particles), dtype=np.int64))
+    w.dt = params.dt
+    return w
