@@ -1,0 +1,335 @@
+#!/usr/bin/env python
+"""Benchmark of the MLS-MPM substep hot path (BASELINE.json: "ms/frame & M particle-substeps/s,
+snow 1.33M MLS-MPM").
+
+    python bench.py --gpus 1 --steps K --warmup W            # CUDA core (this repo)
+    python bench.py --impl reference --gpus N --steps K ...  # the reference's CPU path
+    torchrun ... bench.py --gpus N ...                       # one rank per GPU
+
+A "step" is one FRAME of the workload: `steps_per_frame` substeps (rebuild-mapping amortised
+inside, as in the reference's run_frame).  `value` = particle-substeps per second with the
+particles resident in HBM; `e2e` = the same through the public API with host buffers: every
+step uploads the particle state from pinned host memory (seed), runs the frame and reads
+the positions back.  One JSON line on stdout (rank 0).
+"""
+import argparse
+import json
+import os
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+import numpy as np  # noqa: E402
+
+METRIC = "particle_substeps_per_s"
+UNIT = "M particle-substeps/s"
+
+
+def parse_args():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=8)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--scene", default="snow", choices=["snow", "snow_fc", "sand64k", "sand_mini",
+                                                        "sand389k", "sand1m", "sand10m"])
+    ap.add_argument("--transfer", default="g2p2g", choices=["split", "g2p2g"])
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--ref-substeps", type=int, default=2,
+                    help="substeps per step of the reference arm (bounded sample)")
+    return ap.parse_args()
+
+
+def build_world(scene):
+    from paper_2111_00699_b200 import scenes
+    if scene == "snow":
+        return scenes.snow(plastic=SNOW_PLASTIC)
+    if scene == "snow_fc":
+        return scenes.snow(plastic=False)
+    if scene == "sand64k":
+        return scenes.sand_blocks(l=20, boxes=1)
+    if scene == "sand_mini":
+        return scenes.sand_blocks(l=12, boxes=4)
+    if scene == "sand389k":
+        return scenes.sand_blocks(l=23, boxes=4)
+    if scene == "sand1m":
+        return scenes.sand_blocks(l=32, boxes=4)
+    if scene == "sand10m":
+        return scenes.sand_blocks(l=43, boxes=16)
+    raise ValueError(scene)
+
+
+# the plastic snow model is used once the CUDA core implements it; until then the
+# reference-pinned fixed-corotated variant of the same scene is timed and named as such
+SNOW_PLASTIC = False
+
+
+class ClockSampler:
+    """nvidia-smi clocks / throttle reasons sampled every 200 ms during the timed region."""
+    QUERY = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+             "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+             "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, gpu_index=0):
+        self.proc = None
+        self.gpu_index = gpu_index
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.gpu_index), f"--query-gpu={self.QUERY}",
+                 "--format=csv,noheader,nounits", "-lms", "200"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+        except OSError:
+            self.proc = None
+
+    def stop(self):
+        if self.proc is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        self.proc.terminate()
+        try:
+            out, _ = self.proc.communicate(timeout=5)
+        except subprocess.TimeoutExpired:
+            self.proc.kill()
+            out, _ = self.proc.communicate()
+        sm, smax, power, reasons = [], [], [], set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for line in out.strip().splitlines():
+            f = [x.strip() for x in line.split(",")]
+            if len(f) < 9:
+                continue
+            try:
+                sm.append(float(f[1])); smax.append(float(f[2])); power.append(float(f[3]))
+            except ValueError:
+                continue
+            for name, v in zip(names, f[5:9]):
+                if v.lower().startswith("active"):
+                    reasons.add(name)
+        if not sm:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["no samples"]}
+        return {"sm_mhz": float(np.median(sm)), "sm_max_mhz": float(max(smax)),
+                "power_w_max": float(max(power)), "samples": len(sm), "reasons": sorted(reasons)}
+
+
+def measured_peak_gbs():
+    path = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(path):
+        with open(path) as fh:
+            return float(json.load(fh)["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs)"
+    return 6650.0, "fallback (B200_PROFILING.md 6.65 TB/s)"
+
+
+def algorithmic_bytes(kind, transfer, n_particles, touched_blocks):
+    """SURVEY.md section 8(d) / DESIGN.md: bytes the dominant transfer kernel must move.
+    fused elastic: read {x3,m,F9}=52 B + write {x3,v3,F9}=60 B per particle; fluid 20+28;
+    plastic scalar +8; grid: gather read 16 B + scatter write-back 16 B per touched node."""
+    if transfer == "g2p2g":
+        per_p = {0: 48, 1: 112, 2: 120, 3: 120}[kind]
+        per_node = 32
+    else:   # split: the P2G kernel alone (dominant of the two)
+        per_p = {0: 68, 1: 100, 2: 104, 3: 104}[kind]
+        per_node = 16
+    return n_particles * per_p + touched_blocks * 64 * per_node
+
+
+def run_ours(args):
+    import torch
+    import torch.distributed as dist
+    from paper_2111_00699_b200 import PipelineOptions, SharedRuntime, _capi
+    from paper_2111_00699_b200.worker import CudaWorker
+
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if world > 1:
+        from paper_2111_00699_b200 import dist as mdist
+        return mdist.run_bench(args, build_world, algorithmic_bytes, ClockSampler,
+                               measured_peak_gbs, METRIC, UNIT)
+    if args.gpus != 1:
+        raise SystemExit("--gpus N>1 must be launched with torch.distributed.run (one rank per GPU)")
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    W = build_world(args.scene)
+    n = len(W.positions)
+    spf = W.params.steps_per_frame
+    opts = PipelineOptions(transfer=args.transfer, fused_threshold=1 << 62)
+    lib = _capi.lib()
+
+    def fresh_worker():
+        rt = SharedRuntime(1, initial_vmax=float(np.abs(W.velocities).max()))
+        w = CudaWorker(0, rt, W.params, W.material, W.boundary, opts, device=dev,
+                       count_stats=False, fuse_clear=True)
+        return w
+
+    ids = np.arange(n, dtype=np.int64)
+    w = fresh_worker()
+    w.seed_particles(W.positions, W.velocities, W.particle_mass, ids=ids)
+    for _ in range(args.warmup):
+        w.run_frame()
+    torch.cuda.synchronize()
+    w.time_kernels = True
+    w.kernel_events.clear()
+    sampler = ClockSampler(local)
+    sampler.start()
+    l0 = lib.mpm_launch_count()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    reb0 = len(w.rebuild_steps)
+    torch.cuda.synchronize()
+    e0.record()
+    for _ in range(args.steps):
+        w.run_frame()
+    e1.record()
+    torch.cuda.synchronize()
+    total_ms = e0.elapsed_time(e1)
+    launches = int(lib.mpm_launch_count() - l0)
+    clocks = sampler.stop()
+    rebuilds = len(w.rebuild_steps) - reb0
+    ms_per_step = total_ms / args.steps
+    value = n * spf * args.steps / (total_ms * 1e-3) / 1e6
+    # dominant kernel: average launch duration from CUDA events on the launching stream
+    w.time_kernels = False
+    dom = "mpm_g2p2g" if args.transfer == "g2p2g" else "mpm_p2g"
+    durs = [a.elapsed_time(b) for name, a, b in w.kernel_events if name == dom]
+    all_kernel_ms = {}
+    for name, a, b in w.kernel_events:
+        all_kernel_ms[name] = all_kernel_ms.get(name, 0.0) + a.elapsed_time(b)
+    touched = int(w.table._touched[0].data[:w.table.count].sum().item()) or \
+        int(w.table._touched[1].data[:w.table.count].sum().item())
+    peak, peak_src = measured_peak_gbs()
+    roofline = None
+    if durs:
+        avg_ms = float(np.mean(durs))
+        abytes = algorithmic_bytes(int(W.material.kind), args.transfer, n, touched)
+        achieved = abytes / (avg_ms * 1e-3) / 1e9
+        roofline = {"bound": "hbm", "kernel": dom, "achieved": round(achieved, 1), "peak": peak,
+                    "unit": "GB/s", "frac": round(achieved / peak, 4), "traffic": None,
+                    "peak_source": peak_src, "avg_launch_ms": round(avg_ms, 4),
+                    "algorithmic_bytes_per_launch": int(abytes), "launches_timed": len(durs),
+                    "kernel_share_of_step": round(sum(durs) / total_ms, 3),
+                    "kernel_ms_per_step": {k: round(v / args.steps, 4) for k, v in all_kernel_ms.items()}}
+
+    # end to end through the public API with host buffers
+    e2e = None
+    if not args.no_e2e:
+        pos32 = np.ascontiguousarray(W.positions, dtype=np.float32)
+        vel32 = np.ascontiguousarray(W.velocities, dtype=np.float32)
+        w2 = fresh_worker()
+        k_e2e = max(2, min(args.steps, 4))
+        for it in range(1 + k_e2e):
+            if it == 1:
+                torch.cuda.synchronize()
+                t0 = time.perf_counter()
+            w2.replace_particles(pos32, vel32, W.particle_mass, ids)
+            w2.run_frame()
+            out_pos, out_ids = w2.store.positions_with_ids(dtype=np.float32)
+        torch.cuda.synchronize()
+        dt_e2e = (time.perf_counter() - t0) / k_e2e
+        e2e = {"value": round(n * spf / dt_e2e / 1e6, 2), "unit": UNIT,
+               "h2d_bytes_per_step": int(n * (w2.store.nch * 4 + 8)),
+               "d2h_bytes_per_step": int(out_pos.nbytes + out_ids.nbytes),
+               "ms_per_step": round(dt_e2e * 1e3, 3), "steps": k_e2e,
+               "api": "CudaWorker.replace_particles(host) + run_frame() + store.positions_with_ids()"}
+
+    cpu = None
+    if not args.no_cpu_baseline:
+        cpu = cpu_baseline(W, substeps=2, threads=1)
+
+    line = {
+        "metric": METRIC, "value": round(value, 2), "unit": UNIT, "n_gpus": 1,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(ms_per_step, 4),
+        "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f32",
+        "data": "synthetic",
+        "config": {"workload": W.name, "particles": n, "substeps_per_step": spf,
+                   "step": "one frame", "dx": W.params.dx, "dt": W.params.dt,
+                   "transfer": args.transfer, "material": W.material.kind.name,
+                   "pblocks": int(w.table.count), "groups": int(w.store.n_groups),
+                   "rebuilds_in_timed_region": rebuilds,
+                   "l2_policy": "working set (particles + grid) exceeds L2: "
+                                f"{n * w.store.nch * 4 / 1e6:.0f} MB particle state"},
+        "ms_per_frame": round(ms_per_step, 4),
+        "clocks": clocks, "gpu_launches": launches, "e2e": e2e, "roofline": roofline,
+        "cpu_baseline": cpu,
+    }
+    print(json.dumps(line), flush=True)
+
+
+def cpu_baseline(W, substeps, threads, warm=True):
+    """The CPU oracle (C restatement of the reference, oracle/) timed on the host cores on a
+    bounded sample: the full scene, rebuild + `substeps` substeps."""
+    from oracle import build as obuild
+    obuild.build()
+    from oracle import mpm_oracle as O
+    from paper_2111_00699_b200 import PipelineOptions
+    n = len(W.positions)
+    threads = max(1, int(threads))
+    cl = O.OracleCluster(threads, W.params, W.material, W.boundary, PipelineOptions(),
+                         initial_vmax=float(np.abs(W.velocities).max()), threads=threads > 1)
+    cl.seed(W.positions, W.velocities, W.particle_mass)
+    cl.run_step(0)        # rebuild + first substep: not timed (amortised in the GPU number too)
+    t0 = time.perf_counter()
+    for s in range(1, 1 + substeps):
+        cl.run_step(s)
+    dt = time.perf_counter() - t0
+    return {"value": round(n * substeps / dt / 1e6, 3), "unit": UNIT, "cores": threads,
+            "kind": "port", "sample": f"full scene ({n} particles), {substeps} substeps after the "
+                                      f"rebuild step, {threads} worker thread(s)",
+            "seconds": round(dt, 2)}
+
+
+def run_reference(args):
+    """Reference arm: the reference's own CPU implementation of the path.  The reference is
+    Python + numba (nothing to compile into oracle/_ref and /root/reference does not exist
+    on the GPU box), so this times the pinned C oracle port with one worker per host core."""
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return
+    W = build_world(args.scene)
+    n = len(W.positions)
+    cores = min(os.cpu_count() or 1, 32)
+    from oracle import build as obuild
+    obuild.build()
+    from oracle import mpm_oracle as O
+    from paper_2111_00699_b200 import PipelineOptions
+    cl = O.OracleCluster(cores, W.params, W.material, W.boundary, PipelineOptions(),
+                         initial_vmax=float(np.abs(W.velocities).max()), threads=cores > 1)
+    cl.seed(W.positions, W.velocities, W.particle_mass)
+    S = args.ref_substeps
+    step = 0
+    cl.run_step(step); step += 1                 # rebuild step (untimed)
+    for _ in range(args.warmup):
+        for _ in range(S):
+            cl.run_step(step); step += 1
+    t0 = time.perf_counter()
+    for _ in range(args.steps):
+        for _ in range(S):
+            cl.run_step(step); step += 1
+    dt = time.perf_counter() - t0
+    value = n * S * args.steps / dt / 1e6
+    sample = (f"full scene ({n} particles), {S} substeps per step, {cores} worker threads "
+              f"(one per core), rebuild step excluded")
+    line = {
+        "impl": "reference", "metric": METRIC, "value": round(value, 3), "unit": UNIT,
+        "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": round(dt / args.steps * 1e3, 3), "higher_is_better": True,
+        "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": {"workload": W.name, "particles": n, "substeps_per_step": S,
+                   "step": f"{S} substeps (bounded sample of one frame)"},
+        "cpu_baseline": {"value": round(value, 3), "unit": UNIT, "cores": cores, "kind": "port",
+                         "sample": sample},
+        "e2e": {"value": round(value, 3), "unit": UNIT, "h2d_bytes_per_step": 0,
+                "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+if __name__ == "__main__":
+    a = parse_args()
+    if a.impl == "reference":
+        run_reference(a)
+    else:
+        run_ours(a)

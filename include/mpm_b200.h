@@ -119,6 +119,7 @@ typedef struct mpm_step_status {
 const char *mpm_version(void);
 const char *mpm_last_error(void);       /* text of the last CUDA error seen by this thread */
 int mpm_device_arch(void);              /* 100 for sm_100 */
+unsigned long long mpm_launch_count(void);  /* kernels launched by this library so far (process-wide) */
 
 /* ---- rebuild-mapping: Worker._rebuild (pipeline.py:958-1015) ------------------------ */
 

@@ -94,8 +94,10 @@ _SIGNATURES = {
     "mpm_version": [],
     "mpm_last_error": [],
     "mpm_device_arch": [],
+    "mpm_launch_count": [],
 }
-_RESTYPES = {"mpm_version": C.c_char_p, "mpm_last_error": C.c_char_p}
+_RESTYPES = {"mpm_version": C.c_char_p, "mpm_last_error": C.c_char_p,
+             "mpm_launch_count": C.c_ulonglong}
 
 EXPORTED_SYMBOLS = tuple(_SIGNATURES)
 

@@ -1,4 +1,5 @@
 // Library-level entry points and CUDA error plumbing of libmpm_b200.so.
+#include <atomic>
 #include <stdio.h>
 #include <string.h>
 
@@ -16,8 +17,11 @@ void set_last_error(const char *what, cudaError_t e)
 
 // Launch-time errors only (bad configuration, no device, no kernel image): the call stays
 // asynchronous.  Execution errors surface at the host's next synchronisation.
-int check_launch(const char *what)
+static std::atomic<unsigned long long> g_launches{0};
+
+int check_launch(const char *what, int n_kernels)
 {
+    g_launches.fetch_add((unsigned long long)n_kernels, std::memory_order_relaxed);
     cudaError_t e = cudaGetLastError();
     if (e == cudaSuccess) return MPM_OK;
     set_last_error(what, e);
@@ -31,6 +35,8 @@ extern "C" {
 const char *mpm_version(void) { return "mpm_b200 0.1 (sm_100a)"; }
 
 const char *mpm_last_error(void) { return mpm::g_last_error; }
+
+unsigned long long mpm_launch_count(void) { return mpm::g_launches.load(std::memory_order_relaxed); }
 
 int mpm_device_arch(void)
 {

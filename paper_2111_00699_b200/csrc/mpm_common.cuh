@@ -25,7 +25,7 @@ namespace mpm {
 
 // ---- error plumbing ---------------------------------------------------------------
 void set_last_error(const char *what, cudaError_t e);
-int check_launch(const char *what);
+int check_launch(const char *what, int n_kernels);   // also counts the kernels just launched
 
 // ---- Morton coding (grid.py:41-70), 21 bits per axis, x lowest ---------------------
 __host__ __device__ __forceinline__ unsigned long long part1by2(unsigned long long x)

@@ -124,9 +124,11 @@ __global__ void __launch_bounds__(256) particle_aggregates_kernel(const float *_
     if (g < n_groups && lane < group_len[g]) {
         const float *gd = data + (size_t)g * nch * 32 + lane;
         m = gd[CH_MASS * 32];
-        const double vx = gd[(CH_VEL + 0) * 32], vy = gd[(CH_VEL + 1) * 32], vz = gd[(CH_VEL + 2) * 32];
-        mx = m * vx; my = m * vy; mz = m * vz;
-        ke = 0.5 * m * (vx * vx + vy * vy + vz * vz);
+        if (m > 0.0) {   // quarantined lanes carry mass 0 and possibly non-finite velocities
+            const double vx = gd[(CH_VEL + 0) * 32], vy = gd[(CH_VEL + 1) * 32], vz = gd[(CH_VEL + 2) * 32];
+            mx = m * vx; my = m * vy; mz = m * vz;
+            ke = 0.5 * m * (vx * vx + vy * vy + vz * vz);
+        }
     }
     m = warp_sum(m); mx = warp_sum(mx); my = warp_sum(my); mz = warp_sum(mz); ke = warp_sum(ke);
     if (lane == 0 && g < n_groups) {
@@ -170,13 +172,13 @@ int mpm_clear(float *raw, uint8_t *touched, int32_t count, int full, int32_t *gu
 {
     if (count <= 0) return MPM_OK;
     clear_kernel<<<(count + 3) / 4, 256, 0, (cudaStream_t)stream>>>((float4 *)raw, touched, count, full, guard);
-    return check_launch("mpm_clear");
+    return check_launch("mpm_clear", 1);
 }
 
 int mpm_status_reset(mpm_step_status *status, int32_t *guard, void *stream)
 {
     status_reset_kernel<<<1, 1, 0, (cudaStream_t)stream>>>(status, guard);
-    return check_launch("mpm_status_reset");
+    return check_launch("mpm_status_reset", 1);
 }
 
 int mpm_grid_update(const float *raw, const uint8_t *touched, float *vel, float *vel_old,
@@ -218,7 +220,7 @@ int mpm_grid_update(const float *raw, const uint8_t *touched, float *vel, float 
     a.touched_mut = touched_mut;
     a.guard = guard;
     grid_update_kernel<<<(a.count + 3) / 4, 256, 0, (cudaStream_t)stream>>>(a);
-    return check_launch("mpm_grid_update");
+    return check_launch("mpm_grid_update", 1);
 }
 
 int mpm_particle_aggregates(const mpm_store_view *store, double *out5, void *stream_)
@@ -229,7 +231,7 @@ int mpm_particle_aggregates(const mpm_store_view *store, double *out5, void *str
     if (G > 0)
         particle_aggregates_kernel<<<(int)(((int64_t)G * 32 + 255) / 256), 256, 0, stream>>>(
             store->data, store->nch, store->group_len, G, out5);
-    return check_launch("mpm_particle_aggregates");
+    return check_launch("mpm_particle_aggregates", 1);
 }
 
 int mpm_grid_aggregates(const float *raw, const uint8_t *touched, int32_t count, double *out4,
@@ -239,7 +241,7 @@ int mpm_grid_aggregates(const float *raw, const uint8_t *touched, int32_t count,
     cudaMemsetAsync(out4, 0, 4 * sizeof(double), stream);
     if (count > 0)
         grid_aggregates_kernel<<<(count + 3) / 4, 256, 0, stream>>>((const float4 *)raw, touched, count, out4);
-    return check_launch("mpm_grid_aggregates");
+    return check_launch("mpm_grid_aggregates", 1);
 }
 
 }  // extern "C"

@@ -542,14 +542,14 @@ int mpm_compact_live(const mpm_store_view *store, int drop_quarantined, int32_t 
     const int G = store->n_groups;
     if (G <= 0) {
         cudaMemsetAsync(n_live, 0, sizeof(int32_t), stream);
-        return check_launch("mpm_compact_live");
+        return check_launch("mpm_compact_live", 5);
     }
     live_count_kernel<<<nblk((int64_t)G * 32, 256), 256, 0, stream>>>(
         store->lane_meta, store->group_len, G, drop_quarantined, group_live_scratch);
     exclusive_scan_i32(group_live_scratch, group_live_scratch, G, scan_scratch, n_live, stream);
     live_write_kernel<<<nblk((int64_t)G * 32, 256), 256, 0, stream>>>(
         store->lane_meta, store->group_len, G, drop_quarantined, group_live_scratch, src_slot);
-    return check_launch("mpm_compact_live");
+    return check_launch("mpm_compact_live", 5);
 }
 
 int mpm_particle_codes(const mpm_store_view *store, const int32_t *src_slot, const int32_t *n_live_dev,
@@ -565,7 +565,7 @@ int mpm_particle_codes(const mpm_store_view *store, const int32_t *src_slot, con
         particle_codes_kernel<<<nblk(n_upper, 256), 256, 0, stream>>>(
             store->data, store->nch, src_slot, n_live_dev, staged, n_staged, n_upper, dx,
             (long long *)codes, bad_index);
-    return check_launch("mpm_particle_codes");
+    return check_launch("mpm_particle_codes", 3);
 }
 
 int mpm_hash_insert_blocks(const int64_t *codes, const int32_t *n_dev, int32_t n_upper,
@@ -581,7 +581,7 @@ int mpm_hash_insert_blocks(const int64_t *codes, const int32_t *n_dev, int32_t n
     cudaMemsetAsync(overflow, 0, sizeof(int32_t), stream);
     if (n_upper <= 0) {
         cudaMemsetAsync(n_gblocks, 0, sizeof(int32_t), stream);
-        return check_launch("mpm_hash_insert_blocks");
+        return check_launch("mpm_hash_insert_blocks", 8);
     }
     const int nb = nblk(n_upper, 256);
     block_insert_kernel<<<nb, 256, 0, stream>>>((const long long *)codes, n_dev, n_upper,
@@ -591,7 +591,7 @@ int mpm_hash_insert_blocks(const int64_t *codes, const int32_t *n_dev, int32_t n
     block_assign_kernel<<<nb, 256, 0, stream>>>((const long long *)codes, pslot, hfirst, flag_scratch,
                                                 n_upper, hvals, (long long *)gcodes);
     gidx_kernel<<<nb, 256, 0, stream>>>(pslot, hvals, n_upper, gidx);
-    return check_launch("mpm_hash_insert_blocks");
+    return check_launch("mpm_hash_insert_blocks", 8);
 }
 
 int mpm_dilate_and_link(const int64_t *gcodes, int32_t n_g, int64_t *hkeys, int32_t *hvals,
@@ -606,7 +606,7 @@ int mpm_dilate_and_link(const int64_t *gcodes, int32_t n_g, int64_t *hkeys, int3
     fill_i32_kernel<<<1, 32, 0, stream>>>(bad_block, 1, MPM_INT_MAX);
     if (n_g <= 0) {
         cudaMemsetAsync(count, 0, sizeof(int32_t), stream);
-        return check_launch("mpm_dilate_and_link");
+        return check_launch("mpm_dilate_and_link", 11);
     }
     if (n_g > pblock_cap) return MPM_ERR_RESOURCE;
     const int n_q = n_g * 27;
@@ -628,7 +628,7 @@ int mpm_dilate_and_link(const int64_t *gcodes, int32_t n_g, int64_t *hkeys, int3
     add_scalar_kernel<<<1, 1, 0, stream>>>(count, count, n_g);
     block_origin_kernel<<<nblk(pblock_cap, 256), 256, 0, stream>>>((const long long *)codes, count,
                                                                    pblock_cap, (int4 *)origin);
-    return check_launch("mpm_dilate_and_link");
+    return check_launch("mpm_dilate_and_link", 11);
 }
 
 int mpm_sort_and_group(const int64_t *codes, const int32_t *gidx, const int32_t *n_dev, int32_t n_upper,
@@ -639,7 +639,7 @@ int mpm_sort_and_group(const int64_t *codes, const int32_t *gidx, const int32_t 
     cudaStream_t stream = (cudaStream_t)stream_;
     if (n_g <= 0 || n_upper <= 0) {
         cudaMemsetAsync(n_groups, 0, sizeof(int32_t), stream);
-        return check_launch("mpm_sort_and_group");
+        return check_launch("mpm_sort_and_group", 13);
     }
     const int n_bins = n_g * 64;
     const int nb = nblk(n_upper, 256);
@@ -655,7 +655,7 @@ int mpm_sort_and_group(const int64_t *codes, const int32_t *gidx, const int32_t 
     // n_g+1 entries so that block_group_first[n_g] = n_groups
     cudaMemsetAsync(block_group_first + n_g, 0, sizeof(int32_t), stream);
     exclusive_scan_i32(block_group_first, block_group_first, n_g + 1, scan_scratch, n_groups, stream);
-    return check_launch("mpm_sort_and_group");
+    return check_launch("mpm_sort_and_group", 13);
 }
 
 int mpm_scatter_sorted(const mpm_store_view *old_store, const int32_t *src_slot, const int32_t *n_live_dev,
@@ -673,7 +673,7 @@ int mpm_scatter_sorted(const mpm_store_view *old_store, const int32_t *src_slot,
         staged, (const long long *)staged_ids, perm, bin_start, block_group_first, n_g,
         (const int4 *)table_origin, inv_dx, new_store->data, (long long *)new_store->orig_id,
         new_store->lane_meta, new_store->group_len, new_store->group_block, new_store->group_start, G);
-    return check_launch("mpm_scatter_sorted");
+    return check_launch("mpm_scatter_sorted", 1);
 }
 
 int mpm_gather_state(const mpm_store_view *store, float *flat, int64_t *ids, void *stream_)
@@ -684,7 +684,7 @@ int mpm_gather_state(const mpm_store_view *store, float *flat, int64_t *ids, voi
     gather_state_kernel<<<nblk((int64_t)G * 32, 256), 256, 0, stream>>>(
         store->data, (const long long *)store->orig_id, store->nch, store->group_len,
         store->group_start, G, flat, (long long *)ids);
-    return check_launch("mpm_gather_state");
+    return check_launch("mpm_gather_state", 1);
 }
 
 int mpm_tag_shared(const int64_t *peer_codes, int32_t n_peer_codes, const int64_t *hkeys,
@@ -699,7 +699,7 @@ int mpm_tag_shared(const int64_t *peer_codes, int32_t n_peer_codes, const int64_
         tag_shared_kernel<<<nblk(n_peer_codes, 256), 256, 0, stream>>>(
             (const long long *)peer_codes, n_peer_codes, (const long long *)hkeys, hvals,
             hash_shift_for(hash_cap), hash_cap - 1, peer_map);
-    return check_launch("mpm_tag_shared");
+    return check_launch("mpm_tag_shared", 2);
 }
 
 }  // extern "C"

@@ -438,7 +438,7 @@ int mpm_p2g(const mpm_store_view *store, const mpm_table_view *table, float *raw
     if (rc != MPM_OK) return rc;
     rc = launch_transfer<false, true>(a, params->mat_kind, (cudaStream_t)stream);
     if (rc != MPM_OK) return rc;
-    return check_launch("mpm_p2g");
+    return check_launch("mpm_p2g", 1);
 }
 
 int mpm_g2p(const mpm_store_view *store, const mpm_table_view *table, const float *vel,
@@ -450,7 +450,7 @@ int mpm_g2p(const mpm_store_view *store, const mpm_table_view *table, const floa
     if (rc != MPM_OK) return rc;
     rc = launch_transfer<true, false>(a, params->mat_kind, (cudaStream_t)stream);
     if (rc != MPM_OK) return rc;
-    return check_launch("mpm_g2p");
+    return check_launch("mpm_g2p", 1);
 }
 
 int mpm_g2p2g(const mpm_store_view *store, const mpm_table_view *table, const float *vel,
@@ -462,7 +462,7 @@ int mpm_g2p2g(const mpm_store_view *store, const mpm_table_view *table, const fl
     if (rc != MPM_OK) return rc;
     rc = launch_transfer<true, true>(a, params->mat_kind, (cudaStream_t)stream);
     if (rc != MPM_OK) return rc;
-    return check_launch("mpm_g2p2g");
+    return check_launch("mpm_g2p2g", 1);
 }
 
 }  // extern "C"

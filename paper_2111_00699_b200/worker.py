@@ -150,6 +150,12 @@ class CudaParticleStore:
     def data(self):
         return self._g(self._data).to(torch.float64).cpu().numpy()
 
+    def set_data(self, array):
+        """Upload particle channels given in the reference layout [n_groups, nch, 32] (the
+        reference's tests write into `store.data` in place, e.g. fault injection)."""
+        a = torch.as_tensor(np.ascontiguousarray(array, dtype=np.float32), device=self.device)
+        self._g(self._data).copy_(a)
+
     @property
     def orig_id(self):
         return self._g(self._orig_id).cpu().numpy()
@@ -186,10 +192,18 @@ class CudaParticleStore:
                                                _stream_ptr()), "mpm_gather_state")
         return flat[:n].to(torch.float64).cpu().numpy(), ids[:n].cpu().numpy()
 
-    def positions_with_ids(self):
-        """particles.py:466-475."""
-        flat, ids = self.state_with_ids()
-        return flat[:, CH_POS:CH_POS + 3].copy(), ids
+    def positions_with_ids(self, dtype=np.float64):
+        """particles.py:466-475: positions of every stored particle (quarantined included) and
+        their ids, in (group, lane) order."""
+        n = self.count
+        flat = torch.empty((max(n, 1), self.nch), dtype=torch.float32, device=self.device)
+        ids = torch.empty(max(n, 1), dtype=torch.int64, device=self.device)
+        if n:
+            v = self.view()
+            check(_capi.lib().mpm_gather_state(C.byref(v), flat.data_ptr(), ids.data_ptr(),
+                                               _stream_ptr()), "mpm_gather_state")
+        pos = flat[:n, CH_POS:CH_POS + 3].contiguous().cpu().numpy()
+        return pos.astype(dtype, copy=False), ids[:n].cpu().numpy()
 
     def _aggregates(self):
         out = torch.zeros(5, dtype=torch.float64, device=self.device)
@@ -291,6 +305,12 @@ class CudaGrid:
     def vel(self):
         return self._ref_layout(self._vel)
 
+    def set_vel(self, array):
+        """Upload nodal velocities given in the reference layout [count, 4, 64] (painted-grid
+        tests, tests/test_pipeline.py:28-37 of the reference)."""
+        a = torch.as_tensor(np.ascontiguousarray(array, dtype=np.float32), device=self.device)
+        self._vel.data[:self.count].copy_(a.permute(0, 2, 1))
+
     @property
     def vel_old(self):
         if self._vel_old is None:
@@ -359,6 +379,8 @@ class CudaWorker:
         self._scratch = {}
         self._scratch_allocs = 0
         self.kernel_calls = 0
+        self.time_kernels = False     # bench: CUDA events around the step kernels
+        self.kernel_events = []
         m = material
         self._tp = TransferParams(
             mat_kind=int(m.kind), nch=self.store.nch, mu=float(m.mu), lam=float(m.lam),
@@ -372,8 +394,17 @@ class CudaWorker:
             / (3.0 - math.sin(math.radians(m.friction_angle))))
 
     # -- small helpers ----------------------------------------------------------------
+    _TIMED = ("mpm_p2g", "mpm_g2p", "mpm_g2p2g", "mpm_grid_update", "mpm_clear")
+
     def _call(self, name, *args):
         self.kernel_calls += 1
+        if self.time_kernels and name in self._TIMED:
+            a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            a.record()
+            check(getattr(self.lib, name)(*args), name)
+            b.record()
+            self.kernel_events.append((name, a, b))
+            return
         check(getattr(self.lib, name)(*args), name)
 
     def _scratch_i32(self, tag, n):
@@ -441,6 +472,16 @@ class CudaWorker:
         if n:
             self.flags.rebuild_needed = True
         return n
+
+    def replace_particles(self, positions, velocities, masses, ids):
+        """Drop the current population and stage a new one from host arrays (the end-to-end
+        entry of bench.py: same effect as a fresh worker + seed_particles, buffers reused)."""
+        if self._pending_gather:
+            self._pending_gather = False
+        self.store.n_groups = 0
+        self.store.count = 0
+        self.flags.fused_mode = False
+        return self.seed_particles(positions, velocities, masses, ids)
 
     # -- per frame (pipeline.py:852-880) ------------------------------------------------
     def begin_frame(self):

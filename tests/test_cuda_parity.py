@@ -1,0 +1,188 @@
+"""Parity of the CUDA substep core (through the C ABI) against the pinned CPU oracle and the
+golden arrays dumped from the reference (tests/golden/*.npz).
+
+Bar (north_star): block assignment, sort permutation and lane structure BIT-EXACT; grid
+mass/momentum and particle x/v/F after one substep within the fp32 tolerances written in
+tests/parity_util.py; bounded drift of aggregates over a short run.
+"""
+import numpy as np
+import pytest
+
+import parity_util as U
+from conftest import elastic_setup, fluid_setup, golden
+from oracle import mpm_oracle as O
+
+pytestmark = pytest.mark.gpu
+
+
+def _pair(name, setup, worker_kw=None, **opts):
+    g = golden(name)
+    material, params, boundary = setup
+    pos, vel, mass = g["pos"], g["vel"], float(g["mass"])
+    wc = U.cuda_worker(pos, vel, mass, material, params, boundary, worker_kw=worker_kw, **opts)
+    wo = U.oracle_worker(pos, vel, mass, material, params, boundary, **opts)
+    edge = float(pos.max() - pos.min())
+    ndef = 1 if int(material.kind) == 0 else 9
+    return g, wc, wo, edge, ndef
+
+
+def _assert_particles(sc, so, edge, ndef, run=False, check_c=True):
+    ex, ev, ef, ec = U.particle_errors(sc, so, edge, ndef)
+    assert ex <= (U.X_RTOL_RUN if run else U.X_RTOL), ex
+    assert ev <= (U.V_RTOL_RUN if run else U.V_RTOL), ev
+    assert ef <= (U.F_ATOL_RUN if run else U.F_ATOL), ef
+    if check_c:
+        assert ec <= 1e-3, ec
+
+
+@pytest.mark.parametrize("name,setup", [("elastic.npz", "elastic"), ("fluid.npz", "fluid")])
+def test_one_substep_against_reference_dump(name, setup):
+    g, wc, wo, edge, ndef = _pair(name, elastic_setup() if setup == "elastic" else fluid_setup())
+    wc.run_step(0)
+    wo.run_step(0)
+    # bit-exact: block table, neighbour rows, lane groups, ids, lane keys, touched flags
+    assert U.structure_mismatches(wc, g) == []
+    assert np.array_equal(wc.last_perm.cpu().numpy(), wo.last_perm)
+    assert np.array_equal(wc.last_gidx.cpu().numpy(), wo.last_gidx)
+    # fp32 tolerance: grid mass/momentum before the update, velocities after it
+    for c, e in enumerate(U.grid_errors(wc.grid.raw[0], g["s0_raw0"])):
+        assert e <= U.GRID_RTOL, ("raw0", c, e)
+    for c, e in enumerate(U.grid_errors(wc.grid.vel, g["s0_vel"])):
+        assert e <= U.GRID_RTOL, ("vel", c, e)
+    _assert_particles(U.state_by_id(wc), g["state_1"], edge, ndef)
+    assert np.array_equal(wc.counters, g["s0_counters"])
+
+
+@pytest.mark.parametrize("name,setup", [("elastic.npz", "elastic"), ("fluid.npz", "fluid")])
+def test_short_run_against_reference_dump(name, setup):
+    g, wc, wo, edge, ndef = _pair(name, elastic_setup() if setup == "elastic" else fluid_setup())
+    for s in range(24):
+        wc.run_step(s)
+        if s == 1:
+            _assert_particles(U.state_by_id(wc), g["state_2"], edge, ndef)
+    _assert_particles(U.state_by_id(wc), g["state_24"], edge, ndef, run=True)
+    assert wc.rebuild_steps == list(g["rebuild_steps"])
+    c = wc.counters
+    assert c[O.C_ADDRESS_ERR] == 0 and c[O.C_QUARANTINE] == 0
+
+
+def test_fused_g2p2g_against_reference_dump():
+    g, wc, wo, edge, ndef = _pair("fused.npz", elastic_setup(), transfer="g2p2g")
+    for s in range(24):
+        wc.run_step(s)
+    assert wc._pending_gather
+    # the fused kernel keeps C in registers: x/v/F are current, C is refreshed by the flush
+    _assert_particles(U.state_by_id(wc), g["state_24"], edge, ndef, run=True, check_c=False)
+    wc._flush_gather()
+    _assert_particles(U.state_by_id(wc), g["state_final_flushed"], edge, ndef, run=True)
+    assert wc.rebuild_steps == list(g["rebuild_steps"])
+
+
+def test_fused_equals_split_within_tolerance():
+    # reference: fused == split bitwise in deterministic mode (tests/test_pipeline.py:255-258);
+    # with float atomics the two orders agree to rounding
+    g, wa, _, edge, ndef = _pair("elastic.npz", elastic_setup(), transfer="split")
+    _, wb, _, _, _ = _pair("elastic.npz", elastic_setup(), transfer="g2p2g")
+    for s in range(12):
+        wa.run_step(s)
+        wb.run_step(s)
+    wb._flush_gather()
+    _assert_particles(U.state_by_id(wb), U.state_by_id(wa), edge, ndef, run=True)
+
+
+def test_flip_blend_against_reference_dump():
+    g, wc, wo, edge, ndef = _pair("flip.npz", elastic_setup(flip_blend=0.8))
+    for s in range(6):
+        wc.run_step(s)
+    _assert_particles(U.state_by_id(wc), g["state_6"], edge, ndef, run=True)
+
+
+def test_fuse_clear_matches_separate_clear():
+    g, wa, _, edge, ndef = _pair("elastic.npz", elastic_setup())
+    _, wb, _, _, _ = _pair("elastic.npz", elastic_setup(), worker_kw=dict(fuse_clear=True))
+    for s in range(24):
+        wa.run_step(s)
+        wb.run_step(s)
+    _assert_particles(U.state_by_id(wb), U.state_by_id(wa), edge, ndef, run=True)
+    assert wa.rebuild_steps == wb.rebuild_steps
+
+
+def test_two_logical_workers_against_reference_dump():
+    """Cross-worker halo reduction inside the grid-update kernel (pipeline.py:1172-1188)."""
+    from paper_2111_00699_b200 import CudaCluster, PipelineOptions
+    g = golden("two_worker.npz")
+    material, params, boundary = elastic_setup()
+    cl = CudaCluster(2, params, material, boundary, PipelineOptions(),
+                     initial_vmax=float(np.linalg.norm(g["vel"], axis=1).max()))
+    cl.seed(g["pos"], g["vel"], float(g["mass"]))
+    cl.run_step(0)
+    for w in cl.workers:
+        assert U.structure_mismatches(w, g, f"w{w.wid}_s0_") == []
+        q = 1 - w.wid
+        got = w._peer_map[q].data[:w.table.count].cpu().numpy()
+        assert np.array_equal(got, g[f"w{w.wid}_peer_map{q}"])
+        for c, e in enumerate(U.grid_errors(w.grid.raw[0], g[f"w{w.wid}_s0_raw0"])):
+            assert e <= U.GRID_RTOL, ("raw0", w.wid, c, e)
+        for c, e in enumerate(U.grid_errors(w.grid.vel, g[f"w{w.wid}_s0_vel"])):
+            assert e <= U.GRID_RTOL, ("vel", w.wid, c, e)
+    edge = float(g["pos"].max() - g["pos"].min())
+    _assert_particles(cl.state_sorted_by_id(), g["state_1"], edge, 9)
+    for s in range(1, 24):
+        cl.run_step(s)
+    _assert_particles(cl.state_sorted_by_id(), g["state_24"], edge, 9, run=True)
+    assert cl.workers[0].rebuild_steps == list(g["rebuild_steps0"])
+    assert cl.workers[1].rebuild_steps == list(g["rebuild_steps1"])
+    assert cl.runtime.generations == 24      # one barrier per step (tests/test_pipeline.py:425-430)
+
+
+def test_worker_count_invariance():
+    """1, 2 and 3 logical workers give the same particles (reference: bit-identical in
+    deterministic mode, <= 1e-5 * domain with atomics, tests/test_multiworker.py:223-233)."""
+    from paper_2111_00699_b200 import CudaCluster, PipelineOptions
+    g = golden("two_worker.npz")
+    material, params, boundary = elastic_setup()
+    states = []
+    for n in (1, 2, 3):
+        cl = CudaCluster(n, params, material, boundary, PipelineOptions())
+        cl.seed(g["pos"], g["vel"], float(g["mass"]))
+        for s in range(10):
+            cl.run_step(s)
+        states.append(cl.state_sorted_by_id())
+    edge = float(g["pos"].max() - g["pos"].min())
+    for s in states[1:]:
+        _assert_particles(s, states[0], edge, 9, run=True)
+
+
+def test_cfl_schedule_against_reference_dump():
+    g = golden("cfl.npz")
+    material, params, boundary = fluid_setup(frame_dt=float(g["frame_dt"]), cfl=0.5)
+    wc = U.cuda_worker(g["pos"], g["vel"], float(g["mass"]), material, params, boundary)
+    wc.cfl_mode = True
+    dts = []
+    orig = wc.run_step
+
+    def spy(step):
+        dts.append(wc.dt)
+        orig(step)
+    wc.run_step = spy
+    wc.run_frame()
+    wc.run_frame()
+    assert len(dts) == len(g["dts"])
+    assert np.allclose(np.array(dts), g["dts"], rtol=1e-5, atol=0)
+    edge = float(g["pos"].max() - g["pos"].min())
+    _assert_particles(U.state_by_id(wc), g["state"], edge, 1, run=True)
+
+
+def test_aggregate_drift_over_a_frame():
+    """Total mass, momentum and kinetic energy track the oracle over one 36-step frame."""
+    g, wc, wo, edge, ndef = _pair("elastic.npz", elastic_setup())
+    m0 = wc  # noqa
+    wc.run_frame()
+    wo.run_frame()
+    assert wc.store.total_mass() == pytest.approx(wo.store.total_mass(), rel=1e-7)
+    pc, po = wc.store.total_momentum(), wo.store.total_momentum()
+    assert np.abs(pc - po).max() <= U.AGG_RTOL * np.abs(po).max()
+    so = U.state_by_id(wo)
+    ke_o = 0.5 * (so[:, 15] * (so[:, 3:6] ** 2).sum(axis=1)).sum()
+    assert wc.store.kinetic_energy() == pytest.approx(ke_o, rel=U.AGG_RTOL)
+    assert wc.rebuild_steps == wo.rebuild_steps
