@@ -109,37 +109,82 @@ __device__ __forceinline__ void svd3(const float *f, float *u, float *s, float *
     s[0] = s0; s[1] = s1; s[2] = s2;
 }
 
-// Fixed-corotated Kirchhoff stress (domain.py:383-441).  Returns 1 when the singular
-// values were floored (J <= 1e-10), as the reference's clamp flag.
-__device__ __forceinline__ int corotated_tau(const float *f, float mu, float lam, float *t)
+// Rotation factor R of the polar decomposition F = R S by Newton's iteration
+// R <- (R + R^-T) / 2 (Higham 1986), R^-T = cof(R) / det(R).  Quadratic convergence; after the
+// first update every singular value is >= 1, so det(R) - 1 bounds the distance to
+// orthogonality and one more update after det - 1 < 1e-3 reaches fp32 resolution.
+// Returns false when F is too close to singular / inverted for the iteration (the caller
+// then takes the reference's SVD route, which also handles reflections and the clamp).
+__device__ __forceinline__ bool polar_rotation(const float *f, float J, float *r)
 {
-    float J = det3(f);
-    float u[9], s[3], v[9];
-    svd3(f, u, s, v);
-    int clamped = 0;
-    float w[9];
-    if (J <= 1e-10f) {
+    if (!(J > 0.02f)) return false;
 #pragma unroll
-        for (int k = 0; k < 3; ++k) if (s[k] < 1e-4f) s[k] = 1e-4f;
-        J = s[0] * s[1] * s[2];
-        clamped = 1;
+    for (int k = 0; k < 9; ++k) r[k] = f[k];
+    float det = J;
+    for (int it = 0; it < 14; ++it) {
+        const float c00 = r[4] * r[8] - r[5] * r[7], c01 = r[5] * r[6] - r[3] * r[8], c02 = r[3] * r[7] - r[4] * r[6];
+        const float c10 = r[2] * r[7] - r[1] * r[8], c11 = r[0] * r[8] - r[2] * r[6], c12 = r[1] * r[6] - r[0] * r[7];
+        const float c20 = r[1] * r[5] - r[2] * r[4], c21 = r[2] * r[3] - r[0] * r[5], c22 = r[0] * r[4] - r[1] * r[3];
+        if (it > 0) det = r[0] * c00 + r[1] * c01 + r[2] * c02;
+        const bool last = it > 0 && det - 1.0f < 1e-3f;
+        const float h = __fdividef(0.5f, det);
+        r[0] = 0.5f * r[0] + h * c00; r[1] = 0.5f * r[1] + h * c01; r[2] = 0.5f * r[2] + h * c02;
+        r[3] = 0.5f * r[3] + h * c10; r[4] = 0.5f * r[4] + h * c11; r[5] = 0.5f * r[5] + h * c12;
+        r[6] = 0.5f * r[6] + h * c20; r[7] = 0.5f * r[7] + h * c21; r[8] = 0.5f * r[8] + h * c22;
+        if (last) return true;
+    }
+    return false;
+}
+
+// Fixed-corotated Kirchhoff stress (domain.py:383-441): tau = 2 mu (F - R) F^T + lam (J-1) J I.
+// Regular states use the Newton polar factor; near-singular or inverted F takes the
+// reference's route (Jacobi SVD, reflection handling, singular values floored at 1e-4 when
+// J <= 1e-10).  Returns 1 when the floor was applied, as the reference's clamp flag.
+// the rare route is kept out of line so that its registers do not weigh on the hot path
+__device__ __noinline__ int corotated_parts_svd(const float *f, float *w, float *dm, float *Jout)
+{
+    float J = *Jout;
+    int clamped = 0;
+    {
+        float u[9], s[3], v[9];
+        svd3(f, u, s, v);
+        if (J <= 1e-10f) {
+#pragma unroll
+            for (int k = 0; k < 3; ++k) if (s[k] < 1e-4f) s[k] = 1e-4f;
+            J = s[0] * s[1] * s[2];
+            clamped = 1;
+#pragma unroll
+            for (int a = 0; a < 3; ++a)
+#pragma unroll
+                for (int b = 0; b < 3; ++b)
+                    w[3 * a + b] = s[0] * u[3 * a] * v[3 * b] + s[1] * u[3 * a + 1] * v[3 * b + 1] +
+                                   s[2] * u[3 * a + 2] * v[3 * b + 2];
+        } else {
+#pragma unroll
+            for (int k = 0; k < 9; ++k) w[k] = f[k];   // U S V^T == F: skip the lossy reconstruction
+        }
 #pragma unroll
         for (int a = 0; a < 3; ++a)
 #pragma unroll
             for (int b = 0; b < 3; ++b)
-                w[3 * a + b] = s[0] * u[3 * a] * v[3 * b] + s[1] * u[3 * a + 1] * v[3 * b + 1] +
-                               s[2] * u[3 * a + 2] * v[3 * b + 2];
-    } else {
-#pragma unroll
-        for (int k = 0; k < 9; ++k) w[k] = f[k];   // U S V^T == F: skip the lossy reconstruction
+                dm[3 * a + b] = w[3 * a + b] - (u[3 * a] * v[3 * b] + u[3 * a + 1] * v[3 * b + 1] +
+                                                u[3 * a + 2] * v[3 * b + 2]);
     }
-    float dm[9];
+    *Jout = J;
+    return clamped;
+}
+
+__device__ __forceinline__ int corotated_tau(const float *f, float mu, float lam, float *t)
+{
+    float J = det3(f);
+    int clamped = 0;
+    float w[9], dm[9];
+    if (polar_rotation(f, J, dm)) {
 #pragma unroll
-    for (int a = 0; a < 3; ++a)
-#pragma unroll
-        for (int b = 0; b < 3; ++b)
-            dm[3 * a + b] = w[3 * a + b] - (u[3 * a] * v[3 * b] + u[3 * a + 1] * v[3 * b + 1] +
-                                            u[3 * a + 2] * v[3 * b + 2]);
+        for (int k = 0; k < 9; ++k) { w[k] = f[k]; dm[k] = f[k] - dm[k]; }
+    } else {
+        clamped = corotated_parts_svd(f, w, dm, &J);
+    }
     const float two_mu = 2.0f * mu;
     const float diag = lam * (J - 1.0f) * J;
 #pragma unroll
