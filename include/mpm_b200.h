@@ -185,48 +185,57 @@ int mpm_scatter_sorted(const mpm_store_view *old_store, const int32_t *src_slot,
 
 /* ---- substep: Worker.run_step (pipeline.py:905-940) ---------------------------------
  *
- * Every substep entry point takes `guard`: NULL, or a device int32.  A kernel launched with a
- * non-NULL guard returns without touching memory when *guard != 0, and the gather kernels
- * set *guard = 1 together with status->zone_violation.  This lets the host enqueue step s+1
- * before it has read step s's rebuild flag: if step s asked for a rebuild, step s+1's
- * kernels are no-ops and the host re-issues the step after rebuilding (and clearing the
- * guard).  Results are identical to the reference's "check flag, then step" order. */
+ * Every substep entry point takes `guard`: NULL, or a host struct naming a device int32 and
+ * the step being enqueued.  The device word holds the first step whose gather found a
+ * particle outside its free zone (INT32_MAX while none; the gather kernels atomicMin their
+ * step into it together with status->zone_violation).  A kernel of step s returns without
+ * touching memory when the word is < s.  This lets the host enqueue step s+1 before it has
+ * read step s's rebuild flag: if step s asked for a rebuild, step s+1's kernels are no-ops
+ * and the host re-issues the step after rebuilding (and resetting the word).  Results are
+ * identical to the reference's "check flag, then step" order (pipeline.py:911-915). */
+typedef struct mpm_guard {
+    int32_t *first_bad_step;     /* device */
+    int32_t step;
+} mpm_guard;
 
 /* Worker._clear (pipeline.py:1022-1037): zero the rows of raw flagged in touched and reset
  * the flags; full=1 clears every row (first use of a parity after a rebuild). */
-int mpm_clear(float *raw, uint8_t *touched, int32_t count, int full, int32_t *guard, void *stream);
+int mpm_clear(float *raw, uint8_t *touched, int32_t count, int full, const mpm_guard *guard, void *stream);
 
 /* _p2g_kernel (pipeline.py:316-356): scatter_prep + subgroup scatter of every group into
  * raw (float4 nodes), touched flags set for every addressed block. */
 int mpm_p2g(const mpm_store_view *store, const mpm_table_view *table, float *raw, uint8_t *touched,
-            const mpm_transfer_params *params, mpm_step_status *status, int32_t *guard, void *stream);
+            const mpm_transfer_params *params, mpm_step_status *status, const mpm_guard *guard, void *stream);
 
 /* _reduce_and_update + _grid_finalize (pipeline.py:1166-1231, 660-722): for every block
  * flagged in touched: vel = raw (+ peer raw rows through peer_map where the peer touched
  * the block) ; zero-mass nodes -> 0 ; v = mom/m ; vel_old saved before gravity when
  * vel_old != NULL ; v += dt*g ; box boundary (inclusive comparisons on node world
- * position).  n_peers may be 0.  peer_map[p][b] = peer p's index of local block b or -1. */
+ * position).  n_peers may be 0.  peer_map[p][b] = peer p's index of local block b or -1.
+ * reset_status (may be NULL): status block whose zone flag / max speed are zeroed by this
+ * kernel for the gather that follows it in stream order. */
 int mpm_grid_update(const float *raw, const uint8_t *touched, float *vel, float *vel_old,
                     const mpm_table_view *table, int32_t n_peers, const float *const *peer_raw,
                     const uint8_t *const *peer_touched, const int32_t *const *peer_map,
                     double dt, const double gravity[3], int apply_bc, int bc_sticky,
                     const double box_lo[3], const double box_hi[3], double dx, int fuse_clear,
-                    float *raw_mut, uint8_t *touched_mut, int32_t *guard, void *stream);
+                    float *raw_mut, uint8_t *touched_mut, mpm_step_status *reset_status,
+                    const mpm_guard *guard, void *stream);
 
 /* _gather_advect (pipeline.py:400-600). */
 int mpm_g2p(const mpm_store_view *store, const mpm_table_view *table, const float *vel,
             const float *vel_old, const mpm_transfer_params *params, mpm_step_status *status,
-            int32_t *guard, void *stream);
+            const mpm_guard *guard, void *stream);
 
 /* _g2p2g_kernel (pipeline.py:604-653): previous step's gather (dt_gather) fused with this
  * step's scatter (dt). */
 int mpm_g2p2g(const mpm_store_view *store, const mpm_table_view *table, const float *vel,
               const float *vel_old, float *raw, uint8_t *touched, const mpm_transfer_params *params,
-              mpm_step_status *status, int32_t *guard, void *stream);
+              mpm_step_status *status, const mpm_guard *guard, void *stream);
 
 /* Reset zone_violation and vmax2_bits of a status block before a gather (the reference
  * passes a fresh out_stats = zeros(2) per call, pipeline.py:1090). */
-int mpm_status_reset(mpm_step_status *status, int32_t *guard, void *stream);
+int mpm_status_reset(mpm_step_status *status, const mpm_guard *guard, void *stream);
 
 /* ---- readback / aggregates ---------------------------------------------------------- */
 

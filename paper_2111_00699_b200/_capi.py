@@ -49,6 +49,10 @@ class TableView(C.Structure):
     ]
 
 
+class Guard(C.Structure):
+    _fields_ = [("first_bad_step", p_void), ("step", i32)]
+
+
 class StepStatus(C.Structure):
     _fields_ = [("zone_violation", i32), ("vmax2_bits", C.c_uint32),
                 ("counters", C.c_ulonglong * N_COUNTERS)]
@@ -75,18 +79,18 @@ _SIGNATURES = {
                            p_void, p_void, p_void],
     "mpm_scatter_sorted": [C.POINTER(StoreView), p_void, p_void, p_void, p_void, p_void, p_void,
                            p_void, i32, p_void, f64, C.POINTER(StoreView), p_void],
-    "mpm_clear": [p_void, p_void, i32, i32, p_void, p_void],
-    "mpm_status_reset": [p_void, p_void, p_void],
+    "mpm_clear": [p_void, p_void, i32, i32, C.POINTER(Guard), p_void],
+    "mpm_status_reset": [p_void, C.POINTER(Guard), p_void],
     "mpm_p2g": [C.POINTER(StoreView), C.POINTER(TableView), p_void, p_void,
-                C.POINTER(TransferParams), p_void, p_void, p_void],
+                C.POINTER(TransferParams), p_void, C.POINTER(Guard), p_void],
     "mpm_grid_update": [p_void, p_void, p_void, p_void, C.POINTER(TableView), i32,
                         C.POINTER(p_void), C.POINTER(p_void), C.POINTER(p_void), f64,
                         C.POINTER(f64), i32, i32, C.POINTER(f64), C.POINTER(f64), f64, i32,
-                        p_void, p_void, p_void, p_void],
+                        p_void, p_void, p_void, C.POINTER(Guard), p_void],
     "mpm_g2p": [C.POINTER(StoreView), C.POINTER(TableView), p_void, p_void,
-                C.POINTER(TransferParams), p_void, p_void, p_void],
+                C.POINTER(TransferParams), p_void, C.POINTER(Guard), p_void],
     "mpm_g2p2g": [C.POINTER(StoreView), C.POINTER(TableView), p_void, p_void, p_void, p_void,
-                  C.POINTER(TransferParams), p_void, p_void, p_void],
+                  C.POINTER(TransferParams), p_void, C.POINTER(Guard), p_void],
     "mpm_gather_state": [C.POINTER(StoreView), p_void, p_void, p_void],
     "mpm_particle_aggregates": [C.POINTER(StoreView), p_void, p_void],
     "mpm_grid_aggregates": [p_void, p_void, i32, p_void, p_void],

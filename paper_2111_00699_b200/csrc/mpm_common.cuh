@@ -75,12 +75,25 @@ __device__ __forceinline__ int node_slot(int cx, int cy, int cz)
            ((cz & 2) << 4);
 }
 
-// Guard word of speculative launches: a step kernel launched with a non-null guard returns
-// without touching memory when *guard != 0 (set by the gather that found a particle outside
-// its free zone), so the host may enqueue step s+1 before it has read step s's flag.
-__device__ __forceinline__ bool guarded_out(const int *guard)
+// Guard of speculative launches (mpm_guard in the header): the device word holds the first
+// step whose gather found a particle outside its free zone (INT_MAX while none).  A kernel
+// of step s returns without touching memory when that word is < s, so the host may enqueue
+// step s+1 before it has read step s's flag; the kernel that raises the flag (step s itself)
+// and the rest of step s still run to completion.
+struct DevGuard {
+    int *word;
+    int step;
+};
+__device__ __forceinline__ bool guarded_out(const DevGuard &g)
 {
-    return guard != nullptr && *((volatile const int *)guard) != 0;
+    return g.word != nullptr && *((volatile const int *)g.word) < g.step;
+}
+inline DevGuard make_guard(const mpm_guard *g)
+{
+    DevGuard d;
+    d.word = g ? g->first_bad_step : nullptr;
+    d.step = g ? g->step : 0;
+    return d;
 }
 
 // exclusive scan of int32 (three kernels, no library): out may alias in; total (device) optional

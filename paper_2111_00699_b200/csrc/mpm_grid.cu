@@ -23,7 +23,7 @@ struct PeerSet {
 };
 
 __global__ void __launch_bounds__(256) clear_kernel(float4 *raw, uint8_t *touched, int count, int full,
-                                                    const int *guard)
+                                                    const DevGuard guard)
 {
     if (guarded_out(guard)) return;
     const int b = blockIdx.x * 4 + (threadIdx.x >> 6);
@@ -52,12 +52,18 @@ struct GridArgs {
     int fuse_clear;
     float4 *raw_mut;
     uint8_t *touched_mut;
-    const int *guard;
+    DevGuard guard;
+    mpm_step_status *reset_status;
 };
 
 __global__ void __launch_bounds__(256) grid_update_kernel(const GridArgs a)
 {
     if (guarded_out(a.guard)) return;
+    if (a.reset_status && blockIdx.x == 0 && threadIdx.x == 0) {
+        // fresh out_stats for the gather that follows this update in stream order
+        a.reset_status->zone_violation = 0;
+        a.reset_status->vmax2_bits = 0;
+    }
     const int b = blockIdx.x * 4 + (threadIdx.x >> 6);
     const int slot = threadIdx.x & 63;
     const bool hit = b < a.count && a.touched[b];
@@ -155,7 +161,7 @@ __global__ void __launch_bounds__(256) grid_aggregates_kernel(const float4 *__re
     }
 }
 
-__global__ void status_reset_kernel(mpm_step_status *status, const int *guard)
+__global__ void status_reset_kernel(mpm_step_status *status, const DevGuard guard)
 {
     if (guarded_out(guard)) return;
     status->zone_violation = 0;
@@ -168,16 +174,16 @@ using namespace mpm;
 
 extern "C" {
 
-int mpm_clear(float *raw, uint8_t *touched, int32_t count, int full, int32_t *guard, void *stream)
+int mpm_clear(float *raw, uint8_t *touched, int32_t count, int full, const mpm_guard *guard, void *stream)
 {
     if (count <= 0) return MPM_OK;
-    clear_kernel<<<(count + 3) / 4, 256, 0, (cudaStream_t)stream>>>((float4 *)raw, touched, count, full, guard);
+    clear_kernel<<<(count + 3) / 4, 256, 0, (cudaStream_t)stream>>>((float4 *)raw, touched, count, full, make_guard(guard));
     return check_launch("mpm_clear", 1);
 }
 
-int mpm_status_reset(mpm_step_status *status, int32_t *guard, void *stream)
+int mpm_status_reset(mpm_step_status *status, const mpm_guard *guard, void *stream)
 {
-    status_reset_kernel<<<1, 1, 0, (cudaStream_t)stream>>>(status, guard);
+    status_reset_kernel<<<1, 1, 0, (cudaStream_t)stream>>>(status, make_guard(guard));
     return check_launch("mpm_status_reset", 1);
 }
 
@@ -186,7 +192,8 @@ int mpm_grid_update(const float *raw, const uint8_t *touched, float *vel, float 
                     const uint8_t *const *peer_touched, const int32_t *const *peer_map,
                     double dt, const double gravity[3], int apply_bc, int bc_sticky,
                     const double box_lo[3], const double box_hi[3], double dx, int fuse_clear,
-                    float *raw_mut, uint8_t *touched_mut, int32_t *guard, void *stream)
+                    float *raw_mut, uint8_t *touched_mut, mpm_step_status *reset_status,
+                    const mpm_guard *guard, void *stream)
 {
     if (!table || !gravity) return MPM_ERR_REJECTED_INPUT;
     if (n_peers < 0 || n_peers > MPM_MAX_PEERS) return MPM_ERR_CONFIG;
@@ -218,7 +225,8 @@ int mpm_grid_update(const float *raw, const uint8_t *touched, float *vel, float 
     a.fuse_clear = fuse_clear;
     a.raw_mut = (float4 *)raw_mut;
     a.touched_mut = touched_mut;
-    a.guard = guard;
+    a.guard = make_guard(guard);
+    a.reset_status = reset_status;
     grid_update_kernel<<<(a.count + 3) / 4, 256, 0, (cudaStream_t)stream>>>(a);
     return check_launch("mpm_grid_update", 1);
 }

@@ -34,7 +34,7 @@ struct TransferArgs {
     float margin_lo, margin_hi;
     float theta_c, theta_s, hardening, sand_alpha;
     int clamp_tension, count_stats;
-    int *guard;
+    DevGuard guard;
 };
 
 constexpr int TW = 8;   // warps (groups) per CTA
@@ -302,7 +302,7 @@ __global__ void __launch_bounds__(TW * 32, 3) transfer_kernel(const TransferArgs
                         const float zz1 = ((float)(org.z - MPM_CELL_BIAS) + 4.0f + a.margin_hi) * a.dx;
                         if (px < zx0 || px >= zx1 || py < zy0 || py >= zy1 || pz < zz0 || pz >= zz1) {
                             a.status->zone_violation = 1;
-                            if (a.guard) *a.guard = 1;
+                            if (a.guard.word) atomicMin(a.guard.word, a.guard.step);
                         }
                         vmax_bits = __float_as_uint(vx * vx + vy * vy + vz * vz);
                         // lane key refresh (pipeline.py:585-599)
@@ -466,7 +466,7 @@ __global__ void __launch_bounds__(TW * 32, 3) transfer_kernel(const TransferArgs
 
 static int fill_args(TransferArgs &a, const mpm_store_view *store, const mpm_table_view *table,
                      const float *vel, const float *vel_old, float *raw, uint8_t *touched,
-                     const mpm_transfer_params *p, mpm_step_status *status, int32_t *guard)
+                     const mpm_transfer_params *p, mpm_step_status *status, const mpm_guard *guard)
 {
     if (!store || !table || !p || !status) return MPM_ERR_REJECTED_INPUT;
     if (!(p->dx > 0.0) || !(p->density > 0.0)) return MPM_ERR_REJECTED_INPUT;
@@ -498,7 +498,7 @@ static int fill_args(TransferArgs &a, const mpm_store_view *store, const mpm_tab
     a.hardening = (float)p->hardening; a.sand_alpha = (float)p->sand_alpha;
     a.clamp_tension = p->clamp_tension;
     a.count_stats = p->count_stats;
-    a.guard = guard;
+    a.guard = make_guard(guard);
     if (a.flip > 0.0f && !vel_old) return MPM_ERR_REJECTED_INPUT;
     return MPM_OK;
 }
@@ -528,7 +528,7 @@ using namespace mpm;
 extern "C" {
 
 int mpm_p2g(const mpm_store_view *store, const mpm_table_view *table, float *raw, uint8_t *touched,
-            const mpm_transfer_params *params, mpm_step_status *status, int32_t *guard, void *stream)
+            const mpm_transfer_params *params, mpm_step_status *status, const mpm_guard *guard, void *stream)
 {
     TransferArgs a;
     int rc = fill_args(a, store, table, nullptr, nullptr, raw, touched, params, status, guard);
@@ -546,7 +546,7 @@ int mpm_p2g(const mpm_store_view *store, const mpm_table_view *table, float *raw
 
 int mpm_g2p(const mpm_store_view *store, const mpm_table_view *table, const float *vel,
             const float *vel_old, const mpm_transfer_params *params, mpm_step_status *status,
-            int32_t *guard, void *stream)
+            const mpm_guard *guard, void *stream)
 {
     TransferArgs a;
     int rc = fill_args(a, store, table, vel, vel_old, nullptr, nullptr, params, status, guard);
@@ -558,7 +558,7 @@ int mpm_g2p(const mpm_store_view *store, const mpm_table_view *table, const floa
 
 int mpm_g2p2g(const mpm_store_view *store, const mpm_table_view *table, const float *vel,
               const float *vel_old, float *raw, uint8_t *touched, const mpm_transfer_params *params,
-              mpm_step_status *status, int32_t *guard, void *stream)
+              mpm_step_status *status, const mpm_guard *guard, void *stream)
 {
     TransferArgs a;
     int rc = fill_args(a, store, table, vel, vel_old, raw, touched, params, status, guard);

@@ -34,6 +34,7 @@ CH_POS, CH_VEL, CH_C, CH_MASS, CH_DEF, CH_PLASTIC = 0, 3, 6, 15, 16, 25
 LW = 32
 _INT_MAX = 0x7FFFFFFF
 _PHASES = ("rebuild", "sort", "p2g", "grid", "g2p")
+_RING = 4
 
 
 def channels_for(kind: int) -> int:
@@ -352,8 +353,15 @@ class CudaWorker:
             self.table = CudaBlockTable(self.device)
             self.grid = CudaGrid(self.device)
             self.store._table = self.table
-            self._status = torch.zeros(_capi.STATUS_BYTES // 8, dtype=torch.int64, device=self.device)
-            self._status_host = torch.zeros(_capi.STATUS_BYTES // 8, dtype=torch.int64).pin_memory()
+            # status ring: one block per in-flight step (zone flag, max speed^2, counters); the
+            # counters of a slot accumulate over every step that used it
+            self._status = torch.zeros((_RING, _capi.STATUS_BYTES // 8), dtype=torch.int64,
+                                       device=self.device)
+            self._status_host = torch.zeros((_RING, _capi.STATUS_BYTES // 8),
+                                            dtype=torch.int64).pin_memory()
+            self._status_events = [torch.cuda.Event() for _ in range(_RING)]
+            self._slot_clean = [True] * _RING
+            self._guard_word = torch.full((1,), _INT_MAX, dtype=torch.int32, device=self.device)
             self._scalars = torch.zeros(16, dtype=torch.int32, device=self.device)
             self._scalars_host = torch.zeros(16, dtype=torch.int32).pin_memory()
         self.flags = StepFlags(deterministic_mode=False)
@@ -372,6 +380,7 @@ class CudaWorker:
         self._frame_steps = 0
         self._frame_rebuilds = 0
         self.cfl_mode = False
+        self.frame_dts = []
         self.count_stats = bool(count_stats)
         self.fuse_clear = bool(fuse_clear)
         self.last_perm = None
@@ -380,7 +389,12 @@ class CudaWorker:
         self._scratch_allocs = 0
         self.kernel_calls = 0
         self.time_kernels = False     # bench: CUDA events around the step kernels
+        self.pipelined = True         # run_frame enqueues step s+1 before reading step s's flag
+        self.speculative_discards = 0
         self.kernel_events = []
+        self._guard = None            # ctypes Guard of the step being enqueued (pipelined frames)
+        self._defer = False           # leave gather statuses unread (pipelined frames)
+        self._unconsumed = None
         m = material
         self._tp = TransferParams(
             mat_kind=int(m.kind), nch=self.store.nch, mu=float(m.mu), lam=float(m.lam),
@@ -436,9 +450,8 @@ class CudaWorker:
 
     @property
     def counters(self):
-        self._status_host.copy_(self._status, non_blocking=True)
-        torch.cuda.current_stream().synchronize()
-        return self._status_host.numpy()[1:1 + N_COUNTERS].astype(np.int64)
+        host = self._status.cpu().numpy()
+        return host[:, 1:1 + N_COUNTERS].sum(axis=0).astype(np.int64)
 
     @property
     def frame_steps(self):
@@ -488,9 +501,15 @@ class CudaWorker:
         self._phase_ms = {k: 0.0 for k in _PHASES}
         self._frame_steps = 0
         self._frame_rebuilds = 0
+        self.frame_dts = []       # step sizes of the current frame, in order
 
     def run_frame(self):
         self.begin_frame()
+        if self.pipelined and self.runtime.n_workers == 1 and \
+                self.options.rebuild != "every_step" and not self.options.collect_conservation:
+            with torch.cuda.device(self.device):
+                self._run_frame_pipelined()
+            return
         with torch.cuda.device(self.device):
             if self.cfl_mode:
                 c_sound = self.material.sound_speed()
@@ -501,13 +520,92 @@ class CudaWorker:
                     self.run_step(self._global_step)
                     t += self.dt
                     self._frame_steps += 1
+                    self.frame_dts.append(self.dt)
             else:
                 self.dt = self.params.dt
                 for _ in range(self.params.steps_per_frame):
                     self.run_step(self._global_step)
                     self._frame_steps += 1
+                    self.frame_dts.append(self.dt)
             if self._pending_gather:
                 self._flush_gather()
+
+    def _run_frame_pipelined(self):
+        """run_frame with the host one step ahead of the device.
+
+        Step s+1 is enqueued (guarded) before step s's status block has been read.  When step
+        s turns out to have asked for a rebuild, the device skipped step s+1 by itself (guard
+        word < s+1), the host restores its bookkeeping and re-issues the step after the
+        rebuild -- the same sequence of steps and rebuilds as the reference's
+        "read flag, then step" loop (pipeline.py:856-880, 905-940), without a device idle
+        gap per step."""
+        c_sound = self.material.sound_speed() if self.cfl_mode else 0.0
+        frame_dt = self.params.frame_dt
+        t = 0.0
+        inflight = None          # (slot, step) of the last enqueued, not yet consumed gather
+        self._defer = True
+        try:
+            while True:
+                more = (t < frame_dt - 1e-12) if self.cfl_mode else \
+                    (self._frame_steps < self.params.steps_per_frame)
+                if not more:
+                    break
+                step = self._global_step
+                if self.flags.rebuild_needed:
+                    # a rebuild synchronises anyway: drain, then step unguarded
+                    if inflight is not None:
+                        self._consume(*inflight)
+                        inflight = None
+                    self._guard = None
+                else:
+                    self._guard = _capi.Guard(self._guard_word.data_ptr(), step)
+                if self.cfl_mode:
+                    vmax = self.runtime.global_vmax((step - 2) % 3)
+                    self.dt = cfl_dt(vmax + c_sound, self.params, frame_dt - t)
+                else:
+                    self.dt = self.params.dt
+                snap = self._snapshot()
+                self._unconsumed = None
+                self.step_pre_barrier(step)
+                self.runtime.barrier_wait(self.wid)
+                self.step_post_barrier(step)
+                cur = self._unconsumed
+                if inflight is not None:
+                    self._consume(*inflight)
+                    inflight = None
+                    if self.flags.rebuild_needed:
+                        # the step just enqueued was skipped on the device: undo it on the host
+                        self._restore(snap)
+                        self._guard_word.fill_(_INT_MAX)
+                        self.speculative_discards += 1
+                        continue
+                inflight = cur
+                t += self.dt
+                self._frame_steps += 1
+                self.frame_dts.append(self.dt)
+            if inflight is not None:
+                self._consume(*inflight)
+                if self.flags.rebuild_needed:
+                    self._guard_word.fill_(_INT_MAX)
+        finally:
+            self._defer = False
+            self._guard = None
+        if self._pending_gather:
+            self._flush_gather()
+
+    def _snapshot(self):
+        f = self.flags
+        return (self._pending_gather, self._pending_full_clear_parity, self._vel_dt,
+                f.steps_since_rebuild, f.fused_mode, self._global_step, self._fused_now,
+                self.runtime.generations, list(self._slot_clean), len(self.kernel_events))
+
+    def _restore(self, snap):
+        f = self.flags
+        (self._pending_gather, self._pending_full_clear_parity, self._vel_dt,
+         f.steps_since_rebuild, f.fused_mode, self._global_step, self._fused_now,
+         self.runtime.generations, clean, n_events) = snap
+        self._slot_clean = clean
+        del self.kernel_events[n_events:]
 
     # -- one step, split around the barrier (pipeline.py:905-940) --------------------------
     def step_pre_barrier(self, step):
@@ -536,7 +634,7 @@ class CudaWorker:
     def step_post_barrier(self, step):
         par = step & 1
         self._post_barrier(par)
-        self._reduce_and_update(par)
+        self._reduce_and_update(par, step)
         if self._fused_now:
             self._pending_gather = True
         else:
@@ -688,7 +786,7 @@ class CudaWorker:
         elif self.fuse_clear and self.runtime.n_workers == 1:
             return   # rows were zeroed by the grid update that consumed them
         self._call("mpm_clear", self.grid._raw[par].ptr, self.table._touched[par].ptr, count, full,
-                   None, _stream_ptr())
+                   self._gref(), _stream_ptr())
 
     def _params(self, margin_shrink=0.0):
         tp = self._tp
@@ -707,14 +805,35 @@ class CudaWorker:
             return gr._vel_old.ptr
         return None
 
+    def _gref(self):
+        return C.byref(self._guard) if self._guard is not None else None
+
+    def _status_ptr(self, slot):
+        return self._status.data_ptr() + slot * _capi.STATUS_BYTES
+
     def _run_p2g(self, step, par):
         st = self.store
         if not st.n_groups:
             return
         sv, tv = st.view(), self.table.view()
         self._call("mpm_p2g", C.byref(sv), C.byref(tv), self.grid._raw[par].ptr,
-                   self.table._touched[par].ptr, C.byref(self._params()), self._status.data_ptr(),
-                   None, _stream_ptr())
+                   self.table._touched[par].ptr, C.byref(self._params()),
+                   self._status_ptr(step % _RING), self._gref(), _stream_ptr())
+
+    def _gather_slot(self, step, stream):
+        slot = step % _RING
+        if not self._slot_clean[slot]:
+            self._call("mpm_status_reset", self._status_ptr(slot), self._gref(), stream)
+        self._slot_clean[slot] = False
+        return slot
+
+    def _after_gather(self, slot, step):
+        self._status_host[slot].copy_(self._status[slot], non_blocking=True)
+        self._status_events[slot].record()
+        if self._defer:
+            self._unconsumed = (slot, step)
+        else:
+            self._consume(slot, step)
 
     def _run_g2p(self, step):
         st = self.store
@@ -723,13 +842,18 @@ class CudaWorker:
             return
         sv, tv = st.view(), self.table.view()
         stream = _stream_ptr()
-        self._call("mpm_status_reset", self._status.data_ptr(), None, stream)
+        slot = self._gather_slot(step, stream)
         self._call("mpm_g2p", C.byref(sv), C.byref(tv), self.grid._vel.ptr, self._vel_old_ptr(),
-                   C.byref(self._params()), self._status.data_ptr(), None, stream)
-        self._consume_status(step)
+                   C.byref(self._params()), self._status_ptr(slot), self._gref(), stream)
+        self._after_gather(slot, step)
 
     def _flush_gather(self):
-        self._run_g2p(self._global_step)
+        guard, defer = self._guard, self._defer
+        self._guard, self._defer = None, False      # a flush is always read back at once
+        try:
+            self._run_g2p(self._global_step)
+        finally:
+            self._guard, self._defer = guard, defer
         self._pending_gather = False
 
     def _run_g2p2g(self, step, par):
@@ -738,19 +862,19 @@ class CudaWorker:
             return
         sv, tv = st.view(), self.table.view()
         stream = _stream_ptr()
-        self._call("mpm_status_reset", self._status.data_ptr(), None, stream)
+        slot = self._gather_slot(step, stream)
         self._call("mpm_g2p2g", C.byref(sv), C.byref(tv), self.grid._vel.ptr, self._vel_old_ptr(),
                    self.grid._raw[par].ptr, self.table._touched[par].ptr,
-                   C.byref(self._params(FUSED_MARGIN_CELLS)), self._status.data_ptr(), None, stream)
-        self._consume_status(step)
+                   C.byref(self._params(FUSED_MARGIN_CELLS)), self._status_ptr(slot), self._gref(),
+                   stream)
+        self._after_gather(slot, step)
 
-    def _consume_status(self, step):
+    def _consume(self, slot, step):
         """Read the status block written by a gather: free-zone flag -> rebuild_needed,
         max speed -> vmax ring (pipeline.py:1102-1104), addressing counter -> exception
         (pipeline.py:1233-1238)."""
-        self._status_host.copy_(self._status, non_blocking=True)
-        torch.cuda.current_stream().synchronize()
-        raw = self._status_host.numpy()
+        self._status_events[slot].synchronize()
+        raw = self._status_host[slot].numpy()
         head = raw[:1].view(np.uint32)
         if head[0]:
             self.flags.rebuild_needed = True
@@ -794,8 +918,10 @@ class CudaWorker:
                            m.ptr, self.table.count, stream)
         self._peer_states = states
 
-    def _reduce_and_update(self, par):
+    def _reduce_and_update(self, par, step=None):
         """pipeline.py:1166-1231 in one kernel: reduce over peers, finalize, boundary."""
+        if step is None:
+            step = self._global_step
         tb, gr = self.table, self.grid
         count = tb.count
         stream = _stream_ptr()
@@ -823,11 +949,16 @@ class CudaWorker:
         fuse = int(self.fuse_clear and self.runtime.n_workers == 1)
         tv = tb.view()
         if count:
+            # the update also zeroes the status block of the gather that follows it in stream
+            # order: this step's G2P, or the next step's fused gather / the frame-end flush
+            nxt = (step + 1 if self._fused_now else step) % _RING
             self._call("mpm_grid_update", gr._raw[par].ptr, tb._touched[par].ptr, gr._vel.ptr,
                        self._vel_old_ptr(), C.byref(tv), n_p, p_raw, p_touched, p_map,
                        float(self.dt), grav, int(bc is not None), sticky, blo, bhi,
                        float(self.params.dx), fuse, gr._raw[par].ptr if fuse else None,
-                       tb._touched[par].ptr if fuse else None, None, stream)
+                       tb._touched[par].ptr if fuse else None, self._status_ptr(nxt),
+                       self._gref(), stream)
+            self._slot_clean[nxt] = True
         self._vel_dt = self.dt
 
     def _collect_conservation(self, par):

@@ -153,20 +153,18 @@ def test_worker_count_invariance():
         _assert_particles(s, states[0], edge, 9, run=True)
 
 
-def test_cfl_schedule_against_reference_dump():
+@pytest.mark.parametrize("pipelined", [False, True])
+def test_cfl_schedule_against_reference_dump(pipelined):
     g = golden("cfl.npz")
     material, params, boundary = fluid_setup(frame_dt=float(g["frame_dt"]), cfl=0.5)
     wc = U.cuda_worker(g["pos"], g["vel"], float(g["mass"]), material, params, boundary)
     wc.cfl_mode = True
+    wc.pipelined = pipelined
     dts = []
-    orig = wc.run_step
-
-    def spy(step):
-        dts.append(wc.dt)
-        orig(step)
-    wc.run_step = spy
     wc.run_frame()
+    dts += wc.frame_dts
     wc.run_frame()
+    dts += wc.frame_dts
     assert len(dts) == len(g["dts"])
     assert np.allclose(np.array(dts), g["dts"], rtol=1e-5, atol=0)
     edge = float(g["pos"].max() - g["pos"].min())
@@ -186,3 +184,21 @@ def test_aggregate_drift_over_a_frame():
     ke_o = 0.5 * (so[:, 15] * (so[:, 3:6] ** 2).sum(axis=1)).sum()
     assert wc.store.kinetic_energy() == pytest.approx(ke_o, rel=U.AGG_RTOL)
     assert wc.rebuild_steps == wo.rebuild_steps
+
+
+def test_pipelined_frame_equals_stepwise_frame():
+    """run_frame with speculative guarded launches (host one step ahead) performs exactly the
+    steps and rebuilds of the synchronous loop: same rebuild steps, bit-identical particles in
+    split mode is not guaranteed (float atomics), so tolerance as everywhere else."""
+    for transfer in ("split", "g2p2g"):
+        g, wa, _, edge, ndef = _pair("elastic.npz", elastic_setup(), transfer=transfer)
+        _, wb, _, _, _ = _pair("elastic.npz", elastic_setup(), transfer=transfer)
+        wa.pipelined, wb.pipelined = False, True
+        for _ in range(3):
+            wa.run_frame()
+            wb.run_frame()
+        assert wa.rebuild_steps == wb.rebuild_steps and len(wa.rebuild_steps) >= 3
+        assert wb.speculative_discards >= 1
+        assert wa._global_step == wb._global_step == 108
+        _assert_particles(U.state_by_id(wb), U.state_by_id(wa), edge, ndef, run=True)
+        assert wb.runtime.generations == 108
