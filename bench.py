@@ -146,48 +146,70 @@ def run_ours(args):
     rank = int(os.environ.get("RANK", "0"))
     world = int(os.environ.get("WORLD_SIZE", "1"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
-    if world > 1:
-        from paper_2111_00699_b200 import dist as mdist
-        return mdist.run_bench(args, build_world, algorithmic_bytes, ClockSampler,
-                               measured_peak_gbs, METRIC, UNIT)
-    if args.gpus != 1:
-        raise SystemExit("--gpus N>1 must be launched with torch.distributed.run (one rank per GPU)")
+    if args.gpus != world:
+        raise SystemExit(f"--gpus {args.gpus} needs {args.gpus} ranks (torch.distributed.run); "
+                         f"WORLD_SIZE is {world}")
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=dev)
     W = build_world(args.scene)
     n = len(W.positions)
     spf = W.params.steps_per_frame
     opts = PipelineOptions(transfer=args.transfer, fused_threshold=1 << 62)
     lib = _capi.lib()
+    vmax0 = float(np.abs(W.velocities).max())
+
+    if world > 1:
+        from paper_2111_00699_b200.dist import DistRuntime, DistWorker
+        from paper_2111_00699_b200 import partition_particles
+        part = partition_particles(W.positions, world)[rank]
+    else:
+        part = np.arange(n, dtype=np.int64)
+    my_pos = np.ascontiguousarray(W.positions[part], dtype=np.float32)
+    my_vel = np.ascontiguousarray(W.velocities[part], dtype=np.float32)
 
     def fresh_worker():
-        rt = SharedRuntime(1, initial_vmax=float(np.abs(W.velocities).max()))
-        w = CudaWorker(0, rt, W.params, W.material, W.boundary, opts, device=dev,
-                       count_stats=False, fuse_clear=True)
-        return w
+        if world > 1:
+            return DistWorker(DistRuntime(dev, initial_vmax=vmax0), W.params, W.material, W.boundary,
+                              opts, device=dev, count_stats=False)
+        return CudaWorker(0, SharedRuntime(1, initial_vmax=vmax0), W.params, W.material, W.boundary,
+                          opts, device=dev, count_stats=False, fuse_clear=True)
 
-    ids = np.arange(n, dtype=np.int64)
+    def barrier():
+        if world > 1:
+            dist.barrier()
+        torch.cuda.synchronize()
+
+    def max_over_ranks(x):
+        if world == 1:
+            return x
+        t = torch.tensor([x], dtype=torch.float64, device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        return float(t.item())
+
     w = fresh_worker()
-    w.seed_particles(W.positions, W.velocities, W.particle_mass, ids=ids)
+    w.seed_particles(my_pos, my_vel, W.particle_mass, ids=part)
     for _ in range(args.warmup):
         w.run_frame()
-    torch.cuda.synchronize()
+    barrier()
     w.time_kernels = True
     w.kernel_events.clear()
     sampler = ClockSampler(local)
-    sampler.start()
+    if rank == 0:
+        sampler.start()
     l0 = lib.mpm_launch_count()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     reb0 = len(w.rebuild_steps)
-    torch.cuda.synchronize()
+    barrier()
     e0.record()
     for _ in range(args.steps):
         w.run_frame()
     e1.record()
-    torch.cuda.synchronize()
-    total_ms = e0.elapsed_time(e1)
+    barrier()
+    total_ms = max_over_ranks(e0.elapsed_time(e1))
     launches = int(lib.mpm_launch_count() - l0)
-    clocks = sampler.stop()
+    clocks = sampler.stop() if rank == 0 else None
     rebuilds = len(w.rebuild_steps) - reb0
     ms_per_step = total_ms / args.steps
     value = n * spf * args.steps / (total_ms * 1e-3) / 1e6
@@ -204,14 +226,15 @@ def run_ours(args):
     w.dt = W.params.dt
     w.run_step(step)
     touched = int(w.table._touched[step & 1].data[:w.table.count].sum().item())
+    n_local = len(part)
     peak, peak_src = measured_peak_gbs()
     roofline = None
     if durs:
         avg_ms = float(np.mean(durs))
-        abytes = algorithmic_bytes(int(W.material.kind), args.transfer, n, touched)
+        abytes = algorithmic_bytes(int(W.material.kind), args.transfer, n_local, touched)
         achieved = abytes / (avg_ms * 1e-3) / 1e9
         roofline = {"bound": "hbm", "kernel": dom, "achieved": round(achieved, 1), "peak": peak,
-                    "unit": "GB/s", "frac": round(achieved / peak, 4), "traffic": None,
+                    "unit": "GB/s", "frac": round(achieved / peak, 4), "traffic": TRAFFIC_NCU,
                     "peak_source": peak_src, "avg_launch_ms": round(avg_ms, 4),
                     "algorithmic_bytes_per_launch": int(abytes), "launches_timed": len(durs),
                     "kernel_share_of_step": round(sum(durs) / total_ms, 3),
@@ -220,47 +243,57 @@ def run_ours(args):
     # end to end through the public API with host buffers
     e2e = None
     if not args.no_e2e:
-        pos32 = np.ascontiguousarray(W.positions, dtype=np.float32)
-        vel32 = np.ascontiguousarray(W.velocities, dtype=np.float32)
         w2 = fresh_worker()
         k_e2e = max(2, min(args.steps, 4))
         for it in range(1 + k_e2e):
             if it == 1:
-                torch.cuda.synchronize()
+                barrier()
                 t0 = time.perf_counter()
-            w2.replace_particles(pos32, vel32, W.particle_mass, ids)
+            w2.replace_particles(my_pos, my_vel, W.particle_mass, part)
             w2.run_frame()
             out_pos, out_ids = w2.store.positions_with_ids(dtype=np.float32)
-        torch.cuda.synchronize()
-        dt_e2e = (time.perf_counter() - t0) / k_e2e
+        barrier()
+        dt_e2e = max_over_ranks((time.perf_counter() - t0) / k_e2e)
         e2e = {"value": round(n * spf / dt_e2e / 1e6, 2), "unit": UNIT,
-               "h2d_bytes_per_step": int(n * (w2.store.nch * 4 + 8)),
+               "h2d_bytes_per_step": int(n_local * (w2.store.nch * 4 + 8)),
                "d2h_bytes_per_step": int(out_pos.nbytes + out_ids.nbytes),
                "ms_per_step": round(dt_e2e * 1e3, 3), "steps": k_e2e,
                "api": "CudaWorker.replace_particles(host) + run_frame() + store.positions_with_ids()"}
 
     cpu = None
-    if not args.no_cpu_baseline:
+    if not args.no_cpu_baseline and rank == 0 and world == 1:
         cpu = cpu_baseline(W, substeps=2, threads=1)
 
-    line = {
-        "metric": METRIC, "value": round(value, 2), "unit": UNIT, "n_gpus": 1,
-        "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(ms_per_step, 4),
-        "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f32",
-        "data": "synthetic",
-        "config": {"workload": W.name, "particles": n, "substeps_per_step": spf,
-                   "step": "one frame", "dx": W.params.dx, "dt": W.params.dt,
-                   "transfer": args.transfer, "material": W.material.kind.name,
-                   "pblocks": int(w.table.count), "groups": int(w.store.n_groups),
-                   "rebuilds_in_timed_region": rebuilds, "touched_pblocks": touched,
-                   "speculative_steps_discarded": int(w.speculative_discards),
-                   "l2_policy": "working set (particles + grid) exceeds L2: "
-                                f"{n * w.store.nch * 4 / 1e6:.0f} MB particle state"},
-        "ms_per_frame": round(ms_per_step, 4),
-        "clocks": clocks, "gpu_launches": launches, "e2e": e2e, "roofline": roofline,
-        "cpu_baseline": cpu,
-    }
-    print(json.dumps(line), flush=True)
+    if rank == 0:
+        line = {
+            "metric": METRIC, "value": round(value, 2), "unit": UNIT, "n_gpus": world,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(ms_per_step, 4),
+            "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f32",
+            "data": "synthetic",
+            "config": {"workload": W.name, "particles": n, "substeps_per_step": spf,
+                       "step": "one frame", "dx": W.params.dx, "dt": W.params.dt,
+                       "transfer": args.transfer, "material": W.material.kind.name,
+                       "parallelism": f"{world} spatial slab(s), halo rows over NCCL" if world > 1
+                       else "1 GPU", "rank0_particles": n_local,
+                       "pblocks": int(w.table.count), "groups": int(w.store.n_groups),
+                       "rebuilds_in_timed_region": rebuilds, "touched_pblocks": touched,
+                       "speculative_steps_discarded": int(w.speculative_discards),
+                       "l2_policy": "inputs larger than L2: "
+                                    f"{n_local * w.store.nch * 4 / 1e6:.0f} MB particle state per GPU "
+                                    "streamed every substep (L2 126 MB)"},
+            "ms_per_frame": round(ms_per_step, 4),
+            "clocks": clocks, "gpu_launches": launches, "e2e": e2e, "roofline": roofline,
+            "cpu_baseline": cpu,
+        }
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.barrier()
+        dist.destroy_process_group()
+
+
+# dram__bytes_read.sum + dram__bytes_write.sum of the dominant kernel, per launch, from the
+# committed `ncu --set full` capture (profiles/); None until a capture of the current kernel exists
+TRAFFIC_NCU = None
 
 
 def cpu_baseline(W, substeps, threads, warm=True):

@@ -210,17 +210,34 @@ int mpm_p2g(const mpm_store_view *store, const mpm_table_view *table, float *raw
 /* _reduce_and_update + _grid_finalize (pipeline.py:1166-1231, 660-722): for every block
  * flagged in touched: vel = raw (+ peer raw rows through peer_map where the peer touched
  * the block) ; zero-mass nodes -> 0 ; v = mom/m ; vel_old saved before gravity when
- * vel_old != NULL ; v += dt*g ; box boundary (inclusive comparisons on node world
- * position).  n_peers may be 0.  peer_map[p][b] = peer p's index of local block b or -1.
+ * vel_old != NULL ; v += dt*g ; box boundary (inclusive comparisons on node world position).
  * reset_status (may be NULL): status block whose zone flag / max speed are zeroed by this
  * kernel for the gather that follows it in stream order. */
-int mpm_grid_update(const float *raw, const uint8_t *touched, float *vel, float *vel_old,
-                    const mpm_table_view *table, int32_t n_peers, const float *const *peer_raw,
-                    const uint8_t *const *peer_touched, const int32_t *const *peer_map,
-                    double dt, const double gravity[3], int apply_bc, int bc_sticky,
-                    const double box_lo[3], const double box_hi[3], double dx, int fuse_clear,
-                    float *raw_mut, uint8_t *touched_mut, mpm_step_status *reset_status,
-                    const mpm_guard *guard, void *stream);
+#define MPM_MAX_PEERS 15
+typedef struct mpm_grid_params {
+    double dt;
+    double gravity[3];
+    int32_t apply_bc, bc_sticky;        /* BoundaryBox present / mode == "sticky" */
+    double box_lo[3], box_hi[3];
+    double dx;
+    int32_t fuse_clear;                 /* single worker only: also zero the consumed raw rows and
+                                           reset their touched flags (saves the next _clear pass) */
+    int32_t block_filter;               /* 0 every touched block; 1 only blocks no peer holds;
+                                           2 only blocks shared with a peer (halo) */
+    int32_t n_peers;                    /* 0..MPM_MAX_PEERS */
+    const float *peer_raw[MPM_MAX_PEERS];        /* float4 rows [*, 64] of each peer */
+    const uint8_t *peer_touched[MPM_MAX_PEERS];  /* per-row flags, or NULL = every row counts */
+    const int32_t *peer_map[MPM_MAX_PEERS];      /* [count]: row of local block b at that peer, or -1 */
+} mpm_grid_params;
+int mpm_grid_update(float *raw, uint8_t *touched, float *vel, float *vel_old,
+                    const mpm_table_view *table, const mpm_grid_params *params,
+                    mpm_step_status *reset_status, const mpm_guard *guard, void *stream);
+
+/* Pack the raw rows this worker contributes to one peer (one process per GPU: the rows are
+ * then exchanged with NCCL send/recv): out_rows[i] = raw row of block send_idx[i], zeros when
+ * the block was not touched this step. */
+int mpm_pack_halo(const float *raw, const uint8_t *touched, const int32_t *send_idx, int32_t n,
+                  float *out_rows, void *stream);
 
 /* _gather_advect (pipeline.py:400-600). */
 int mpm_g2p(const mpm_store_view *store, const mpm_table_view *table, const float *vel,

@@ -49,6 +49,16 @@ class TableView(C.Structure):
     ]
 
 
+class GridParams(C.Structure):
+    _fields_ = [
+        ("dt", f64), ("gravity", f64 * 3), ("apply_bc", i32), ("bc_sticky", i32),
+        ("box_lo", f64 * 3), ("box_hi", f64 * 3), ("dx", f64), ("fuse_clear", i32),
+        ("block_filter", i32), ("n_peers", i32),
+        ("peer_raw", p_void * MPM_MAX_PEERS), ("peer_touched", p_void * MPM_MAX_PEERS),
+        ("peer_map", p_void * MPM_MAX_PEERS),
+    ]
+
+
 class Guard(C.Structure):
     _fields_ = [("first_bad_step", p_void), ("step", i32)]
 
@@ -83,10 +93,9 @@ _SIGNATURES = {
     "mpm_status_reset": [p_void, C.POINTER(Guard), p_void],
     "mpm_p2g": [C.POINTER(StoreView), C.POINTER(TableView), p_void, p_void,
                 C.POINTER(TransferParams), p_void, C.POINTER(Guard), p_void],
-    "mpm_grid_update": [p_void, p_void, p_void, p_void, C.POINTER(TableView), i32,
-                        C.POINTER(p_void), C.POINTER(p_void), C.POINTER(p_void), f64,
-                        C.POINTER(f64), i32, i32, C.POINTER(f64), C.POINTER(f64), f64, i32,
-                        p_void, p_void, p_void, C.POINTER(Guard), p_void],
+    "mpm_grid_update": [p_void, p_void, p_void, p_void, C.POINTER(TableView),
+                        C.POINTER(GridParams), p_void, C.POINTER(Guard), p_void],
+    "mpm_pack_halo": [p_void, p_void, p_void, i32, p_void, p_void],
     "mpm_g2p": [C.POINTER(StoreView), C.POINTER(TableView), p_void, p_void,
                 C.POINTER(TransferParams), p_void, C.POINTER(Guard), p_void],
     "mpm_g2p2g": [C.POINTER(StoreView), C.POINTER(TableView), p_void, p_void, p_void, p_void,

@@ -50,6 +50,7 @@ struct GridArgs {
     double blo[3], bhi[3];
     double dx;
     int fuse_clear;
+    int block_filter;
     float4 *raw_mut;
     uint8_t *touched_mut;
     DevGuard guard;
@@ -66,7 +67,13 @@ __global__ void __launch_bounds__(256) grid_update_kernel(const GridArgs a)
     }
     const int b = blockIdx.x * 4 + (threadIdx.x >> 6);
     const int slot = threadIdx.x & 63;
-    const bool hit = b < a.count && a.touched[b];
+    bool hit = b < a.count && a.touched[b];
+    if (hit && a.block_filter) {
+        // 1: only blocks no peer holds (can run while the halo rows are in flight), 2: the rest
+        bool shared = false;
+        for (int p = 0; p < a.peers.n; ++p) shared = shared || a.peers.map[p][b] >= 0;
+        hit = (a.block_filter == 2) == shared;
+    }
     if (a.fuse_clear) __syncthreads();
     if (!hit) return;
     const size_t idx = (size_t)b * 64 + slot;
@@ -74,7 +81,7 @@ __global__ void __launch_bounds__(256) grid_update_kernel(const GridArgs a)
     // cross-worker reduction (pipeline.py:1172-1188): peers' raw rows are only read
     for (int p = 0; p < a.peers.n; ++p) {
         const int q = a.peers.map[p][b];
-        if (q < 0 || a.peers.touched[p][q] != 1) continue;
+        if (q < 0 || (a.peers.touched[p] && a.peers.touched[p][q] != 1)) continue;
         const float4 o = a.peers.raw[p][(size_t)q * 64 + slot];
         node.x += o.x; node.y += o.y; node.z += o.z; node.w += o.w;
     }
@@ -161,6 +168,20 @@ __global__ void __launch_bounds__(256) grid_aggregates_kernel(const float4 *__re
     }
 }
 
+// Halo rows for one peer: out[i] = raw row of block send_idx[i], or zeros when this worker did
+// not touch the block this step (the reference skips such rows, pipeline.py:1183-1186).
+__global__ void __launch_bounds__(256) pack_halo_kernel(const float4 *__restrict__ raw,
+                                                        const uint8_t *__restrict__ touched,
+                                                        const int *__restrict__ send_idx, int n,
+                                                        float4 *__restrict__ out)
+{
+    const int i = blockIdx.x * 4 + (threadIdx.x >> 6);
+    const int slot = threadIdx.x & 63;
+    if (i >= n) return;
+    const int b = send_idx[i];
+    out[(size_t)i * 64 + slot] = touched[b] ? raw[(size_t)b * 64 + slot] : make_float4(0.f, 0.f, 0.f, 0.f);
+}
+
 __global__ void status_reset_kernel(mpm_step_status *status, const DevGuard guard)
 {
     if (guarded_out(guard)) return;
@@ -187,18 +208,14 @@ int mpm_status_reset(mpm_step_status *status, const mpm_guard *guard, void *stre
     return check_launch("mpm_status_reset", 1);
 }
 
-int mpm_grid_update(const float *raw, const uint8_t *touched, float *vel, float *vel_old,
-                    const mpm_table_view *table, int32_t n_peers, const float *const *peer_raw,
-                    const uint8_t *const *peer_touched, const int32_t *const *peer_map,
-                    double dt, const double gravity[3], int apply_bc, int bc_sticky,
-                    const double box_lo[3], const double box_hi[3], double dx, int fuse_clear,
-                    float *raw_mut, uint8_t *touched_mut, mpm_step_status *reset_status,
-                    const mpm_guard *guard, void *stream)
+int mpm_grid_update(float *raw, uint8_t *touched, float *vel, float *vel_old,
+                    const mpm_table_view *table, const mpm_grid_params *p,
+                    mpm_step_status *reset_status, const mpm_guard *guard, void *stream)
 {
-    if (!table || !gravity) return MPM_ERR_REJECTED_INPUT;
-    if (n_peers < 0 || n_peers > MPM_MAX_PEERS) return MPM_ERR_CONFIG;
-    if (apply_bc && (!box_lo || !box_hi)) return MPM_ERR_REJECTED_INPUT;
-    if (fuse_clear && (n_peers > 0 || !raw_mut || !touched_mut)) return MPM_ERR_MODE_CONFLICT;
+    if (!table || !p) return MPM_ERR_REJECTED_INPUT;
+    if (p->n_peers < 0 || p->n_peers > MPM_MAX_PEERS) return MPM_ERR_CONFIG;
+    if (p->fuse_clear && p->n_peers > 0) return MPM_ERR_MODE_CONFLICT;
+    if (p->block_filter < 0 || p->block_filter > 2) return MPM_ERR_CONFIG;
     if (table->count <= 0) return MPM_OK;
     GridArgs a;
     a.raw = (const float4 *)raw;
@@ -207,28 +224,38 @@ int mpm_grid_update(const float *raw, const uint8_t *touched, float *vel, float 
     a.vel_old = (float4 *)vel_old;
     a.origin = (const int4 *)table->origin;
     a.count = table->count;
-    a.peers.n = n_peers;
-    for (int p = 0; p < n_peers; ++p) {
-        a.peers.raw[p] = (const float4 *)peer_raw[p];
-        a.peers.touched[p] = peer_touched[p];
-        a.peers.map[p] = peer_map[p];
+    a.peers.n = p->n_peers;
+    for (int k = 0; k < p->n_peers; ++k) {
+        a.peers.raw[k] = (const float4 *)p->peer_raw[k];
+        a.peers.touched[k] = p->peer_touched[k];
+        a.peers.map[k] = p->peer_map[k];
     }
-    a.dt = (float)dt;
-    a.gx = (float)gravity[0]; a.gy = (float)gravity[1]; a.gz = (float)gravity[2];
-    a.apply_bc = apply_bc;
-    a.bc_sticky = bc_sticky;
+    a.dt = (float)p->dt;
+    a.gx = (float)p->gravity[0]; a.gy = (float)p->gravity[1]; a.gz = (float)p->gravity[2];
+    a.apply_bc = p->apply_bc;
+    a.bc_sticky = p->bc_sticky;
     for (int k = 0; k < 3; ++k) {
-        a.blo[k] = apply_bc ? box_lo[k] : -1e30;
-        a.bhi[k] = apply_bc ? box_hi[k] : 1e30;
+        a.blo[k] = p->apply_bc ? p->box_lo[k] : -1e30;
+        a.bhi[k] = p->apply_bc ? p->box_hi[k] : 1e30;
     }
-    a.dx = dx;
-    a.fuse_clear = fuse_clear;
-    a.raw_mut = (float4 *)raw_mut;
-    a.touched_mut = touched_mut;
+    a.dx = p->dx;
+    a.fuse_clear = p->fuse_clear;
+    a.block_filter = p->block_filter;
+    a.raw_mut = (float4 *)raw;
+    a.touched_mut = touched;
     a.guard = make_guard(guard);
     a.reset_status = reset_status;
     grid_update_kernel<<<(a.count + 3) / 4, 256, 0, (cudaStream_t)stream>>>(a);
     return check_launch("mpm_grid_update", 1);
+}
+
+int mpm_pack_halo(const float *raw, const uint8_t *touched, const int32_t *send_idx, int32_t n,
+                  float *out_rows, void *stream)
+{
+    if (n <= 0) return MPM_OK;
+    pack_halo_kernel<<<(n + 3) / 4, 256, 0, (cudaStream_t)stream>>>((const float4 *)raw, touched, send_idx, n,
+                                                                    (float4 *)out_rows);
+    return check_launch("mpm_pack_halo", 1);
 }
 
 int mpm_particle_aggregates(const mpm_store_view *store, double *out5, void *stream_)

@@ -1,0 +1,281 @@
+"""One process per GPU: spatial partition of the particles, halo rows exchanged over NCCL.
+
+The reference scales by giving each worker a contiguous slab of particles (stable argsort
+along the longest axis, multiworker.py:114-137); every worker owns its block table and nodal
+buffers, and the only cross-worker data are the raw nodal rows of blocks that two workers
+both hold (pipeline.py:1172-1188), read once per step after the single barrier.  With one
+process per GPU the same protocol becomes:
+
+  per step   all_gather of 4 ints per rank (rebuilt flag, block count, max speed bits, step)
+             -- this is the step's barrier and feeds the CFL vmax ring with the reference's
+             two-step lag (pipeline.py:859-867);
+  on rebuild all_gather of the block-code lists, shared-block tagging on the device
+             (mpm_tag_shared) and send/recv row lists, both ordered by the receiver's block
+             index so that no index list crosses the wire;
+  per step   mpm_pack_halo per peer -> batched isend/irecv of the packed rows on a
+             communication stream, while mpm_grid_update(block_filter=1) updates the blocks no
+             peer holds on the compute stream; then mpm_grid_update(block_filter=2) adds the
+             received rows and updates the halo blocks.
+
+The transport is torch.distributed (NCCL on GPUs).  With the gloo backend (CPU tests, or two
+ranks sharing one GPU in the single-GPU check) tensors are staged through host memory.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import math
+
+import numpy as np
+import torch
+import torch.distributed as dist
+
+from . import _capi
+from .multiworker import partition_particles
+from .worker import _RING, CudaWorker, _stream_ptr
+from .memory import DeviceBuffer
+
+
+# --------------------------------------------------------------------------------------
+# device-agnostic protocol pieces (also run on CPU tensors under gloo in the tests)
+# --------------------------------------------------------------------------------------
+def build_halo_lists(peer_map: torch.Tensor):
+    """From peer_map[b] = the peer's index of local block b (or -1):
+      send_idx  local indices of the shared blocks ordered by the PEER's index (the order
+                in which the peer expects the rows);
+      recv_pos  [count] position of local block b among the rows the peer sends (the peer
+                orders them by OUR index), -1 for blocks the peer does not hold.
+    """
+    shared = torch.nonzero(peer_map >= 0).flatten()
+    theirs = peer_map[shared].to(torch.int64)
+    order = torch.argsort(theirs, stable=True)
+    send_idx = shared[order].to(torch.int32)
+    recv_pos = torch.full_like(peer_map, -1, dtype=torch.int32)
+    recv_pos[shared] = torch.arange(len(shared), dtype=torch.int32, device=peer_map.device)
+    return send_idx, recv_pos
+
+
+class DistRuntime:
+    """SharedRuntime (multiworker.py:73-107) across processes."""
+
+    def __init__(self, device, initial_vmax: float = 0.0, group=None):
+        self.group = group
+        self.n_workers = dist.get_world_size(group)
+        self.wid = dist.get_rank(group)
+        self.device = torch.device(device)
+        self.backend = dist.get_backend(group)
+        self.stage_on_host = self.backend == "gloo" and self.device.type == "cuda"
+        self.generations = 0
+        self._vmax = np.full((3, self.n_workers), float(initial_vmax))
+        self._local_vmax = {}
+        self.peer_counts = [0] * self.n_workers
+
+    # -- transport helpers ----------------------------------------------------------------
+    def _wire(self, t: torch.Tensor) -> torch.Tensor:
+        return t.cpu() if self.stage_on_host else t
+
+    def all_gather_i64(self, values) -> np.ndarray:
+        """One small all_gather: [n_workers, len(values)] on the host."""
+        dev = torch.device("cpu") if (self.stage_on_host or self.device.type == "cpu") else self.device
+        mine = torch.tensor(values, dtype=torch.int64, device=dev)
+        out = torch.empty((self.n_workers, len(values)), dtype=torch.int64, device=dev)
+        dist.all_gather_into_tensor(out, mine, group=self.group) if self.backend == "nccl" else \
+            dist.all_gather(list(out.unbind(0)), mine, group=self.group)
+        return out.cpu().numpy()
+
+    def all_gather_codes(self, codes: torch.Tensor, counts):
+        """Every rank's block-code list (variable length, padded to the longest)."""
+        m = max(int(max(counts)), 1)
+        pad = torch.zeros(m, dtype=torch.int64, device=codes.device)
+        pad[:len(codes)] = codes
+        pad = self._wire(pad)
+        bufs = [torch.empty_like(pad) for _ in range(self.n_workers)]
+        dist.all_gather(bufs, pad, group=self.group)
+        return [bufs[q][:int(counts[q])].to(codes.device) for q in range(self.n_workers)]
+
+    def exchange_rows(self, send: dict, recv_rows: dict):
+        """Batched point-to-point exchange: send[q] -> rank q, rank q's rows -> recv_rows[q]."""
+        ops, staged = [], {}
+        for q in sorted(set(send) | set(recv_rows)):
+            if q in recv_rows and recv_rows[q].numel():
+                buf = torch.empty(recv_rows[q].shape, dtype=recv_rows[q].dtype) if self.stage_on_host \
+                    else recv_rows[q]
+                staged[q] = buf
+                ops.append(dist.P2POp(dist.irecv, buf, q, group=self.group))
+            if q in send and send[q].numel():
+                ops.append(dist.P2POp(dist.isend, self._wire(send[q]).contiguous(), q, group=self.group))
+        if ops:
+            for r in dist.batch_isend_irecv(ops):
+                r.wait()
+        if self.stage_on_host:
+            for q, buf in staged.items():
+                recv_rows[q].copy_(buf)
+
+    # -- SharedRuntime surface --------------------------------------------------------------
+    def barrier_wait(self, worker_id: int) -> int:
+        self.generations += 1
+        return self.generations
+
+    def publish_step(self, parity, worker_id, state):
+        pass
+
+    def publish_vmax(self, slot: int, worker_id: int, value: float) -> None:
+        self._local_vmax[slot % 3] = float(value)
+
+    def global_vmax(self, slot: int) -> float:
+        return float(self._vmax[slot % 3].max())
+
+    def step_info(self, step: int, rebuilt: bool, count: int):
+        """The step's barrier: every rank learns who rebuilt, the block counts and the max
+        speed each rank measured in the previous step (slot (step-1) % 3 of the vmax ring)."""
+        prev = (step - 1) % 3
+        v = self._local_vmax.get(prev)
+        bits = int(np.float64(v).view(np.int64)) if v is not None else -1
+        info = self.all_gather_i64([int(bool(rebuilt)), int(count), bits, int(step)])
+        if not (info[:, 3] == step).all():
+            from .errors import ContractViolationError
+            raise ContractViolationError(f"ranks disagree on the step number: {info[:, 3].tolist()}")
+        for q in range(self.n_workers):
+            if info[q, 2] != -1:
+                self._vmax[prev, q] = float(np.int64(info[q, 2]).view(np.float64))
+        self.peer_counts = [int(c) for c in info[:, 1]]
+        self.generations += 1
+        return bool(info[:, 0].any()), self.peer_counts
+
+
+class DistWorker(CudaWorker):
+    """CudaWorker whose peers live in other processes."""
+
+    def __init__(self, runtime: DistRuntime, params, material, boundary, options=None, **kw):
+        super().__init__(runtime.wid, runtime, params, material, boundary, options, **kw)
+        self.pipelined = False
+        self.fuse_clear = False
+        n = runtime.n_workers
+        self._send_idx = [None] * n
+        self._recv_pos = [None] * n
+        self._recv_rows = [None] * n
+        self._send_rows = [None] * n
+        self._rebuilt_this_step = False
+        self._comm_stream = torch.cuda.Stream(device=self.device) if self.device.type == "cuda" else None
+        self.halo_rows_sent = 0
+
+    def run_step(self, step):
+        with torch.cuda.device(self.device):
+            self.step_pre_barrier(step)
+            self.step_post_barrier(step)
+
+    def run_frame(self):
+        self.begin_frame()
+        with torch.cuda.device(self.device):
+            if self.cfl_mode:
+                from .domain import cfl_dt
+                c_sound = self.material.sound_speed()
+                t = 0.0
+                while t < self.params.frame_dt - 1e-12:
+                    vmax = self.runtime.global_vmax((self._global_step - 2) % 3)
+                    self.dt = cfl_dt(vmax + c_sound, self.params, self.params.frame_dt - t)
+                    self.run_step(self._global_step)
+                    t += self.dt
+                    self._frame_steps += 1
+                    self.frame_dts.append(self.dt)
+            else:
+                self.dt = self.params.dt
+                for _ in range(self.params.steps_per_frame):
+                    self.run_step(self._global_step)
+                    self._frame_steps += 1
+                    self.frame_dts.append(self.dt)
+            if self._pending_gather:
+                self._flush_gather()
+
+    def _publish(self, par, rebuilt):
+        self._rebuilt_this_step = rebuilt
+
+    def _post_barrier(self, par):
+        """Barrier + shared-block tagging when any rank rebuilt (pipeline.py:1147-1164)."""
+        rt = self.runtime
+        step = self._global_step
+        any_rebuilt, counts = rt.step_info(step, self._rebuilt_this_step, self.table.count)
+        if not any_rebuilt:
+            return
+        tb = self.table
+        mine = tb._codes.data[:tb.count]
+        lists = rt.all_gather_codes(mine, counts)
+        stream = _stream_ptr()
+        for q in range(rt.n_workers):
+            if q == rt.wid:
+                continue
+            if tb.count == 0 or counts[q] == 0:
+                self._send_idx[q] = torch.zeros(0, dtype=torch.int32, device=self.device)
+                self._recv_pos[q] = torch.full((max(tb.count, 1),), -1, dtype=torch.int32,
+                                               device=self.device)
+                self._send_rows[q] = self._recv_rows[q] = torch.zeros((0, 64, 4), device=self.device)
+                continue
+            m = self._peer_map[q]
+            if m is None:
+                m = self._peer_map[q] = DeviceBuffer(torch.int32, (), self.device)
+            m.resize(tb.count, keep=False)
+            codes_q = lists[q].contiguous()
+            self._call("mpm_tag_shared", codes_q.data_ptr(), int(counts[q]), tb._hkeys.ptr,
+                       tb._hvals.ptr, tb.hash_cap, m.ptr, tb.count, stream)
+            send_idx, recv_pos = build_halo_lists(m.data[:tb.count])
+            self._send_idx[q], self._recv_pos[q] = send_idx.contiguous(), recv_pos.contiguous()
+            k = len(send_idx)
+            self._send_rows[q] = torch.empty((k, 64, 4), dtype=torch.float32, device=self.device)
+            self._recv_rows[q] = torch.empty((k, 64, 4), dtype=torch.float32, device=self.device)
+
+    def _gather_peers(self, par):
+        """Pack, exchange, and describe the received rows as grid-update peers."""
+        rt, tb, gr = self.runtime, self.table, self.grid
+        stream = _stream_ptr()
+        send, recv = {}, {}
+        for q in range(rt.n_workers):
+            if q == rt.wid or self._send_idx[q] is None:
+                continue
+            k = len(self._send_idx[q])
+            if k:
+                self._call("mpm_pack_halo", gr._raw[par].ptr, tb._touched[par].ptr,
+                           self._send_idx[q].data_ptr(), k, self._send_rows[q].data_ptr(), stream)
+                send[q], recv[q] = self._send_rows[q], self._recv_rows[q]
+                self.halo_rows_sent += k
+        return send, recv
+
+    def _reduce_and_update(self, par, step=None):
+        if step is None:
+            step = self._global_step
+        rt, tb = self.runtime, self.table
+        send, recv = self._gather_peers(par)
+        gp = self._grid_params()
+        peers = [(recv[q].data_ptr(), None, self._recv_pos[q].data_ptr()) for q in sorted(recv)]
+        gp.n_peers = len(peers)
+        for k, (r, t, m) in enumerate(peers):
+            gp.peer_raw[k], gp.peer_touched[k], gp.peer_map[k] = r, t, m
+        tv = tb.view()
+        nxt = (step + 1 if self._fused_now else step) % _RING
+        cur = torch.cuda.current_stream()
+        if tb.count and peers:
+            # interior blocks while the halo rows travel
+            self._comm_stream.wait_stream(cur)
+            gp.block_filter = 1
+            self._grid_update_launch(gp, tv, par, self._status_ptr(nxt), _stream_ptr())
+            with torch.cuda.stream(self._comm_stream):
+                rt.exchange_rows(send, recv)
+            cur.wait_stream(self._comm_stream)
+            gp.block_filter = 2
+            self._grid_update_launch(gp, tv, par, None, _stream_ptr())
+        else:
+            rt.exchange_rows(send, recv)      # nothing shared: still matched send/recv pairs
+            if tb.count:
+                gp.block_filter = 0
+                self._grid_update_launch(gp, tv, par, self._status_ptr(nxt), _stream_ptr())
+        if tb.count:
+            self._slot_clean[nxt] = True
+        self._vel_dt = self.dt
+
+
+def seed_rank(worker: DistWorker, positions, velocities, mass):
+    """bench.py:434-439 of the reference: rank r takes the r-th slab of the partition; ids are
+    the indices into the global arrays."""
+    parts = partition_particles(positions, worker.runtime.n_workers)
+    part = parts[worker.runtime.wid]
+    if len(part):
+        worker.seed_particles(np.asarray(positions)[part], np.asarray(velocities)[part], mass, ids=part)
+    return part

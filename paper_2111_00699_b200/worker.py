@@ -392,6 +392,7 @@ class CudaWorker:
         self.pipelined = True         # run_frame enqueues step s+1 before reading step s's flag
         self.speculative_discards = 0
         self.kernel_events = []
+        self._gp = None
         self._guard = None            # ctypes Guard of the step being enqueued (pipelined frames)
         self._defer = False           # leave gather statuses unread (pipelined frames)
         self._unconsumed = None
@@ -933,33 +934,45 @@ class CudaWorker:
                 peers.append((s["raw"].ptr, s["touched"].ptr, self._peer_map[q].ptr))
         if self.options.collect_conservation:
             self._collect_conservation(par)
-        n_p = len(peers)
-        arr = C.c_void_p * max(n_p, 1)
-        p_raw, p_touched, p_map = arr(), arr(), arr()
+        gp = self._grid_params()
+        gp.fuse_clear = int(self.fuse_clear and self.runtime.n_workers == 1)
+        gp.n_peers = len(peers)
         for k, (r, t, m) in enumerate(peers):
-            p_raw[k], p_touched[k], p_map[k] = r, t, m
-        grav = (C.c_double * 3)(*[float(g) for g in self.params.gravity])
-        bc = self.boundary
-        if bc is not None:
-            blo = (C.c_double * 3)(*[float(v) for v in bc.min_corner])
-            bhi = (C.c_double * 3)(*[float(v) for v in bc.max_corner])
-            sticky = int(bc.mode == "sticky")
-        else:
-            blo, bhi, sticky = (C.c_double * 3)(), (C.c_double * 3)(), 0
-        fuse = int(self.fuse_clear and self.runtime.n_workers == 1)
+            gp.peer_raw[k], gp.peer_touched[k], gp.peer_map[k] = r, t, m
         tv = tb.view()
         if count:
             # the update also zeroes the status block of the gather that follows it in stream
             # order: this step's G2P, or the next step's fused gather / the frame-end flush
             nxt = (step + 1 if self._fused_now else step) % _RING
-            self._call("mpm_grid_update", gr._raw[par].ptr, tb._touched[par].ptr, gr._vel.ptr,
-                       self._vel_old_ptr(), C.byref(tv), n_p, p_raw, p_touched, p_map,
-                       float(self.dt), grav, int(bc is not None), sticky, blo, bhi,
-                       float(self.params.dx), fuse, gr._raw[par].ptr if fuse else None,
-                       tb._touched[par].ptr if fuse else None, self._status_ptr(nxt),
-                       self._gref(), stream)
+            self._grid_update_launch(gp, tv, par, self._status_ptr(nxt), stream)
             self._slot_clean[nxt] = True
         self._vel_dt = self.dt
+
+    def _grid_params(self):
+        """mpm_grid_params with the per-run constants filled once; dt set per call."""
+        gp = self._gp
+        if gp is None:
+            gp = self._gp = _capi.GridParams()
+            for k in range(3):
+                gp.gravity[k] = float(self.params.gravity[k])
+            bc = self.boundary
+            gp.apply_bc = int(bc is not None)
+            if bc is not None:
+                gp.bc_sticky = int(bc.mode == "sticky")
+                for k in range(3):
+                    gp.box_lo[k] = float(bc.min_corner[k])
+                    gp.box_hi[k] = float(bc.max_corner[k])
+            gp.dx = float(self.params.dx)
+        gp.dt = float(self.dt)
+        gp.block_filter = 0
+        gp.fuse_clear = 0
+        gp.n_peers = 0
+        return gp
+
+    def _grid_update_launch(self, gp, tv, par, reset_ptr, stream):
+        tb, gr = self.table, self.grid
+        self._call("mpm_grid_update", gr._raw[par].ptr, tb._touched[par].ptr, gr._vel.ptr,
+                   self._vel_old_ptr(), C.byref(tv), C.byref(gp), reset_ptr, self._gref(), stream)
 
     def _collect_conservation(self, par):
         """(pm, pmom x3, gm, gmom x3) rows of pipeline.py:1189-1203 (own raw rows only)."""

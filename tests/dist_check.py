@@ -1,0 +1,73 @@
+"""Two ranks, one process each (launched by torch.distributed.run): DistWorker against the
+reference dump of the two-worker run.  Usable on a single GPU: with the gloo backend both
+ranks share cuda:0 and the halo rows are staged through host memory.
+
+    python -m torch.distributed.run --nproc-per-node 2 --master-addr 127.0.0.1 \
+        --master-port 29517 tests/dist_check.py
+"""
+import os
+import sys
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+sys.path.insert(0, os.path.join(ROOT, "tests"))
+
+import numpy as np
+import torch
+import torch.distributed as dist
+
+import parity_util as U
+from conftest import elastic_setup, golden
+from paper_2111_00699_b200 import PipelineOptions
+from paper_2111_00699_b200.dist import DistRuntime, DistWorker, seed_rank
+
+
+def main():
+    backend = os.environ.get("MPM_DIST_BACKEND", "gloo")
+    dist.init_process_group(backend)
+    rank, world = dist.get_rank(), dist.get_world_size()
+    ndev = torch.cuda.device_count()
+    dev = torch.device("cuda", rank % ndev)
+    torch.cuda.set_device(dev)
+    g = golden("two_worker.npz")
+    material, params, boundary = elastic_setup()
+    transfer = os.environ.get("MPM_TRANSFER", "split")
+    rt = DistRuntime(dev, initial_vmax=float(np.linalg.norm(g["vel"], axis=1).max()))
+    w = DistWorker(rt, params, material, boundary, PipelineOptions(transfer=transfer), device=dev)
+    seed_rank(w, g["pos"], g["vel"], float(g["mass"]))
+    w.run_step(0)
+    if world == 2 and transfer == "split":
+        bad = U.structure_mismatches(w, g, f"w{rank}_s0_")
+        assert bad == [], bad
+        for c, e in enumerate(U.grid_errors(w.grid.vel, g[f"w{rank}_s0_vel"])):
+            assert e <= U.GRID_RTOL, ("vel", rank, c, e)
+    for s in range(1, 24):
+        w.run_step(s)
+    if w._pending_gather:
+        w._flush_gather()
+    flat, ids = w.store.state_with_ids()
+    # collect everything on rank 0
+    parts = [None] * world
+    dist.all_gather_object(parts, (flat, ids, list(w.rebuild_steps), int(w.halo_rows_sent)))
+    if rank == 0:
+        flat = np.concatenate([p[0] for p in parts])
+        ids = np.concatenate([p[1] for p in parts])
+        state = flat[np.argsort(ids, kind="stable")]
+        edge = float(g["pos"].max() - g["pos"].min())
+        ex, ev, ef, ec = U.particle_errors(state, g["state_24"], edge, 9)
+        print(f"dist_check world={world} transfer={transfer} x {ex:.2e} v {ev:.2e} F {ef:.2e} "
+              f"rebuilds {[p[2] for p in parts]} halo_rows {[p[3] for p in parts]}")
+        if transfer == "split":
+            assert ex <= U.X_RTOL_RUN and ev <= U.V_RTOL_RUN and ef <= U.F_ATOL_RUN, (ex, ev, ef)
+            if world == 2:
+                assert parts[0][2] == list(g["rebuild_steps0"]) and parts[1][2] == list(g["rebuild_steps1"])
+        else:
+            assert ex <= 10 * U.X_RTOL_RUN and ev <= 10 * U.V_RTOL_RUN, (ex, ev)
+        assert all(p[3] > 0 for p in parts)
+        print("DIST_CHECK_OK")
+    dist.barrier()
+    dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

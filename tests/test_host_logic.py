@@ -1,0 +1,144 @@
+"""CPU tests of the host side: C-ABI surface, value types, partitioning, growth policy, scenes.
+No compute call is made (there is no GPU here); the CUDA path must fail loudly instead of
+falling back."""
+import ctypes
+import os
+import re
+import subprocess
+
+import numpy as np
+import pytest
+
+from oracle import mpm_oracle as O
+import paper_2111_00699_b200 as P
+from paper_2111_00699_b200 import _capi, memory, scenes
+from paper_2111_00699_b200.build import build as build_core
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+HEADER = os.path.join(ROOT, "include", "mpm_b200.h")
+
+
+def _declared_functions():
+    text = open(HEADER).read()
+    text = re.sub(r"/\*.*?\*/", "", text, flags=re.S)
+    return sorted(set(re.findall(r"\b(mpm_[a-z0-9_]+)\s*\(", text)))
+
+
+def test_library_exports_every_declared_symbol():
+    build_core()
+    lib = ctypes.CDLL(_capi.LIB_PATH)
+    names = _declared_functions()
+    assert len(names) >= 20
+    for name in names:
+        assert hasattr(lib, name), f"{name} declared in include/mpm_b200.h but not exported"
+    # and the binding covers exactly the declared surface
+    assert sorted(_capi.EXPORTED_SYMBOLS) == names
+
+
+def test_ctypes_structs_match_the_header(tmp_path):
+    src = tmp_path / "sizes.c"
+    src.write_text('#include <stdio.h>\n#include "mpm_b200.h"\nint main(void){printf("%zu %zu %zu %zu %zu %zu\\n",'
+                   'sizeof(mpm_transfer_params),sizeof(mpm_store_view),sizeof(mpm_table_view),'
+                   'sizeof(mpm_step_status),sizeof(mpm_grid_params),sizeof(mpm_guard));return 0;}\n')
+    exe = tmp_path / "sizes"
+    subprocess.check_call(["gcc", "-I", os.path.join(ROOT, "include"), "-o", str(exe), str(src)])
+    sizes = [int(x) for x in subprocess.check_output([str(exe)]).split()]
+    assert sizes == [ctypes.sizeof(_capi.TransferParams), ctypes.sizeof(_capi.StoreView),
+                     ctypes.sizeof(_capi.TableView), ctypes.sizeof(_capi.StepStatus),
+                     ctypes.sizeof(_capi.GridParams), ctypes.sizeof(_capi.Guard)]
+
+
+def test_no_cpu_fallback_without_a_device():
+    import torch
+    if torch.cuda.is_available():
+        pytest.skip("a CUDA device is present")
+    from paper_2111_00699_b200.worker import CudaWorker
+    with pytest.raises(P.ResourceError):
+        CudaWorker(0, P.SharedRuntime(1), P.SimParams(dx=0.5, dt=1e-4),
+                   P.Material.fixed_corotated(2.0, 1e5, 0.3), None)
+
+
+def test_product_package_never_imports_the_oracle():
+    pkg = os.path.join(ROOT, "paper_2111_00699_b200")
+    for dirpath, _, files in os.walk(pkg):
+        for f in files:
+            if f.endswith((".py", ".cu", ".cuh")):
+                text = open(os.path.join(dirpath, f)).read()
+                assert "import oracle" not in text and "from oracle" not in text, f
+                assert "mpm_oracle" not in text, f
+
+
+def test_partition_matches_reference_restatement(rng):
+    # multiworker.py:114-137 / tests/test_multiworker.py: sizes differ by <= 1, remainder from worker 0
+    pos = rng.uniform(0, 1, (1003, 3)) * np.array([1.0, 5.0, 2.0])
+    for n in (1, 2, 3, 4, 8):
+        a, b = P.partition_particles(pos, n), O.partition_particles(pos, n)
+        assert all(np.array_equal(x, y) for x, y in zip(a, b))
+        sizes = [len(x) for x in a]
+        assert max(sizes) - min(sizes) <= 1 and sizes == sorted(sizes, reverse=True)
+        assert np.array_equal(np.sort(np.concatenate(a)), np.arange(1003))
+        # slabs along the longest axis (y)
+        for lo, hi in zip(a[:-1], a[1:]):
+            assert pos[lo, 1].max() <= pos[hi, 1].min()
+    with pytest.raises(P.RejectedInputError):
+        P.partition_particles(pos, 0)
+    assert [len(x) for x in P.partition_particles(np.zeros((0, 3)), 3)] == [0, 0, 0]
+
+
+def test_growth_policy():
+    # memory.py:18-22
+    assert memory.grown_capacity(0, 0) == 0
+    assert memory.grown_capacity(0, 10) == 40
+    assert memory.grown_capacity(40, 20) == 40
+    assert memory.grown_capacity(40, 21) == 84
+
+
+def test_runtime_vmax_ring_and_efficiency():
+    rt = P.SharedRuntime(3, initial_vmax=2.0)
+    rt.publish_vmax(4, 1, 9.0)
+    assert rt.global_vmax(1) == 9.0 and rt.global_vmax(0) == 2.0
+    assert P.efficiency(100.0, 30.0, 4).e == pytest.approx(100.0 / 120.0)
+    with pytest.raises(P.RejectedInputError):
+        P.efficiency(0.0, 1.0, 2)
+
+
+def test_value_types_validate_like_the_reference():
+    with pytest.raises(P.RejectedInputError):
+        P.SimParams(dx=0.0, dt=1e-4)
+    with pytest.raises(P.RejectedInputError):
+        P.SimParams(dx=0.5, dt=1e-4, lane_width=24)
+    with pytest.raises(P.ConfigError):
+        P.PipelineOptions(transfer="fused")
+    with pytest.raises(P.ConfigError):
+        P.BoundaryBox((0, 0, 0), (1, 1, 0))
+    m = P.Material.fixed_corotated(2.0, 1.0e5, 0.3)
+    assert m.mu == pytest.approx(1.0e5 / 2.6) and m.lam == pytest.approx(1.0e5 * 0.3 / (1.3 * 0.4))
+    assert P.Material.fluid(1.0, 1.0e5).sound_speed() == pytest.approx(np.sqrt(7.0e5))
+    p = P.SimParams(dx=0.5, dt=1e-4, cfl=0.5)
+    assert P.cfl_dt(100.0, p, 1.0) == pytest.approx(0.5 * 0.5 / 100.0)
+    assert P.cfl_dt(0.0, p, 0.01) == 0.01
+    assert not P.free_zone_check((1.0, 1.0, 1.0), (0.0, 0.0, 0.0), 0.5)
+    assert P.free_zone_check((6.5 * 0.5, 1.0, 1.0), (0.0, 0.0, 0.0), 0.5)
+
+
+def test_scene_counts_and_reproducibility():
+    # tests/test_bench.py:14-24 of the reference: 55 296 / 389 344 / 12 459 008 particles
+    assert len(scenes.sand_blocks(l=12, boxes=4).positions) == 55296
+    assert 4 * 23 ** 3 * 8 == 389344 and 16 * 46 ** 3 * 8 == 12459008
+    a = scenes.sand_blocks(l=6, boxes=4, seed=5)
+    b = scenes.sand_blocks(l=6, boxes=4, seed=5)
+    assert np.array_equal(a.positions, b.positions)
+    assert a.particle_mass == pytest.approx(2.0 * (25 / 64) ** 3 / 8)
+    lo, hi = np.array(a.boundary.min_corner), np.array(a.boundary.max_corner)
+    assert (a.positions > lo).all() and (a.positions < hi).all()
+    # stratified: exactly ppc samples in every occupied cell
+    cells = np.floor(a.positions / a.params.dx).astype(np.int64)
+    _, counts = np.unique(cells, axis=0, return_counts=True)
+    assert (counts == 8).all()
+    f = scenes.fountain()
+    pos, vel = f.emission.sample(3)
+    pos2, _ = f.emission.sample(3)
+    assert len(pos) == f.emission.per_frame == 27 * len(f.emission.cells) and np.array_equal(pos, pos2)
+    assert (vel[:, 2] == 160.0).all()
+    s = scenes.snow(l=5, boxes=1)
+    assert len(s.positions) == 1000 and s.params.dx == 1.35
