@@ -255,7 +255,7 @@ def run_ours(args):
         barrier()
         dt_e2e = max_over_ranks((time.perf_counter() - t0) / k_e2e)
         e2e = {"value": round(n * spf / dt_e2e / 1e6, 2), "unit": UNIT,
-               "h2d_bytes_per_step": int(n_local * (w2.store.nch * 4 + 8)),
+               "h2d_bytes_per_step": int(n_local * (7 * 4 + 8)),   # x3, v3, m fp32 + id int64
                "d2h_bytes_per_step": int(out_pos.nbytes + out_ids.nbytes),
                "ms_per_step": round(dt_e2e * 1e3, 3), "steps": k_e2e,
                "api": "CudaWorker.replace_particles(host) + run_frame() + store.positions_with_ids()"}

@@ -259,6 +259,8 @@ int mpm_status_reset(mpm_step_status *status, const mpm_guard *guard, void *stre
 /* ParticleStore.positions_with_ids / state readback (particles.py:466-475): all stored
  * lanes (quarantined included) in (group, lane) order as flat[n][nch] + ids[n]. */
 int mpm_gather_state(const mpm_store_view *store, float *flat, int64_t *ids, void *stream);
+/* positions only: pos[n][3] + ids[n] (the per-frame snapshot readback, bench.py:398-403). */
+int mpm_gather_positions(const mpm_store_view *store, float *pos, int64_t *ids, void *stream);
 
 /* total_mass / total_momentum (particles.py:477-487) and kinetic energy, accumulated in
  * float64: out[0]=mass, out[1..3]=momentum, out[4]=kinetic energy. */

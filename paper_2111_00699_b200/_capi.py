@@ -13,7 +13,7 @@ import os
 from . import errors as E
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libmpm_b200.so")
+LIB_PATH = os.environ.get("MPM_B200_LIB", os.path.join(_HERE, "libmpm_b200.so"))   # override: kernel experiments
 
 MPM_MAX_PEERS = 15
 N_COUNTERS = 6
@@ -101,6 +101,7 @@ _SIGNATURES = {
     "mpm_g2p2g": [C.POINTER(StoreView), C.POINTER(TableView), p_void, p_void, p_void, p_void,
                   C.POINTER(TransferParams), p_void, C.POINTER(Guard), p_void],
     "mpm_gather_state": [C.POINTER(StoreView), p_void, p_void, p_void],
+    "mpm_gather_positions": [C.POINTER(StoreView), p_void, p_void, p_void],
     "mpm_particle_aggregates": [C.POINTER(StoreView), p_void, p_void],
     "mpm_grid_aggregates": [p_void, p_void, i32, p_void, p_void],
     "mpm_tag_shared": [p_void, i32, p_void, p_void, i32, p_void, i32, p_void],

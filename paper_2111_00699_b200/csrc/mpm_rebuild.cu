@@ -510,6 +510,24 @@ __global__ void __launch_bounds__(256) gather_state_kernel(const float *__restri
     out_ids[j] = ids[g * 32 + lane];
 }
 
+__global__ void __launch_bounds__(256) gather_positions_kernel(const float *__restrict__ data,
+                                                               const long long *__restrict__ ids, int nch,
+                                                               const int *__restrict__ group_len,
+                                                               const int *__restrict__ group_start,
+                                                               int n_groups, float *__restrict__ pos,
+                                                               long long *__restrict__ out_ids)
+{
+    const int g = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    const int lane = threadIdx.x & 31;
+    if (g >= n_groups || lane >= group_len[g]) return;
+    const size_t j = (size_t)group_start[g] + lane;
+    const float *src = data + (size_t)g * nch * 32 + lane;
+    pos[j * 3 + 0] = src[(CH_POS + 0) * 32];
+    pos[j * 3 + 1] = src[(CH_POS + 1) * 32];
+    pos[j * 3 + 2] = src[(CH_POS + 2) * 32];
+    out_ids[j] = ids[g * 32 + lane];
+}
+
 __global__ void __launch_bounds__(256) tag_shared_kernel(const long long *__restrict__ peer_codes,
                                                          int n_peer, const long long *__restrict__ hkeys,
                                                          const int *__restrict__ hvals, int shift,
@@ -685,6 +703,17 @@ int mpm_gather_state(const mpm_store_view *store, float *flat, int64_t *ids, voi
         store->data, (const long long *)store->orig_id, store->nch, store->group_len,
         store->group_start, G, flat, (long long *)ids);
     return check_launch("mpm_gather_state", 1);
+}
+
+int mpm_gather_positions(const mpm_store_view *store, float *pos, int64_t *ids, void *stream_)
+{
+    cudaStream_t stream = (cudaStream_t)stream_;
+    const int G = store->n_groups;
+    if (G <= 0) return MPM_OK;
+    gather_positions_kernel<<<nblk((int64_t)G * 32, 256), 256, 0, stream>>>(
+        store->data, (const long long *)store->orig_id, store->nch, store->group_len,
+        store->group_start, G, pos, (long long *)ids);
+    return check_launch("mpm_gather_positions", 1);
 }
 
 int mpm_tag_shared(const int64_t *peer_codes, int32_t n_peer_codes, const int64_t *hkeys,

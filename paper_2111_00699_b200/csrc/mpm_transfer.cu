@@ -37,7 +37,13 @@ struct TransferArgs {
     DevGuard guard;
 };
 
-constexpr int TW = 8;   // warps (groups) per CTA
+#ifndef MPM_TW
+#define MPM_TW 8
+#endif
+#ifndef MPM_MINBLOCKS
+#define MPM_MINBLOCKS 3
+#endif
+constexpr int TW = MPM_TW;   // warps (groups) per CTA
 
 __device__ __forceinline__ void red_add_v4(float4 *addr, float a, float b, float c, float d)
 {
@@ -185,7 +191,7 @@ __device__ __forceinline__ void gather27_delta(const float4 *__restrict__ vel,
 }
 
 template <int MAT, bool GATHER, bool SCATTER>
-__global__ void __launch_bounds__(TW * 32, 3) transfer_kernel(const TransferArgs a)
+__global__ void __launch_bounds__(TW * 32, MPM_MINBLOCKS) transfer_kernel(const TransferArgs a)
 {
     if (guarded_out(a.guard)) return;
     __shared__ int s_nrow[TW][28];

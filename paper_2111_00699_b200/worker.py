@@ -78,6 +78,7 @@ class CudaParticleStore:
         self._staged = []
         self.staged_count = 0
         self._next_id = 0
+        self._pin = {}
         self._table = None   # set by the worker: group_origin comes from the block table
 
     # -- views for the C ABI --
@@ -100,6 +101,8 @@ class CudaParticleStore:
         return np.tile(np.eye(3, dtype=np.float32).reshape(9), (n, 1))
 
     def stage_append(self, positions, velocities, masses, deformation=None, affine=None, ids=None):
+        """Queue host particles for the next rebuild (particles.py:309-334).  Arrays are kept
+        compact (x, v, m [, F|J, C]); the channel rows are laid out on the device."""
         pos = np.atleast_2d(np.asarray(positions))
         n = pos.shape[0]
         if n == 0:
@@ -109,39 +112,79 @@ class CudaParticleStore:
         vel = np.atleast_2d(np.asarray(velocities))
         if vel.shape != pos.shape:
             raise RejectedInputError(f"velocities must have shape {pos.shape}, got {vel.shape}")
-        flat = np.zeros((n, self.nch), dtype=np.float32)
-        flat[:, CH_POS:CH_POS + 3] = pos
-        flat[:, CH_VEL:CH_VEL + 3] = vel
-        if affine is not None:
-            flat[:, CH_C:CH_C + 9] = np.asarray(affine).reshape(n, 9)
-        flat[:, CH_MASS] = np.broadcast_to(np.asarray(masses), (n,))
-        defo = self.default_deformation(n) if deformation is None \
-            else np.asarray(deformation, dtype=np.float32).reshape(n, -1)
-        flat[:, CH_DEF:CH_DEF + defo.shape[1]] = defo
-        if self.nch > CH_PLASTIC:
-            flat[:, CH_PLASTIC] = 1.0 if self.kind == MaterialKind.SNOW else 0.0
+        pos = np.ascontiguousarray(pos, dtype=np.float32)
+        vel = np.ascontiguousarray(vel, dtype=np.float32)
+        mass = np.asarray(masses, dtype=np.float32)
+        if mass.ndim:
+            mass = np.ascontiguousarray(np.broadcast_to(mass, (n,)))
+        defo = None if deformation is None else \
+            np.ascontiguousarray(np.asarray(deformation, dtype=np.float32).reshape(n, -1))
+        aff = None if affine is None else \
+            np.ascontiguousarray(np.asarray(affine, dtype=np.float32).reshape(n, 9))
         if ids is None:
             ids = np.arange(self._next_id, self._next_id + n, dtype=np.int64)
             self._next_id += n
         else:
-            ids = np.asarray(ids, dtype=np.int64).reshape(n)
+            ids = np.ascontiguousarray(np.asarray(ids, dtype=np.int64).reshape(n))
             self._next_id = max(self._next_id, int(ids.max()) + 1)
-        self._staged.append((flat, ids))
+        self._staged.append((pos, vel, mass, defo, aff, ids))
         self.staged_count += n
         return n
 
+    def _pinned(self, tag, shape, dtype):
+        """Grow-only pinned host staging buffers (reused across uploads / readbacks)."""
+        need = int(np.prod(shape))
+        buf = self._pin.get(tag)
+        if buf is None or buf.numel() < need or buf.dtype != dtype:
+            buf = self._pin[tag] = torch.empty(max(need, 1), dtype=dtype).pin_memory()
+        return buf[:need].view(*shape)
+
     def take_staged(self):
-        """Staged host arrays as pinned -> device tensors (flat fp32 [n, nch], ids int64 [n])."""
+        """Upload the staged particles: pinned host buffers -> device, then the flat channel rows
+        [n, nch] (fp32) and ids [n] that the rebuild kernels read."""
         if not self._staged:
             return None, None, 0
-        flat = np.concatenate([s[0] for s in self._staged], axis=0)
-        ids = np.concatenate([s[1] for s in self._staged], axis=0)
-        self._staged.clear()
         n = self.staged_count
+        dev = self.device
+        hpos = self._pinned("pos", (n, 3), torch.float32)
+        hvel = self._pinned("vel", (n, 3), torch.float32)
+        hids = self._pinned("ids", (n,), torch.int64)
+        hmass = self._pinned("mass", (n,), torch.float32)
+        o = 0
+        extras = []
+        for pos, vel, mass, defo, aff, ids in self._staged:
+            k = len(ids)
+            hpos[o:o + k].copy_(torch.from_numpy(pos))
+            hvel[o:o + k].copy_(torch.from_numpy(vel))
+            hids[o:o + k].copy_(torch.from_numpy(ids))
+            if mass.ndim:
+                hmass[o:o + k].copy_(torch.from_numpy(mass))
+            else:
+                hmass[o:o + k].fill_(float(mass))
+            if defo is not None or aff is not None:
+                extras.append((o, k, defo, aff))
+            o += k
+        self._staged.clear()
         self.staged_count = 0
-        dflat = torch.from_numpy(flat).pin_memory().to(self.device, non_blocking=True)
-        dids = torch.from_numpy(ids).pin_memory().to(self.device, non_blocking=True)
-        return dflat, dids, n
+        flat = torch.zeros((n, self.nch), dtype=torch.float32, device=dev)
+        flat[:, CH_POS:CH_POS + 3] = hpos.to(dev, non_blocking=True)
+        flat[:, CH_VEL:CH_VEL + 3] = hvel.to(dev, non_blocking=True)
+        flat[:, CH_MASS] = hmass.to(dev, non_blocking=True)
+        if self.kind == MaterialKind.WEAKLY_COMPRESSIBLE_FLUID:
+            flat[:, CH_DEF] = 1.0
+        else:
+            flat[:, CH_DEF] = 1.0
+            flat[:, CH_DEF + 4] = 1.0
+            flat[:, CH_DEF + 8] = 1.0
+        if self.nch > CH_PLASTIC:
+            flat[:, CH_PLASTIC] = 1.0 if self.kind == MaterialKind.SNOW else 0.0
+        for o, k, defo, aff in extras:
+            if defo is not None:
+                flat[o:o + k, CH_DEF:CH_DEF + defo.shape[1]] = torch.from_numpy(defo).to(dev)
+            if aff is not None:
+                flat[o:o + k, CH_C:CH_C + 9] = torch.from_numpy(aff).to(dev)
+        dids = hids.to(dev, non_blocking=True)
+        return flat, dids, n
 
     # -- readback (lazy D2H views in the reference's layout / dtype) --
     def _g(self, bufs):
@@ -197,14 +240,19 @@ class CudaParticleStore:
         """particles.py:466-475: positions of every stored particle (quarantined included) and
         their ids, in (group, lane) order."""
         n = self.count
-        flat = torch.empty((max(n, 1), self.nch), dtype=torch.float32, device=self.device)
-        ids = torch.empty(max(n, 1), dtype=torch.int64, device=self.device)
-        if n:
-            v = self.view()
-            check(_capi.lib().mpm_gather_state(C.byref(v), flat.data_ptr(), ids.data_ptr(),
-                                               _stream_ptr()), "mpm_gather_state")
-        pos = flat[:n, CH_POS:CH_POS + 3].contiguous().cpu().numpy()
-        return pos.astype(dtype, copy=False), ids[:n].cpu().numpy()
+        if not n:
+            return np.zeros((0, 3), dtype=dtype), np.zeros(0, dtype=np.int64)
+        pos = torch.empty((n, 3), dtype=torch.float32, device=self.device)
+        ids = torch.empty(n, dtype=torch.int64, device=self.device)
+        v = self.view()
+        check(_capi.lib().mpm_gather_positions(C.byref(v), pos.data_ptr(), ids.data_ptr(),
+                                               _stream_ptr()), "mpm_gather_positions")
+        hpos = self._pinned("out_pos", (n, 3), torch.float32)
+        hids = self._pinned("out_ids", (n,), torch.int64)
+        hpos.copy_(pos, non_blocking=True)
+        hids.copy_(ids, non_blocking=True)
+        torch.cuda.current_stream().synchronize()
+        return hpos.numpy().astype(dtype), hids.numpy().copy()
 
     def _aggregates(self):
         out = torch.zeros(5, dtype=torch.float64, device=self.device)
