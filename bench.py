@@ -64,9 +64,9 @@ def build_world(scene):
     raise ValueError(scene)
 
 
-# the plastic snow model is used once the CUDA core implements it; until then the
-# reference-pinned fixed-corotated variant of the same scene is timed and named as such
-SNOW_PLASTIC = False
+# headline scene: snow with the clamp+hardening plasticity (parity unpinned: no reference model);
+# --scene snow_fc times the reference-pinned fixed-corotated variant of the same scene
+SNOW_PLASTIC = True
 
 
 class ClockSampler:

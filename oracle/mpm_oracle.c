@@ -6,7 +6,13 @@
  * and bench.py's cpu_baseline / --impl reference legs may load it.  The product path
  * (paper_2111_00699_b200) never links or calls anything in oracle/.
  *
- * Parity status: PINNED.  tests/test_oracle_golden.py checks every function here
+ * Parity status: PINNED for material kinds 0 (weakly compressible fluid) and 1 (fixed
+ * corotated), see below.  Kinds 2 (snow: singular-value clamp + hardening) and 3 (sand:
+ * Drucker-Prager return mapping) DO NOT EXIST IN THE REFERENCE: their
+ * float64 statement below is this repository's own definition of those models --
+ * "parity unpinned" -- built on the reference's SVD (orc_svd3) and transfer structure.
+ *
+ * Parity status of kinds 0/1: PINNED.  tests/test_oracle_golden.py checks every function here
  * bit-for-bit against arrays dumped from the reference itself
  * (tests/golden/make_golden.py, run in the build container against /root/reference)
  * and against the reference tests' own known-answer vectors.
@@ -430,7 +436,86 @@ typedef struct {
     i64 clamp_tension;
     double density, dx;
     i64 det, do_lane_sort;
+    /* plastic kinds only (not in the reference) */
+    double theta_c, theta_s, hardening, sand_alpha;
 } OrcTransferParams;
+
+#define CH_PLASTIC 25
+
+/* ---- plastic models (kinds 2, 3): this repository's float64 definition, unpinned ---------
+ * Snow (Stomakhin et al. 2013): F_trial = U S V^T, S' = clamp(S, 1-theta_c, 1+theta_s),
+ *   F_E = U S' V^T, Jp <- clamp(Jp * prod(S) / prod(S'), 0.1, 10);
+ *   stress = fixed-corotated on F_E with mu, lam scaled by exp(hardening * (1 - Jp)).
+ * Sand (Klar et al. 2016, Drucker-Prager): e = log|S|, tr = sum e, dev = e - tr/3;
+ *   tr > 0 or |dev| == 0 -> S' = I (and the plastic scalar accumulates tr);
+ *   dg = |dev| + (3 lam + 2 mu) / (2 mu) * tr * alpha; dg <= 0 -> S' = S;
+ *   else S' = exp(e - dg dev / |dev|).  Stress = U (2 mu e' + lam tr(e') I) U^T, e' = log S'. */
+void orc_snow_project(double *F, double *Jp, double theta_c, double theta_s)
+{
+    double u[9], s[3], v[9], sc[3];
+    orc_svd3(F, u, s, v);
+    double num = s[0] * s[1] * s[2], den = 1.0;
+    for (int k = 0; k < 3; ++k) {
+        double c = s[k];
+        if (c < 1.0 - theta_c) c = 1.0 - theta_c;
+        if (c > 1.0 + theta_s) c = 1.0 + theta_s;
+        sc[k] = c;
+        den *= c;
+    }
+    for (int a = 0; a < 3; ++a)
+        for (int b = 0; b < 3; ++b)
+            F[3 * a + b] = sc[0] * u[3 * a] * v[3 * b] + sc[1] * u[3 * a + 1] * v[3 * b + 1] +
+                           sc[2] * u[3 * a + 2] * v[3 * b + 2];
+    double j = *Jp * num / den;
+    if (!(j > 0.1)) j = 0.1;
+    if (j > 10.0) j = 10.0;
+    *Jp = j;
+}
+
+void orc_sand_project(double *F, double *vc, double mu, double lam, double alpha)
+{
+    double u[9], s[3], v[9], e[3], sc[3];
+    orc_svd3(F, u, s, v);
+    for (int k = 0; k < 3; ++k) {
+        double a = fabs(s[k]);
+        e[k] = log(a > 1e-6 ? a : 1e-6);
+    }
+    double tr = e[0] + e[1] + e[2];
+    double d0 = e[0] - tr / 3.0, d1 = e[1] - tr / 3.0, d2 = e[2] - tr / 3.0;
+    double dn = sqrt(d0 * d0 + d1 * d1 + d2 * d2);
+    if (tr > 0.0 || dn == 0.0) {
+        sc[0] = sc[1] = sc[2] = 1.0;
+        *vc += tr;
+    } else {
+        double dg = dn + (3.0 * lam + 2.0 * mu) / (2.0 * mu) * tr * alpha;
+        if (dg <= 0.0) { sc[0] = fabs(s[0]); sc[1] = fabs(s[1]); sc[2] = fabs(s[2]); if (sc[0] < 1e-6) sc[0] = 1e-6; if (sc[1] < 1e-6) sc[1] = 1e-6; if (sc[2] < 1e-6) sc[2] = 1e-6; }
+        else {
+            sc[0] = exp(e[0] - dg * d0 / dn);
+            sc[1] = exp(e[1] - dg * d1 / dn);
+            sc[2] = exp(e[2] - dg * d2 / dn);
+        }
+    }
+    for (int a = 0; a < 3; ++a)
+        for (int b = 0; b < 3; ++b)
+            F[3 * a + b] = sc[0] * u[3 * a] * v[3 * b] + sc[1] * u[3 * a + 1] * v[3 * b + 1] +
+                           sc[2] * u[3 * a + 2] * v[3 * b + 2];
+}
+
+void orc_sand_tau(const double *F, double mu, double lam, double *t)
+{
+    double u[9], s[3], v[9], e[3], d[3];
+    orc_svd3(F, u, s, v);
+    for (int k = 0; k < 3; ++k) {
+        double a = fabs(s[k]);
+        e[k] = log(a > 1e-6 ? a : 1e-6);
+    }
+    double tr = e[0] + e[1] + e[2];
+    for (int k = 0; k < 3; ++k) d[k] = 2.0 * mu * e[k] + lam * tr;
+    for (int a = 0; a < 3; ++a)
+        for (int b = 0; b < 3; ++b)
+            t[3 * a + b] = d[0] * u[3 * a] * u[3 * b] + d[1] * u[3 * a + 1] * u[3 * b + 1] +
+                           d[2] * u[3 * a + 2] * u[3 * b + 2];
+}
 
 #define MAXLW 64
 typedef struct {
@@ -482,10 +567,20 @@ static void scatter_prep(double *data, u8 *quarantined, i64 g, i64 L, const OrcT
             S->Q[l][0] += coeff * tau;
             S->Q[l][4] += coeff * tau;
             S->Q[l][8] += coeff * tau;
-        } else {
+        } else if (P->mat_kind == 1) {
             double F[9], t[9];
             for (int r = 0; r < 9; ++r) F[r] = dg[(CH_DEF + r) * LW + l];
             if (orc_corotated_tau(F, P->mu, P->lam, t)) counters[C_SVD_CLAMP] += 1;
+            for (int r = 0; r < 9; ++r) S->Q[l][r] = m * dg[(CH_C + r) * LW + l] + coeff * t[r];
+        } else {
+            double F[9], t[9];
+            for (int r = 0; r < 9; ++r) F[r] = dg[(CH_DEF + r) * LW + l];
+            if (P->mat_kind == 2) {
+                double h = exp(P->hardening * (1.0 - dg[CH_PLASTIC * LW + l]));
+                if (orc_corotated_tau(F, P->mu * h, P->lam * h, t)) counters[C_SVD_CLAMP] += 1;
+            } else {
+                orc_sand_tau(F, P->mu, P->lam, t);
+            }
             for (int r = 0; r < 9; ++r) S->Q[l][r] = m * dg[(CH_C + r) * LW + l] + coeff * t[r];
         }
         S->valid[l] = 1;
@@ -683,10 +778,20 @@ void orc_gather_advect(double *data, i64 *lane_key, u8 *quarantined, const i32 *
                 for (int r = 0; r < 9; ++r) F[r] = dg[(CH_DEF + r) * LW + l];
                 for (int r = 0; r < 9; ++r) A[r] = dt * c[r];
                 A[0] = 1.0 + dt * c[0]; A[4] = 1.0 + dt * c[4]; A[8] = 1.0 + dt * c[8];
+                double Fn[9];
                 for (int a = 0; a < 3; ++a)
                     for (int b = 0; b < 3; ++b)
-                        dg[(CH_DEF + 3 * a + b) * LW + l] =
-                            A[3 * a] * F[b] + A[3 * a + 1] * F[3 + b] + A[3 * a + 2] * F[6 + b];
+                        Fn[3 * a + b] = A[3 * a] * F[b] + A[3 * a + 1] * F[3 + b] + A[3 * a + 2] * F[6 + b];
+                if (P->mat_kind == 2) {
+                    double jp = dg[CH_PLASTIC * LW + l];
+                    orc_snow_project(Fn, &jp, P->theta_c, P->theta_s);
+                    dg[CH_PLASTIC * LW + l] = jp;
+                } else if (P->mat_kind == 3) {
+                    double vc = dg[CH_PLASTIC * LW + l];
+                    orc_sand_project(Fn, &vc, P->mu, P->lam, P->sand_alpha);
+                    dg[CH_PLASTIC * LW + l] = vc;
+                }
+                for (int r = 0; r < 9; ++r) dg[(CH_DEF + r) * LW + l] = Fn[r];
             }
             if (npx < zx0 || npx >= zx1 || npy < zy0 || npy >= zy1 || npz < zz0 || npz >= zz1)
                 out_stats[0] = 1.0;

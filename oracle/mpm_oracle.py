@@ -65,7 +65,9 @@ class _TransferParams(C.Structure):
                 ("mu", C.c_double), ("lam", C.c_double), ("kappa", C.c_double),
                 ("gamma", C.c_double), ("clamp_tension", C.c_int64),
                 ("density", C.c_double), ("dx", C.c_double),
-                ("det", C.c_int64), ("do_lane_sort", C.c_int64)]
+                ("det", C.c_int64), ("do_lane_sort", C.c_int64),
+                ("theta_c", C.c_double), ("theta_s", C.c_double), ("hardening", C.c_double),
+                ("sand_alpha", C.c_double)]
 
 
 _lib = None
@@ -327,7 +329,8 @@ class OracleStore:
     def __init__(self, kind, lane_width=32):
         self.kind = int(kind)
         self.lane_width = int(lane_width)
-        self.nch = 17 if self.kind == 0 else 25
+        # kinds 2/3 (snow, sand: not in the reference) carry one plastic scalar in channel 25
+        self.nch = 17 if self.kind == 0 else (25 if self.kind == 1 else 26)
         LW = self.lane_width
         self.data = np.zeros((1, self.nch, LW))
         self.orig_id = np.zeros((1, LW), dtype=np.int64)
@@ -394,6 +397,8 @@ class OracleStore:
             flat[n:n + m, CH_C:CH_C + 9] = Cm
             flat[n:n + m, CH_MASS] = mass
             flat[n:n + m, CH_DEF:CH_DEF + defo.shape[1]] = defo
+            if self.nch > 25 and defo.shape[1] <= 9:
+                flat[n:n + m, 25] = 1.0 if self.kind == 2 else 0.0
             ids[n:n + m] = sid
             n += m
         self._staged.clear()
@@ -546,7 +551,11 @@ class OracleWorker:
             mu=float(m.mu), lam=float(m.lam), kappa=float(m.bulk_modulus), gamma=float(m.gamma),
             clamp_tension=int(bool(m.clamp_tension)), density=float(m.density),
             dx=float(params.dx), det=int(bool(self.options.deterministic)),
-            do_lane_sort=int(self.options.sort != "none_between"))
+            do_lane_sort=int(self.options.sort != "none_between"),
+            theta_c=float(getattr(m, "theta_c", 0.0)), theta_s=float(getattr(m, "theta_s", 0.0)),
+            hardening=float(getattr(m, "hardening", 0.0)),
+            sand_alpha=math.sqrt(2.0 / 3.0) * 2.0 * math.sin(math.radians(getattr(m, "friction_angle", 30.0)))
+            / (3.0 - math.sin(math.radians(getattr(m, "friction_angle", 30.0)))))
 
     # -- population --
     def seed_particles(self, positions, velocities, masses, ids):

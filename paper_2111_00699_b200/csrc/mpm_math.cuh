@@ -17,9 +17,11 @@ __device__ __forceinline__ float det3(const float *f)
            f[2] * (f[3] * f[7] - f[4] * f[6]);
 }
 
-// One Jacobi rotation zeroing a_pq (domain.py:232-303).  vp/vq: columns p,q of V (stride 3).
+// One Jacobi rotation zeroing a_pq (domain.py:232-303).  P, Q: columns of V it mixes
+// (compile-time so that V stays in registers).
+template <int P, int Q>
 __device__ __forceinline__ void jacobi_rotate(float &app, float &aqq, float &apq, float &arp,
-                                              float &arq, float *vp, float *vq)
+                                              float &arq, float *v)
 {
     const float a_pq = apq;
     const float theta = 0.5f * (aqq - app) / a_pq;
@@ -36,9 +38,9 @@ __device__ __forceinline__ void jacobi_rotate(float &app, float &aqq, float &apq
     arq = s * rp + c * rq;
 #pragma unroll
     for (int k = 0; k < 3; ++k) {
-        const float tmp = vp[3 * k];
-        vp[3 * k] = c * tmp - s * vq[3 * k];
-        vq[3 * k] = s * tmp + c * vq[3 * k];
+        const float tmp = v[3 * k + P];
+        v[3 * k + P] = c * tmp - s * v[3 * k + Q];
+        v[3 * k + Q] = s * tmp + c * v[3 * k + Q];
     }
 }
 
@@ -60,9 +62,9 @@ __device__ __forceinline__ void svd3(const float *f, float *u, float *s, float *
         if (m02 > big) { big = m02; pair = 1; }
         if (m12 > big) { big = m12; pair = 2; }
         if (big <= tol) break;
-        if (pair == 0) jacobi_rotate(a00, a11, a01, a02, a12, v + 0, v + 1);
-        else if (pair == 1) jacobi_rotate(a00, a22, a02, a01, a12, v + 0, v + 2);
-        else jacobi_rotate(a11, a22, a12, a01, a02, v + 1, v + 2);
+        if (pair == 0) jacobi_rotate<0, 1>(a00, a11, a01, a02, a12, v);
+        else if (pair == 1) jacobi_rotate<0, 2>(a00, a22, a02, a01, a12, v);
+        else jacobi_rotate<1, 2>(a11, a22, a12, a01, a02, v);
     }
     float w0 = a00, w1 = a11, w2 = a22, tmp;
 #define MPM_SWAPCOL(p, q)                                                                   \
@@ -196,6 +198,113 @@ __device__ __forceinline__ int corotated_tau(const float *f, float mu, float lam
             t[3 * a + b] = (a == b) ? acc + diag : acc;
         }
     return clamped;
+}
+
+// ---- plastic models (not in the reference; float64 definition in oracle/mpm_oracle.c) -------
+// Both return the Kirchhoff stress of the projected elastic state from its SVD:
+//   tau = U diag(d) U^T.
+struct PlasticParams {
+    float mu, lam, theta_c, theta_s, hardening, sand_alpha;
+};
+
+__device__ __forceinline__ void tau_from_principal(const float *u, const float *d, float *t)
+{
+#pragma unroll
+    for (int a = 0; a < 3; ++a)
+#pragma unroll
+        for (int b = 0; b < 3; ++b)
+            t[3 * a + b] = d[0] * u[3 * a] * u[3 * b] + d[1] * u[3 * a + 1] * u[3 * b + 1] +
+                           d[2] * u[3 * a + 2] * u[3 * b + 2];
+}
+
+__device__ __forceinline__ void rebuild_from_svd(const float *u, const float *sc, const float *v, float *f)
+{
+#pragma unroll
+    for (int a = 0; a < 3; ++a)
+#pragma unroll
+        for (int b = 0; b < 3; ++b)
+            f[3 * a + b] = sc[0] * u[3 * a] * v[3 * b] + sc[1] * u[3 * a + 1] * v[3 * b + 1] +
+                           sc[2] * u[3 * a + 2] * v[3 * b + 2];
+}
+
+// snow: fixed-corotated on F_E = U S' V^T with hardened moduli:
+//   (F_E - R) F_E^T = U (S' - I) S' U^T  =>  d_k = 2 mu_h (s_k - 1) s_k + lam_h (J - 1) J
+__device__ __forceinline__ void snow_principal(const float *sc, float jp, const PlasticParams &p, float *d)
+{
+    const float h = expf(p.hardening * (1.0f - jp));
+    const float J = sc[0] * sc[1] * sc[2];
+    const float diag = p.lam * h * (J - 1.0f) * J;
+#pragma unroll
+    for (int k = 0; k < 3; ++k) d[k] = 2.0f * p.mu * h * (sc[k] - 1.0f) * sc[k] + diag;
+}
+
+// sand: Hencky strain e = log S, d_k = 2 mu e_k + lam tr(e)
+__device__ __forceinline__ void sand_principal(const float *e, const PlasticParams &p, float *d)
+{
+    const float tr = e[0] + e[1] + e[2];
+#pragma unroll
+    for (int k = 0; k < 3; ++k) d[k] = 2.0f * p.mu * e[k] + p.lam * tr;
+}
+
+// Return mapping of the trial elastic deformation (in place), plastic scalar update, and the
+// stress of the projected state.  MAT: 2 snow, 3 sand.
+template <int MAT>
+__device__ __forceinline__ void plastic_project(float *f, float &plastic, const PlasticParams &p, float *tau)
+{
+    float u[9], s[3], v[9], sc[3], d[3];
+    svd3(f, u, s, v);
+    if (MAT == MPM_MAT_SNOW) {
+        const float num = s[0] * s[1] * s[2];
+        float den = 1.0f;
+#pragma unroll
+        for (int k = 0; k < 3; ++k) {
+            sc[k] = fminf(fmaxf(s[k], 1.0f - p.theta_c), 1.0f + p.theta_s);
+            den *= sc[k];
+        }
+        float j = plastic * num / den;
+        j = j > 0.1f ? j : 0.1f;
+        plastic = fminf(j, 10.0f);
+        snow_principal(sc, plastic, p, d);
+    } else {
+        float e[3];
+#pragma unroll
+        for (int k = 0; k < 3; ++k) e[k] = logf(fmaxf(fabsf(s[k]), 1e-6f));
+        const float tr = e[0] + e[1] + e[2];
+        const float d0 = e[0] - tr * (1.0f / 3.0f), d1 = e[1] - tr * (1.0f / 3.0f), d2 = e[2] - tr * (1.0f / 3.0f);
+        const float dn = sqrtf(d0 * d0 + d1 * d1 + d2 * d2);
+        if (tr > 0.0f || dn == 0.0f) {
+            e[0] = e[1] = e[2] = 0.0f;
+            plastic += tr;
+        } else {
+            const float dg = dn + (3.0f * p.lam + 2.0f * p.mu) / (2.0f * p.mu) * tr * p.sand_alpha;
+            if (dg > 0.0f) {
+                const float k = dg / dn;
+                e[0] -= k * d0; e[1] -= k * d1; e[2] -= k * d2;
+            }
+        }
+#pragma unroll
+        for (int k = 0; k < 3; ++k) sc[k] = expf(e[k]);
+        sand_principal(e, p, d);
+    }
+    rebuild_from_svd(u, sc, v, f);
+    tau_from_principal(u, d, tau);
+}
+
+// Stress of an already projected state (split P2G): one SVD of the stored F_E.
+template <int MAT>
+__device__ __forceinline__ void plastic_tau(const float *f, float plastic, const PlasticParams &p, float *tau)
+{
+    float u[9], s[3], v[9], d[3];
+    svd3(f, u, s, v);
+    if (MAT == MPM_MAT_SNOW) {
+        snow_principal(s, plastic, p, d);
+    } else {
+        float e[3];
+#pragma unroll
+        for (int k = 0; k < 3; ++k) e[k] = logf(fmaxf(fabsf(s[k]), 1e-6f));
+        sand_principal(e, p, d);
+    }
+    tau_from_principal(u, d, tau);
 }
 
 __device__ __forceinline__ float fluid_tau(float J, float kappa, float gamma, int clamp_tension)

@@ -169,25 +169,31 @@ __device__ __forceinline__ void gather27(const float4 *__restrict__ vel, const i
     }
 }
 
-// FLIP increment sum w (v_n - v_old_n) (pipeline.py:489-495); only evaluated when blending
-__device__ __forceinline__ void gather27_delta(const float4 *__restrict__ vel,
-                                               const float4 *__restrict__ vel_old, const int *nrow,
-                                               const AxisAddr &ax, const AxisAddr &ay, const AxisAddr &az,
-                                               const float *wx, const float *wy, const float *wz, float *dv)
+// FLIP increment sum w (v_n - v_old_n) (pipeline.py:489-495).  Only evaluated when blending,
+// kept out of line and rolled: its dynamically indexed copies of the weights / address terms
+// live in its own frame and cost the APIC path nothing.
+struct StencilCopy {
+    int nx[3], ny[3], nz[3], sx[3], sy[3], sz[3];
+    float wx[3], wy[3], wz[3];
+};
+__device__ __noinline__ void gather27_delta(const float4 *__restrict__ vel,
+                                            const float4 *__restrict__ vel_old, const int *nrow,
+                                            const StencilCopy st, float *dv)
 {
-    dv[0] = dv[1] = dv[2] = 0.f;
+    float d0 = 0.f, d1 = 0.f, d2 = 0.f;
 #pragma unroll 1
     for (int i = 0; i < 3; ++i)
 #pragma unroll 1
         for (int j = 0; j < 3; ++j)
-#pragma unroll
+#pragma unroll 1
             for (int k = 0; k < 3; ++k) {
-                const int nb = nrow[ax.nterm[i] + ay.nterm[j] + az.nterm[k]];
-                const size_t idx = (size_t)nb * 64 + (ax.sterm[i] | ay.sterm[j] | az.sterm[k]);
+                const int nb = nrow[st.nx[i] + st.ny[j] + st.nz[k]];
+                const size_t idx = (size_t)nb * 64 + (st.sx[i] | st.sy[j] | st.sz[k]);
                 const float4 vn = __ldg(&vel[idx]), vo = __ldg(&vel_old[idx]);
-                const float w = wx[i] * wy[j] * wz[k];
-                dv[0] += w * (vn.y - vo.y); dv[1] += w * (vn.z - vo.z); dv[2] += w * (vn.w - vo.w);
+                const float w = st.wx[i] * st.wy[j] * st.wz[k];
+                d0 += w * (vn.y - vo.y); d1 += w * (vn.z - vo.z); d2 += w * (vn.w - vo.w);
             }
+    dv[0] = d0; dv[1] = d1; dv[2] = d2;
 }
 
 template <int MAT, bool GATHER, bool SCATTER>
@@ -220,6 +226,9 @@ __global__ void __launch_bounds__(TW * 32, MPM_MINBLOCKS) transfer_kernel(const 
         float px = 0.f, py = 0.f, pz = 0.f, vx = 0.f, vy = 0.f, vz = 0.f;
         float C[9];
         float F[9];   // F (elastic kinds) or F[0] = J (fluid)
+        float tau[9]; // plastic kinds: stress of the projected state, produced by the gather
+        float plastic = 0.f;
+        const PlasticParams pp = {a.mu, a.lam, a.theta_c, a.theta_s, a.hardening, a.sand_alpha};
         int addr_err = 0;
         if (active) {
             px = gd[(CH_POS + 0) * 32]; py = gd[(CH_POS + 1) * 32]; pz = gd[(CH_POS + 2) * 32];
@@ -227,6 +236,7 @@ __global__ void __launch_bounds__(TW * 32, MPM_MINBLOCKS) transfer_kernel(const 
             else {
 #pragma unroll
                 for (int r = 0; r < 9; ++r) F[r] = gd[(CH_DEF + r) * 32];
+                if (MAT >= MPM_MAT_SNOW) plastic = gd[CH_PLASTIC * 32];
             }
         }
 
@@ -257,7 +267,14 @@ __global__ void __launch_bounds__(TW * 32, MPM_MINBLOCKS) transfer_kernel(const 
                     for (int r = 0; r < 9; ++r) C[r] = a.d_inv * G.B[r];
                     if (a.flip > 0.0f) {
                         float dv[3];
-                        gather27_delta(a.vel, a.vel_old, nrow, ax, ay, az, wx, wy, wz, dv);
+                        StencilCopy st;
+#pragma unroll
+                        for (int q = 0; q < 3; ++q) {
+                            st.nx[q] = ax.nterm[q]; st.ny[q] = ay.nterm[q]; st.nz[q] = az.nterm[q];
+                            st.sx[q] = ax.sterm[q]; st.sy[q] = ay.sterm[q]; st.sz[q] = az.sterm[q];
+                            st.wx[q] = wx[q]; st.wy[q] = wy[q]; st.wz[q] = wz[q];
+                        }
+                        gather27_delta(a.vel, a.vel_old, nrow, st, dv);
                         const float ovx = gd[(CH_VEL + 0) * 32], ovy = gd[(CH_VEL + 1) * 32],
                                     ovz = gd[(CH_VEL + 2) * 32];
                         nvx = (1.0f - a.flip) * nvx + a.flip * (ovx + dv[0]);
@@ -296,6 +313,11 @@ __global__ void __launch_bounds__(TW * 32, MPM_MINBLOCKS) transfer_kernel(const 
 #pragma unroll
                                 for (int c = 0; c < 3; ++c)
                                     Fn[3 * r + c] = A[3 * r] * F[c] + A[3 * r + 1] * F[3 + c] + A[3 * r + 2] * F[6 + c];
+                            if (MAT >= MPM_MAT_SNOW) {
+                                // return mapping (not in the reference; oracle: orc_snow_project / orc_sand_project)
+                                plastic_project<MAT>(Fn, plastic, pp, tau);
+                                gd[CH_PLASTIC * 32] = plastic;
+                            }
 #pragma unroll
                             for (int r = 0; r < 9; ++r) { F[r] = Fn[r]; gd[(CH_DEF + r) * 32] = Fn[r]; }
                         }
@@ -365,12 +387,16 @@ __global__ void __launch_bounds__(TW * 32, MPM_MINBLOCKS) transfer_kernel(const 
 #pragma unroll
                     for (int r = 0; r < 9; ++r) Q[r] = m * C[r];
                     Q[0] += coeff * tau; Q[4] += coeff * tau; Q[8] += coeff * tau;
-                } else {
+                } else if (MAT == MPM_MAT_FIXED_COROTATED) {
                     float t[9];
                     if (corotated_tau(F, a.mu, a.lam, t))
                         atomicAdd(&a.status->counters[MPM_C_SVD_CLAMP], 1ull);
 #pragma unroll
                     for (int r = 0; r < 9; ++r) Q[r] = m * C[r] + coeff * t[r];
+                } else {
+                    if (!GATHER) plastic_tau<MAT>(F, plastic, pp, tau);
+#pragma unroll
+                    for (int r = 0; r < 9; ++r) Q[r] = m * C[r] + coeff * tau[r];
                 }
             }
             // runs of consecutive active lanes with equal keys
@@ -520,6 +546,12 @@ static int launch_transfer(const TransferArgs &a, int mat, cudaStream_t stream)
         break;
     case MPM_MAT_FIXED_COROTATED:
         transfer_kernel<MPM_MAT_FIXED_COROTATED, GATHER, SCATTER><<<grid, TW * 32, 0, stream>>>(a);
+        break;
+    case MPM_MAT_SNOW:
+        transfer_kernel<MPM_MAT_SNOW, GATHER, SCATTER><<<grid, TW * 32, 0, stream>>>(a);
+        break;
+    case MPM_MAT_SAND:
+        transfer_kernel<MPM_MAT_SAND, GATHER, SCATTER><<<grid, TW * 32, 0, stream>>>(a);
         break;
     default:
         return MPM_ERR_CONFIG;

@@ -394,8 +394,6 @@ class CudaWorker:
                               "(the other arms re-measure CPU ablations, SURVEY.md section 2 row 13)")
         if self.options.deterministic:
             raise ConfigError("deterministic fixed-point accumulation is not implemented on the CUDA core")
-        if int(material.kind) not in (0, 1):
-            raise ConfigError(f"material kind {material.kind!r} is not implemented on the CUDA core yet")
         with torch.cuda.device(self.device):
             self.store = CudaParticleStore(material.kind, params.lane_width, self.device)
             self.table = CudaBlockTable(self.device)

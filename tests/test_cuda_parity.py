@@ -202,3 +202,46 @@ def test_pipelined_frame_equals_stepwise_frame():
         assert wa._global_step == wb._global_step == 108
         _assert_particles(U.state_by_id(wb), U.state_by_id(wa), edge, ndef, run=True)
         assert wb.runtime.generations == 108
+
+
+# ---- plastic kinds (snow, sand): NOT in the reference -- parity unpinned -------------------
+# The oracle's float64 statement of these models (oracle/mpm_oracle.c: orc_snow_project,
+# orc_sand_project, orc_sand_tau) is this repository's own definition; the CUDA kernels are
+# held to it with the same one-substep tolerances and a looser short-run bound (return
+# mapping branches amplify rounding).
+def _plastic_pair(kind, transfer):
+    from paper_2111_00699_b200 import BoundaryBox, Material, SimParams
+    dx = 25.0 / 64.0
+    pos, vel = U.block_scene(6, 11, dx, origin_cells=(10, 10, 9), speed=-60.0)
+    material = Material.snow(2.0, 5.0e4, 0.3, hardening=5.0) if kind == "snow" \
+        else Material.sand(2.0, 1.0e5, 0.3)
+    params = SimParams(dx=dx, dt=(1.0 / 48.0) / 36.0)
+    boundary = BoundaryBox((8 * dx,) * 3, (40 * dx,) * 3, mode="slip")
+    mass = 2.0 * dx ** 3 / 8
+    wc = U.cuda_worker(pos, vel, mass, material, params, boundary, transfer=transfer)
+    wo = U.oracle_worker(pos, vel, mass, material, params, boundary, transfer=transfer)
+    return wc, wo, float(pos.max() - pos.min())
+
+
+@pytest.mark.parametrize("kind", ["snow", "sand"])
+@pytest.mark.parametrize("transfer", ["split", "g2p2g"])
+def test_plastic_models_against_float64_definition(kind, transfer):
+    wc, wo, edge = _plastic_pair(kind, transfer)
+    for s in range(30):
+        wc.run_step(s)
+        wo.run_step(s)
+        if s == 1:
+            sc, so = U.state_by_id(wc), U.state_by_id(wo)
+            _assert_particles(sc, so, edge, 9, check_c=False)
+            assert np.abs(sc[:, 25] - so[:, 25]).max() <= 1e-5
+    if wc._pending_gather:
+        wc._flush_gather()
+        wo._flush_gather()
+    sc, so = U.state_by_id(wc), U.state_by_id(wo)
+    ex, ev, ef, _ = U.particle_errors(sc, so, edge, 9)
+    print(kind, transfer, "30 steps: x %.2e v %.2e F %.2e plastic %.2e" %
+          (ex, ev, ef, np.abs(sc[:, 25] - so[:, 25]).max()), "range", so[:, 25].min(), so[:, 25].max())
+    assert ex <= 1e-4 and ev <= 2e-2 and ef <= 1e-2
+    assert wc.rebuild_steps == wo.rebuild_steps
+    # the models did something: snow compacted / sand yielded
+    assert (so[:, 25] != (1.0 if kind == "snow" else 0.0)).any()
