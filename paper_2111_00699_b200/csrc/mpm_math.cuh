@@ -24,9 +24,11 @@ __device__ __forceinline__ void jacobi_rotate(float &app, float &aqq, float &apq
                                               float &arq, float *v)
 {
     const float a_pq = apq;
-    const float theta = 0.5f * (aqq - app) / a_pq;
-    const float r = sqrtf(1.0f + theta * theta);
-    const float t = theta >= 0.0f ? 1.0f / (theta + r) : -1.0f / (r - theta);
+    // rotation angle from approximate (2 ulp) reciprocal / square root: c^2 + s^2 = 1 holds to
+    // rounding whatever t is, so V stays orthogonal; accuracy of t only affects convergence
+    const float theta = __fdividef(0.5f * (aqq - app), a_pq);
+    const float r = __fsqrt_rn(1.0f + theta * theta);
+    const float t = theta >= 0.0f ? __fdividef(1.0f, theta + r) : -__fdividef(1.0f, r - theta);
     const float c = rsqrtf(1.0f + t * t);
     const float s = t * c;
     const float pp = app, qq = aqq;
@@ -251,6 +253,39 @@ __device__ __forceinline__ void sand_principal(const float *e, const PlasticPara
 template <int MAT>
 __device__ __forceinline__ void plastic_project(float *f, float &plastic, const PlasticParams &p, float *tau)
 {
+    if (MAT == MPM_MAT_SNOW) {
+        // Elastic fast path: when every singular value lies inside the yield interval nothing is
+        // clamped and the projection is the identity.  Gershgorin discs of the symmetric
+        // stretch S = R^T F (R from the Newton polar factor) bound the singular values without
+        // an SVD; the stress is then the fixed-corotated form with hardened moduli.
+        float r[9];
+        const float J = det3(f);
+        if (polar_rotation(f, J, r)) {
+            const float s00 = r[0] * f[0] + r[3] * f[3] + r[6] * f[6];
+            const float s11 = r[1] * f[1] + r[4] * f[4] + r[7] * f[7];
+            const float s22 = r[2] * f[2] + r[5] * f[5] + r[8] * f[8];
+            const float s01 = fabsf(r[0] * f[1] + r[3] * f[4] + r[6] * f[7]);
+            const float s02 = fabsf(r[0] * f[2] + r[3] * f[5] + r[6] * f[8]);
+            const float s12 = fabsf(r[1] * f[2] + r[4] * f[5] + r[7] * f[8]);
+            const float lo = fminf(fminf(s00 - s01 - s02, s11 - s01 - s12), s22 - s02 - s12);
+            const float hi = fmaxf(fmaxf(s00 + s01 + s02, s11 + s01 + s12), s22 + s02 + s12);
+            if (lo >= 1.0f - p.theta_c && hi <= 1.0f + p.theta_s) {
+                plastic = fminf(plastic > 0.1f ? plastic : 0.1f, 10.0f);
+                const float h = expf(p.hardening * (1.0f - plastic));
+                const float two_mu = 2.0f * p.mu * h, diag = p.lam * h * (J - 1.0f) * J;
+#pragma unroll
+                for (int a = 0; a < 3; ++a)
+#pragma unroll
+                    for (int b = 0; b < 3; ++b) {
+                        const float acc = two_mu * ((f[3 * a] - r[3 * a]) * f[3 * b] +
+                                                    (f[3 * a + 1] - r[3 * a + 1]) * f[3 * b + 1] +
+                                                    (f[3 * a + 2] - r[3 * a + 2]) * f[3 * b + 2]);
+                        tau[3 * a + b] = (a == b) ? acc + diag : acc;
+                    }
+                return;
+            }
+        }
+    }
     float u[9], s[3], v[9], sc[3], d[3];
     svd3(f, u, s, v);
     if (MAT == MPM_MAT_SNOW) {

@@ -40,6 +40,9 @@ struct TransferArgs {
 #ifndef MPM_TW
 #define MPM_TW 8
 #endif
+#ifndef MPM_SUBRUN
+#define MPM_SUBRUN 32
+#endif
 #ifndef MPM_MINBLOCKS
 #define MPM_MINBLOCKS 3
 #endif
@@ -402,8 +405,19 @@ __global__ void __launch_bounds__(TW * 32, MPM_MINBLOCKS) transfer_kernel(const 
             // runs of consecutive active lanes with equal keys
             const unsigned act = __ballot_sync(FULL, active);
             const int prev_key = __shfl_up_sync(FULL, key, 1);
-            const bool head = !active || lane == 0 || prev_key != key || !((act >> (lane - 1)) & 1u);
-            const unsigned heads = __ballot_sync(FULL, head);
+            bool head = !active || lane == 0 || prev_key != key || !((act >> (lane - 1)) & 1u);
+            unsigned heads = __ballot_sync(FULL, head);
+#if MPM_SUBRUN < 32
+            {
+                // experiment knob: cut runs longer than MPM_SUBRUN lanes into sub-runs with their
+                // own leader (fewer shuffle steps, more reductions to L2); 32 = the reference's
+                // "one += per (subgroup, node)" contract
+                const unsigned below = heads & ((2u << lane) - 1u);
+                const int seg_first = 31 - __clz(below);
+                head = head || (((lane - seg_first) & (MPM_SUBRUN - 1)) == 0);
+                heads = __ballot_sync(FULL, head);
+            }
+#endif
             const unsigned above = lane == 31 ? 0u : (heads & ~((2u << lane) - 1u));
             const int seg_last = above ? (__ffs(above) - 2) : 31;
             const int maxd = __reduce_max_sync(FULL, seg_last - lane);
