@@ -36,7 +36,7 @@ def parse_args():
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--scene", default="snow", choices=["snow", "snow_fc", "sand64k", "sand_mini",
-                                                        "sand389k", "sand1m", "sand10m"])
+                                                        "sand389k", "sand1m", "sand10m", "sand32m"])
     ap.add_argument("--transfer", default="g2p2g", choices=["split", "g2p2g"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
@@ -61,6 +61,8 @@ def build_world(scene):
         return scenes.sand_blocks(l=32, boxes=4)
     if scene == "sand10m":
         return scenes.sand_blocks(l=43, boxes=16)
+    if scene == "sand32m":
+        return scenes.sand_blocks(l=63, boxes=16)
     raise ValueError(scene)
 
 
@@ -234,7 +236,8 @@ def run_ours(args):
         abytes = algorithmic_bytes(int(W.material.kind), args.transfer, n_local, touched)
         achieved = abytes / (avg_ms * 1e-3) / 1e9
         roofline = {"bound": "hbm", "kernel": dom, "achieved": round(achieved, 1), "peak": peak,
-                    "unit": "GB/s", "frac": round(achieved / peak, 4), "traffic": TRAFFIC_NCU,
+                    "unit": "GB/s", "frac": round(achieved / peak, 4),
+                    "traffic": TRAFFIC_NCU.get(args.scene) if (world == 1 and args.transfer == "g2p2g") else None,
                     "peak_source": peak_src, "avg_launch_ms": round(avg_ms, 4),
                     "algorithmic_bytes_per_launch": int(abytes), "launches_timed": len(durs),
                     "kernel_share_of_step": round(sum(durs) / total_ms, 3),
@@ -292,8 +295,9 @@ def run_ours(args):
 
 
 # dram__bytes_read.sum + dram__bytes_write.sum of the dominant kernel, per launch, from the
-# committed `ncu --set full` capture (profiles/); None until a capture of the current kernel exists
-TRAFFIC_NCU = None
+# committed `ncu --set full` capture of the fused kernel on the 1.37 M scene
+# (profiles/r1_b_fused_fc_metrics.csv: 81.9 MB read + 48.7 MB write); only quoted for that scene
+TRAFFIC_NCU = {"snow": 130.6e6, "snow_fc": 130.6e6}
 
 
 def cpu_baseline(W, substeps, threads, warm=True):

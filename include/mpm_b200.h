@@ -254,6 +254,33 @@ int mpm_g2p2g(const mpm_store_view *store, const mpm_table_view *table, const fl
  * passes a fresh out_stats = zeros(2) per call, pipeline.py:1090). */
 int mpm_status_reset(mpm_step_status *status, const mpm_guard *guard, void *stream);
 
+/* Batched enqueue of n_steps guarded no-rebuild substeps of ONE worker (the inner loop of
+ * Worker.run_frame, pipeline.py:872-876, issued from C: small scenes are bound by launch
+ * overhead, not by the kernels).  Step s uses raw/touched[s & 1] and status slot s % ring; the
+ * slot is copied to `status_host` (pinned) and `events[slot]` (cudaEvent_t handles owned by the
+ * caller) is recorded after the copy.  Fused: g2p2g -> copy -> grid update.  Split: [clear] ->
+ * p2g -> grid update -> g2p -> copy.  Every kernel carries the guard {guard_word, s}. */
+#define MPM_MAX_STATUS_RING 32
+typedef struct mpm_step_plan {
+    mpm_store_view store;
+    mpm_table_view table;
+    float *raw[2];
+    uint8_t *touched[2];
+    float *vel, *vel_old;
+    mpm_transfer_params transfer;      /* dt, dt_gather of the first step, split-mode free zone */
+    double fused_margin_lo, fused_margin_hi;   /* free zone of the fused gather (shrunk, pipeline.py:1128) */
+    mpm_grid_params grid;
+    int32_t fused;                     /* 1: transfer = g2p2g with a pending gather; 0: split */
+    int32_t status_ring;               /* slots in status_dev / status_host / events */
+    mpm_step_status *status_dev;       /* device [status_ring] */
+    mpm_step_status *status_host;      /* pinned host [status_ring] */
+    void *events[MPM_MAX_STATUS_RING]; /* cudaEvent_t per slot */
+    int32_t *guard_word;               /* device */
+    void *time_events[2 * MPM_MAX_STATUS_RING]; /* optional (NULL): cudaEvent_t pairs recorded around the
+                                          dominant transfer kernel (g2p2g / p2g) of step first+k */
+} mpm_step_plan;
+int mpm_enqueue_steps(const mpm_step_plan *plan, int32_t first_step, int32_t n_steps, void *stream);
+
 /* ---- readback / aggregates ---------------------------------------------------------- */
 
 /* ParticleStore.positions_with_ids / state readback (particles.py:466-475): all stored

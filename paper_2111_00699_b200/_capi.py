@@ -69,6 +69,19 @@ class StepStatus(C.Structure):
 
 
 STATUS_BYTES = C.sizeof(StepStatus)
+MAX_STATUS_RING = 32
+
+
+class StepPlan(C.Structure):
+    _fields_ = [
+        ("store", StoreView), ("table", TableView), ("raw", p_void * 2), ("touched", p_void * 2),
+        ("vel", p_void), ("vel_old", p_void), ("transfer", TransferParams),
+        ("fused_margin_lo", f64), ("fused_margin_hi", f64), ("grid", GridParams),
+        ("fused", i32), ("status_ring", i32), ("status_dev", p_void), ("status_host", p_void),
+        ("events", p_void * MAX_STATUS_RING), ("guard_word", p_void),
+        ("time_events", p_void * (2 * MAX_STATUS_RING)),
+    ]
+
 
 _STATUS_TO_ERROR = {
     -1: E.RejectedInputError, -2: E.SpatialDomainError, -3: E.ResourceError,
@@ -100,6 +113,7 @@ _SIGNATURES = {
                 C.POINTER(TransferParams), p_void, C.POINTER(Guard), p_void],
     "mpm_g2p2g": [C.POINTER(StoreView), C.POINTER(TableView), p_void, p_void, p_void, p_void,
                   C.POINTER(TransferParams), p_void, C.POINTER(Guard), p_void],
+    "mpm_enqueue_steps": [C.POINTER(StepPlan), i32, i32, p_void],
     "mpm_gather_state": [C.POINTER(StoreView), p_void, p_void, p_void],
     "mpm_gather_positions": [C.POINTER(StoreView), p_void, p_void, p_void],
     "mpm_particle_aggregates": [C.POINTER(StoreView), p_void, p_void],

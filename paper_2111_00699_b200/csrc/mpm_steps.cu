@@ -1,0 +1,67 @@
+// Batched enqueue of guarded substeps: the host side of Worker.run_frame's inner loop
+// (pipeline.py:872-876 + run_step :905-940, no-rebuild path) for a single worker, issued from C
+// so that small scenes are not bound by per-launch interpreter overhead.
+//
+// For every step s in [first_step, first_step + n_steps):
+//   fused (transfer = g2p2g):  [clear(par)] -> g2p2g(s) -> status slot s % ring copied to pinned host memory,
+//                              event recorded -> grid update(s)
+//   split:                     [clear(par)] -> p2g(s) -> grid update(s) -> g2p(s) -> status copy,
+//                              event
+// All kernels carry the guard {word, s}: once a gather raises the word to its step, every later
+// step of the batch is a no-op on the device and the host re-issues from there after rebuilding.
+#include "mpm_common.cuh"
+
+extern "C" int mpm_enqueue_steps(const mpm_step_plan *p, int32_t first_step, int32_t n_steps, void *stream_)
+{
+    if (!p || n_steps < 0 || n_steps > MPM_MAX_STATUS_RING) return MPM_ERR_REJECTED_INPUT;
+    if (p->status_ring < 2 || p->status_ring > MPM_MAX_STATUS_RING) return MPM_ERR_CONFIG;
+    if (!p->guard_word || !p->status_dev || !p->status_host) return MPM_ERR_REJECTED_INPUT;
+    cudaStream_t stream = (cudaStream_t)stream_;
+    mpm_transfer_params tp = p->transfer;
+    mpm_grid_params gp = p->grid;
+    for (int k = 0; k < n_steps; ++k) {
+        const int s = first_step + k;
+        const int par = s & 1;
+        const int slot = s % p->status_ring;
+        mpm_guard guard = {p->guard_word, s};
+        mpm_step_status *st_dev = p->status_dev + slot;
+        int rc;
+        // after the first step of a batch the gather dt is the batch's own dt (pipeline.py:1230)
+        if (k > 0) tp.dt_gather = tp.dt;
+        if (!gp.fuse_clear) {
+            // Worker._clear (pipeline.py:1022-1037): rows of this parity touched two steps ago
+            rc = mpm_clear(p->raw[par], p->touched[par], p->table.count, 0, &guard, stream);
+            if (rc != MPM_OK) return rc;
+        }
+        if (p->fused) {
+            mpm_transfer_params fp = tp;
+            fp.margin_lo = p->fused_margin_lo;
+            fp.margin_hi = p->fused_margin_hi;
+            if (p->time_events[2 * k]) cudaEventRecord((cudaEvent_t)p->time_events[2 * k], stream);
+            rc = mpm_g2p2g(&p->store, &p->table, p->vel, p->vel_old, p->raw[par], p->touched[par], &fp,
+                           st_dev, &guard, stream);
+            if (rc != MPM_OK) return rc;
+            if (p->time_events[2 * k + 1]) cudaEventRecord((cudaEvent_t)p->time_events[2 * k + 1], stream);
+            cudaMemcpyAsync(p->status_host + slot, st_dev, sizeof(mpm_step_status), cudaMemcpyDeviceToHost, stream);
+            cudaEventRecord((cudaEvent_t)p->events[slot], stream);
+            rc = mpm_grid_update(p->raw[par], p->touched[par], p->vel, p->vel_old, &p->table, &gp,
+                                 p->status_dev + (s + 1) % p->status_ring, &guard, stream);
+            if (rc != MPM_OK) return rc;
+        } else {
+            if (p->time_events[2 * k]) cudaEventRecord((cudaEvent_t)p->time_events[2 * k], stream);
+            rc = mpm_p2g(&p->store, &p->table, p->raw[par], p->touched[par], &tp, st_dev, &guard, stream);
+            if (rc != MPM_OK) return rc;
+            if (p->time_events[2 * k + 1]) cudaEventRecord((cudaEvent_t)p->time_events[2 * k + 1], stream);
+            rc = mpm_grid_update(p->raw[par], p->touched[par], p->vel, p->vel_old, &p->table, &gp, st_dev,
+                                 &guard, stream);
+            if (rc != MPM_OK) return rc;
+            mpm_transfer_params g2 = tp;
+            g2.dt_gather = tp.dt;            // split G2P advects with the dt of the update just done
+            rc = mpm_g2p(&p->store, &p->table, p->vel, p->vel_old, &g2, st_dev, &guard, stream);
+            if (rc != MPM_OK) return rc;
+            cudaMemcpyAsync(p->status_host + slot, st_dev, sizeof(mpm_step_status), cudaMemcpyDeviceToHost, stream);
+            cudaEventRecord((cudaEvent_t)p->events[slot], stream);
+        }
+    }
+    return mpm::check_launch("mpm_enqueue_steps", 0);
+}

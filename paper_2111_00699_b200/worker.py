@@ -34,7 +34,8 @@ CH_POS, CH_VEL, CH_C, CH_MASS, CH_DEF, CH_PLASTIC = 0, 3, 6, 15, 16, 25
 LW = 32
 _INT_MAX = 0x7FFFFFFF
 _PHASES = ("rebuild", "sort", "p2g", "grid", "g2p")
-_RING = 4
+_RING = 16          # status slots: two batches of speculative steps in flight
+_BATCH = 4          # steps enqueued per C call in steady state
 
 
 def channels_for(kind: int) -> int:
@@ -406,6 +407,9 @@ class CudaWorker:
             self._status_host = torch.zeros((_RING, _capi.STATUS_BYTES // 8),
                                             dtype=torch.int64).pin_memory()
             self._status_events = [torch.cuda.Event() for _ in range(_RING)]
+            self._time_events = [torch.cuda.Event(enable_timing=True) for _ in range(2 * _BATCH * 2)]
+            for ev in self._status_events + self._time_events:
+                ev.record()          # events are created lazily: force the handles into existence
             self._slot_clean = [True] * _RING
             self._guard_word = torch.full((1,), _INT_MAX, dtype=torch.int32, device=self.device)
             self._scalars = torch.zeros(16, dtype=torch.int32, device=self.device)
@@ -436,6 +440,8 @@ class CudaWorker:
         self.kernel_calls = 0
         self.time_kernels = False     # bench: CUDA events around the step kernels
         self.pipelined = True         # run_frame enqueues step s+1 before reading step s's flag
+        self.batch_steps = _BATCH     # fixed-dt frames: steps per mpm_enqueue_steps call (0 = off)
+        self._plan = None
         self.speculative_discards = 0
         self.kernel_events = []
         self._gp = None
@@ -555,7 +561,10 @@ class CudaWorker:
         if self.pipelined and self.runtime.n_workers == 1 and \
                 self.options.rebuild != "every_step" and not self.options.collect_conservation:
             with torch.cuda.device(self.device):
-                self._run_frame_pipelined()
+                if self.batch_steps > 0 and not self.cfl_mode:
+                    self._run_frame_batched()
+                else:
+                    self._run_frame_pipelined()
             return
         with torch.cuda.device(self.device):
             if self.cfl_mode:
@@ -637,6 +646,111 @@ class CudaWorker:
         finally:
             self._defer = False
             self._guard = None
+        if self._pending_gather:
+            self._flush_gather()
+
+    # -- batched steady state (fixed dt): mpm_enqueue_steps ------------------------------------
+    def _can_batch(self):
+        if self.flags.rebuild_needed or self._pending_full_clear_parity != -1:
+            return False
+        if not self.store.n_groups or self.store.staged_count:
+            return False
+        if self.options.transfer == "g2p2g":
+            return self._fused_active() and self._pending_gather
+        return not self._pending_gather
+
+    def _step_plan(self):
+        plan = self._plan
+        if plan is None:
+            plan = self._plan = _capi.StepPlan()
+            st, tb, gr = self.store, self.table, self.grid
+            plan.store, plan.table = st.view(), tb.view()
+            for k in (0, 1):
+                plan.raw[k], plan.touched[k] = gr._raw[k].ptr, tb._touched[k].ptr
+            plan.vel = gr._vel.ptr
+            plan.vel_old = self._vel_old_ptr()
+            plan.fused = int(self.options.transfer == "g2p2g")
+            plan.status_ring = _RING
+            plan.status_dev = self._status.data_ptr()
+            plan.status_host = self._status_host.data_ptr()
+            for k, ev in enumerate(self._status_events):
+                plan.events[k] = ev.cuda_event
+            plan.guard_word = self._guard_word.data_ptr()
+            plan.fused_margin_lo = FREE_ZONE_LO_CELLS - FUSED_MARGIN_CELLS
+            plan.fused_margin_hi = FREE_ZONE_HI_CELLS - 4.0 - FUSED_MARGIN_CELLS
+        C.memmove(C.byref(plan.transfer), C.byref(self._params()), C.sizeof(TransferParams))
+        gp = self._grid_params()
+        gp.fuse_clear = int(self.fuse_clear)
+        C.memmove(C.byref(plan.grid), C.byref(gp), C.sizeof(_capi.GridParams))
+        return plan
+
+    def _run_frame_batched(self):
+        """Fixed-dt frame with the steady-state steps enqueued in batches from C
+        (mpm_enqueue_steps), two batches in flight.  Same guard protocol as
+        _run_frame_pipelined: a step that raises the rebuild flag turns every later enqueued
+        step into a no-op on the device; the host drops them, rebuilds and carries on from the
+        step after the one that raised the flag -- the reference's sequence of steps."""
+        spf = self.params.steps_per_frame
+        self.dt = self.params.dt
+        pending = []            # batches in flight: (first_step, n, time-event base or None)
+        enq = 0                 # steps of this frame enqueued (confirmed + speculative)
+        next_step = self._global_step
+        tbase = 0
+        while self._frame_steps < spf:
+            while len(pending) < 2 and enq < spf and self._can_batch():
+                n = min(self.batch_steps, spf - enq)
+                plan = self._step_plan()
+                tev = None
+                if self.time_kernels:
+                    tev = tbase
+                    for k in range(n):
+                        plan.time_events[2 * k] = self._time_events[2 * (tbase + k)].cuda_event
+                        plan.time_events[2 * k + 1] = self._time_events[2 * (tbase + k) + 1].cuda_event
+                    tbase = (tbase + _BATCH) % (2 * _BATCH)
+                else:
+                    for k in range(2 * n):
+                        plan.time_events[k] = None
+                # the first step of a batch gathers with the dt of the last grid update done
+                plan.transfer.dt_gather = float(self._vel_dt if not pending else self.dt)
+                self.kernel_calls += 1
+                check(self.lib.mpm_enqueue_steps(C.byref(plan), next_step, n, _stream_ptr()),
+                      "mpm_enqueue_steps")
+                pending.append((next_step, n, tev))
+                next_step += n
+                enq += n
+            if not pending:
+                # rebuild step, first fused step after a rebuild, pending full clear: one plain step
+                self._guard = None
+                self._defer = False
+                self.run_step(self._global_step)
+                self._frame_steps += 1
+                self.frame_dts.append(self.dt)
+                enq = self._frame_steps
+                next_step = self._global_step
+                continue
+            first, n, tev = pending.pop(0)
+            for k in range(n):
+                step = first + k
+                self._slot_clean[step % _RING] = False
+                self._consume(step % _RING, step)
+                if tev is not None:
+                    name = "mpm_g2p2g" if self.options.transfer == "g2p2g" else "mpm_p2g"
+                    self.kernel_events.append((name, self._time_events[2 * (tev + k)],
+                                               self._time_events[2 * (tev + k) + 1]))
+                # step `step` itself ran to completion (the guard only stops LATER steps)
+                self._global_step = step + 1
+                self._vel_dt = self.dt
+                self.flags.steps_since_rebuild += 1
+                self.runtime.generations += 1
+                self._frame_steps += 1
+                self.frame_dts.append(self.dt)
+                if self.flags.rebuild_needed:
+                    self.speculative_discards += (n - 1 - k) + sum(b[1] for b in pending)
+                    pending = []
+                    enq = self._frame_steps
+                    next_step = self._global_step
+                    self._guard_word.fill_(_INT_MAX)
+                    break
         if self._pending_gather:
             self._flush_gather()
 
@@ -816,6 +930,7 @@ class CudaWorker:
         for k in (0, 1):
             tb._touched[k].len = count
         self._pending_full_clear_parity = 1 - par
+        self._plan = None             # buffers may have moved: the batched-step plan is rebuilt
         self._published_codes = (tb._codes, count)
         self.flags.rebuild_needed = False
         self.flags.steps_since_rebuild = 0
