@@ -103,7 +103,28 @@ class CudaParticleStore:
 
     def stage_append(self, positions, velocities, masses, deformation=None, affine=None, ids=None):
         """Queue host particles for the next rebuild (particles.py:309-334).  Arrays are kept
-        compact (x, v, m [, F|J, C]); the channel rows are laid out on the device."""
+        compact (x, v, m [, F|J, C]); the channel rows are laid out on the device.  Pinned
+        float32 / int64 torch tensors are uploaded as they are (no staging copy)."""
+        if isinstance(positions, torch.Tensor) and deformation is None and affine is None:
+            tp, tv = positions, velocities
+            n = tp.shape[0]
+            if n == 0:
+                return 0
+            if tp.ndim != 2 or tp.shape[1] != 3 or tuple(tv.shape) != tuple(tp.shape):
+                raise RejectedInputError(f"positions / velocities must have shape (n, 3), got "
+                                         f"{tuple(tp.shape)} / {tuple(tv.shape)}")
+            tp = tp.to(torch.float32).contiguous()
+            tv = tv.to(torch.float32).contiguous()
+            tm = masses if isinstance(masses, torch.Tensor) else np.asarray(masses, dtype=np.float32)
+            if ids is None:
+                ti = torch.arange(self._next_id, self._next_id + n, dtype=torch.int64)
+                self._next_id += n
+            else:
+                ti = torch.as_tensor(ids, dtype=torch.int64).contiguous()
+                self._next_id = max(self._next_id, int(ti.max()) + 1)
+            self._staged.append((tp, tv, tm, None, None, ti))
+            self.staged_count += n
+            return n
         pos = np.atleast_2d(np.asarray(positions))
         n = pos.shape[0]
         if n == 0:
@@ -132,6 +153,15 @@ class CudaParticleStore:
         self.staged_count += n
         return n
 
+    def _default_state(self, flat):
+        """F = I (J = 1), C = 0, plastic scalar at rest (particles.py:309-320)."""
+        flat[:, CH_DEF] = 1.0
+        if self.kind != MaterialKind.WEAKLY_COMPRESSIBLE_FLUID:
+            flat[:, CH_DEF + 4] = 1.0
+            flat[:, CH_DEF + 8] = 1.0
+        if self.nch > CH_PLASTIC:
+            flat[:, CH_PLASTIC] = 1.0 if self.kind == MaterialKind.SNOW else 0.0
+
     def _pinned(self, tag, shape, dtype):
         """Grow-only pinned host staging buffers (reused across uploads / readbacks)."""
         need = int(np.prod(shape))
@@ -147,6 +177,29 @@ class CudaParticleStore:
             return None, None, 0
         n = self.staged_count
         dev = self.device
+        if all(isinstance(e[0], torch.Tensor) for e in self._staged):
+            # tensors (ideally pinned): straight H2D copies into the flat rows
+            flat = torch.zeros((n, self.nch), dtype=torch.float32, device=dev)
+            dids = torch.empty(n, dtype=torch.int64, device=dev)
+            o = 0
+            for tp, tv, tm, _, _, ti in self._staged:
+                k = tp.shape[0]
+                flat[o:o + k, CH_POS:CH_POS + 3] = tp.to(dev, non_blocking=True)
+                flat[o:o + k, CH_VEL:CH_VEL + 3] = tv.to(dev, non_blocking=True)
+                if isinstance(tm, torch.Tensor):
+                    flat[o:o + k, CH_MASS] = tm.to(dev, torch.float32, non_blocking=True)
+                elif tm.ndim:
+                    flat[o:o + k, CH_MASS] = torch.from_numpy(np.broadcast_to(tm, (k,)).copy()).to(dev)
+                else:
+                    flat[o:o + k, CH_MASS] = float(tm)
+                dids[o:o + k] = ti.to(dev, non_blocking=True)
+                o += k
+            self._staged.clear()
+            self.staged_count = 0
+            self._default_state(flat)
+            return flat, dids, n
+        self._staged = [tuple(x.numpy() if isinstance(x, torch.Tensor) else x for x in e)
+                        for e in self._staged]
         hpos = self._pinned("pos", (n, 3), torch.float32)
         hvel = self._pinned("vel", (n, 3), torch.float32)
         hids = self._pinned("ids", (n,), torch.int64)
@@ -171,14 +224,7 @@ class CudaParticleStore:
         flat[:, CH_POS:CH_POS + 3] = hpos.to(dev, non_blocking=True)
         flat[:, CH_VEL:CH_VEL + 3] = hvel.to(dev, non_blocking=True)
         flat[:, CH_MASS] = hmass.to(dev, non_blocking=True)
-        if self.kind == MaterialKind.WEAKLY_COMPRESSIBLE_FLUID:
-            flat[:, CH_DEF] = 1.0
-        else:
-            flat[:, CH_DEF] = 1.0
-            flat[:, CH_DEF + 4] = 1.0
-            flat[:, CH_DEF + 8] = 1.0
-        if self.nch > CH_PLASTIC:
-            flat[:, CH_PLASTIC] = 1.0 if self.kind == MaterialKind.SNOW else 0.0
+        self._default_state(flat)
         for o, k, defo, aff in extras:
             if defo is not None:
                 flat[o:o + k, CH_DEF:CH_DEF + defo.shape[1]] = torch.from_numpy(defo).to(dev)
@@ -253,6 +299,9 @@ class CudaParticleStore:
         hpos.copy_(pos, non_blocking=True)
         hids.copy_(ids, non_blocking=True)
         torch.cuda.current_stream().synchronize()
+        if dtype is None:
+            # zero-copy views of the pinned readback buffers, valid until the next readback
+            return hpos.numpy(), hids.numpy()
         return hpos.numpy().astype(dtype), hids.numpy().copy()
 
     def _aggregates(self):

@@ -257,3 +257,28 @@ def test_steady_state_allocates_nothing():
     w.run_frame()
     assert len(w.rebuild_steps) >= 3
     assert w.realloc_count == before
+
+
+def test_pinned_tensor_upload_and_zero_copy_readback(rng):
+    """The host-buffer entry used by bench.py's e2e leg: pinned torch tensors are uploaded as they
+    are and positions come back through the pinned readback buffers."""
+    import torch
+    pos = rng.uniform(6.0, 10.0, (300, 3)).astype(np.float32)
+    vel = rng.normal(0, 10, (300, 3)).astype(np.float32)
+    ids = np.arange(300, dtype=np.int64)[::-1].copy()
+    params = SimParams(dx=0.5, dt=1e-4)
+    wa = _mk(pos.astype(np.float64), vel.astype(np.float64), params=params, mass=0.5)
+    wb = _mk(np.zeros((0, 3)), params=params)
+    wa.store._staged.clear(); wa.store.staged_count = 0
+    wa.seed_particles(pos, vel, 0.5, ids=ids)
+    wb.replace_particles(torch.from_numpy(pos).pin_memory(), torch.from_numpy(vel).pin_memory(), 0.5,
+                         torch.from_numpy(ids).pin_memory())
+    for s in range(3):
+        wa.run_step(s)
+        wb.run_step(s)
+    pa, ia = wa.store.positions_with_ids()
+    pb, ib = wb.store.positions_with_ids(dtype=None)
+    assert pb.dtype == np.float32 and np.array_equal(ia, ib)
+    # same inputs, same kernels; float atomics may reorder sums between two runs
+    assert np.allclose(pa, pb, rtol=0, atol=1e-5)
+    assert np.allclose(wa.store.data, wb.store.data, rtol=1e-4, atol=1e-4)
