@@ -36,7 +36,7 @@ def parse_args():
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--scene", default="snow", choices=["snow", "snow_fc", "sand64k", "sand_mini",
-                                                        "sand389k", "sand1m", "sand10m", "sand32m"])
+                                                        "sand389k", "sand1m", "sand10m", "sand32m", "fountain"])
     ap.add_argument("--transfer", default="g2p2g", choices=["split", "g2p2g"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
@@ -63,6 +63,9 @@ def build_world(scene):
         return scenes.sand_blocks(l=43, boxes=16)
     if scene == "sand32m":
         return scenes.sand_blocks(l=63, boxes=16)
+    if scene == "fountain":
+        # configs[1]: 14 256 particles emitted per frame (radius 5 dx) up to the paper's 143.5 K
+        return scenes.fountain(radius=5 * 0.66)
     raise ValueError(scene)
 
 
@@ -323,6 +326,53 @@ def run_ours(args):
 TRAFFIC_NCU = {"snow": 130.6e6, "snow_fc": 130.6e6}
 
 
+def run_fountain(args):
+    """configs[1]: water fountain with a per-frame emitter, CFL-auto dt, split transfers (the
+    emitter forbids the fused transfer, bench.py:116-118 of the reference).  Particles are emitted
+    for 10 frames (142 560 particles), then K frames are timed with the emitter still running."""
+    import torch
+    from paper_2111_00699_b200 import PipelineOptions, SharedRuntime, _capi
+    from paper_2111_00699_b200.worker import CudaWorker
+    torch.cuda.set_device(0)
+    W = build_world("fountain")
+    w = CudaWorker(0, SharedRuntime(1, initial_vmax=160.0), W.params, W.material, W.boundary,
+                   PipelineOptions(transfer="split"), count_stats=False)
+    w.cfl_mode = True
+    frame = 0
+    while w.store.count + w.store.staged_count < 142000:
+        pos, vel = W.emission.sample(frame)
+        w.append_particles(pos.astype(np.float32), vel.astype(np.float32), W.particle_mass)
+        w.run_frame()
+        frame += 1
+    torch.cuda.synchronize()
+    l0 = _capi.lib().mpm_launch_count()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    work, steps = 0, 0
+    e0.record()
+    for _ in range(args.steps):
+        pos, vel = W.emission.sample(frame)
+        w.append_particles(pos.astype(np.float32), vel.astype(np.float32), W.particle_mass)
+        w.run_frame()
+        work += w.store.count * w.frame_steps
+        steps += w.frame_steps
+        frame += 1
+    e1.record()
+    torch.cuda.synchronize()
+    ms = e0.elapsed_time(e1)
+    line = {"metric": METRIC, "value": round(work / (ms * 1e-3) / 1e6, 2), "unit": UNIT, "n_gpus": 1,
+            "steps": args.steps, "warmup": frame - args.steps, "ms_per_step": round(ms / args.steps, 4),
+            "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f32",
+            "data": "synthetic",
+            "config": {"workload": "fountain (emitter radius 5 dx, 14 256 particles / frame, CFL-auto dt)",
+                       "particles": int(w.store.count), "substeps_per_step": round(steps / args.steps, 2),
+                       "step": "one frame incl. emission upload", "transfer": "split",
+                       "material": W.material.kind.name, "fps": round(1e3 * args.steps / ms, 1)},
+            "ms_per_frame": round(ms / args.steps, 4),
+            "gpu_launches": int(_capi.lib().mpm_launch_count() - l0), "e2e": None, "roofline": None,
+            "cpu_baseline": None, "clocks": None}
+    print(json.dumps(line), flush=True)
+
+
 def cpu_baseline(W, substeps, threads, warm=True):
     """The CPU oracle (C restatement of the reference, oracle/) timed on the host cores on a
     bounded sample: the full scene, rebuild + `substeps` substeps."""
@@ -396,5 +446,7 @@ if __name__ == "__main__":
     a = parse_args()
     if a.impl == "reference":
         run_reference(a)
+    elif a.scene == "fountain":
+        run_fountain(a)
     else:
         run_ours(a)

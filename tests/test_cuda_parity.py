@@ -245,3 +245,38 @@ def test_plastic_models_against_float64_definition(kind, transfer):
     assert wc.rebuild_steps == wo.rebuild_steps
     # the models did something: snow compacted / sand yielded
     assert (so[:, 25] != (1.0 if kind == "snow" else 0.0)).any()
+
+
+def test_fountain_frames_with_emission_against_oracle():
+    """configs[1] in miniature: per-frame emission (append_particles forces a rebuild per frame,
+    pipeline.py:837-850), weakly compressible fluid, CFL-auto dt (pipeline.py:858-871)."""
+    from paper_2111_00699_b200 import PipelineOptions, SharedRuntime, scenes
+    from paper_2111_00699_b200.worker import CudaWorker
+    W = scenes.fountain(radius=2.5 * 0.66)
+    f32r = lambda a: np.asarray(a, dtype=np.float64).astype(np.float32).astype(np.float64)
+    vmax0 = 160.0
+    wc = CudaWorker(0, SharedRuntime(1, initial_vmax=vmax0), W.params, W.material, W.boundary,
+                    PipelineOptions())
+    wo = O.OracleWorker(0, O.OracleRuntime(1, vmax0), W.params, W.material, W.boundary,
+                        PipelineOptions())
+    wc.cfl_mode = wo.cfl_mode = True
+    dts_c, dts_o = [], []
+    orig = wo.run_step
+
+    def spy(step):
+        dts_o.append(wo.dt)
+        orig(step)
+    wo.run_step = spy
+    for frame in range(3):
+        pos, vel = W.emission.sample(frame)
+        pos, vel = f32r(pos), f32r(vel)
+        for w in (wc, wo):
+            w.append_particles(pos, vel, W.particle_mass)
+        wc.run_frame()
+        wo.run_frame()
+        dts_c += wc.frame_dts
+    assert wc.store.count == wo.store.count == 3 * W.emission.per_frame
+    assert len(dts_c) == len(dts_o) and np.allclose(dts_c, dts_o, rtol=1e-5, atol=0)
+    assert wc.rebuild_steps == wo.rebuild_steps
+    edge = 64 * 0.66
+    _assert_particles(U.state_by_id(wc), U.state_by_id(wo), edge, 1, run=True)
