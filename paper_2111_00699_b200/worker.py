@@ -16,6 +16,7 @@ from __future__ import annotations
 
 import ctypes as C
 import math
+import time
 
 import numpy as np
 import torch
@@ -493,6 +494,7 @@ class CudaWorker:
         self._plan = None
         self.speculative_discards = 0
         self.kernel_events = []
+        self._frame_event_start = 0
         self._gp = None
         self._guard = None            # ctypes Guard of the step being enqueued (pipelined frames)
         self._defer = False           # leave gather statuses unread (pipelined frames)
@@ -565,7 +567,24 @@ class CudaWorker:
 
     @property
     def phase_ms(self):
-        return dict(self._phase_ms)
+        """Per-frame phase times in the reference's five columns (pipeline.py:785).  rebuild / sort
+        are host-timed (the rebuild synchronises anyway); the kernel phases come from CUDA events
+        when `time_kernels` is on, the fused kernel split 50/50 (pipeline.py:1137-1138)."""
+        out = dict(self._phase_ms)
+        if self.time_kernels and self.kernel_events:
+            torch.cuda.synchronize(self.device)
+            for name, a, b in self.kernel_events[self._frame_event_start:]:
+                ms = a.elapsed_time(b)
+                if name == "mpm_p2g":
+                    out["p2g"] += ms
+                elif name == "mpm_g2p":
+                    out["g2p"] += ms
+                elif name == "mpm_g2p2g":
+                    out["p2g"] += 0.5 * ms
+                    out["g2p"] += 0.5 * ms
+                else:
+                    out["grid"] += ms
+        return out
 
     @property
     def realloc_count(self):
@@ -603,6 +622,7 @@ class CudaWorker:
         self._phase_ms = {k: 0.0 for k in _PHASES}
         self._frame_steps = 0
         self._frame_rebuilds = 0
+        self._frame_event_start = len(self.kernel_events)
         self.frame_dts = []       # step sizes of the current frame, in order
 
     def run_frame(self):
@@ -874,6 +894,7 @@ class CudaWorker:
         then pblock + group counts) -- the paper's CPU-GPU sync points."""
         lib, st, tb, gr = self.lib, self.store, self.table, self.grid
         stream = _stream_ptr()
+        t_rebuild = time.perf_counter()
         staged, staged_ids, n_staged = st.take_staged()
         n_upper = st.count + n_staged
         old = st.view()
@@ -985,6 +1006,7 @@ class CudaWorker:
         self.flags.steps_since_rebuild = 0
         self.rebuild_steps.append(step)
         self._frame_rebuilds += 1
+        self._phase_ms["rebuild"] += (time.perf_counter() - t_rebuild) * 1e3
 
     def _clear(self, par):
         """Worker._clear (pipeline.py:1022-1037)."""
