@@ -74,6 +74,9 @@ typedef struct mpm_transfer_params {
     double kappa, gamma;     /* fluid bulk modulus / exponent */
     int32_t clamp_tension;   /* fluid: clamp negative pressure (pipeline.py:151-156) */
     int32_t count_stats;     /* also maintain C_ACCUM / C_SUBGROUPS (costs atomics) */
+    int32_t deterministic;   /* fixed-point accumulation (pipeline.py:43-44, 297-301): raw nodes are
+                                four int64 = rint(c 2^40) mass, rint(c 2^32) momentum (32 B per node) */
+    int32_t reserved0;
     double density;
     double dx;
     double dt;               /* scatter dt (this step) */
@@ -200,7 +203,8 @@ typedef struct mpm_guard {
 
 /* Worker._clear (pipeline.py:1022-1037): zero the rows of raw flagged in touched and reset
  * the flags; full=1 clears every row (first use of a parity after a rebuild). */
-int mpm_clear(float *raw, uint8_t *touched, int32_t count, int full, const mpm_guard *guard, void *stream);
+int mpm_clear(float *raw, uint8_t *touched, int32_t count, int full, int32_t node_bytes,
+              const mpm_guard *guard, void *stream);   /* node_bytes: 16 (float4) or 32 (deterministic) */
 
 /* _p2g_kernel (pipeline.py:316-356): scatter_prep + subgroup scatter of every group into
  * raw (float4 nodes), touched flags set for every addressed block. */
@@ -224,6 +228,7 @@ typedef struct mpm_grid_params {
                                            reset their touched flags (saves the next _clear pass) */
     int32_t block_filter;               /* 0 every touched block; 1 only blocks no peer holds;
                                            2 only blocks shared with a peer (halo) */
+    int32_t deterministic;              /* raw / peer_raw hold int64 fixed-point nodes (pipeline.py:682-686) */
     int32_t n_peers;                    /* 0..MPM_MAX_PEERS */
     const float *peer_raw[MPM_MAX_PEERS];        /* float4 rows [*, 64] of each peer */
     const uint8_t *peer_touched[MPM_MAX_PEERS];  /* per-row flags, or NULL = every row counts */
@@ -294,8 +299,8 @@ int mpm_gather_positions(const mpm_store_view *store, float *pos, int64_t *ids, 
 int mpm_particle_aggregates(const mpm_store_view *store, double *out5, void *stream);
 
 /* grid mass / momentum over touched blocks of raw (pipeline.py:1189-1203): out[0..3]. */
-int mpm_grid_aggregates(const float *raw, const uint8_t *touched, int32_t count, double *out4,
-                        void *stream);
+int mpm_grid_aggregates(const float *raw, const uint8_t *touched, int32_t count, int32_t deterministic,
+                        double *out4, void *stream);
 
 /* Shared-block tagging (Worker._post_barrier, pipeline.py:1147-1164; _hash_lookup_batch,
  * grid.py:161-173): peer_map[local index of code] = position in peer_codes, -1 elsewhere. */

@@ -28,7 +28,7 @@ class TransferParams(C.Structure):
     _fields_ = [
         ("mat_kind", i32), ("nch", i32),
         ("mu", f64), ("lam", f64), ("kappa", f64), ("gamma", f64),
-        ("clamp_tension", i32), ("count_stats", i32),
+        ("clamp_tension", i32), ("count_stats", i32), ("deterministic", i32), ("reserved0", i32),
         ("density", f64), ("dx", f64), ("dt", f64), ("dt_gather", f64), ("flip_blend", f64),
         ("margin_lo", f64), ("margin_hi", f64),
         ("theta_c", f64), ("theta_s", f64), ("hardening", f64), ("sand_alpha", f64),
@@ -53,7 +53,7 @@ class GridParams(C.Structure):
     _fields_ = [
         ("dt", f64), ("gravity", f64 * 3), ("apply_bc", i32), ("bc_sticky", i32),
         ("box_lo", f64 * 3), ("box_hi", f64 * 3), ("dx", f64), ("fuse_clear", i32),
-        ("block_filter", i32), ("n_peers", i32),
+        ("block_filter", i32), ("deterministic", i32), ("n_peers", i32),
         ("peer_raw", p_void * MPM_MAX_PEERS), ("peer_touched", p_void * MPM_MAX_PEERS),
         ("peer_map", p_void * MPM_MAX_PEERS),
     ]
@@ -102,7 +102,7 @@ _SIGNATURES = {
                            p_void, p_void, p_void],
     "mpm_scatter_sorted": [C.POINTER(StoreView), p_void, p_void, p_void, p_void, p_void, p_void,
                            p_void, i32, p_void, f64, C.POINTER(StoreView), p_void],
-    "mpm_clear": [p_void, p_void, i32, i32, C.POINTER(Guard), p_void],
+    "mpm_clear": [p_void, p_void, i32, i32, i32, C.POINTER(Guard), p_void],
     "mpm_status_reset": [p_void, C.POINTER(Guard), p_void],
     "mpm_p2g": [C.POINTER(StoreView), C.POINTER(TableView), p_void, p_void,
                 C.POINTER(TransferParams), p_void, C.POINTER(Guard), p_void],
@@ -117,7 +117,7 @@ _SIGNATURES = {
     "mpm_gather_state": [C.POINTER(StoreView), p_void, p_void, p_void],
     "mpm_gather_positions": [C.POINTER(StoreView), p_void, p_void, p_void],
     "mpm_particle_aggregates": [C.POINTER(StoreView), p_void, p_void],
-    "mpm_grid_aggregates": [p_void, p_void, i32, p_void, p_void],
+    "mpm_grid_aggregates": [p_void, p_void, i32, i32, p_void, p_void],
     "mpm_tag_shared": [p_void, i32, p_void, p_void, i32, p_void, i32, p_void],
     "mpm_version": [],
     "mpm_last_error": [],

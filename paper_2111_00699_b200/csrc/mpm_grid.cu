@@ -23,7 +23,7 @@ struct PeerSet {
 };
 
 __global__ void __launch_bounds__(256) clear_kernel(float4 *raw, uint8_t *touched, int count, int full,
-                                                    const DevGuard guard)
+                                                    int vec_per_node, const DevGuard guard)
 {
     if (guarded_out(guard)) return;
     const int b = blockIdx.x * 4 + (threadIdx.x >> 6);
@@ -31,7 +31,8 @@ __global__ void __launch_bounds__(256) clear_kernel(float4 *raw, uint8_t *touche
     const bool hit = b < count && (full || touched[b]);
     __syncthreads();   // every thread has read the flag before it is reset
     if (hit) {
-        raw[(size_t)b * 64 + slot] = make_float4(0.f, 0.f, 0.f, 0.f);
+        for (int v = 0; v < vec_per_node; ++v)
+            raw[((size_t)b * 64 + slot) * vec_per_node + v] = make_float4(0.f, 0.f, 0.f, 0.f);
         if (slot == 0) touched[b] = 0;
     }
 }
@@ -51,6 +52,7 @@ struct GridArgs {
     double dx;
     int fuse_clear;
     int block_filter;
+    int deterministic;
     float4 *raw_mut;
     uint8_t *touched_mut;
     DevGuard guard;
@@ -77,24 +79,49 @@ __global__ void __launch_bounds__(256) grid_update_kernel(const GridArgs a)
     if (a.fuse_clear) __syncthreads();
     if (!hit) return;
     const size_t idx = (size_t)b * 64 + slot;
-    float4 node = a.raw[idx];
-    // cross-worker reduction (pipeline.py:1172-1188): peers' raw rows are only read
-    for (int p = 0; p < a.peers.n; ++p) {
-        const int q = a.peers.map[p][b];
-        if (q < 0 || (a.peers.touched[p] && a.peers.touched[p][q] != 1)) continue;
-        const float4 o = a.peers.raw[p][(size_t)q * 64 + slot];
-        node.x += o.x; node.y += o.y; node.z += o.z; node.w += o.w;
+    float m, vx, vy, vz;
+    if (a.deterministic) {
+        // integer sums (pipeline.py:682-686): mass = m 2^-40, v = (p 2^-32) / mass, in float64
+        const longlong4 *rawd = (const longlong4 *)a.raw;
+        longlong4 node = rawd[idx];
+        for (int p = 0; p < a.peers.n; ++p) {
+            const int q = a.peers.map[p][b];
+            if (q < 0 || (a.peers.touched[p] && a.peers.touched[p][q] != 1)) continue;
+            const longlong4 o = ((const longlong4 *)a.peers.raw[p])[(size_t)q * 64 + slot];
+            node.x += o.x; node.y += o.y; node.z += o.z; node.w += o.w;
+        }
+        if (a.fuse_clear) {
+            ((longlong4 *)a.raw_mut)[idx] = make_longlong4(0, 0, 0, 0);
+            if (slot == 0) a.touched_mut[b] = 0;
+        }
+        if (node.x <= 0) {
+            a.vel[idx] = make_float4(0.f, 0.f, 0.f, 0.f);
+            return;
+        }
+        const double mass = (double)node.x * (1.0 / 1099511627776.0);
+        const double inv = (1.0 / 4294967296.0) / mass;
+        m = (float)mass;
+        vx = (float)((double)node.y * inv); vy = (float)((double)node.z * inv); vz = (float)((double)node.w * inv);
+    } else {
+        float4 node = a.raw[idx];
+        // cross-worker reduction (pipeline.py:1172-1188): peers' raw rows are only read
+        for (int p = 0; p < a.peers.n; ++p) {
+            const int q = a.peers.map[p][b];
+            if (q < 0 || (a.peers.touched[p] && a.peers.touched[p][q] != 1)) continue;
+            const float4 o = a.peers.raw[p][(size_t)q * 64 + slot];
+            node.x += o.x; node.y += o.y; node.z += o.z; node.w += o.w;
+        }
+        if (a.fuse_clear) {
+            a.raw_mut[idx] = make_float4(0.f, 0.f, 0.f, 0.f);
+            if (slot == 0) a.touched_mut[b] = 0;
+        }
+        m = node.x;
+        if (!(m > 0.0f)) {   // m <= 0 (pipeline.py:676-681)
+            a.vel[idx] = make_float4(0.f, 0.f, 0.f, 0.f);
+            return;
+        }
+        vx = node.y / m; vy = node.z / m; vz = node.w / m;
     }
-    if (a.fuse_clear) {
-        a.raw_mut[idx] = make_float4(0.f, 0.f, 0.f, 0.f);
-        if (slot == 0) a.touched_mut[b] = 0;
-    }
-    const float m = node.x;
-    if (!(m > 0.0f)) {   // m <= 0 (pipeline.py:676-681)
-        a.vel[idx] = make_float4(0.f, 0.f, 0.f, 0.f);
-        return;
-    }
-    float vx = node.y / m, vy = node.z / m, vz = node.w / m;
     if (a.vel_old) a.vel_old[idx] = make_float4(0.f, vx, vy, vz);   // saved before gravity (:692-698)
     vx += a.dt * a.gx; vy += a.dt * a.gy; vz += a.dt * a.gz;
     if (a.apply_bc) {
@@ -152,15 +179,21 @@ __global__ void __launch_bounds__(256) particle_aggregates_kernel(const float *_
 
 __global__ void __launch_bounds__(256) grid_aggregates_kernel(const float4 *__restrict__ raw,
                                                               const uint8_t *__restrict__ touched,
-                                                              int count, double *out4)
+                                                              int count, int det, double *out4)
 {
     const int b = blockIdx.x * 4 + (threadIdx.x >> 6);
     const int slot = threadIdx.x & 63;
     const int lane = threadIdx.x & 31;
     double m = 0, mx = 0, my = 0, mz = 0;
     if (b < count && touched[b]) {
-        const float4 n = raw[(size_t)b * 64 + slot];
-        m = n.x; mx = n.y; my = n.z; mz = n.w;
+        if (det) {
+            const longlong4 n = ((const longlong4 *)raw)[(size_t)b * 64 + slot];
+            m = (double)n.x / 1099511627776.0;
+            mx = (double)n.y / 4294967296.0; my = (double)n.z / 4294967296.0; mz = (double)n.w / 4294967296.0;
+        } else {
+            const float4 n = raw[(size_t)b * 64 + slot];
+            m = n.x; mx = n.y; my = n.z; mz = n.w;
+        }
     }
     m = warp_sum(m); mx = warp_sum(mx); my = warp_sum(my); mz = warp_sum(mz);
     if (lane == 0 && m != 0.0) {
@@ -195,10 +228,13 @@ using namespace mpm;
 
 extern "C" {
 
-int mpm_clear(float *raw, uint8_t *touched, int32_t count, int full, const mpm_guard *guard, void *stream)
+int mpm_clear(float *raw, uint8_t *touched, int32_t count, int full, int32_t node_bytes,
+              const mpm_guard *guard, void *stream)
 {
     if (count <= 0) return MPM_OK;
-    clear_kernel<<<(count + 3) / 4, 256, 0, (cudaStream_t)stream>>>((float4 *)raw, touched, count, full, make_guard(guard));
+    if (node_bytes != 16 && node_bytes != 32) return MPM_ERR_REJECTED_INPUT;
+    clear_kernel<<<(count + 3) / 4, 256, 0, (cudaStream_t)stream>>>((float4 *)raw, touched, count, full,
+                                                                    node_bytes / 16, make_guard(guard));
     return check_launch("mpm_clear", 1);
 }
 
@@ -241,6 +277,7 @@ int mpm_grid_update(float *raw, uint8_t *touched, float *vel, float *vel_old,
     a.dx = p->dx;
     a.fuse_clear = p->fuse_clear;
     a.block_filter = p->block_filter;
+    a.deterministic = p->deterministic;
     a.raw_mut = (float4 *)raw;
     a.touched_mut = touched;
     a.guard = make_guard(guard);
@@ -269,13 +306,14 @@ int mpm_particle_aggregates(const mpm_store_view *store, double *out5, void *str
     return check_launch("mpm_particle_aggregates", 1);
 }
 
-int mpm_grid_aggregates(const float *raw, const uint8_t *touched, int32_t count, double *out4,
-                        void *stream_)
+int mpm_grid_aggregates(const float *raw, const uint8_t *touched, int32_t count, int32_t deterministic,
+                        double *out4, void *stream_)
 {
     cudaStream_t stream = (cudaStream_t)stream_;
     cudaMemsetAsync(out4, 0, 4 * sizeof(double), stream);
     if (count > 0)
-        grid_aggregates_kernel<<<(count + 3) / 4, 256, 0, stream>>>((const float4 *)raw, touched, count, out4);
+        grid_aggregates_kernel<<<(count + 3) / 4, 256, 0, stream>>>((const float4 *)raw, touched, count,
+                                                                  deterministic, out4);
     return check_launch("mpm_grid_aggregates", 1);
 }
 

@@ -30,7 +30,8 @@ extern "C" int mpm_enqueue_steps(const mpm_step_plan *p, int32_t first_step, int
         if (k > 0) tp.dt_gather = tp.dt;
         if (!gp.fuse_clear) {
             // Worker._clear (pipeline.py:1022-1037): rows of this parity touched two steps ago
-            rc = mpm_clear(p->raw[par], p->touched[par], p->table.count, 0, &guard, stream);
+            rc = mpm_clear(p->raw[par], p->touched[par], p->table.count, 0, gp.deterministic ? 32 : 16, &guard,
+                           stream);
             if (rc != MPM_OK) return rc;
         }
         if (p->fused) {

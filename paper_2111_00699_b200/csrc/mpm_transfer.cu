@@ -11,6 +11,8 @@
 // segmented shuffle reduction and the run leader issues ONE vector reduction
 // (RED.E.ADD.F32x4) per grid node -- the reference's "one += per (subgroup, node)" contract
 // (pipeline.py:293-311) without sorting lanes first (its sort=none_between arm).
+#include <type_traits>
+
 #include "mpm_math.cuh"
 
 namespace mpm {
@@ -33,7 +35,7 @@ struct TransferArgs {
     float mu, lam, kappa, gamma, flip;
     float margin_lo, margin_hi;
     float theta_c, theta_s, hardening, sand_alpha;
-    int clamp_tension, count_stats;
+    int clamp_tension, count_stats, deterministic;
     DevGuard guard;
 };
 
@@ -51,6 +53,20 @@ constexpr int TW = MPM_TW;   // warps (groups) per CTA
 __device__ __forceinline__ void red_add_v4(float4 *addr, float a, float b, float c, float d)
 {
     atomicAdd(addr, make_float4(a, b, c, d));   // RED.E.ADD.F32x4 on sm_90+
+}
+
+// Deterministic mode (pipeline.py:43-44, 297-301): contributions are quantised to integers,
+// rint(c * 2^40) for mass and rint(c * 2^32) for momentum, and summed as int64 -- integer sums
+// do not depend on the order of the atomics, so results are identical across worker counts,
+// rebuild cadence and split / fused transfers.  A node is four int64 (32 bytes).
+#define MPM_MASS_SCALE 1099511627776.0f
+#define MPM_MOM_SCALE 4294967296.0f
+__device__ __forceinline__ void red_add_det(long long *node, long long a, long long b, long long c, long long d)
+{
+    atomicAdd((unsigned long long *)node + 0, (unsigned long long)a);
+    atomicAdd((unsigned long long *)node + 1, (unsigned long long)b);
+    atomicAdd((unsigned long long *)node + 2, (unsigned long long)c);
+    atomicAdd((unsigned long long *)node + 3, (unsigned long long)d);
 }
 
 __device__ __forceinline__ void quad_weights(float f, float *w)
@@ -199,7 +215,7 @@ __device__ __noinline__ void gather27_delta(const float4 *__restrict__ vel,
     dv[0] = d0; dv[1] = d1; dv[2] = d2;
 }
 
-template <int MAT, bool GATHER, bool SCATTER>
+template <int MAT, bool GATHER, bool SCATTER, bool DET>
 __global__ void __launch_bounds__(TW * 32, MPM_MINBLOCKS) transfer_kernel(const TransferArgs a)
 {
     if (guarded_out(a.guard)) return;
@@ -458,16 +474,25 @@ __global__ void __launch_bounds__(TW * 32, MPM_MINBLOCKS) transfer_kernel(const 
 #pragma unroll
                         for (int k = 0; k < 3; ++k) {
                             const float w = wxy * wz[k];
-                            float c0 = w * mm;
-                            float c1 = w * (XY0 + QZ[k][0]);
-                            float c2 = w * (XY1 + QZ[k][1]);
-                            float c3 = w * (XY2 + QZ[k][2]);
+                            typedef typename std::conditional<DET, long long, float>::type acc_t;
+                            acc_t c0, c1, c2, c3;
+                            if (DET) {
+                                c0 = (acc_t)__float2ll_rn((w * mm) * MPM_MASS_SCALE);
+                                c1 = (acc_t)__float2ll_rn((w * (XY0 + QZ[k][0])) * MPM_MOM_SCALE);
+                                c2 = (acc_t)__float2ll_rn((w * (XY1 + QZ[k][1])) * MPM_MOM_SCALE);
+                                c3 = (acc_t)__float2ll_rn((w * (XY2 + QZ[k][2])) * MPM_MOM_SCALE);
+                            } else {
+                                c0 = (acc_t)(w * mm);
+                                c1 = (acc_t)(w * (XY0 + QZ[k][0]));
+                                c2 = (acc_t)(w * (XY1 + QZ[k][1]));
+                                c3 = (acc_t)(w * (XY2 + QZ[k][2]));
+                            }
 #define MPM_SEG_STEP(D, P)                                                      \
     if (maxd >= D) {                                                            \
-        const float t0 = __shfl_down_sync(FULL, c0, D);                         \
-        const float t1 = __shfl_down_sync(FULL, c1, D);                         \
-        const float t2 = __shfl_down_sync(FULL, c2, D);                         \
-        const float t3 = __shfl_down_sync(FULL, c3, D);                         \
+        const acc_t t0 = __shfl_down_sync(FULL, c0, D);                         \
+        const acc_t t1 = __shfl_down_sync(FULL, c1, D);                         \
+        const acc_t t2 = __shfl_down_sync(FULL, c2, D);                         \
+        const acc_t t3 = __shfl_down_sync(FULL, c3, D);                         \
         if (P) { c0 += t0; c1 += t1; c2 += t2; c3 += t3; }                      \
     }
                             MPM_SEG_STEP(1, p1)
@@ -478,7 +503,10 @@ __global__ void __launch_bounds__(TW * 32, MPM_MINBLOCKS) transfer_kernel(const 
 #undef MPM_SEG_STEP
                             if (leader) {
                                 const int nb = nrow[nxy + az.nterm[k]];
-                                red_add_v4(&a.raw[(size_t)nb * 64 + (sxy | az.sterm[k])], c0, c1, c2, c3);
+                                const size_t node = (size_t)nb * 64 + (sxy | az.sterm[k]);
+                                if (DET) red_add_det((long long *)a.raw + node * 4, (long long)c0, (long long)c1,
+                                                     (long long)c2, (long long)c3);
+                                else red_add_v4(&a.raw[node], (float)c0, (float)c1, (float)c2, (float)c3);
                             }
                         }
                     }
@@ -544,6 +572,7 @@ static int fill_args(TransferArgs &a, const mpm_store_view *store, const mpm_tab
     a.hardening = (float)p->hardening; a.sand_alpha = (float)p->sand_alpha;
     a.clamp_tension = p->clamp_tension;
     a.count_stats = p->count_stats;
+    a.deterministic = p->deterministic;
     a.guard = make_guard(guard);
     if (a.flip > 0.0f && !vel_old) return MPM_ERR_REJECTED_INPUT;
     return MPM_OK;
@@ -554,18 +583,31 @@ static int launch_transfer(const TransferArgs &a, int mat, cudaStream_t stream)
 {
     if (a.n_groups <= 0) return MPM_OK;
     const int grid = (a.n_groups + TW - 1) / TW;
+    if (a.deterministic && SCATTER) {
+        // fixed-point accumulation exists for the reference's own material kinds
+        switch (mat) {
+        case MPM_MAT_FLUID:
+            transfer_kernel<MPM_MAT_FLUID, GATHER, SCATTER, true><<<grid, TW * 32, 0, stream>>>(a);
+            return MPM_OK;
+        case MPM_MAT_FIXED_COROTATED:
+            transfer_kernel<MPM_MAT_FIXED_COROTATED, GATHER, SCATTER, true><<<grid, TW * 32, 0, stream>>>(a);
+            return MPM_OK;
+        default:
+            return MPM_ERR_CONFIG;
+        }
+    }
     switch (mat) {
     case MPM_MAT_FLUID:
-        transfer_kernel<MPM_MAT_FLUID, GATHER, SCATTER><<<grid, TW * 32, 0, stream>>>(a);
+        transfer_kernel<MPM_MAT_FLUID, GATHER, SCATTER, false><<<grid, TW * 32, 0, stream>>>(a);
         break;
     case MPM_MAT_FIXED_COROTATED:
-        transfer_kernel<MPM_MAT_FIXED_COROTATED, GATHER, SCATTER><<<grid, TW * 32, 0, stream>>>(a);
+        transfer_kernel<MPM_MAT_FIXED_COROTATED, GATHER, SCATTER, false><<<grid, TW * 32, 0, stream>>>(a);
         break;
     case MPM_MAT_SNOW:
-        transfer_kernel<MPM_MAT_SNOW, GATHER, SCATTER><<<grid, TW * 32, 0, stream>>>(a);
+        transfer_kernel<MPM_MAT_SNOW, GATHER, SCATTER, false><<<grid, TW * 32, 0, stream>>>(a);
         break;
     case MPM_MAT_SAND:
-        transfer_kernel<MPM_MAT_SAND, GATHER, SCATTER><<<grid, TW * 32, 0, stream>>>(a);
+        transfer_kernel<MPM_MAT_SAND, GATHER, SCATTER, false><<<grid, TW * 32, 0, stream>>>(a);
         break;
     default:
         return MPM_ERR_CONFIG;

@@ -147,6 +147,10 @@ class DistWorker(CudaWorker):
 
     def __init__(self, runtime: DistRuntime, params, material, boundary, options=None, **kw):
         super().__init__(runtime.wid, runtime, params, material, boundary, options, **kw)
+        if self.options.deterministic:
+            from .errors import ConfigError
+            raise ConfigError("deterministic mode is implemented for workers of one process "
+                              "(CudaCluster); halo rows are exchanged as float4 between processes")
         self.pipelined = False
         self.fuse_clear = False
         n = runtime.n_workers

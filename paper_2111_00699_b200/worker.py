@@ -382,9 +382,12 @@ class CudaGrid:
     """raw[0], raw[1], vel (+ vel_old): float4 nodes [pblock][64] on the device.  The numpy
     properties return the reference's channel-major float64 layout [pblock, 4, 64]."""
 
-    def __init__(self, device):
+    def __init__(self, device, deterministic=False):
         self.device = device
-        self._raw = [DeviceBuffer(torch.float32, (64, 4), device), DeviceBuffer(torch.float32, (64, 4), device)]
+        # deterministic mode: a raw node is four int64 (rint(c 2^40), rint(c 2^32) x3), pipeline.py:43-44
+        rdt = torch.int64 if deterministic else torch.float32
+        self.deterministic = bool(deterministic)
+        self._raw = [DeviceBuffer(rdt, (64, 4), device), DeviceBuffer(rdt, (64, 4), device)]
         self._vel = DeviceBuffer(torch.float32, (64, 4), device)
         self._vel_old = None
         self.count = 0
@@ -443,12 +446,13 @@ class CudaWorker:
         if self.options.fusion != "merged" or self.options.sort == "full_every_step":
             raise ConfigError("the CUDA core implements fusion=merged and sort=amortized|none_between "
                               "(the other arms re-measure CPU ablations, SURVEY.md section 2 row 13)")
-        if self.options.deterministic:
-            raise ConfigError("deterministic fixed-point accumulation is not implemented on the CUDA core")
+        if self.options.deterministic and int(material.kind) not in (0, 1):
+            raise ConfigError("deterministic fixed-point accumulation covers the reference's material "
+                              "kinds (fluid, fixed-corotated)")
         with torch.cuda.device(self.device):
             self.store = CudaParticleStore(material.kind, params.lane_width, self.device)
             self.table = CudaBlockTable(self.device)
-            self.grid = CudaGrid(self.device)
+            self.grid = CudaGrid(self.device, self.options.deterministic)
             self.store._table = self.table
             # status ring: one block per in-flight step (zone flag, max speed^2, counters); the
             # counters of a slot accumulate over every step that used it
@@ -464,7 +468,8 @@ class CudaWorker:
             self._guard_word = torch.full((1,), _INT_MAX, dtype=torch.int32, device=self.device)
             self._scalars = torch.zeros(16, dtype=torch.int32, device=self.device)
             self._scalars_host = torch.zeros(16, dtype=torch.int32).pin_memory()
-        self.flags = StepFlags(deterministic_mode=False)
+        self.flags = StepFlags(deterministic_mode=bool(self.options.deterministic))
+        self._node_bytes = 32 if self.options.deterministic else 16
         self.conservation = []
         self.rebuild_steps = []
         self.dt = params.dt
@@ -504,6 +509,7 @@ class CudaWorker:
             mat_kind=int(m.kind), nch=self.store.nch, mu=float(m.mu), lam=float(m.lam),
             kappa=float(m.bulk_modulus), gamma=float(m.gamma),
             clamp_tension=int(bool(m.clamp_tension)), count_stats=int(self.count_stats),
+            deterministic=int(bool(self.options.deterministic)),
             density=float(m.density), dx=float(params.dx), dt=float(params.dt),
             dt_gather=float(params.dt), flip_blend=float(params.flip_blend),
             margin_lo=FREE_ZONE_LO_CELLS, margin_hi=FREE_ZONE_HI_CELLS - 4.0,
@@ -996,7 +1002,8 @@ class CudaWorker:
         gr.count = count
         gr._vel.data[:count].zero_()
         if count:
-            self._call("mpm_clear", gr._raw[par].ptr, tb._touched[par].ptr, count, 1, None, stream)
+            self._call("mpm_clear", gr._raw[par].ptr, tb._touched[par].ptr, count, 1, self._node_bytes,
+                       None, stream)
         for k in (0, 1):
             tb._touched[k].len = count
         self._pending_full_clear_parity = 1 - par
@@ -1019,7 +1026,7 @@ class CudaWorker:
         elif self.fuse_clear and self.runtime.n_workers == 1:
             return   # rows were zeroed by the grid update that consumed them
         self._call("mpm_clear", self.grid._raw[par].ptr, self.table._touched[par].ptr, count, full,
-                   self._gref(), _stream_ptr())
+                   self._node_bytes, self._gref(), _stream_ptr())
 
     def _params(self, margin_shrink=0.0):
         tp = self._tp
@@ -1196,6 +1203,7 @@ class CudaWorker:
                     gp.box_hi[k] = float(bc.max_corner[k])
             gp.dx = float(self.params.dx)
         gp.dt = float(self.dt)
+        gp.deterministic = int(bool(self.options.deterministic))
         gp.block_filter = 0
         gp.fuse_clear = 0
         gp.n_peers = 0
@@ -1210,7 +1218,7 @@ class CudaWorker:
         """(pm, pmom x3, gm, gmom x3) rows of pipeline.py:1189-1203 (own raw rows only)."""
         out = torch.zeros(4, dtype=torch.float64, device=self.device)
         self._call("mpm_grid_aggregates", self.grid._raw[par].ptr, self.table._touched[par].ptr,
-                   self.table.count, out.data_ptr(), _stream_ptr())
+                   self.table.count, int(self.options.deterministic), out.data_ptr(), _stream_ptr())
         p = self.store._aggregates()
         g = out.cpu().numpy()
         self.conservation.append((p[0], p[1], p[2], p[3], g[0], g[1], g[2], g[3]))

@@ -280,3 +280,46 @@ def test_fountain_frames_with_emission_against_oracle():
     assert wc.rebuild_steps == wo.rebuild_steps
     edge = 64 * 0.66
     _assert_particles(U.state_by_id(wc), U.state_by_id(wo), edge, 1, run=True)
+
+
+# ---- deterministic fixed-point mode (pipeline.py:43-44, 297-301, 682-686) -----------------------
+# Integer sums do not depend on the order of the atomics, which gives the reference's strongest
+# oracles (tests/test_acceptance.py:85-151, tests/test_multiworker.py:223-226): bit-identical
+# particles across worker counts, rebuild cadence and split / fused transfers.
+def _det_state(n_workers, steps=10, **opts):
+    from paper_2111_00699_b200 import CudaCluster, PipelineOptions
+    g = golden("det.npz")
+    material, params, boundary = elastic_setup()
+    cl = CudaCluster(n_workers, params, material, boundary, PipelineOptions(deterministic=True, **opts))
+    cl.seed(g["pos"], g["vel"], float(g["mass"]))
+    for s in range(steps):
+        cl.run_step(s)
+    for w in cl.workers:
+        if w._pending_gather:
+            w._flush_gather()
+    return g, cl
+
+
+def test_deterministic_mode_bit_identical_across_worker_counts():
+    g, c1 = _det_state(1)
+    s1 = c1.state_sorted_by_id()
+    for n in (2, 3):
+        _, cn = _det_state(n)
+        assert np.array_equal(cn.state_sorted_by_id(), s1), n
+    # and within fp32 tolerance of the reference's own deterministic run (8 steps)
+    _, c8 = _det_state(1, steps=8)
+    edge = float(g["pos"].max() - g["pos"].min())
+    _assert_particles(c8.state_sorted_by_id(), g["state_8_n1"], edge, 9, run=True)
+
+
+def test_deterministic_mode_bit_identical_across_rebuild_cadence_and_fusion():
+    _, a = _det_state(1, steps=12)
+    ref = a.state_sorted_by_id()
+    _, b = _det_state(1, steps=12, rebuild="every_step")
+    assert np.array_equal(b.state_sorted_by_id(), ref)             # tests/test_pipeline.py:314-319
+    _, c = _det_state(1, steps=12, transfer="g2p2g")
+    assert np.array_equal(c.state_sorted_by_id()[:, [0, 1, 2, 3, 4, 5, 15] + list(range(16, 25))],
+                          ref[:, [0, 1, 2, 3, 4, 5, 15] + list(range(16, 25))])   # :255-258
+    assert a.workers[0].grid.raw[0].dtype == np.float64
+    raw = a.workers[0].grid.raw[1]
+    assert np.array_equal(raw, np.rint(raw))                       # integer-valued sums
