@@ -42,11 +42,11 @@ struct TransferArgs {
 #ifndef MPM_TW
 #define MPM_TW 8
 #endif
-#ifndef MPM_SUBRUN
-#define MPM_SUBRUN 32
-#endif
 #ifndef MPM_MINBLOCKS
 #define MPM_MINBLOCKS 3
+#endif
+#ifndef MPM_LATE_F
+#define MPM_LATE_F 1
 #endif
 constexpr int TW = MPM_TW;   // warps (groups) per CTA
 
@@ -76,82 +76,110 @@ __device__ __forceinline__ void quad_weights(float f, float *w)
     w[1] = 0.75f - (f - 1.0f) * (f - 1.0f);
     w[2] = 0.5f * ((f - 0.5f) * (f - 0.5f));
 }
+// the same weight for a loop index that is not a compile-time constant: with d = f - i,
+// w_1 = 0.75 - d^2 and w_0, w_2 = 0.5 (1.5 - |d|)^2
+__device__ __forceinline__ float quad_weight_at(float f, int i)
+{
+    const float d = f - (float)i;
+    const float e = 1.5f - fabsf(d);
+    return i == 1 ? 0.75f - d * d : 0.5f * (e * e);
+}
 
-// base cell (unbiased) of the quadratic stencil: floor(p * inv_dx - 0.5); one shared form so
-// the gather, the lane-key refresh and the scatter all see the same rounding.
+// base cell (unbiased) of the quadratic stencil: floor(p * inv_dx - 0.5)
 __device__ __forceinline__ float stencil_base(float p, float inv_dx, float *g)
 {
     *g = p * inv_dx;
     return floorf(*g - 0.5f);
 }
 
-// Per-axis addressing of the three stencil cells: term of the neighbour-row index and term of
-// the node slot.  The 27 node addresses are nrow[nx+ny+nz] * 64 + (sx|sy|sz): no branch per
-// node; validity (every cell inside the 3x3x3 pblock set, pipeline.py:266-275) is decided
-// once per particle and axis.
-struct AxisAddr {
-    int nterm[3];
-    int sterm[3];
-    int rmask;      // bit r set for every neighbour coordinate used on this axis
-    int bad;        // stencil cells outside the neighbourhood
-};
+// ---------------------------------------------------------------------------------------
+// Addressing from the lane key (pipeline.py:261-275).  A key digit k in 0..9 is the stencil
+// base cell relative to (origin - 4); origin = 4 * block coordinate, so stencil cell
+// t = k + i (0..11) lies in neighbour block t >> 2 (0..2) at in-block coordinate t & 3: every
+// address is arithmetic on t, always inside the 3x3x3 neighbourhood, no validity branch.
+// The node index is nrow[rx + 3 ry + 9 rz] + (sx | sy | sz) where nrow (shared memory) holds
+// 64 * pblock of the 27 neighbours and s* are the slot bits of the axis (pipeline.py:144-147).
+// ---------------------------------------------------------------------------------------
 template <int AXIS>
-__device__ __forceinline__ void axis_addr(int cell, int block_coord, AxisAddr &a)
+__device__ __forceinline__ int slot_bits(int t)
 {
-    constexpr int nstride = AXIS == 0 ? 1 : (AXIS == 1 ? 3 : 9);
-    a.rmask = 0;
-    a.bad = 0;
-#pragma unroll
-    for (int i = 0; i < 3; ++i) {
-        const int c = cell + i;
-        int r = (c >> 2) - block_coord + 1;
-        if (r < 0 || r > 2) { ++a.bad; r = 1; }
-        a.nterm[i] = r * nstride;
-        a.sterm[i] = ((c & 1) << AXIS) | ((c & 2) << (AXIS + 2));
-        a.rmask |= 1 << r;
-    }
+    return ((t & 1) << AXIS) | ((t & 2) << (AXIS + 2));
+}
+__device__ __forceinline__ int axis_block_bits(int k)
+{
+    return (1 << (k >> 2)) | (1 << ((k + 2) >> 2));   // neighbour coordinates a stencil at digit k uses
+}
+// 27-bit mask of the neighbour blocks addressed by a stencil = outer product of the per-axis sets
+__device__ __forceinline__ unsigned block_mask27(int kx, int ky, int kz)
+{
+    const unsigned row = (unsigned)axis_block_bits(kx);
+    const int my = axis_block_bits(ky), mz = axis_block_bits(kz);
+    const unsigned plane = ((my & 1) ? row : 0u) | ((my & 2) ? row << 3 : 0u) | ((my & 4) ? row << 6 : 0u);
+    return ((mz & 1) ? plane : 0u) | ((mz & 2) ? plane << 9 : 0u) | ((mz & 4) ? plane << 18 : 0u);
 }
 
-// 27-bit mask of the neighbour blocks addressed by a stencil = outer product of the per-axis sets
-__device__ __forceinline__ unsigned block_mask27(const AxisAddr &ax, const AxisAddr &ay, const AxisAddr &az)
+// number of stencil cells that fall outside the 3x3x3 block neighbourhood, from the position
+// (pipeline.py:266-275, 462-475): only evaluated for a particle whose key does not match its
+// position any more (it left the neighbourhood: a contract violation, pipeline.py:1233-1238)
+__device__ __noinline__ int count_bad_nodes(float px, float py, float pz, float inv_dx, int ox, int oy, int oz)
 {
-    const unsigned row = (unsigned)ax.rmask;
-    const unsigned plane = ((ay.rmask & 1) ? row : 0u) | ((ay.rmask & 2) ? row << 3 : 0u) |
-                           ((ay.rmask & 4) ? row << 6 : 0u);
-    return ((az.rmask & 1) ? plane : 0u) | ((az.rmask & 2) ? plane << 9 : 0u) |
-           ((az.rmask & 4) ? plane << 18 : 0u);
+    const float p[3] = {px, py, pz};
+    const int o[3] = {ox, oy, oz};
+    int good[3];
+#pragma unroll 1
+    for (int a = 0; a < 3; ++a) {
+        float g;
+        const int cell = (int)stencil_base(p[a], inv_dx, &g) + MPM_CELL_BIAS;
+        int n = 0;
+#pragma unroll 1
+        for (int i = 0; i < 3; ++i) {
+            const int r = ((cell + i) >> 2) - (o[a] >> 2) + 1;
+            n += (r >= 0 && r <= 2);
+        }
+        good[a] = n;
+    }
+    const int bad = 27 - good[0] * good[1] * good[2];
+    return bad ? bad : 27;
 }
 
 // ---------------------------------------------------------------------------------------
 // gather (pipeline.py:459-501): v = sum w v_n and B = sum w v_n (x) dpos evaluated as
 // separable partial sums along z, then y, then x.  With node indices centred on the middle
 // node (i-1 in {-1,0,1}) the first moments are M = sum w v_n (i-1), and
-// B = dx (M - (f-1) v): ~240 flops instead of ~460 for the direct triple loop.
+// B = dx (M - (f-1) v): ~240 flops instead of ~460 for the direct triple loop.  The x loop is
+// kept rolled (nine nodes per trip): a third of the code, which matters because the kernel
+// is far larger than the 32 KB instruction cache level next to the SM.
 // ---------------------------------------------------------------------------------------
 struct Gathered {
     float v[3];
     float B[9];     // row-major, B[a][b] = sum w v_a dpos_b
 };
 
-__device__ __forceinline__ void gather27(const float4 *__restrict__ vel, const int *nrow,
-                                         const AxisAddr &ax, const AxisAddr &ay, const AxisAddr &az,
-                                         const float *wx, const float *wy, const float *wz,
-                                         float fx, float fy, float fz, float dx, Gathered &out)
+__device__ __forceinline__ void gather27(const float4 *__restrict__ vel, const int *nrow, int kx, int ky,
+                                         int kz, float fx, float fy, float fz, float dx, Gathered &out)
 {
-    float V[3] = {0.f, 0.f, 0.f}, Mx[3] = {0.f, 0.f, 0.f}, My[3] = {0.f, 0.f, 0.f}, Mz[3] = {0.f, 0.f, 0.f};
+    float wy[3], wz[3];
+    quad_weights(fy, wy); quad_weights(fz, wz);
+    int ry[3], rz[3], sy[3], sz[3];
 #pragma unroll
+    for (int q = 0; q < 3; ++q) {
+        ry[q] = ((ky + q) >> 2) * 3; sy[q] = slot_bits<1>(ky + q);
+        rz[q] = ((kz + q) >> 2) * 9; sz[q] = slot_bits<2>(kz + q);
+    }
+    float V[3] = {0.f, 0.f, 0.f}, Mx[3] = {0.f, 0.f, 0.f}, My[3] = {0.f, 0.f, 0.f}, Mz[3] = {0.f, 0.f, 0.f};
+#pragma unroll 1
     for (int i = 0; i < 3; ++i) {
+        const int rx = (kx + i) >> 2, sx = slot_bits<0>(kx + i);
+        const float wxi = quad_weight_at(fx, i);
+        const float cmi = (float)(i - 1) * wxi;
         float S[3] = {0.f, 0.f, 0.f}, Ty[3] = {0.f, 0.f, 0.f}, Tz[3] = {0.f, 0.f, 0.f};
 #pragma unroll
         for (int j = 0; j < 3; ++j) {
-            const int nxy = ax.nterm[i] + ay.nterm[j];
-            const int sxy = ax.sterm[i] | ay.sterm[j];
+            const int rxy = rx + ry[j];
+            const int sxy = sx + sy[j];
             float4 n[3];
 #pragma unroll
-            for (int k = 0; k < 3; ++k) {
-                const int nb = nrow[nxy + az.nterm[k]];
-                n[k] = __ldg(&vel[(size_t)nb * 64 + (sxy | az.sterm[k])]);
-            }
+            for (int k = 0; k < 3; ++k) n[k] = __ldg(&vel[nrow[rxy + rz[k]] + sxy + sz[k]]);
             // along z: s = sum_k wz_k v_k, t = wz_2 v_2 - wz_0 v_0
             const float s0 = wz[0] * n[0].y + wz[1] * n[1].y + wz[2] * n[2].y;
             const float s1 = wz[0] * n[0].z + wz[1] * n[1].z + wz[2] * n[2].z;
@@ -168,14 +196,10 @@ __device__ __forceinline__ void gather27(const float4 *__restrict__ vel, const i
         }
 #pragma unroll
         for (int c = 0; c < 3; ++c) {
-            V[c] += wx[i] * S[c];
-            My[c] += wx[i] * Ty[c];
-            Mz[c] += wx[i] * Tz[c];
-        }
-        if (i != 1) {
-            const float wi = i == 0 ? -wx[0] : wx[2];
-#pragma unroll
-            for (int c = 0; c < 3; ++c) Mx[c] += wi * S[c];
+            V[c] += wxi * S[c];
+            My[c] += wxi * Ty[c];
+            Mz[c] += wxi * Tz[c];
+            Mx[c] += cmi * S[c];
         }
     }
     const float gx = fx - 1.0f, gy = fy - 1.0f, gz = fz - 1.0f;
@@ -188,31 +212,133 @@ __device__ __forceinline__ void gather27(const float4 *__restrict__ vel, const i
     }
 }
 
-// FLIP increment sum w (v_n - v_old_n) (pipeline.py:489-495).  Only evaluated when blending,
-// kept out of line and rolled: its dynamically indexed copies of the weights / address terms
-// live in its own frame and cost the APIC path nothing.
-struct StencilCopy {
-    int nx[3], ny[3], nz[3], sx[3], sy[3], sz[3];
-    float wx[3], wy[3], wz[3];
-};
+// FLIP increment sum w (v_n - v_old_n) (pipeline.py:489-495).  Only evaluated when blending:
+// out of line and fully rolled, it costs the APIC path nothing.
 __device__ __noinline__ void gather27_delta(const float4 *__restrict__ vel,
                                             const float4 *__restrict__ vel_old, const int *nrow,
-                                            const StencilCopy st, float *dv)
+                                            int kx, int ky, int kz, float fx, float fy, float fz,
+                                            float *dv)
 {
     float d0 = 0.f, d1 = 0.f, d2 = 0.f;
 #pragma unroll 1
-    for (int i = 0; i < 3; ++i)
+    for (int i = 0; i < 3; ++i) {
+        const float wxi = quad_weight_at(fx, i);
 #pragma unroll 1
-        for (int j = 0; j < 3; ++j)
+        for (int j = 0; j < 3; ++j) {
+            const float wxy = wxi * quad_weight_at(fy, j);
 #pragma unroll 1
             for (int k = 0; k < 3; ++k) {
-                const int nb = nrow[st.nx[i] + st.ny[j] + st.nz[k]];
-                const size_t idx = (size_t)nb * 64 + (st.sx[i] | st.sy[j] | st.sz[k]);
+                const int r = ((kx + i) >> 2) + ((ky + j) >> 2) * 3 + ((kz + k) >> 2) * 9;
+                const int idx = nrow[r] + (slot_bits<0>(kx + i) | slot_bits<1>(ky + j) | slot_bits<2>(kz + k));
                 const float4 vn = __ldg(&vel[idx]), vo = __ldg(&vel_old[idx]);
-                const float w = st.wx[i] * st.wy[j] * st.wz[k];
+                const float w = wxy * quad_weight_at(fz, k);
                 d0 += w * (vn.y - vo.y); d1 += w * (vn.z - vo.z); d2 += w * (vn.w - vo.w);
             }
+        }
+    }
     dv[0] = d0; dv[1] = d1; dv[2] = d2;
+}
+
+// ---------------------------------------------------------------------------------------
+// scatter (pipeline.py:242-312).  Momentum of node (i,j,k): w (m v + Q dpos) with
+// dpos = ((i,j,k) - f) dx, built up axis by axis.  Runs of consecutive lanes with the same key
+// are summed with a segmented shuffle reduction of NSTEPS = ceil(log2(longest run of the warp))
+// steps and the run leader issues one vector reduction per node.  `reach` = lanes of my run
+// after me; the step of distance D adds lane + D when reach >= D, expressed as a multiply by a
+// 0/1 float so that the 27 x NSTEPS adds need no predicate.  NSTEPS is a template parameter
+// (one dispatch per warp instead of a uniform branch per node and step); x loop rolled.
+// ---------------------------------------------------------------------------------------
+template <int NSTEPS, bool DET>
+__device__ __forceinline__ void scatter27(float4 *__restrict__ raw, const int *nrow, int kx, int ky, int kz,
+                                          float fx, float fy, float fz, float dx, float mm, float vx,
+                                          float vy, float vz, const float *Q, int reach, int maxd,
+                                          bool leader)
+{
+    const unsigned FULL = 0xffffffffu;
+    typedef typename std::conditional<DET, long long, float>::type acc_t;
+    float wy[3], wz[3];
+    quad_weights(fy, wy); quad_weights(fz, wz);
+    int ry[3], rz[3], sy[3], sz[3];
+#pragma unroll
+    for (int q = 0; q < 3; ++q) {
+        ry[q] = ((ky + q) >> 2) * 3; sy[q] = slot_bits<1>(ky + q);
+        rz[q] = ((kz + q) >> 2) * 9; sz[q] = slot_bits<2>(kz + q);
+    }
+    float QZ[3][3];
+#pragma unroll
+    for (int k = 0; k < 3; ++k) {
+        const float dpz = ((float)k - fz) * dx;
+        QZ[k][0] = Q[2] * dpz; QZ[k][1] = Q[5] * dpz; QZ[k][2] = Q[8] * dpz;
+    }
+    const float f1 = reach >= 1 ? 1.0f : 0.0f, f2 = reach >= 2 ? 1.0f : 0.0f, f4 = reach >= 4 ? 1.0f : 0.0f,
+                f8 = reach >= 8 ? 1.0f : 0.0f, f16 = reach >= 16 ? 1.0f : 0.0f;
+#pragma unroll 1
+    for (int i = 0; i < 3; ++i) {
+        const int rx = (kx + i) >> 2, sx = slot_bits<0>(kx + i);
+        const float wxi = mm > 0.0f ? quad_weight_at(fx, i) : 0.0f;   // inactive lanes contribute zeros
+        const float dpx = ((float)i - fx) * dx;
+        const float X0 = mm * vx + Q[0] * dpx, X1 = mm * vy + Q[3] * dpx, X2 = mm * vz + Q[6] * dpx;
+#pragma unroll
+        for (int j = 0; j < 3; ++j) {
+            const float dpy = ((float)j - fy) * dx;
+            const float wxy = wxi * wy[j];
+            const float XY0 = X0 + Q[1] * dpy, XY1 = X1 + Q[4] * dpy, XY2 = X2 + Q[7] * dpy;
+            const int rxy = rx + ry[j];
+            const int sxy = sx + sy[j];
+#pragma unroll
+            for (int k = 0; k < 3; ++k) {
+                const float w = wxy * wz[k];
+                acc_t c0, c1, c2, c3;
+                if (DET) {
+                    c0 = (acc_t)__float2ll_rn((w * mm) * MPM_MASS_SCALE);
+                    c1 = (acc_t)__float2ll_rn((w * (XY0 + QZ[k][0])) * MPM_MOM_SCALE);
+                    c2 = (acc_t)__float2ll_rn((w * (XY1 + QZ[k][1])) * MPM_MOM_SCALE);
+                    c3 = (acc_t)__float2ll_rn((w * (XY2 + QZ[k][2])) * MPM_MOM_SCALE);
+                } else {
+                    c0 = (acc_t)(w * mm);
+                    c1 = (acc_t)(w * (XY0 + QZ[k][0]));
+                    c2 = (acc_t)(w * (XY1 + QZ[k][1]));
+                    c3 = (acc_t)(w * (XY2 + QZ[k][2]));
+                }
+#define MPM_SEG_STEP(D, FD)                                                                         \
+    if ((1 << (NSTEPS - 1)) >= D && (!DET || maxd >= D)) {                                          \
+        const acc_t t0 = __shfl_down_sync(FULL, c0, D);                                             \
+        const acc_t t1 = __shfl_down_sync(FULL, c1, D);                                             \
+        const acc_t t2 = __shfl_down_sync(FULL, c2, D);                                             \
+        const acc_t t3 = __shfl_down_sync(FULL, c3, D);                                             \
+        if (DET) {                                                                                  \
+            if (reach >= D) { c0 += t0; c1 += t1; c2 += t2; c3 += t3; }                             \
+        } else {                                                                                    \
+            c0 = (acc_t)fmaf((float)t0, FD, (float)c0); c1 = (acc_t)fmaf((float)t1, FD, (float)c1); \
+            c2 = (acc_t)fmaf((float)t2, FD, (float)c2); c3 = (acc_t)fmaf((float)t3, FD, (float)c3); \
+        }                                                                                           \
+    }
+                MPM_SEG_STEP(1, f1)
+                MPM_SEG_STEP(2, f2)
+                MPM_SEG_STEP(4, f4)
+                MPM_SEG_STEP(8, f8)
+                MPM_SEG_STEP(16, f16)
+#undef MPM_SEG_STEP
+                if (leader) {
+                    const int node = nrow[rxy + rz[k]] + sxy + sz[k];
+                    if (DET) red_add_det((long long *)raw + (size_t)node * 4, (long long)c0, (long long)c1,
+                                         (long long)c2, (long long)c3);
+                    else red_add_v4(&raw[node], (float)c0, (float)c1, (float)c2, (float)c3);
+                }
+            }
+        }
+    }
+}
+
+template <int MAT>
+__device__ __forceinline__ void load_deformation(const float *gd, float *F, float &plastic)
+{
+    if (MAT == MPM_MAT_FLUID) F[0] = gd[CH_DEF * 32];
+    else {
+#pragma unroll
+        for (int r = 0; r < 9; ++r) F[r] = gd[(CH_DEF + r) * 32];
+        if (MAT >= MPM_MAT_SNOW) plastic = gd[CH_PLASTIC * 32];
+    }
 }
 
 template <int MAT, bool GATHER, bool SCATTER, bool DET>
@@ -220,322 +346,221 @@ __global__ void __launch_bounds__(TW * 32, MPM_MINBLOCKS) transfer_kernel(const 
 {
     if (guarded_out(a.guard)) return;
     __shared__ int s_nrow[TW][28];
-    __shared__ unsigned s_vmax[TW];
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int g = blockIdx.x * TW + warp;
     const unsigned FULL = 0xffffffffu;
+    if (g >= a.n_groups) return;     // warps are independent: no CTA-wide barrier below
+
+    const int len = a.group_len[g];
+    const int block = a.group_block[g];
+    const int4 org = a.origin[block];
+    if (lane < 27) s_nrow[warp][lane] = a.neighbor[block * 27 + lane] * 64;   // node index of slot 0
+    __syncwarp();
+    const int *nrow = s_nrow[warp];
+
+    float *gd = a.data + (size_t)g * a.nch * 32 + lane;
+    uint16_t meta = a.meta[g * 32 + lane];
+    bool active = lane < len && !(meta & MPM_LANE_QUARANTINED);
+    float m = active ? gd[CH_MASS * 32] : 0.0f;
+    active = active && (m > 0.0f);
+    int key = meta & 0x3ff;
+
+    float px = 0.f, py = 0.f, pz = 0.f, vx = 0.f, vy = 0.f, vz = 0.f;
+    float C[9];
+    float F[9];   // F (elastic kinds) or F[0] = J (fluid)
+    float tau[9]; // plastic kinds: stress of the projected state, produced by the gather
+    float plastic = 0.f;
+    const PlasticParams pp = {a.mu, a.lam, a.theta_c, a.theta_s, a.hardening, a.sand_alpha};
+    int addr_err = 0;
     unsigned vmax_bits = 0;
+    // the deformation state is loaded after the 27-node gather (MPM_LATE_F): nine registers less
+    // across the gather loop
+    if (active) {
+        px = gd[(CH_POS + 0) * 32]; py = gd[(CH_POS + 1) * 32]; pz = gd[(CH_POS + 2) * 32];
+        if (!(GATHER && MPM_LATE_F)) load_deformation<MAT>(gd, F, plastic);
+    }
 
-    if (g < a.n_groups) {
-        const int len = a.group_len[g];
-        const int block = a.group_block[g];
-        const int4 org = a.origin[block];
-        if (lane < 27) s_nrow[warp][lane] = a.neighbor[block * 27 + lane];
-        __syncwarp();
-        const int *nrow = s_nrow[warp];
-        const int bcx = org.x >> 2, bcy = org.y >> 2, bcz = org.z >> 2;
-
-        float *gd = a.data + (size_t)g * a.nch * 32 + lane;
-        uint16_t meta = a.meta[g * 32 + lane];
-        bool active = lane < len && !(meta & MPM_LANE_QUARANTINED);
-        float m = active ? gd[CH_MASS * 32] : 0.0f;
-        active = active && (m > 0.0f);
-        int key = meta & 0x3ff;
-
-        float px = 0.f, py = 0.f, pz = 0.f, vx = 0.f, vy = 0.f, vz = 0.f;
-        float C[9];
-        float F[9];   // F (elastic kinds) or F[0] = J (fluid)
-        float tau[9]; // plastic kinds: stress of the projected state, produced by the gather
-        float plastic = 0.f;
-        const PlasticParams pp = {a.mu, a.lam, a.theta_c, a.theta_s, a.hardening, a.sand_alpha};
-        int addr_err = 0;
+    // =========================== gather (pipeline.py:400-600) ===========================
+    if (GATHER) {
         if (active) {
-            px = gd[(CH_POS + 0) * 32]; py = gd[(CH_POS + 1) * 32]; pz = gd[(CH_POS + 2) * 32];
-            if (MAT == MPM_MAT_FLUID) F[0] = gd[CH_DEF * 32];
-            else {
+            // The key was refreshed from this very position by the previous gather (or computed at
+            // the rebuild), so its digits are the stencil base; the position relative to that base
+            // must lie in [0.5, 1.5) cells.  If it does not, the particle has left the
+            // neighbourhood its key can express (the digits were clamped).
+            const int kx = key % 10, ky = (key / 10) % 10, kz = key / 100;
+            const float fx = px * a.inv_dx - (float)(org.x - 4 + kx - MPM_CELL_BIAS);
+            const float fy = py * a.inv_dx - (float)(org.y - 4 + ky - MPM_CELL_BIAS);
+            const float fz = pz * a.inv_dx - (float)(org.z - 4 + kz - MPM_CELL_BIAS);
+            if (!(fabsf(fx - 1.0f) <= 0.501f && fabsf(fy - 1.0f) <= 0.501f && fabsf(fz - 1.0f) <= 0.501f)) {
+                // contract violation (pipeline.py:1233-1238): counted, particle left untouched
+                addr_err += count_bad_nodes(px, py, pz, a.inv_dx, org.x, org.y, org.z);
+                active = false;
+            } else {
+                Gathered G;
+                gather27(a.vel, nrow, kx, ky, kz, fx, fy, fz, a.dx, G);
+                if (MPM_LATE_F) load_deformation<MAT>(gd, F, plastic);
+                float nvx = G.v[0], nvy = G.v[1], nvz = G.v[2];
 #pragma unroll
-                for (int r = 0; r < 9; ++r) F[r] = gd[(CH_DEF + r) * 32];
-                if (MAT >= MPM_MAT_SNOW) plastic = gd[CH_PLASTIC * 32];
-            }
-        }
-
-        // =========================== gather (pipeline.py:400-600) ===========================
-        if (GATHER) {
-            if (active) {
-                float gx, gy, gz;
-                const float bxf = stencil_base(px, a.inv_dx, &gx);
-                const float byf = stencil_base(py, a.inv_dx, &gy);
-                const float bzf = stencil_base(pz, a.inv_dx, &gz);
-                const float fx = gx - bxf, fy = gy - byf, fz = gz - bzf;
-                float wx[3], wy[3], wz[3];
-                quad_weights(fx, wx); quad_weights(fy, wy); quad_weights(fz, wz);
-                AxisAddr ax, ay, az;
-                axis_addr<0>((int)bxf + MPM_CELL_BIAS, bcx, ax);
-                axis_addr<1>((int)byf + MPM_CELL_BIAS, bcy, ay);
-                axis_addr<2>((int)bzf + MPM_CELL_BIAS, bcz, az);
-                const int bad = 27 - (3 - ax.bad) * (3 - ay.bad) * (3 - az.bad);
-                if (bad) {
-                    // contract violation (pipeline.py:1233-1238): counted, particle left untouched
-                    addr_err += bad;
-                    active = false;
-                } else {
-                    Gathered G;
-                    gather27(a.vel, nrow, ax, ay, az, wx, wy, wz, fx, fy, fz, a.dx, G);
-                    float nvx = G.v[0], nvy = G.v[1], nvz = G.v[2];
-#pragma unroll
-                    for (int r = 0; r < 9; ++r) C[r] = a.d_inv * G.B[r];
-                    if (a.flip > 0.0f) {
-                        float dv[3];
-                        StencilCopy st;
-#pragma unroll
-                        for (int q = 0; q < 3; ++q) {
-                            st.nx[q] = ax.nterm[q]; st.ny[q] = ay.nterm[q]; st.nz[q] = az.nterm[q];
-                            st.sx[q] = ax.sterm[q]; st.sy[q] = ay.sterm[q]; st.sz[q] = az.sterm[q];
-                            st.wx[q] = wx[q]; st.wy[q] = wy[q]; st.wz[q] = wz[q];
-                        }
-                        gather27_delta(a.vel, a.vel_old, nrow, st, dv);
-                        const float ovx = gd[(CH_VEL + 0) * 32], ovy = gd[(CH_VEL + 1) * 32],
-                                    ovz = gd[(CH_VEL + 2) * 32];
-                        nvx = (1.0f - a.flip) * nvx + a.flip * (ovx + dv[0]);
-                        nvy = (1.0f - a.flip) * nvy + a.flip * (ovy + dv[1]);
-                        nvz = (1.0f - a.flip) * nvz + a.flip * (ovz + dv[2]);
-                    }
-                    const float dtg = a.dt_gather;
-                    const float npx = px + dtg * nvx, npy = py + dtg * nvy, npz = pz + dtg * nvz;
-                    if (!(isfinite(npx) && isfinite(npy) && isfinite(npz) && isfinite(nvx) &&
-                          isfinite(nvy) && isfinite(nvz))) {
-                        // quarantine (pipeline.py:525-531): state left as it was, mass zeroed
-                        meta |= MPM_LANE_QUARANTINED;
-                        a.meta[g * 32 + lane] = meta;
-                        gd[CH_MASS * 32] = 0.0f;
-                        atomicAdd(&a.status->counters[MPM_C_QUARANTINE], 1ull);
-                        active = false;
-                    } else {
-                        px = npx; py = npy; pz = npz; vx = nvx; vy = nvy; vz = nvz;
-                        gd[(CH_POS + 0) * 32] = px; gd[(CH_POS + 1) * 32] = py; gd[(CH_POS + 2) * 32] = pz;
-                        gd[(CH_VEL + 0) * 32] = vx; gd[(CH_VEL + 1) * 32] = vy; gd[(CH_VEL + 2) * 32] = vz;
-                        if (!SCATTER) {
-                            // the fused kernel keeps C in registers; the split path stores it for P2G
-#pragma unroll
-                            for (int r = 0; r < 9; ++r) gd[(CH_C + r) * 32] = C[r];
-                        }
-                        if (MAT == MPM_MAT_FLUID) {
-                            F[0] *= 1.0f + dtg * (C[0] + C[4] + C[8]);
-                            gd[CH_DEF * 32] = F[0];
-                        } else {
-                            float A[9], Fn[9];
-#pragma unroll
-                            for (int r = 0; r < 9; ++r) A[r] = dtg * C[r];
-                            A[0] += 1.0f; A[4] += 1.0f; A[8] += 1.0f;
-#pragma unroll
-                            for (int r = 0; r < 3; ++r)
-#pragma unroll
-                                for (int c = 0; c < 3; ++c)
-                                    Fn[3 * r + c] = A[3 * r] * F[c] + A[3 * r + 1] * F[3 + c] + A[3 * r + 2] * F[6 + c];
-                            if (MAT >= MPM_MAT_SNOW) {
-                                // return mapping (not in the reference; oracle: orc_snow_project / orc_sand_project)
-                                plastic_project<MAT>(Fn, plastic, pp, tau);
-                                gd[CH_PLASTIC * 32] = plastic;
-                            }
-#pragma unroll
-                            for (int r = 0; r < 9; ++r) { F[r] = Fn[r]; gd[(CH_DEF + r) * 32] = Fn[r]; }
-                        }
-                        // free zone [origin - margin_lo, origin + 4 + margin_hi) cells (pipeline.py:560-575)
-                        const float zx0 = ((float)(org.x - MPM_CELL_BIAS) - a.margin_lo) * a.dx;
-                        const float zy0 = ((float)(org.y - MPM_CELL_BIAS) - a.margin_lo) * a.dx;
-                        const float zz0 = ((float)(org.z - MPM_CELL_BIAS) - a.margin_lo) * a.dx;
-                        const float zx1 = ((float)(org.x - MPM_CELL_BIAS) + 4.0f + a.margin_hi) * a.dx;
-                        const float zy1 = ((float)(org.y - MPM_CELL_BIAS) + 4.0f + a.margin_hi) * a.dx;
-                        const float zz1 = ((float)(org.z - MPM_CELL_BIAS) + 4.0f + a.margin_hi) * a.dx;
-                        if (px < zx0 || px >= zx1 || py < zy0 || py >= zy1 || pz < zz0 || pz >= zz1) {
-                            a.status->zone_violation = 1;
-                            if (a.guard.word) atomicMin(a.guard.word, a.guard.step);
-                        }
-                        vmax_bits = __float_as_uint(vx * vx + vy * vy + vz * vz);
-                        // lane key refresh (pipeline.py:585-599)
-                        float tmp;
-                        int kx = (int)stencil_base(px, a.inv_dx, &tmp) + MPM_CELL_BIAS - (org.x - 4);
-                        int ky = (int)stencil_base(py, a.inv_dx, &tmp) + MPM_CELL_BIAS - (org.y - 4);
-                        int kz = (int)stencil_base(pz, a.inv_dx, &tmp) + MPM_CELL_BIAS - (org.z - 4);
-                        kx = min(max(kx, 0), 9); ky = min(max(ky, 0), 9); kz = min(max(kz, 0), 9);
-                        key = kx + 10 * (ky + 10 * kz);
-                        a.meta[g * 32 + lane] = (uint16_t)key;
-                    }
+                for (int r = 0; r < 9; ++r) C[r] = a.d_inv * G.B[r];
+                if (a.flip > 0.0f) {
+                    float dv[3];
+                    gather27_delta(a.vel, a.vel_old, nrow, kx, ky, kz, fx, fy, fz, dv);
+                    const float ovx = gd[(CH_VEL + 0) * 32], ovy = gd[(CH_VEL + 1) * 32],
+                                ovz = gd[(CH_VEL + 2) * 32];
+                    nvx = (1.0f - a.flip) * nvx + a.flip * (ovx + dv[0]);
+                    nvy = (1.0f - a.flip) * nvy + a.flip * (ovy + dv[1]);
+                    nvz = (1.0f - a.flip) * nvz + a.flip * (ovz + dv[2]);
                 }
-            }
-        } else if (SCATTER) {
-            if (active) {
-                vx = gd[(CH_VEL + 0) * 32]; vy = gd[(CH_VEL + 1) * 32]; vz = gd[(CH_VEL + 2) * 32];
-#pragma unroll
-                for (int r = 0; r < 9; ++r) C[r] = gd[(CH_C + r) * 32];
-            }
-        }
-
-        // =========================== scatter (pipeline.py:160-312) ==========================
-        if (SCATTER) {
-            float Q[9];
-            if (active && !GATHER) {
-                if (!(isfinite(px) && isfinite(py) && isfinite(pz) && isfinite(vx) && isfinite(vy) &&
-                      isfinite(vz))) {
+                const float dtg = a.dt_gather;
+                const float npx = px + dtg * nvx, npy = py + dtg * nvy, npz = pz + dtg * nvz;
+                if (!(isfinite(npx) && isfinite(npy) && isfinite(npz) && isfinite(nvx) &&
+                      isfinite(nvy) && isfinite(nvz))) {
+                    // quarantine (pipeline.py:525-531): state left as it was, mass zeroed
                     meta |= MPM_LANE_QUARANTINED;
                     a.meta[g * 32 + lane] = meta;
                     gd[CH_MASS * 32] = 0.0f;
                     atomicAdd(&a.status->counters[MPM_C_QUARANTINE], 1ull);
                     active = false;
-                }
-            }
-            // addressing from the lane key (pipeline.py:261-272); weights relative to that base
-            const int kx = key % 10, ky = (key / 10) % 10, kz = key / 100;
-            const int basex = org.x - 4 + kx, basey = org.y - 4 + ky, basez = org.z - 4 + kz;
-            AxisAddr ax, ay, az;
-            axis_addr<0>(basex, bcx, ax);
-            axis_addr<1>(basey, bcy, ay);
-            axis_addr<2>(basez, bcz, az);
-            if (active) {
-                const int bad = 27 - (3 - ax.bad) * (3 - ay.bad) * (3 - az.bad);
-                if (bad) { addr_err += bad; active = false; }
-            }
-            if (active) {
-                const float coeff = a.coeff_base * m;
-                if (MAT == MPM_MAT_FLUID) {
-                    float tau;
-                    if (F[0] <= 0.0f) {
-                        atomicAdd(&a.status->counters[MPM_C_DEGENERATE], 1ull);
-                        tau = 0.0f;
-                    } else tau = fluid_tau(F[0], a.kappa, a.gamma, a.clamp_tension);
-#pragma unroll
-                    for (int r = 0; r < 9; ++r) Q[r] = m * C[r];
-                    Q[0] += coeff * tau; Q[4] += coeff * tau; Q[8] += coeff * tau;
-                } else if (MAT == MPM_MAT_FIXED_COROTATED) {
-                    float t[9];
-                    if (corotated_tau(F, a.mu, a.lam, t))
-                        atomicAdd(&a.status->counters[MPM_C_SVD_CLAMP], 1ull);
-#pragma unroll
-                    for (int r = 0; r < 9; ++r) Q[r] = m * C[r] + coeff * t[r];
                 } else {
-                    if (!GATHER) plastic_tau<MAT>(F, plastic, pp, tau);
+                    px = npx; py = npy; pz = npz; vx = nvx; vy = nvy; vz = nvz;
+                    gd[(CH_POS + 0) * 32] = px; gd[(CH_POS + 1) * 32] = py; gd[(CH_POS + 2) * 32] = pz;
+                    gd[(CH_VEL + 0) * 32] = vx; gd[(CH_VEL + 1) * 32] = vy; gd[(CH_VEL + 2) * 32] = vz;
+                    if (!SCATTER) {
+                        // the fused kernel keeps C in registers; the split path stores it for P2G
 #pragma unroll
-                    for (int r = 0; r < 9; ++r) Q[r] = m * C[r] + coeff * tau[r];
-                }
-            }
-            // runs of consecutive active lanes with equal keys
-            const unsigned act = __ballot_sync(FULL, active);
-            const int prev_key = __shfl_up_sync(FULL, key, 1);
-            bool head = !active || lane == 0 || prev_key != key || !((act >> (lane - 1)) & 1u);
-            unsigned heads = __ballot_sync(FULL, head);
-#if MPM_SUBRUN < 32
-            {
-                // experiment knob: cut runs longer than MPM_SUBRUN lanes into sub-runs with their
-                // own leader (fewer shuffle steps, more reductions to L2); 32 = the reference's
-                // "one += per (subgroup, node)" contract
-                const unsigned below = heads & ((2u << lane) - 1u);
-                const int seg_first = 31 - __clz(below);
-                head = head || (((lane - seg_first) & (MPM_SUBRUN - 1)) == 0);
-                heads = __ballot_sync(FULL, head);
-            }
-#endif
-            const unsigned above = lane == 31 ? 0u : (heads & ~((2u << lane) - 1u));
-            const int seg_last = above ? (__ffs(above) - 2) : 31;
-            const int maxd = __reduce_max_sync(FULL, seg_last - lane);
-            if (act) {
-                const float fx = px * a.inv_dx - (float)(basex - MPM_CELL_BIAS);
-                const float fy = py * a.inv_dx - (float)(basey - MPM_CELL_BIAS);
-                const float fz = pz * a.inv_dx - (float)(basez - MPM_CELL_BIAS);
-                float wx[3], wy[3], wz[3];
-                quad_weights(fx, wx); quad_weights(fy, wy); quad_weights(fz, wz);
-                const float mm = active ? m : 0.0f;
-                if (!active) {
-#pragma unroll
-                    for (int r = 0; r < 9; ++r) Q[r] = 0.0f;
-                    wx[0] = wx[1] = wx[2] = 0.0f;
-                }
-                // momentum of node (i,j,k): w (m v + Q dpos) with dpos = ((i,j,k) - f) dx, built up
-                // axis by axis: X_i = m v + Q[:,0] dpx_i ; XY_ij = X_i + Q[:,1] dpy_j ; + Q[:,2] dpz_k
-                float QZ[3][3];
-#pragma unroll
-                for (int k = 0; k < 3; ++k) {
-                    const float dpz = ((float)k - fz) * a.dx;
-                    QZ[k][0] = Q[2] * dpz; QZ[k][1] = Q[5] * dpz; QZ[k][2] = Q[8] * dpz;
-                }
-                const bool leader = head && active;
-                const bool p1 = lane + 1 <= seg_last, p2 = lane + 2 <= seg_last, p4 = lane + 4 <= seg_last,
-                           p8 = lane + 8 <= seg_last, p16 = lane + 16 <= seg_last;
-#pragma unroll
-                for (int i = 0; i < 3; ++i) {
-                    const float dpx = ((float)i - fx) * a.dx;
-                    const float X0 = mm * vx + Q[0] * dpx, X1 = mm * vy + Q[3] * dpx, X2 = mm * vz + Q[6] * dpx;
-#pragma unroll
-                    for (int j = 0; j < 3; ++j) {
-                        const float dpy = ((float)j - fy) * a.dx;
-                        const float wxy = wx[i] * wy[j];
-                        const float XY0 = X0 + Q[1] * dpy, XY1 = X1 + Q[4] * dpy, XY2 = X2 + Q[7] * dpy;
-                        const int nxy = ax.nterm[i] + ay.nterm[j];
-                        const int sxy = ax.sterm[i] | ay.sterm[j];
-#pragma unroll
-                        for (int k = 0; k < 3; ++k) {
-                            const float w = wxy * wz[k];
-                            typedef typename std::conditional<DET, long long, float>::type acc_t;
-                            acc_t c0, c1, c2, c3;
-                            if (DET) {
-                                c0 = (acc_t)__float2ll_rn((w * mm) * MPM_MASS_SCALE);
-                                c1 = (acc_t)__float2ll_rn((w * (XY0 + QZ[k][0])) * MPM_MOM_SCALE);
-                                c2 = (acc_t)__float2ll_rn((w * (XY1 + QZ[k][1])) * MPM_MOM_SCALE);
-                                c3 = (acc_t)__float2ll_rn((w * (XY2 + QZ[k][2])) * MPM_MOM_SCALE);
-                            } else {
-                                c0 = (acc_t)(w * mm);
-                                c1 = (acc_t)(w * (XY0 + QZ[k][0]));
-                                c2 = (acc_t)(w * (XY1 + QZ[k][1]));
-                                c3 = (acc_t)(w * (XY2 + QZ[k][2]));
-                            }
-#define MPM_SEG_STEP(D, P)                                                      \
-    if (maxd >= D) {                                                            \
-        const acc_t t0 = __shfl_down_sync(FULL, c0, D);                         \
-        const acc_t t1 = __shfl_down_sync(FULL, c1, D);                         \
-        const acc_t t2 = __shfl_down_sync(FULL, c2, D);                         \
-        const acc_t t3 = __shfl_down_sync(FULL, c3, D);                         \
-        if (P) { c0 += t0; c1 += t1; c2 += t2; c3 += t3; }                      \
-    }
-                            MPM_SEG_STEP(1, p1)
-                            MPM_SEG_STEP(2, p2)
-                            MPM_SEG_STEP(4, p4)
-                            MPM_SEG_STEP(8, p8)
-                            MPM_SEG_STEP(16, p16)
-#undef MPM_SEG_STEP
-                            if (leader) {
-                                const int nb = nrow[nxy + az.nterm[k]];
-                                const size_t node = (size_t)nb * 64 + (sxy | az.sterm[k]);
-                                if (DET) red_add_det((long long *)a.raw + node * 4, (long long)c0, (long long)c1,
-                                                     (long long)c2, (long long)c3);
-                                else red_add_v4(&a.raw[node], (float)c0, (float)c1, (float)c2, (float)c3);
-                            }
-                        }
+                        for (int r = 0; r < 9; ++r) gd[(CH_C + r) * 32] = C[r];
                     }
-                }
-                unsigned nbmask = leader ? block_mask27(ax, ay, az) : 0u;
-                nbmask = __reduce_or_sync(FULL, nbmask);
-                if (lane < 27 && ((nbmask >> lane) & 1u)) a.touched[nrow[lane]] = 1;
-                if (a.count_stats && lane == 0) {
-                    const int runs = __popc(heads & act);
-                    atomicAdd(&a.status->counters[MPM_C_SUBGROUPS], (unsigned long long)runs);
-                    atomicAdd(&a.status->counters[MPM_C_ACCUM], (unsigned long long)runs * 27ull);
+                    if (MAT == MPM_MAT_FLUID) {
+                        F[0] *= 1.0f + dtg * (C[0] + C[4] + C[8]);
+                        gd[CH_DEF * 32] = F[0];
+                    } else {
+                        float A[9], Fn[9];
+#pragma unroll
+                        for (int r = 0; r < 9; ++r) A[r] = dtg * C[r];
+                        A[0] += 1.0f; A[4] += 1.0f; A[8] += 1.0f;
+#pragma unroll
+                        for (int r = 0; r < 3; ++r)
+#pragma unroll
+                            for (int c = 0; c < 3; ++c)
+                                Fn[3 * r + c] = A[3 * r] * F[c] + A[3 * r + 1] * F[3 + c] + A[3 * r + 2] * F[6 + c];
+                        if (MAT >= MPM_MAT_SNOW) {
+                            // return mapping (not in the reference; oracle: orc_snow_project / orc_sand_project)
+                            plastic_project<MAT>(Fn, plastic, pp, tau);
+                            gd[CH_PLASTIC * 32] = plastic;
+                        }
+#pragma unroll
+                        for (int r = 0; r < 9; ++r) { F[r] = Fn[r]; gd[(CH_DEF + r) * 32] = Fn[r]; }
+                    }
+                    // new stencil base relative to (origin - 4): the lane key digits before clamping
+                    // (pipeline.py:585-599); the free zone [origin - margin_lo, origin + 4 + margin_hi)
+                    // cells is tested on the position itself (pipeline.py:560-575)
+                    const float zx0 = ((float)(org.x - MPM_CELL_BIAS) - a.margin_lo) * a.dx;
+                    const float zy0 = ((float)(org.y - MPM_CELL_BIAS) - a.margin_lo) * a.dx;
+                    const float zz0 = ((float)(org.z - MPM_CELL_BIAS) - a.margin_lo) * a.dx;
+                    const float zx1 = ((float)(org.x - MPM_CELL_BIAS) + 4.0f + a.margin_hi) * a.dx;
+                    const float zy1 = ((float)(org.y - MPM_CELL_BIAS) + 4.0f + a.margin_hi) * a.dx;
+                    const float zz1 = ((float)(org.z - MPM_CELL_BIAS) + 4.0f + a.margin_hi) * a.dx;
+                    if (px < zx0 || px >= zx1 || py < zy0 || py >= zy1 || pz < zz0 || pz >= zz1) {
+                        a.status->zone_violation = 1;
+                        if (a.guard.word) atomicMin(a.guard.word, a.guard.step);
+                    }
+                    vmax_bits = __float_as_uint(vx * vx + vy * vy + vz * vz);
+                    float tmp;
+                    int nkx = (int)stencil_base(px, a.inv_dx, &tmp) + MPM_CELL_BIAS - (org.x - 4);
+                    int nky = (int)stencil_base(py, a.inv_dx, &tmp) + MPM_CELL_BIAS - (org.y - 4);
+                    int nkz = (int)stencil_base(pz, a.inv_dx, &tmp) + MPM_CELL_BIAS - (org.z - 4);
+                    nkx = min(max(nkx, 0), 9); nky = min(max(nky, 0), 9); nkz = min(max(nkz, 0), 9);
+                    key = nkx + 10 * (nky + 10 * nkz);
+                    a.meta[g * 32 + lane] = (uint16_t)key;
                 }
             }
         }
-        if (addr_err) atomicAdd(&a.status->counters[MPM_C_ADDRESS_ERR], (unsigned long long)addr_err);
+        // max |v|^2 of the warp -> one conditional atomicMax (pipeline.py:576-578)
+        vmax_bits = __reduce_max_sync(FULL, vmax_bits);
+        if (lane == 0 && vmax_bits > *((volatile unsigned *)&a.status->vmax2_bits))
+            atomicMax(&a.status->vmax2_bits, vmax_bits);
+    } else if (SCATTER) {
+        if (active) {
+            vx = gd[(CH_VEL + 0) * 32]; vy = gd[(CH_VEL + 1) * 32]; vz = gd[(CH_VEL + 2) * 32];
+#pragma unroll
+            for (int r = 0; r < 9; ++r) C[r] = gd[(CH_C + r) * 32];
+        }
     }
 
-    if (GATHER) {
-        // max |v|^2 of the CTA -> one conditional atomicMax (pipeline.py:576-578)
-        vmax_bits = __reduce_max_sync(FULL, vmax_bits);
-        if (lane == 0) s_vmax[warp] = vmax_bits;
-        __syncthreads();
-        if (threadIdx.x == 0) {
-            unsigned mx = 0;
+    // =========================== scatter (pipeline.py:160-312) ==========================
+    if (SCATTER) {
+        float Q[9];
+        if (active && !GATHER) {
+            if (!(isfinite(px) && isfinite(py) && isfinite(pz) && isfinite(vx) && isfinite(vy) &&
+                  isfinite(vz))) {
+                meta |= MPM_LANE_QUARANTINED;
+                a.meta[g * 32 + lane] = meta;
+                gd[CH_MASS * 32] = 0.0f;
+                atomicAdd(&a.status->counters[MPM_C_QUARANTINE], 1ull);
+                active = false;
+            }
+        }
+        if (active) {
+            const float coeff = a.coeff_base * m;
+            if (MAT == MPM_MAT_FLUID) {
+                float tau;
+                if (F[0] <= 0.0f) {
+                    atomicAdd(&a.status->counters[MPM_C_DEGENERATE], 1ull);
+                    tau = 0.0f;
+                } else tau = fluid_tau(F[0], a.kappa, a.gamma, a.clamp_tension);
 #pragma unroll
-            for (int w = 0; w < TW; ++w) mx = max(mx, s_vmax[w]);
-            if (mx > *((volatile unsigned *)&a.status->vmax2_bits)) atomicMax(&a.status->vmax2_bits, mx);
+                for (int r = 0; r < 9; ++r) Q[r] = m * C[r];
+                Q[0] += coeff * tau; Q[4] += coeff * tau; Q[8] += coeff * tau;
+            } else if (MAT == MPM_MAT_FIXED_COROTATED) {
+                float t[9];
+                if (corotated_tau(F, a.mu, a.lam, t))
+                    atomicAdd(&a.status->counters[MPM_C_SVD_CLAMP], 1ull);
+#pragma unroll
+                for (int r = 0; r < 9; ++r) Q[r] = m * C[r] + coeff * t[r];
+            } else {
+                if (!GATHER) plastic_tau<MAT>(F, plastic, pp, tau);
+#pragma unroll
+                for (int r = 0; r < 9; ++r) Q[r] = m * C[r] + coeff * tau[r];
+            }
+        } else {
+            // lanes outside any run still take part in the shuffles: their payload must be exact
+            // zeros (a 0/1 multiplier does not stop a NaN)
+#pragma unroll
+            for (int r = 0; r < 9; ++r) Q[r] = 0.0f;
+            px = py = pz = 0.0f; vx = vy = vz = 0.0f;
+        }
+        // runs of consecutive active lanes with equal keys
+        const unsigned act = __ballot_sync(FULL, active);
+        const int prev_key = __shfl_up_sync(FULL, key, 1);
+        const bool head = !active || lane == 0 || prev_key != key || !((act >> (lane - 1)) & 1u);
+        const unsigned heads = __ballot_sync(FULL, head);
+        const unsigned above = lane == 31 ? 0u : (heads & ~((2u << lane) - 1u));
+        const int reach = (above ? (__ffs(above) - 2) : 31) - lane;
+        const int maxd = __reduce_max_sync(FULL, reach);
+        if (act) {
+            // addressing from the lane key (pipeline.py:261-272); weights relative to that base
+            const int kx = key % 10, ky = (key / 10) % 10, kz = key / 100;
+            const float fx = px * a.inv_dx - (float)(org.x - 4 + kx - MPM_CELL_BIAS);
+            const float fy = py * a.inv_dx - (float)(org.y - 4 + ky - MPM_CELL_BIAS);
+            const float fz = pz * a.inv_dx - (float)(org.z - 4 + kz - MPM_CELL_BIAS);
+            const float mm = active ? m : 0.0f;
+            const bool leader = head && active;
+            if (DET) scatter27<5, true>((float4 *)a.raw, nrow, kx, ky, kz, fx, fy, fz, a.dx, mm, vx, vy, vz, Q, reach, maxd, leader);
+            else if (maxd < 2) scatter27<1, false>(a.raw, nrow, kx, ky, kz, fx, fy, fz, a.dx, mm, vx, vy, vz, Q, reach, maxd, leader);
+            else if (maxd < 4) scatter27<2, false>(a.raw, nrow, kx, ky, kz, fx, fy, fz, a.dx, mm, vx, vy, vz, Q, reach, maxd, leader);
+            else if (maxd < 8) scatter27<3, false>(a.raw, nrow, kx, ky, kz, fx, fy, fz, a.dx, mm, vx, vy, vz, Q, reach, maxd, leader);
+            else scatter27<5, false>(a.raw, nrow, kx, ky, kz, fx, fy, fz, a.dx, mm, vx, vy, vz, Q, reach, maxd, leader);
+            unsigned nbmask = leader ? block_mask27(kx, ky, kz) : 0u;
+            nbmask = __reduce_or_sync(FULL, nbmask);
+            if (lane < 27 && ((nbmask >> lane) & 1u)) a.touched[nrow[lane] >> 6] = 1;
+            if (a.count_stats && lane == 0) {
+                const int runs = __popc(heads & act);
+                atomicAdd(&a.status->counters[MPM_C_SUBGROUPS], (unsigned long long)runs);
+                atomicAdd(&a.status->counters[MPM_C_ACCUM], (unsigned long long)runs * 27ull);
+            }
         }
     }
+    if (addr_err) atomicAdd(&a.status->counters[MPM_C_ADDRESS_ERR], (unsigned long long)addr_err);
 }
 
 static int fill_args(TransferArgs &a, const mpm_store_view *store, const mpm_table_view *table,
