@@ -36,7 +36,8 @@ def parse_args():
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--scene", default="snow", choices=["snow", "snow_fc", "sand64k", "sand_mini",
-                                                        "sand389k", "sand1m", "sand10m", "sand32m", "fountain"])
+                                                        "sand389k", "sand1m", "sand10m", "sand32m", "fountain",
+                                                        "mixed4m", "mixed32m"])
     ap.add_argument("--transfer", default="g2p2g", choices=["split", "g2p2g"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
@@ -373,6 +374,50 @@ def run_fountain(args):
     print(json.dumps(line), flush=True)
 
 
+def run_mixed(args):
+    """configs[4]: mixed snow / sand populations on a 512^3 sparse grid.  `mixed32m` is the whole
+    32 M-particle scene on one GPU (6.6 GB of particle state), `mixed4m` its one-eighth (the
+    per-GPU share of the 8-GPU configuration).  Two logical workers (one per material) share
+    the grid through the in-kernel peer-row reduction of the grid update."""
+    import torch
+    from paper_2111_00699_b200 import CudaCluster, PipelineOptions, _capi, scenes
+    torch.cuda.set_device(0)
+    W = scenes.mixed_sparse(l=50, pairs_side=4) if args.scene == "mixed32m" else scenes.mixed_sparse(l=40, pairs_side=2)
+    cl = CudaCluster(2, W.params, [p.material for p in W.populations], W.boundary,
+                     PipelineOptions(transfer=args.transfer, fused_threshold=1 << 62), initial_vmax=150.0,
+                     count_stats=False)
+    cl.seed_populations([(p.positions.astype(np.float32), p.velocities.astype(np.float32), p.particle_mass)
+                         for p in W.populations])
+    n, spf = W.n_particles, W.params.steps_per_frame
+    for _ in range(args.warmup):
+        cl.run_frame()
+    torch.cuda.synchronize()
+    l0 = _capi.lib().mpm_launch_count()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record()
+    for _ in range(args.steps):
+        cl.run_frame()
+    e1.record()
+    torch.cuda.synchronize()
+    ms = e0.elapsed_time(e1)
+    tables = [int(w.table.count) for w in cl.workers]
+    shared = int(len(np.intersect1d(cl.workers[0].table.codes, cl.workers[1].table.codes)))
+    line = {"metric": METRIC, "value": round(n * spf * args.steps / (ms * 1e-3) / 1e6, 2), "unit": UNIT,
+            "n_gpus": 1, "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(ms / args.steps, 4),
+            "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f32",
+            "data": "synthetic",
+            "config": {"workload": W.name, "particles": n, "substeps_per_step": spf, "step": "one frame",
+                       "transfer": args.transfer, "material": "SNOW + SAND populations",
+                       "pblocks_per_population": tables, "shared_pblocks": shared,
+                       "grid_cells": f"{W.domain_cells}^3",
+                       "occupied_fraction_of_grid": round(sum(tables) * 64 / W.domain_cells ** 3, 4),
+                       "rebuilds": [len(w.rebuild_steps) for w in cl.workers]},
+            "ms_per_frame": round(ms / args.steps, 4),
+            "gpu_launches": int(_capi.lib().mpm_launch_count() - l0), "e2e": None, "roofline": None,
+            "cpu_baseline": None, "clocks": None}
+    print(json.dumps(line), flush=True)
+
+
 def cpu_baseline(W, substeps, threads, warm=True):
     """The CPU oracle (C restatement of the reference, oracle/) timed on the host cores on a
     bounded sample: the full scene, rebuild + `substeps` substeps."""
@@ -448,5 +493,7 @@ if __name__ == "__main__":
         run_reference(a)
     elif a.scene == "fountain":
         run_fountain(a)
+    elif a.scene.startswith("mixed"):
+        run_mixed(a)
     else:
         run_ours(a)

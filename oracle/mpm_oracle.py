@@ -822,7 +822,10 @@ class OracleCluster:
     def __init__(self, n, params, material, boundary, options=None, initial_vmax=0.0,
                  threads=False):
         self.runtime = OracleRuntime(n, initial_vmax)
-        self.workers = [OracleWorker(w, self.runtime, params, material, boundary, options)
+        # one Material per worker = material populations sharing the grid (not in the reference,
+        # which has one material per run; the grid reduction is pipeline.py:1172-1188 unchanged)
+        materials = list(material) if isinstance(material, (list, tuple)) else [material] * n
+        self.workers = [OracleWorker(w, self.runtime, params, materials[w], boundary, options)
                         for w in range(n)]
         self.params = params
         self.threads = threads and n > 1
@@ -835,6 +838,15 @@ class OracleCluster:
             if len(part):
                 w.seed_particles(positions[part], velocities[part], mass, ids=part)
         return parts
+
+    def seed_populations(self, populations):
+        base = 0
+        for w, pop in zip(self.workers, populations):
+            n = len(pop[0])
+            ids = np.asarray(pop[3], dtype=np.int64) if len(pop) > 3 else np.arange(base, base + n, dtype=np.int64)
+            if n:
+                w.seed_particles(pop[0], pop[1], pop[2], ids=ids)
+            base += n
 
     def _phase(self, fn):
         if not self.threads:
@@ -865,7 +877,7 @@ class OracleCluster:
         ws = self.workers
         self.frame_steps = 0
         if self.cfl_mode:
-            c_sound = sound_speed(ws[0].material)
+            c_sound = max(sound_speed(w.material) for w in ws)
             t = 0.0
             while t < self.params.frame_dt - 1e-12:
                 vmax = self.runtime.global_vmax((ws[0]._global_step - 2) % 3)
@@ -893,6 +905,8 @@ class OracleCluster:
 
     def state_sorted_by_id(self):
         chunks = [w.store.state_with_ids() for w in self.workers]
+        nch = max(c[0].shape[1] for c in chunks)
+        chunks = [(np.pad(c[0], ((0, 0), (0, nch - c[0].shape[1]))), c[1]) for c in chunks]
         flat = np.concatenate([c[0] for c in chunks], axis=0)
         ids = np.concatenate([c[1] for c in chunks], axis=0)
         return flat[np.argsort(ids, kind="stable")]

@@ -7,6 +7,13 @@ post-barrier phase of every worker" on one CUDA stream is the same schedule with
 realised by stream order.  This is how the cross-worker halo reduction (peer rows read inside
 the grid-update kernel) is exercised on a single GPU; with one process per GPU the same
 worker code runs under `DistRuntime` (dist.py).
+
+Populations: `material` may be a sequence with one Material per worker.  Each worker then
+carries one material population (its own constitutive kernel instantiation and channel
+count) and the populations meet on the grid exactly as spatial partitions do -- mass and
+momentum rows of blocks present in several tables are summed in the grid update
+(pipeline.py:1172-1188).  This is how mixed snow / sand scenes (BASELINE.json configs[4]) run;
+the reference itself has one material per run.
 """
 from __future__ import annotations
 
@@ -14,6 +21,7 @@ import numpy as np
 import torch
 
 from .domain import cfl_dt
+from .errors import ConfigError
 from .multiworker import SharedRuntime, partition_particles
 from .options import PipelineOptions
 from .worker import CudaWorker
@@ -24,7 +32,10 @@ class CudaCluster:
                  **worker_kw):
         self.runtime = SharedRuntime(n, initial_vmax=initial_vmax)
         options = options if options is not None else PipelineOptions()
-        self.workers = [CudaWorker(w, self.runtime, params, material, boundary, options,
+        materials = list(material) if isinstance(material, (list, tuple)) else [material] * n
+        if len(materials) != n:
+            raise ConfigError(f"{n} workers need {n} materials, got {len(materials)}")
+        self.workers = [CudaWorker(w, self.runtime, params, materials[w], boundary, options,
                                    device=device, **worker_kw) for w in range(n)]
         self.params = params
         self.cfl_mode = False
@@ -40,6 +51,20 @@ class CudaCluster:
                 w.seed_particles(positions[part], velocities[part], mass, ids=part)
         return parts
 
+    def seed_populations(self, populations):
+        """One population per worker: (positions, velocities, mass) or (positions, velocities,
+        mass, ids).  Ids default to consecutive ranges in population order."""
+        if len(populations) != len(self.workers):
+            raise ConfigError(f"{len(self.workers)} workers need {len(self.workers)} populations")
+        base = 0
+        for w, pop in zip(self.workers, populations):
+            pos, vel, mass = pop[0], pop[1], pop[2]
+            n = len(pos)
+            ids = np.asarray(pop[3], dtype=np.int64) if len(pop) > 3 else np.arange(base, base + n, dtype=np.int64)
+            if n:
+                w.seed_particles(pos, vel, mass, ids=ids)
+            base += n
+
     def run_step(self, step):
         for w in self.workers:
             w.step_pre_barrier(step)
@@ -53,7 +78,7 @@ class CudaCluster:
         for w in ws:
             w.begin_frame()
         if self.cfl_mode:
-            c_sound = ws[0].material.sound_speed()
+            c_sound = max(w.material.sound_speed() for w in ws)
             t = 0.0
             while t < self.params.frame_dt - 1e-12:
                 vmax = self.runtime.global_vmax((ws[0]._global_step - 2) % 3)
@@ -75,6 +100,8 @@ class CudaCluster:
 
     def state_sorted_by_id(self):
         chunks = [w.store.state_with_ids() for w in self.workers]
+        nch = max(c[0].shape[1] for c in chunks)      # populations may differ in channel count
+        chunks = [(np.pad(c[0], ((0, 0), (0, nch - c[0].shape[1]))), c[1]) for c in chunks]
         flat = np.concatenate([c[0] for c in chunks], axis=0)
         ids = np.concatenate([c[1] for c in chunks], axis=0)
         return flat[np.argsort(ids, kind="stable")]

@@ -159,3 +159,62 @@ def free_fall(dx=25.0 / 64.0, steps_per_frame=36, frame_dt=1.0 / 48.0) -> World:
     material = Material.fixed_corotated(2.0, 1.0e5, 0.3)
     pos = np.array([[domain * dx / 2.0] * 3])
     return World(params, material, None, pos, np.zeros((1, 3)), 2.0 * dx ** 3, name="free_fall")
+
+
+@dataclass
+class Population:
+    material: Material
+    positions: np.ndarray
+    velocities: np.ndarray
+    particle_mass: float
+
+
+@dataclass
+class MixedWorld:
+    """Several material populations sharing one grid (run with CudaCluster, one worker each)."""
+    params: SimParams
+    boundary: BoundaryBox | None
+    populations: list
+    name: str = ""
+    domain_cells: int = 0
+
+    @property
+    def n_particles(self) -> int:
+        return sum(len(p.positions) for p in self.populations)
+
+
+def mixed_sparse(l=50, pairs_side=4, ppc=8, dx=1.0, seed=2024, domain_cells=512, frame_dt=1.0 / 60.0,
+                 steps_per_frame=30, init_speed=-150.0, gap_cells=4, gravity_z=-981.0) -> MixedWorld:
+    """Large sparse-grid stress test (BASELINE.json configs[4]): `pairs_side`^2 separated
+    clusters on a `domain_cells`^3 grid, each a sand box dropped onto a snow box, i.e. two
+    material populations of equal size that meet on the grid.  Defaults: 16 clusters x 2 boxes
+    x 50^3 cells x 8 = 32 000 000 particles on 512^3; (l=40, pairs_side=2) is the 4.1 M
+    per-GPU share of that scene.  Not a reference scene (one material per run there): the
+    generator follows sand_blocks (stratified samples, wall margin, CGS units)."""
+    m = WALL_MARGIN_CELLS
+    pitch = (domain_cells - 2 * m) // pairs_side
+    if pitch < l + 8 or 2 * l + gap_cells + 2 + 2 * m > domain_cells:
+        raise ConfigError(f"{pairs_side}^2 clusters of {l}-cell boxes do not fit {domain_cells}^3 cells")
+    rng = np.random.default_rng(seed)
+    cells = _box_cells(l)
+    snow_parts, sand_parts = [], []
+    for by in range(pairs_side):
+        for bx in range(pairs_side):
+            ox = m + bx * pitch + (pitch - l) // 2
+            oy = m + by * pitch + (pitch - l) // 2
+            snow_parts.append((np.array([ox, oy, m + 2]) + _stratified(rng, cells, ppc)) * dx)
+            sand_parts.append((np.array([ox, oy, m + 2 + l + gap_cells]) + _stratified(rng, cells, ppc)) * dx)
+    snow_pos = np.concatenate(snow_parts, axis=0)
+    sand_pos = np.concatenate(sand_parts, axis=0)
+    snow_mat = Material.snow(0.4, 6.0e5, 0.3, hardening=5.0)
+    sand_mat = Material.sand(2.0, 1.0e5, 0.3)
+    snow_vel = np.zeros_like(snow_pos)
+    sand_vel = np.zeros_like(sand_pos)
+    sand_vel[:, 2] = init_speed
+    params = SimParams(dx=dx, dt=frame_dt / steps_per_frame, gravity=(0.0, 0.0, gravity_z),
+                       frame_dt=frame_dt, steps_per_frame=steps_per_frame)
+    boundary = BoundaryBox((m * dx,) * 3, ((domain_cells - m) * dx,) * 3, mode="slip")
+    pops = [Population(snow_mat, snow_pos, snow_vel, snow_mat.density * dx ** 3 / ppc),
+            Population(sand_mat, sand_pos, sand_vel, sand_mat.density * dx ** 3 / ppc)]
+    return MixedWorld(params, boundary, pops, domain_cells=domain_cells,
+                      name=f"mixed snow/sand l={l} clusters={pairs_side ** 2} on {domain_cells}^3")

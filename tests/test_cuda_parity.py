@@ -323,3 +323,49 @@ def test_deterministic_mode_bit_identical_across_rebuild_cadence_and_fusion():
     assert a.workers[0].grid.raw[0].dtype == np.float64
     raw = a.workers[0].grid.raw[1]
     assert np.array_equal(raw, np.rint(raw))                       # integer-valued sums
+
+
+# ---- material populations sharing one grid (BASELINE.json configs[4]) -----------------------------
+# Not in the reference (one material per run): two workers, one per material, meet on the grid
+# through the reference's own cross-worker reduction (pipeline.py:1172-1188).  Checked against
+# the oracle cluster built the same way (parity unpinned for the plastic kinds themselves).
+@pytest.mark.parametrize("transfer", ["split", "g2p2g"])
+def test_mixed_populations_share_one_grid(transfer):
+    from paper_2111_00699_b200 import CudaCluster, PipelineOptions, scenes
+    W = scenes.mixed_sparse(l=5, pairs_side=1, dx=25.0 / 64.0, domain_cells=64, gap_cells=1,
+                            steps_per_frame=36, frame_dt=1.0 / 48.0)
+    f32r = lambda a: np.asarray(a, dtype=np.float64).astype(np.float32).astype(np.float64)
+    pops = [(f32r(p.positions), f32r(p.velocities), p.particle_mass) for p in W.populations]
+    mats = [p.material for p in W.populations]
+    cc = CudaCluster(2, W.params, mats, W.boundary, PipelineOptions(transfer=transfer), initial_vmax=150.0)
+    co = O.OracleCluster(2, W.params, mats, W.boundary, PipelineOptions(transfer=transfer), initial_vmax=150.0)
+    cc.seed_populations(pops)
+    co.seed_populations(pops)
+    n_snow = len(pops[0][0])
+    p0 = sum(w.store.total_momentum() for w in cc.workers)
+    for s in range(40):
+        cc.run_step(s)
+        co.run_step(s)
+    for cl in (cc, co):
+        for w in cl.workers:
+            if w._pending_gather:
+                w._flush_gather()
+    sc, so = cc.state_sorted_by_id(), co.state_sorted_by_id()
+    edge = 64 * 25.0 / 64.0
+    ex, ev, ef, _ = U.particle_errors(sc, so, edge, 9)
+    print("mixed", transfer, "40 steps: x %.2e v %.2e F %.2e" % (ex, ev, ef))
+    assert ex <= 1e-4 and ev <= 2e-2 and ef <= 1e-2
+    assert [w.rebuild_steps for w in cc.workers] == [w.rebuild_steps for w in co.workers]
+    # the populations interacted: the snow box (initially at rest, lighter) was pushed down by more
+    # than gravity alone would do, and both plastic scalars moved
+    t = 40 * W.params.dt
+    assert so[:n_snow, 5].min() < -981.0 * t * 1.5
+    assert (so[:n_snow, 25] != 1.0).any() and (so[n_snow:, 25] != 0.0).any()
+    # shared blocks exist in both tables
+    shared = np.intersect1d(cc.workers[0].table.codes, cc.workers[1].table.codes)
+    assert len(shared) > 0
+    # momentum exchanged through the grid is conserved up to gravity and wall contact: compare with the oracle
+    pc = sum(w.store.total_momentum() for w in cc.workers)
+    po = sum(np.asarray(w.store.total_momentum()) for w in co.workers)
+    assert np.allclose(pc, po, rtol=1e-4, atol=1e-4 * np.abs(po).max())
+    assert not np.allclose(pc, p0)
