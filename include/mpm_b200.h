@@ -196,9 +196,16 @@ int mpm_scatter_sorted(const mpm_store_view *old_store, const int32_t *src_slot,
  * read step s's rebuild flag: if step s asked for a rebuild, step s+1's kernels are no-ops
  * and the host re-issues the step after rebuilding (and resetting the word).  Results are
  * identical to the reference's "check flag, then step" order (pipeline.py:911-915). */
+#define MPM_MAX_PEERS 15
 typedef struct mpm_guard {
     int32_t *first_bad_step;     /* device */
     int32_t step;
+    /* One process per GPU with peer-mapped memory (paper_2111_00699_b200/peer.py): the guard
+     * words of the other ranks (their HBM, mapped over NVLink).  The gather that raises the local
+     * word raises them too (system-scope atomicMin), so that every rank stops after the same step;
+     * the write is ordered before this rank's step signal (mpm_signal_step). */
+    int32_t n_peer_words;
+    int32_t *peer_words[MPM_MAX_PEERS];
 } mpm_guard;
 
 /* Worker._clear (pipeline.py:1022-1037): zero the rows of raw flagged in touched and reset
@@ -217,7 +224,6 @@ int mpm_p2g(const mpm_store_view *store, const mpm_table_view *table, float *raw
  * vel_old != NULL ; v += dt*g ; box boundary (inclusive comparisons on node world position).
  * reset_status (may be NULL): status block whose zone flag / max speed are zeroed by this
  * kernel for the gather that follows it in stream order. */
-#define MPM_MAX_PEERS 15
 typedef struct mpm_grid_params {
     double dt;
     double gravity[3];
@@ -233,10 +239,29 @@ typedef struct mpm_grid_params {
     const float *peer_raw[MPM_MAX_PEERS];        /* float4 rows [*, 64] of each peer */
     const uint8_t *peer_touched[MPM_MAX_PEERS];  /* per-row flags, or NULL = every row counts */
     const int32_t *peer_map[MPM_MAX_PEERS];      /* [count]: row of local block b at that peer, or -1 */
+    /* Device-side step barrier for peer rows read in place (no packing, no send/recv): CTAs that
+     * hold a block shared with a peer, and CTA 0, spin (ld.acquire.sys) until every wait_flags[k]
+     * >= wait_value before any peer row is read; CTAs of interior blocks do not wait, so interior
+     * work overlaps the peers' scatter.  After wait_timeout_ms the kernel
+     * stores 1 to *wait_error and carries on (the host raises BarrierTimeoutError). */
+    int32_t n_wait;                     /* 0 = no device-side wait */
+    int32_t wait_value;
+    int32_t wait_timeout_ms;
+    int32_t reserved1;
+    const int32_t *wait_flags[MPM_MAX_PEERS];    /* peers' step words (written by mpm_signal_step) */
+    int32_t *wait_error;                         /* local device word */
 } mpm_grid_params;
 int mpm_grid_update(float *raw, uint8_t *touched, float *vel, float *vel_old,
                     const mpm_table_view *table, const mpm_grid_params *params,
                     mpm_step_status *reset_status, const mpm_guard *guard, void *stream);
+
+/* Publish "my scatter of this step is complete" to the peers: after everything enqueued before
+ * it on `stream`, *word = value with system scope (release).  Peers wait for it inside
+ * mpm_grid_update (wait_flags).  Guarded like every step kernel. */
+int mpm_signal_step(int32_t *word, int32_t value, const mpm_guard *guard, void *stream);
+/* The step barrier of mpm_grid_update on its own (wait_flags / wait_value / wait_timeout_ms /
+ * wait_error of `params`): for a rank whose block table is empty. */
+int mpm_wait_step(const mpm_grid_params *params, const mpm_guard *guard, void *stream);
 
 /* Pack the raw rows this worker contributes to one peer (one process per GPU: the rows are
  * then exchanged with NCCL send/recv): out_rows[i] = raw row of block send_idx[i], zeros when
@@ -281,6 +306,15 @@ typedef struct mpm_step_plan {
     mpm_step_status *status_host;      /* pinned host [status_ring] */
     void *events[MPM_MAX_STATUS_RING]; /* cudaEvent_t per slot */
     int32_t *guard_word;               /* device */
+    /* peer-mapped stepping (all optional, zero = single worker): guard words of the other ranks,
+     * this rank's step word (signalled with s + 1 after the scatter of step s; the grid update of
+     * step s waits for grid.wait_flags >= s + 1), and a pinned host ring that receives the guard
+     * word next to each status slot */
+    int32_t n_peer_words;
+    int32_t reserved2;
+    int32_t *peer_guard_words[MPM_MAX_PEERS];
+    int32_t *signal_word;
+    int32_t *guard_host;               /* pinned host [status_ring] or NULL */
     void *time_events[2 * MPM_MAX_STATUS_RING]; /* optional (NULL): cudaEvent_t pairs recorded around the
                                           dominant transfer kernel (g2p2g / p2g) of step first+k */
 } mpm_step_plan;

@@ -56,11 +56,14 @@ class GridParams(C.Structure):
         ("block_filter", i32), ("deterministic", i32), ("n_peers", i32),
         ("peer_raw", p_void * MPM_MAX_PEERS), ("peer_touched", p_void * MPM_MAX_PEERS),
         ("peer_map", p_void * MPM_MAX_PEERS),
+        ("n_wait", i32), ("wait_value", i32), ("wait_timeout_ms", i32), ("reserved1", i32),
+        ("wait_flags", p_void * MPM_MAX_PEERS), ("wait_error", p_void),
     ]
 
 
 class Guard(C.Structure):
-    _fields_ = [("first_bad_step", p_void), ("step", i32)]
+    _fields_ = [("first_bad_step", p_void), ("step", i32), ("n_peer_words", i32),
+                ("peer_words", p_void * MPM_MAX_PEERS)]
 
 
 class StepStatus(C.Structure):
@@ -79,6 +82,8 @@ class StepPlan(C.Structure):
         ("fused_margin_lo", f64), ("fused_margin_hi", f64), ("grid", GridParams),
         ("fused", i32), ("status_ring", i32), ("status_dev", p_void), ("status_host", p_void),
         ("events", p_void * MAX_STATUS_RING), ("guard_word", p_void),
+        ("n_peer_words", i32), ("reserved2", i32), ("peer_guard_words", p_void * MPM_MAX_PEERS),
+        ("signal_word", p_void), ("guard_host", p_void),
         ("time_events", p_void * (2 * MAX_STATUS_RING)),
     ]
 
@@ -109,6 +114,8 @@ _SIGNATURES = {
     "mpm_grid_update": [p_void, p_void, p_void, p_void, C.POINTER(TableView),
                         C.POINTER(GridParams), p_void, C.POINTER(Guard), p_void],
     "mpm_pack_halo": [p_void, p_void, p_void, i32, p_void, p_void],
+    "mpm_signal_step": [p_void, i32, C.POINTER(Guard), p_void],
+    "mpm_wait_step": [C.POINTER(GridParams), C.POINTER(Guard), p_void],
     "mpm_g2p": [C.POINTER(StoreView), C.POINTER(TableView), p_void, p_void,
                 C.POINTER(TransferParams), p_void, C.POINTER(Guard), p_void],
     "mpm_g2p2g": [C.POINTER(StoreView), C.POINTER(TableView), p_void, p_void, p_void, p_void,

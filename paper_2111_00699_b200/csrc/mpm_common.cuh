@@ -83,7 +83,16 @@ __device__ __forceinline__ int node_slot(int cx, int cy, int cz)
 struct DevGuard {
     int *word;
     int step;
+    int n_peers;
+    int *peer_words[MPM_MAX_PEERS];
 };
+// raise the guard: this rank's word and, with peer-mapped memory, every peer's (system scope)
+__device__ __forceinline__ void guard_raise(const DevGuard &g)
+{
+    if (!g.word) return;
+    atomicMin(g.word, g.step);
+    for (int p = 0; p < g.n_peers; ++p) atomicMin_system(g.peer_words[p], g.step);
+}
 __device__ __forceinline__ bool guarded_out(const DevGuard &g)
 {
     return g.word != nullptr && *((volatile const int *)g.word) < g.step;
@@ -93,6 +102,9 @@ inline DevGuard make_guard(const mpm_guard *g)
     DevGuard d;
     d.word = g ? g->first_bad_step : nullptr;
     d.step = g ? g->step : 0;
+    d.n_peers = g ? g->n_peer_words : 0;
+    if (d.n_peers < 0 || d.n_peers > MPM_MAX_PEERS) d.n_peers = 0;
+    for (int p = 0; p < MPM_MAX_PEERS; ++p) d.peer_words[p] = (g && p < d.n_peers) ? g->peer_words[p] : nullptr;
     return d;
 }
 

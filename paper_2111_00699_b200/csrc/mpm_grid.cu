@@ -11,8 +11,6 @@
 // table and no compacted index list (the reference's flatnonzero) is needed.
 #include "mpm_common.cuh"
 
-#define MPM_MAX_PEERS 15
-
 namespace mpm {
 
 struct PeerSet {
@@ -57,7 +55,24 @@ struct GridArgs {
     uint8_t *touched_mut;
     DevGuard guard;
     mpm_step_status *reset_status;
+    // device-side step barrier (peer rows read in place)
+    int n_wait, wait_value, wait_timeout_ms;
+    const int *wait_flags[MPM_MAX_PEERS];
+    int *wait_error;
 };
+
+__device__ __forceinline__ int ld_acquire_sys(const int *p)
+{
+    int v;
+    asm volatile("ld.acquire.sys.global.s32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+    return v;
+}
+__device__ __forceinline__ unsigned long long global_timer_ns()
+{
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+    return t;
+}
 
 __global__ void __launch_bounds__(256) grid_update_kernel(const GridArgs a)
 {
@@ -70,6 +85,36 @@ __global__ void __launch_bounds__(256) grid_update_kernel(const GridArgs a)
     const int b = blockIdx.x * 4 + (threadIdx.x >> 6);
     const int slot = threadIdx.x & 63;
     bool hit = b < a.count && a.touched[b];
+    if (a.n_wait) {
+        // Step barrier on the device: the peers' scatter of this step must be complete before
+        // their rows are read.  Only CTAs that own a block shared with a peer wait (and CTA 0, so
+        // that the kernel as a whole -- hence everything after it in the stream -- is ordered
+        // after every peer's signal and after any guard the peers raised).
+        __shared__ int s_wait;
+        if (threadIdx.x == 0) s_wait = blockIdx.x == 0;
+        __syncthreads();
+        if (hit && slot == 0) {
+            bool shared = false;
+            for (int p = 0; p < a.peers.n; ++p) shared = shared || a.peers.map[p][b] >= 0;
+            if (shared) s_wait = 1;
+        }
+        __syncthreads();
+        if (s_wait) {
+            if (threadIdx.x < a.n_wait) {
+                const int *flag = a.wait_flags[threadIdx.x];
+                const unsigned long long t0 = global_timer_ns();
+                const unsigned long long limit = (unsigned long long)a.wait_timeout_ms * 1000000ull;
+                while (ld_acquire_sys(flag) < a.wait_value) {
+                    if (global_timer_ns() - t0 > limit) {
+                        if (a.wait_error) atomicExch(a.wait_error, 1);
+                        break;
+                    }
+                    __nanosleep(200);
+                }
+            }
+            __syncthreads();
+        }
+    }
     if (hit && a.block_filter) {
         // 1: only blocks no peer holds (can run while the halo rows are in flight), 2: the rest
         bool shared = false;
@@ -86,8 +131,10 @@ __global__ void __launch_bounds__(256) grid_update_kernel(const GridArgs a)
         longlong4 node = rawd[idx];
         for (int p = 0; p < a.peers.n; ++p) {
             const int q = a.peers.map[p][b];
-            if (q < 0 || (a.peers.touched[p] && a.peers.touched[p][q] != 1)) continue;
-            const longlong4 o = ((const longlong4 *)a.peers.raw[p])[(size_t)q * 64 + slot];
+            if (q < 0 || (a.peers.touched[p] && __ldcv(&a.peers.touched[p][q]) != 1)) continue;
+            const longlong2 *src = (const longlong2 *)a.peers.raw[p] + ((size_t)q * 64 + slot) * 2;
+            const longlong2 lo = __ldcg(src), hi = __ldcg(src + 1);
+            const longlong4 o = make_longlong4(lo.x, lo.y, hi.x, hi.y);
             node.x += o.x; node.y += o.y; node.z += o.z; node.w += o.w;
         }
         if (a.fuse_clear) {
@@ -107,8 +154,8 @@ __global__ void __launch_bounds__(256) grid_update_kernel(const GridArgs a)
         // cross-worker reduction (pipeline.py:1172-1188): peers' raw rows are only read
         for (int p = 0; p < a.peers.n; ++p) {
             const int q = a.peers.map[p][b];
-            if (q < 0 || (a.peers.touched[p] && a.peers.touched[p][q] != 1)) continue;
-            const float4 o = a.peers.raw[p][(size_t)q * 64 + slot];
+            if (q < 0 || (a.peers.touched[p] && __ldcv(&a.peers.touched[p][q]) != 1)) continue;
+            const float4 o = __ldcg(&a.peers.raw[p][(size_t)q * 64 + slot]);
             node.x += o.x; node.y += o.y; node.z += o.z; node.w += o.w;
         }
         if (a.fuse_clear) {
@@ -215,6 +262,38 @@ __global__ void __launch_bounds__(256) pack_halo_kernel(const float4 *__restrict
     out[(size_t)i * 64 + slot] = touched[b] ? raw[(size_t)b * 64 + slot] : make_float4(0.f, 0.f, 0.f, 0.f);
 }
 
+__global__ void signal_step_kernel(int *word, int value, const DevGuard guard)
+{
+    if (guarded_out(guard)) return;
+    // everything enqueued before this kernel on the stream has completed; make it visible to the
+    // peers before the word they poll changes
+    __threadfence_system();
+    asm volatile("st.release.sys.global.s32 [%0], %1;" :: "l"(word), "r"(value) : "memory");
+}
+
+struct WaitArgs {
+    int n_wait, wait_value, wait_timeout_ms;
+    const int *wait_flags[MPM_MAX_PEERS];
+    int *wait_error;
+};
+// the step barrier alone (a rank whose block table is empty has no grid update to hang it on)
+__global__ void wait_step_kernel(const WaitArgs a, const DevGuard guard)
+{
+    if (guarded_out(guard)) return;
+    if (threadIdx.x < a.n_wait) {
+        const int *flag = a.wait_flags[threadIdx.x];
+        const unsigned long long t0 = global_timer_ns();
+        const unsigned long long limit = (unsigned long long)a.wait_timeout_ms * 1000000ull;
+        while (ld_acquire_sys(flag) < a.wait_value) {
+            if (global_timer_ns() - t0 > limit) {
+                if (a.wait_error) atomicExch(a.wait_error, 1);
+                break;
+            }
+            __nanosleep(200);
+        }
+    }
+}
+
 __global__ void status_reset_kernel(mpm_step_status *status, const DevGuard guard)
 {
     if (guarded_out(guard)) return;
@@ -282,8 +361,35 @@ int mpm_grid_update(float *raw, uint8_t *touched, float *vel, float *vel_old,
     a.touched_mut = touched;
     a.guard = make_guard(guard);
     a.reset_status = reset_status;
+    if (p->n_wait < 0 || p->n_wait > MPM_MAX_PEERS) return MPM_ERR_CONFIG;
+    a.n_wait = p->n_wait;
+    a.wait_value = p->wait_value;
+    a.wait_timeout_ms = p->wait_timeout_ms > 0 ? p->wait_timeout_ms : 10000;
+    for (int k = 0; k < MPM_MAX_PEERS; ++k) a.wait_flags[k] = k < p->n_wait ? p->wait_flags[k] : nullptr;
+    a.wait_error = p->wait_error;
     grid_update_kernel<<<(a.count + 3) / 4, 256, 0, (cudaStream_t)stream>>>(a);
     return check_launch("mpm_grid_update", 1);
+}
+
+int mpm_signal_step(int32_t *word, int32_t value, const mpm_guard *guard, void *stream)
+{
+    if (!word) return MPM_ERR_REJECTED_INPUT;
+    signal_step_kernel<<<1, 1, 0, (cudaStream_t)stream>>>(word, value, make_guard(guard));
+    return check_launch("mpm_signal_step", 1);
+}
+
+int mpm_wait_step(const mpm_grid_params *p, const mpm_guard *guard, void *stream)
+{
+    if (!p || p->n_wait < 0 || p->n_wait > MPM_MAX_PEERS) return MPM_ERR_REJECTED_INPUT;
+    if (p->n_wait == 0) return MPM_OK;
+    WaitArgs a;
+    a.n_wait = p->n_wait;
+    a.wait_value = p->wait_value;
+    a.wait_timeout_ms = p->wait_timeout_ms > 0 ? p->wait_timeout_ms : 10000;
+    for (int k = 0; k < MPM_MAX_PEERS; ++k) a.wait_flags[k] = k < p->n_wait ? p->wait_flags[k] : nullptr;
+    a.wait_error = p->wait_error;
+    wait_step_kernel<<<1, 32, 0, (cudaStream_t)stream>>>(a, make_guard(guard));
+    return check_launch("mpm_wait_step", 1);
 }
 
 int mpm_pack_halo(const float *raw, const uint8_t *touched, const int32_t *send_idx, int32_t n,

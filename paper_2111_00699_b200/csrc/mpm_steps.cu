@@ -23,7 +23,12 @@ extern "C" int mpm_enqueue_steps(const mpm_step_plan *p, int32_t first_step, int
         const int s = first_step + k;
         const int par = s & 1;
         const int slot = s % p->status_ring;
-        mpm_guard guard = {p->guard_word, s};
+        mpm_guard guard;
+        guard.first_bad_step = p->guard_word;
+        guard.step = s;
+        guard.n_peer_words = p->n_peer_words;
+        for (int q = 0; q < MPM_MAX_PEERS; ++q) guard.peer_words[q] = p->peer_guard_words[q];
+        if (gp.n_wait > 0) gp.wait_value = s + 1;
         mpm_step_status *st_dev = p->status_dev + slot;
         int rc;
         // after the first step of a batch the gather dt is the batch's own dt (pipeline.py:1230)
@@ -43,7 +48,13 @@ extern "C" int mpm_enqueue_steps(const mpm_step_plan *p, int32_t first_step, int
                            st_dev, &guard, stream);
             if (rc != MPM_OK) return rc;
             if (p->time_events[2 * k + 1]) cudaEventRecord((cudaEvent_t)p->time_events[2 * k + 1], stream);
+            if (p->signal_word) {
+                rc = mpm_signal_step(p->signal_word, s + 1, &guard, stream);
+                if (rc != MPM_OK) return rc;
+            }
             cudaMemcpyAsync(p->status_host + slot, st_dev, sizeof(mpm_step_status), cudaMemcpyDeviceToHost, stream);
+            if (p->guard_host)
+                cudaMemcpyAsync(p->guard_host + slot, p->guard_word, sizeof(int32_t), cudaMemcpyDeviceToHost, stream);
             cudaEventRecord((cudaEvent_t)p->events[slot], stream);
             rc = mpm_grid_update(p->raw[par], p->touched[par], p->vel, p->vel_old, &p->table, &gp,
                                  p->status_dev + (s + 1) % p->status_ring, &guard, stream);
@@ -53,6 +64,10 @@ extern "C" int mpm_enqueue_steps(const mpm_step_plan *p, int32_t first_step, int
             rc = mpm_p2g(&p->store, &p->table, p->raw[par], p->touched[par], &tp, st_dev, &guard, stream);
             if (rc != MPM_OK) return rc;
             if (p->time_events[2 * k + 1]) cudaEventRecord((cudaEvent_t)p->time_events[2 * k + 1], stream);
+            if (p->signal_word) {
+                rc = mpm_signal_step(p->signal_word, s + 1, &guard, stream);
+                if (rc != MPM_OK) return rc;
+            }
             rc = mpm_grid_update(p->raw[par], p->touched[par], p->vel, p->vel_old, &p->table, &gp, st_dev,
                                  &guard, stream);
             if (rc != MPM_OK) return rc;
@@ -61,6 +76,8 @@ extern "C" int mpm_enqueue_steps(const mpm_step_plan *p, int32_t first_step, int
             rc = mpm_g2p(&p->store, &p->table, p->vel, p->vel_old, &g2, st_dev, &guard, stream);
             if (rc != MPM_OK) return rc;
             cudaMemcpyAsync(p->status_host + slot, st_dev, sizeof(mpm_step_status), cudaMemcpyDeviceToHost, stream);
+            if (p->guard_host)
+                cudaMemcpyAsync(p->guard_host + slot, p->guard_word, sizeof(int32_t), cudaMemcpyDeviceToHost, stream);
             cudaEventRecord((cudaEvent_t)p->events[slot], stream);
         }
     }

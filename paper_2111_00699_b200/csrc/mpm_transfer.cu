@@ -462,7 +462,7 @@ __global__ void __launch_bounds__(TW * 32, MPM_MINBLOCKS) transfer_kernel(const 
                     const float zz1 = ((float)(org.z - MPM_CELL_BIAS) + 4.0f + a.margin_hi) * a.dx;
                     if (px < zx0 || px >= zx1 || py < zy0 || py >= zy1 || pz < zz0 || pz >= zz1) {
                         a.status->zone_violation = 1;
-                        if (a.guard.word) atomicMin(a.guard.word, a.guard.step);
+                        guard_raise(a.guard);
                     }
                     vmax_bits = __float_as_uint(vx * vx + vy * vy + vz * vz);
                     float tmp;

@@ -1,0 +1,319 @@
+"""One process per GPU, halo rows read in place over NVLink, device-paced steps.
+
+`DistWorker` (dist.py) follows the reference's protocol literally: one host collective per step
+(the barrier), halo rows packed and exchanged with send/recv.  At eight GPUs a substep of the
+1.33 M-particle scene is tens of microseconds of kernel time, so a host round trip per step is
+the bound.  `PeerDistWorker` keeps the reference's data flow (pipeline.py:1166-1188: after the
+step's one barrier every worker adds its peers' raw rows of the shared blocks) but moves the
+barrier and the exchange onto the devices, the way the paper does it (PAPER.md:393,548-551:
+peers' nodal rows are read through NVLink inside the grid kernel, interior blocks overlap):
+
+  memory    every rank maps the others' raw[2], touched[2] and a small mailbox (CUDA IPC via
+            torch's tensor reductions; re-exchanged only when a buffer was reallocated);
+  signal    after the scatter of step s a rank stores s + 1 to its mailbox word
+            (mpm_signal_step, release at system scope);
+  wait+sum  mpm_grid_update spins on the peers' words (acquire, system scope) in the CTAs that
+            own shared blocks -- and in CTA 0, which makes the kernel a full barrier -- then adds
+            the peers' rows straight from their HBM; interior CTAs never wait;
+  guard     the "rebuild needed" guard word of the speculative pipeline (worker.py) is
+            replicated: the gather that raises it raises every rank's copy (system-scope
+            atomicMin) before its rank signals, so all ranks stop after the same step;
+  host      enqueues `depth` steps ahead and only reads status blocks; host collectives happen
+            on the first step of a frame and on rebuild steps (code lists, re-tagging of the
+            shared blocks, remapping), never on a steady-state step.
+
+Raw rows alternate by step parity exactly as in the reference (pipeline.py:10-14): a rank
+clears raw[par] at step s + 2, after its grid update of step s + 1 has waited for every peer's
+signal of step s + 1, which those peers issue after their own grid update of step s -- the
+read of raw[par] at step s is therefore complete.
+
+The same sequence of steps and rebuilds as the reference results (tests/dist_check.py compares
+against the reference's two-worker dump).  CFL-auto frames need the global max speed on the host
+every step and use collective (host-paced) steps throughout.
+"""
+from __future__ import annotations
+
+import ctypes as C
+
+import numpy as np
+import torch
+import torch.distributed as dist
+
+from . import _capi
+from .dist import DistRuntime, DistWorker
+from .errors import BarrierTimeoutError, ContractViolationError
+from .memory import DeviceBuffer
+from .worker import _INT_MAX, _RING, _stream_ptr
+
+MAILBOX_WORDS = 16
+MB_STEP, MB_GUARD, MB_WAIT_ERR = 0, 1, 2
+
+SKIPPED, DONE, RAISED = 0, 1, 2
+
+
+class PeerRuntime(DistRuntime):
+    """DistRuntime + mapping of the other ranks' device buffers into this process."""
+
+    def host_barrier(self):
+        self.all_gather_i64([0])
+
+    def exchange_tensors(self, named: dict):
+        """Collective.  Returns one dict per rank with tensors aliasing THAT rank's device memory
+        (this rank's own entry holds the tensors passed in)."""
+        from torch.multiprocessing.reductions import reduce_tensor
+        payload = {k: reduce_tensor(t) for k, t in named.items()}
+        gathered = [None] * self.n_workers
+        dist.all_gather_object(gathered, payload, group=self.group)
+        out = []
+        for q, pl in enumerate(gathered):
+            if q == self.wid:
+                out.append(dict(named))
+            else:
+                out.append({k: fn(*args) for k, (fn, args) in pl.items()})
+        return out
+
+
+class PeerDistWorker(DistWorker):
+    def __init__(self, runtime: PeerRuntime, params, material, boundary, options=None,
+                 wait_timeout_ms: int = 20000, depth: int = 2, **kw):
+        super().__init__(runtime, params, material, boundary, options, **kw)
+        with torch.cuda.device(self.device):
+            self._mailbox = torch.zeros(MAILBOX_WORDS, dtype=torch.int32, device=self.device)
+            self._mailbox[MB_GUARD] = _INT_MAX
+            # the replicated guard word lives in memory the peers can reach
+            self._guard_word = self._mailbox[MB_GUARD:MB_GUARD + 1]
+            self._guard_host = torch.full((_RING,), _INT_MAX, dtype=torch.int32).pin_memory()
+        self.wait_timeout_ms = int(wait_timeout_ms)
+        self.depth = max(1, int(depth))
+        self._peer_mem = None
+        self._exported_sig = None
+        self._peer_counts = [0] * runtime.n_workers
+        self._collective = False
+        self.collective_steps = 0
+        self.device_paced_steps = 0
+
+    # -- exported memory -------------------------------------------------------------------
+    def _exports(self):
+        gr, tb = self.grid, self.table
+        named = {"raw0": gr._raw[0].data, "raw1": gr._raw[1].data,
+                 "touched0": tb._touched[0].data, "touched1": tb._touched[1].data,
+                 "mailbox": self._mailbox}
+        # a rank without blocks has nothing to map; peers never dereference its rows (count 0)
+        return {k: (t if t.numel() else self._mailbox) for k, t in named.items()}
+
+    def _export_sig(self):
+        return tuple((t.data_ptr(), t.numel()) for t in self._exports().values())
+
+    def _make_guard(self, step):
+        g = _capi.Guard(self._guard_word.data_ptr(), step)
+        k = 0
+        if self._peer_mem is not None:
+            for q, mem in enumerate(self._peer_mem):
+                if q == self.runtime.wid:
+                    continue
+                g.peer_words[k] = mem["mailbox"].data_ptr() + 4 * MB_GUARD
+                k += 1
+        g.n_peer_words = k
+        return g
+
+    # -- step phases ------------------------------------------------------------------------
+    def _publish(self, par, rebuilt):
+        self._rebuilt_this_step = rebuilt
+        # "my scatter of this step is complete": peers wait for it inside their grid update
+        self._call("mpm_signal_step", self._mailbox.data_ptr() + 4 * MB_STEP, self._global_step + 1,
+                   self._gref(), _stream_ptr())
+
+    def _post_barrier(self, par):
+        """Host collectives of a collective step: who rebuilt, remapping of reallocated buffers,
+        re-tagging of the shared blocks (pipeline.py:1147-1164).  A device-paced step keeps the
+        maps of the last collective step (no table changed since)."""
+        if not self._collective:
+            return
+        rt, tb = self.runtime, self.table
+        step = self._global_step
+        any_rebuilt, counts = rt.step_info(step, self._rebuilt_this_step, tb.count)
+        sig = self._export_sig()
+        changed = rt.all_gather_i64([int(sig != self._exported_sig)])[:, 0].any()
+        if changed or self._peer_mem is None:
+            self._peer_mem = None        # drop the old mappings first
+            self._peer_mem = rt.exchange_tensors(self._exports())
+            self._exported_sig = sig
+            self._guard = self._make_guard(step)
+        self._peer_counts = list(counts)
+        if not any_rebuilt:
+            return
+        mine = tb._codes.data[:tb.count]
+        lists = rt.all_gather_codes(mine, counts)
+        stream = _stream_ptr()
+        for q in range(rt.n_workers):
+            if q == rt.wid:
+                continue
+            if tb.count == 0 or counts[q] == 0:
+                self._peer_map[q] = None
+                continue
+            m = self._peer_map[q]
+            if m is None:
+                m = self._peer_map[q] = DeviceBuffer(torch.int32, (), self.device)
+            m.resize(tb.count, keep=False)
+            codes_q = lists[q].contiguous()
+            self._call("mpm_tag_shared", codes_q.data_ptr(), int(counts[q]), tb._hkeys.ptr,
+                       tb._hvals.ptr, tb.hash_cap, m.ptr, tb.count, stream)
+
+    def _reduce_and_update(self, par, step=None):
+        if step is None:
+            step = self._global_step
+        rt, tb = self.runtime, self.table
+        gp = self._grid_params()
+        k = w = 0
+        for q in range(rt.n_workers):
+            if q == rt.wid:
+                continue
+            mem = self._peer_mem[q]
+            gp.wait_flags[w] = mem["mailbox"].data_ptr() + 4 * MB_STEP
+            w += 1
+            if self._peer_map[q] is None or self._peer_counts[q] == 0:
+                continue
+            gp.peer_raw[k] = mem[f"raw{par}"].data_ptr()
+            gp.peer_touched[k] = mem[f"touched{par}"].data_ptr()
+            gp.peer_map[k] = self._peer_map[q].ptr
+            k += 1
+        gp.n_peers = k
+        gp.n_wait = w
+        gp.wait_value = step + 1
+        gp.wait_timeout_ms = self.wait_timeout_ms
+        gp.wait_error = self._mailbox.data_ptr() + 4 * MB_WAIT_ERR
+        gp.block_filter = 0
+        nxt = (step + 1 if self._fused_now else step) % _RING
+        if tb.count:
+            self._grid_update_launch(gp, tb.view(), par, self._status_ptr(nxt), _stream_ptr())
+            self._slot_clean[nxt] = True
+        else:
+            # no blocks, nothing to update: still a party to the step barrier
+            self._call("mpm_wait_step", C.byref(gp), self._gref(), _stream_ptr())
+        self._vel_dt = self.dt
+
+    def _after_gather(self, slot, step):
+        self._status_host[slot].copy_(self._status[slot], non_blocking=True)
+        self._guard_host[slot:slot + 1].copy_(self._guard_word, non_blocking=True)
+        self._status_events[slot].record()
+        if self._defer:
+            self._unconsumed = (slot, step)
+        else:
+            self._consume(slot, step)
+
+    # -- collective (host-paced) step ---------------------------------------------------------
+    def _check_wait_error(self):
+        if int(self._mailbox[MB_WAIT_ERR].item()):
+            raise BarrierTimeoutError(
+                f"worker {self.wid}: a peer's step signal did not arrive within "
+                f"{self.wait_timeout_ms} ms (device-side barrier of the grid update)")
+
+    def _collective_step(self):
+        """Drain, agree, reset the replicated guard, then one step with the host collectives of
+        _post_barrier.  Returns True when some rank still needs a rebuild afterwards."""
+        rt = self.runtime
+        torch.cuda.current_stream().synchronize()     # none of my kernels / remote atomics in flight
+        self._check_wait_error()
+        rt.host_barrier()                             # ... nor anybody else's
+        self._guard_word.fill_(_INT_MAX)
+        torch.cuda.current_stream().synchronize()
+        rt.host_barrier()                             # every copy of the guard is reset
+        step = self._global_step
+        self._guard = self._make_guard(step)
+        self._defer = False
+        self._collective = True
+        try:
+            self.step_pre_barrier(step)
+            self.step_post_barrier(step)
+        finally:
+            self._collective = False
+            self._guard = None
+        self.collective_steps += 1
+        return bool(rt.all_gather_i64([int(self.flags.rebuild_needed)])[:, 0].any())
+
+    def run_step(self, step):
+        """One host-paced step (peer rows still read in place, barrier still on the device)."""
+        if step != self._global_step:
+            raise ContractViolationError(f"steps run in order: expected {self._global_step}, got {step}")
+        with torch.cuda.device(self.device):
+            self._collective_step()
+
+    # -- device-paced frame ----------------------------------------------------------------------
+    def _enqueue_guarded(self):
+        step = self._global_step
+        snap = self._snapshot()
+        self._guard = self._make_guard(step)
+        self._defer = True
+        self._unconsumed = None
+        try:
+            self.step_pre_barrier(step)
+            self.step_post_barrier(step)
+        finally:
+            self._defer = False
+            self._guard = None
+        cur = self._unconsumed
+        if cur is None:
+            # a rank without particles ran no gather: still record where the guard stood
+            slot = step % _RING
+            self._status_host[slot].zero_()
+            self._guard_host[slot:slot + 1].copy_(self._guard_word, non_blocking=True)
+            self._status_events[slot].record()
+            cur = (slot, step)
+        return cur[0], step, snap
+
+    def _consume_peer(self, slot, step):
+        self._status_events[slot].synchronize()
+        g = int(self._guard_host[slot])
+        if g < step:
+            return SKIPPED          # the device skipped this step: some rank asked for a rebuild before it
+        self._consume(slot, step)
+        return RAISED if g == step else DONE
+
+    def run_frame(self):
+        self.begin_frame()
+        spf = self.params.steps_per_frame
+        with torch.cuda.device(self.device):
+            if self.cfl_mode:
+                self._run_frame_collective_cfl()
+            else:
+                self.dt = self.params.dt
+                inflight = []
+                collective = True          # first step of a frame: agree on pending rebuilds
+                while self._frame_steps < spf:
+                    if collective:
+                        collective = self._collective_step()
+                        self._frame_steps += 1
+                        self.frame_dts.append(self.dt)
+                        continue
+                    if self._frame_steps + len(inflight) < spf and len(inflight) < self.depth:
+                        inflight.append(self._enqueue_guarded())
+                        continue
+                    slot, step, snap = inflight.pop(0)
+                    outcome = self._consume_peer(slot, step)
+                    if outcome == SKIPPED:
+                        self._restore(snap)
+                        self.speculative_discards += 1 + len(inflight)
+                        inflight, collective = [], True
+                        continue
+                    self._frame_steps += 1
+                    self.device_paced_steps += 1
+                    self.frame_dts.append(self.dt)
+                    if outcome == RAISED or self.flags.rebuild_needed:
+                        if inflight:
+                            self._restore(inflight[0][2])
+                            self.speculative_discards += len(inflight)
+                        inflight, collective = [], True
+            if self._pending_gather:
+                self._flush_gather()
+
+    def _run_frame_collective_cfl(self):
+        from .domain import cfl_dt
+        c_sound = self.material.sound_speed()
+        t = 0.0
+        while t < self.params.frame_dt - 1e-12:
+            vmax = self.runtime.global_vmax((self._global_step - 2) % 3)
+            self.dt = cfl_dt(vmax + c_sound, self.params, self.params.frame_dt - t)
+            self._collective_step()
+            t += self.dt
+            self._frame_steps += 1
+            self.frame_dts.append(self.dt)

@@ -20,6 +20,7 @@ import parity_util as U
 from conftest import elastic_setup, golden
 from paper_2111_00699_b200 import PipelineOptions
 from paper_2111_00699_b200.dist import DistRuntime, DistWorker, seed_rank
+from paper_2111_00699_b200.peer import PeerDistWorker, PeerRuntime
 
 
 def main():
@@ -32,9 +33,25 @@ def main():
     g = golden("two_worker.npz")
     material, params, boundary = elastic_setup()
     transfer = os.environ.get("MPM_TRANSFER", "split")
-    rt = DistRuntime(dev, initial_vmax=float(np.linalg.norm(g["vel"], axis=1).max()))
-    w = DistWorker(rt, params, material, boundary, PipelineOptions(transfer=transfer), device=dev)
+    halo = os.environ.get("MPM_HALO", "sendrecv")     # sendrecv: DistWorker, peer: PeerDistWorker
+    frames = os.environ.get("MPM_MODE", "steps") == "frames"
+    vmax0 = float(np.linalg.norm(g["vel"], axis=1).max())
+    if frames:
+        # 24 steps as two device-paced frames of 12 (rebuilds and rollbacks inside)
+        import dataclasses
+        params = dataclasses.replace(params, steps_per_frame=12, frame_dt=12 * params.dt)
+    if halo == "peer":
+        rt = PeerRuntime(dev, initial_vmax=vmax0)
+        w = PeerDistWorker(rt, params, material, boundary, PipelineOptions(transfer=transfer), device=dev,
+                           wait_timeout_ms=20000)
+    else:
+        rt = DistRuntime(dev, initial_vmax=vmax0)
+        w = DistWorker(rt, params, material, boundary, PipelineOptions(transfer=transfer), device=dev)
     seed_rank(w, g["pos"], g["vel"], float(g["mass"]))
+    if frames:
+        w.run_frame()
+        w.run_frame()
+        return finish(w, g, rank, world, transfer, halo, frames)
     w.run_step(0)
     if world == 2 and transfer == "split":
         bad = U.structure_mismatches(w, g, f"w{rank}_s0_")
@@ -43,20 +60,30 @@ def main():
             assert e <= U.GRID_RTOL, ("vel", rank, c, e)
     for s in range(1, 24):
         w.run_step(s)
+    finish(w, g, rank, world, transfer, halo, frames)
+
+
+def finish(w, g, rank, world, transfer, halo, frames):
     if w._pending_gather:
         w._flush_gather()
     flat, ids = w.store.state_with_ids()
     # collect everything on rank 0
     parts = [None] * world
-    dist.all_gather_object(parts, (flat, ids, list(w.rebuild_steps), int(w.halo_rows_sent)))
+    moved = int(w.halo_rows_sent) if halo != "peer" else \
+        int(w.device_paced_steps if frames else w.collective_steps)
+    dist.all_gather_object(parts, (flat, ids, list(w.rebuild_steps), moved))
     if rank == 0:
         flat = np.concatenate([p[0] for p in parts])
         ids = np.concatenate([p[1] for p in parts])
         state = flat[np.argsort(ids, kind="stable")]
         edge = float(g["pos"].max() - g["pos"].min())
         ex, ev, ef, ec = U.particle_errors(state, g["state_24"], edge, 9)
-        print(f"dist_check world={world} transfer={transfer} x {ex:.2e} v {ev:.2e} F {ef:.2e} "
-              f"rebuilds {[p[2] for p in parts]} halo_rows {[p[3] for p in parts]}")
+        print(f"dist_check world={world} transfer={transfer} halo={halo} frames={frames} "
+              f"x {ex:.2e} v {ev:.2e} F {ef:.2e} "
+              f"rebuilds {[p[2] for p in parts]} halo_rows/steps {[p[3] for p in parts]}")
+        if halo == "peer":
+            print("peer: collective steps", w.collective_steps, "device-paced", w.device_paced_steps,
+                  "discarded", w.speculative_discards)
         if transfer == "split":
             assert ex <= U.X_RTOL_RUN and ev <= U.V_RTOL_RUN and ef <= U.F_ATOL_RUN, (ex, ev, ef)
             if world == 2:

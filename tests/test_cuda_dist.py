@@ -11,11 +11,11 @@ pytestmark = pytest.mark.gpu
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 
 
-def _run(world, transfer):
+def _run(world, transfer, halo="sendrecv", mode="steps"):
     with socket.socket() as s:
         s.bind(("127.0.0.1", 0))
         port = s.getsockname()[1]
-    env = dict(os.environ, MPM_DIST_BACKEND="gloo", MPM_TRANSFER=transfer)
+    env = dict(os.environ, MPM_DIST_BACKEND="gloo", MPM_TRANSFER=transfer, MPM_HALO=halo, MPM_MODE=mode)
     cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={world}",
            "--master-addr", "127.0.0.1", "--master-port", str(port),
            os.path.join(ROOT, "tests", "dist_check.py")]
@@ -30,3 +30,19 @@ def test_two_ranks_split_against_reference_dump():
 
 def test_three_ranks_fused():
     _run(3, "g2p2g")
+
+
+# ---- peer-mapped halo rows + device-side step barrier (paper_2111_00699_b200/peer.py) ----------
+# Two / three processes share cuda:0: each maps the others' raw rows through CUDA IPC (on a
+# multi-GPU node the same mapping is NVLink peer memory), the grid update waits for the peers'
+# step signals on the device and adds their rows in place.
+def test_peer_mapped_two_ranks_host_paced_steps():
+    _run(2, "split", halo="peer")
+
+
+def test_peer_mapped_two_ranks_device_paced_frames_split():
+    _run(2, "split", halo="peer", mode="frames")
+
+
+def test_peer_mapped_three_ranks_device_paced_frames_fused():
+    _run(3, "g2p2g", halo="peer", mode="frames")
