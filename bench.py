@@ -171,10 +171,17 @@ def run_ours(args):
     if args.gpus != world:
         raise SystemExit(f"--gpus {args.gpus} needs {args.gpus} ranks (torch.distributed.run); "
                          f"WORLD_SIZE is {world}")
+    # MPM_DIST_BACKEND=gloo lets several ranks share one GPU (functional check of the N > 1 path
+    # on a single-GPU box); the product configuration is one rank per GPU over NCCL
+    backend = os.environ.get("MPM_DIST_BACKEND", "nccl")
+    local = local % max(torch.cuda.device_count(), 1)
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
     if world > 1:
-        dist.init_process_group("nccl", device_id=dev)
+        if backend == "nccl":
+            dist.init_process_group("nccl", device_id=dev)
+        else:
+            dist.init_process_group(backend)
     W = build_world(args.scene)
     n = len(W.positions)
     spf = W.params.steps_per_frame
@@ -195,8 +202,14 @@ def run_ours(args):
     pin_vel = torch.from_numpy(my_vel).pin_memory()
     pin_ids = torch.from_numpy(np.ascontiguousarray(part, dtype=np.int64)).pin_memory()
 
+    halo = os.environ.get("MPM_HALO", "peer")   # peer: rows read in place over NVLink (peer.py); sendrecv: NCCL
+
     def fresh_worker():
         if world > 1:
+            if halo == "peer":
+                from paper_2111_00699_b200.peer import PeerDistWorker, PeerRuntime
+                return PeerDistWorker(PeerRuntime(dev, initial_vmax=vmax0), W.params, W.material,
+                                      W.boundary, opts, device=dev, count_stats=False)
             return DistWorker(DistRuntime(dev, initial_vmax=vmax0), W.params, W.material, W.boundary,
                               opts, device=dev, count_stats=False)
         return CudaWorker(0, SharedRuntime(1, initial_vmax=vmax0), W.params, W.material, W.boundary,
@@ -210,7 +223,7 @@ def run_ours(args):
     def max_over_ranks(x):
         if world == 1:
             return x
-        t = torch.tensor([x], dtype=torch.float64, device=dev)
+        t = torch.tensor([x], dtype=torch.float64, device=dev if backend == "nccl" else "cpu")
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         return float(t.item())
 
@@ -288,7 +301,9 @@ def run_ours(args):
                "d2h_bytes_per_step": int(out_pos.nbytes + out_ids.nbytes),
                "ms_per_step": round(dt_e2e * 1e3, 3), "steps": k_e2e,
                "api": "CudaWorker.replace_particles(pinned x, v, ids) + run_frame() + "
-                      "store.positions_with_ids() into pinned buffers"}
+                      "store.positions_with_ids() into pinned buffers; every step re-seeds the scene's "
+                      "initial state from the host, so it times the scene's first frame (fewer rebuilds "
+                      "and less yielding than the frames `value` is taken over)"}
 
     cpu = None
     if not args.no_cpu_baseline and rank == 0 and world == 1:
@@ -303,7 +318,9 @@ def run_ours(args):
             "config": {"workload": W.name, "particles": n, "substeps_per_step": spf,
                        "step": "one frame", "dx": W.params.dx, "dt": W.params.dt,
                        "transfer": args.transfer, "material": W.material.kind.name,
-                       "parallelism": f"{world} spatial slab(s), halo rows over NCCL" if world > 1
+                       "parallelism": (f"{world} spatial slabs, halo rows read in place over NVLink peer memory, "
+                                       "device-side step barrier" if halo == "peer" else
+                                       f"{world} spatial slabs, halo rows over NCCL send/recv") if world > 1
                        else "1 GPU", "rank0_particles": n_local,
                        "pblocks": int(w.table.count), "groups": int(w.store.n_groups),
                        "rebuilds_in_timed_region": rebuilds, "touched_pblocks": touched,
@@ -323,8 +340,9 @@ def run_ours(args):
 
 # dram__bytes_read.sum + dram__bytes_write.sum of the dominant kernel, per launch, from the
 # committed `ncu --set full` capture of the fused kernel on the 1.37 M scene
-# (profiles/r1_b_fused_fc_metrics.csv: 81.9 MB read + 48.7 MB write); only quoted for that scene
-TRAFFIC_NCU = {"snow": 130.6e6, "snow_fc": 130.6e6}
+# (profiles/r1_e_fused_snow_v2_metrics.csv: 90.8 MB read + 39.8 MB write; r1_e_fused_fc_v2: 85.3 + 46.2);
+# only quoted for those scenes
+TRAFFIC_NCU = {"snow": 130.6e6, "snow_fc": 131.6e6}
 
 
 def run_fountain(args):
