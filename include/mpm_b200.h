@@ -315,6 +315,10 @@ typedef struct mpm_step_plan {
     int32_t *peer_guard_words[MPM_MAX_PEERS];
     int32_t *signal_word;
     int32_t *guard_host;               /* pinned host [status_ring] or NULL */
+    /* peers' raw rows / touched flags per step parity (grid.n_peers entries each; grid.peer_map
+     * holds the maps, grid.peer_raw / peer_touched are filled per step from these) */
+    const float *peer_raw[2][MPM_MAX_PEERS];
+    const uint8_t *peer_touched[2][MPM_MAX_PEERS];
     void *time_events[2 * MPM_MAX_STATUS_RING]; /* optional (NULL): cudaEvent_t pairs recorded around the
                                           dominant transfer kernel (g2p2g / p2g) of step first+k */
 } mpm_step_plan;

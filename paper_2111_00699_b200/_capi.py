@@ -84,6 +84,7 @@ class StepPlan(C.Structure):
         ("events", p_void * MAX_STATUS_RING), ("guard_word", p_void),
         ("n_peer_words", i32), ("reserved2", i32), ("peer_guard_words", p_void * MPM_MAX_PEERS),
         ("signal_word", p_void), ("guard_host", p_void),
+        ("peer_raw", (p_void * MPM_MAX_PEERS) * 2), ("peer_touched", (p_void * MPM_MAX_PEERS) * 2),
         ("time_events", p_void * (2 * MAX_STATUS_RING)),
     ]
 

@@ -21,14 +21,19 @@ extern "C" int mpm_enqueue_steps(const mpm_step_plan *p, int32_t first_step, int
     mpm_grid_params gp = p->grid;
     for (int k = 0; k < n_steps; ++k) {
         const int s = first_step + k;
-        const int par = s & 1;
         const int slot = s % p->status_ring;
+        const int par = s & 1;
         mpm_guard guard;
         guard.first_bad_step = p->guard_word;
         guard.step = s;
         guard.n_peer_words = p->n_peer_words;
         for (int q = 0; q < MPM_MAX_PEERS; ++q) guard.peer_words[q] = p->peer_guard_words[q];
         if (gp.n_wait > 0) gp.wait_value = s + 1;
+        if (p->signal_word)
+            for (int q = 0; q < gp.n_peers; ++q) {
+                gp.peer_raw[q] = p->peer_raw[par][q];
+                gp.peer_touched[q] = p->peer_touched[par][q];
+            }
         mpm_step_status *st_dev = p->status_dev + slot;
         int rc;
         // after the first step of a batch the gather dt is the batch's own dt (pipeline.py:1230)

@@ -91,6 +91,8 @@ class PeerDistWorker(DistWorker):
         self._collective = False
         self.collective_steps = 0
         self.device_paced_steps = 0
+        self.batched_steps = 0
+        self.batch_steps = 4          # steps per mpm_enqueue_steps call (0 = one guarded step per call)
 
     # -- exported memory -------------------------------------------------------------------
     def _exports(self):
@@ -159,11 +161,10 @@ class PeerDistWorker(DistWorker):
             self._call("mpm_tag_shared", codes_q.data_ptr(), int(counts[q]), tb._hkeys.ptr,
                        tb._hvals.ptr, tb.hash_cap, m.ptr, tb.count, stream)
 
-    def _reduce_and_update(self, par, step=None):
-        if step is None:
-            step = self._global_step
-        rt, tb = self.runtime, self.table
-        gp = self._grid_params()
+    def _fill_peers(self, gp, par=None, plan=None):
+        """Peers' rows / flags / maps and the device-side barrier of a grid update.  With `plan`
+        the rows of both parities go into the step plan (mpm_enqueue_steps picks per step)."""
+        rt = self.runtime
         k = w = 0
         for q in range(rt.n_workers):
             if q == rt.wid:
@@ -173,16 +174,29 @@ class PeerDistWorker(DistWorker):
             w += 1
             if self._peer_map[q] is None or self._peer_counts[q] == 0:
                 continue
-            gp.peer_raw[k] = mem[f"raw{par}"].data_ptr()
-            gp.peer_touched[k] = mem[f"touched{par}"].data_ptr()
+            if plan is None:
+                gp.peer_raw[k] = mem[f"raw{par}"].data_ptr()
+                gp.peer_touched[k] = mem[f"touched{par}"].data_ptr()
+            else:
+                for pp in (0, 1):
+                    plan.peer_raw[pp][k] = mem[f"raw{pp}"].data_ptr()
+                    plan.peer_touched[pp][k] = mem[f"touched{pp}"].data_ptr()
             gp.peer_map[k] = self._peer_map[q].ptr
             k += 1
         gp.n_peers = k
         gp.n_wait = w
-        gp.wait_value = step + 1
         gp.wait_timeout_ms = self.wait_timeout_ms
         gp.wait_error = self._mailbox.data_ptr() + 4 * MB_WAIT_ERR
         gp.block_filter = 0
+        gp.fuse_clear = 0
+
+    def _reduce_and_update(self, par, step=None):
+        if step is None:
+            step = self._global_step
+        tb = self.table
+        gp = self._grid_params()
+        self._fill_peers(gp, par)
+        gp.wait_value = step + 1
         nxt = (step + 1 if self._fused_now else step) % _RING
         if tb.count:
             self._grid_update_launch(gp, tb.view(), par, self._status_ptr(nxt), _stream_ptr())
@@ -269,6 +283,62 @@ class PeerDistWorker(DistWorker):
         self._consume(slot, step)
         return RAISED if g == step else DONE
 
+    def _peer_plan(self):
+        """The single-worker step plan (worker.py) plus the peer fields of mpm_step_plan."""
+        self.fuse_clear = False
+        plan = self._step_plan()
+        gp = self._grid_params()
+        self._fill_peers(gp, plan=plan)
+        C.memmove(C.byref(plan.grid), C.byref(gp), C.sizeof(_capi.GridParams))
+        g = self._make_guard(0)
+        plan.n_peer_words = g.n_peer_words
+        for k in range(g.n_peer_words):
+            plan.peer_guard_words[k] = g.peer_words[k]
+        plan.signal_word = self._mailbox.data_ptr() + 4 * MB_STEP
+        plan.guard_host = self._guard_host.data_ptr()
+        plan.guard_word = self._guard_word.data_ptr()
+        for k in range(2 * _capi.MAX_STATUS_RING):
+            plan.time_events[k] = None
+        return plan
+
+    def _device_paced_batched(self, spf):
+        """Steady-state steps enqueued from C (mpm_enqueue_steps), up to two batches in flight.
+        Host bookkeeping advances when a step's status block is read.  Returns True when the
+        next step must be collective (some rank asked for a rebuild)."""
+        pending = []
+        next_step = self._global_step
+        enq = self._frame_steps
+        while self._frame_steps < spf:
+            while len(pending) <= self.batch_steps and enq < spf:
+                n = min(self.batch_steps, spf - enq)
+                plan = self._peer_plan()
+                plan.transfer.dt_gather = float(self._vel_dt if not pending else self.dt)
+                self.kernel_calls += 1
+                _capi.check(self.lib.mpm_enqueue_steps(C.byref(plan), next_step, n, _stream_ptr()),
+                            "mpm_enqueue_steps")
+                pending += list(range(next_step, next_step + n))
+                next_step += n
+                enq += n
+            step = pending.pop(0)
+            slot = step % _RING
+            self._slot_clean[slot] = False
+            outcome = self._consume_peer(slot, step)
+            if outcome == SKIPPED:
+                self.speculative_discards += 1 + len(pending)
+                return True
+            # step `step` ran to completion on every rank
+            self._global_step = step + 1
+            self._vel_dt = self.dt
+            self.flags.steps_since_rebuild += 1
+            self._frame_steps += 1
+            self.device_paced_steps += 1
+            self.batched_steps += 1
+            self.frame_dts.append(self.dt)
+            if outcome == RAISED or self.flags.rebuild_needed:
+                self.speculative_discards += len(pending)
+                return True
+        return False
+
     def run_frame(self):
         self.begin_frame()
         spf = self.params.steps_per_frame
@@ -285,7 +355,11 @@ class PeerDistWorker(DistWorker):
                         self._frame_steps += 1
                         self.frame_dts.append(self.dt)
                         continue
-                    if self._frame_steps + len(inflight) < spf and len(inflight) < self.depth:
+                    if not inflight and self.batch_steps > 0 and self._can_batch():
+                        collective = self._device_paced_batched(spf)
+                        continue
+                    if self._frame_steps + len(inflight) < spf and len(inflight) < self.depth \
+                            and not (inflight and self.batch_steps > 0 and self._can_batch()):
                         inflight.append(self._enqueue_guarded())
                         continue
                     slot, step, snap = inflight.pop(0)

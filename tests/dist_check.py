@@ -44,6 +44,7 @@ def main():
         rt = PeerRuntime(dev, initial_vmax=vmax0)
         w = PeerDistWorker(rt, params, material, boundary, PipelineOptions(transfer=transfer), device=dev,
                            wait_timeout_ms=20000)
+        w.batch_steps = int(os.environ.get("MPM_PEER_BATCH", "4"))   # 0: one guarded step per host call
     else:
         rt = DistRuntime(dev, initial_vmax=vmax0)
         w = DistWorker(rt, params, material, boundary, PipelineOptions(transfer=transfer), device=dev)
@@ -83,7 +84,7 @@ def finish(w, g, rank, world, transfer, halo, frames):
               f"rebuilds {[p[2] for p in parts]} halo_rows/steps {[p[3] for p in parts]}")
         if halo == "peer":
             print("peer: collective steps", w.collective_steps, "device-paced", w.device_paced_steps,
-                  "discarded", w.speculative_discards)
+                  "of which enqueued from C", w.batched_steps, "discarded", w.speculative_discards)
         if transfer == "split":
             assert ex <= U.X_RTOL_RUN and ev <= U.V_RTOL_RUN and ef <= U.F_ATOL_RUN, (ex, ev, ef)
             if world == 2:

@@ -11,11 +11,12 @@ pytestmark = pytest.mark.gpu
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 
 
-def _run(world, transfer, halo="sendrecv", mode="steps"):
+def _run(world, transfer, halo="sendrecv", mode="steps", batch=4):
     with socket.socket() as s:
         s.bind(("127.0.0.1", 0))
         port = s.getsockname()[1]
-    env = dict(os.environ, MPM_DIST_BACKEND="gloo", MPM_TRANSFER=transfer, MPM_HALO=halo, MPM_MODE=mode)
+    env = dict(os.environ, MPM_DIST_BACKEND="gloo", MPM_TRANSFER=transfer, MPM_HALO=halo, MPM_MODE=mode,
+               MPM_PEER_BATCH=str(batch))
     cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={world}",
            "--master-addr", "127.0.0.1", "--master-port", str(port),
            os.path.join(ROOT, "tests", "dist_check.py")]
@@ -46,3 +47,7 @@ def test_peer_mapped_two_ranks_device_paced_frames_split():
 
 def test_peer_mapped_three_ranks_device_paced_frames_fused():
     _run(3, "g2p2g", halo="peer", mode="frames")
+
+
+def test_peer_mapped_two_ranks_one_guarded_step_per_host_call():
+    _run(2, "g2p2g", halo="peer", mode="frames", batch=0)
