@@ -97,6 +97,12 @@ typedef struct mpm_store_view {
     int32_t *group_start;    /* [n_groups] sorted position of lane 0 (exclusive scan of group_len) */
     int32_t n_groups;
     int32_t nch;
+    /* Per-group context row [n_groups][32] (one 128-byte line, written by mpm_build_group_ctx after
+     * every rebuild): words 0..26 = 64 * pblock of the 27 neighbours of the group's block
+     * (neighbor[group_block]), 27..29 = origin of the block, 30 = group_len, 31 = group_block.
+     * The transfer kernels read this one line instead of the dependent chain group_block ->
+     * origin / neighbor row.  NULL = read the tables. */
+    int32_t *group_ctx;
 } mpm_store_view;
 
 /* Block table view: BlockTable (grid.py:325-386). */
@@ -217,6 +223,10 @@ int mpm_clear(float *raw, uint8_t *touched, int32_t count, int full, int32_t nod
  * raw (float4 nodes), touched flags set for every addressed block. */
 int mpm_p2g(const mpm_store_view *store, const mpm_table_view *table, float *raw, uint8_t *touched,
             const mpm_transfer_params *params, mpm_step_status *status, const mpm_guard *guard, void *stream);
+
+/* Fill store->group_ctx from the block table (after mpm_scatter_sorted; groups do not change
+ * between rebuilds). */
+int mpm_build_group_ctx(const mpm_store_view *store, const mpm_table_view *table, void *stream);
 
 /* _reduce_and_update + _grid_finalize (pipeline.py:1166-1231, 660-722): for every block
  * flagged in touched: vel = raw (+ peer raw rows through peer_map where the peer touched

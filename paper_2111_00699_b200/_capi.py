@@ -39,6 +39,7 @@ class StoreView(C.Structure):
     _fields_ = [
         ("data", p_void), ("orig_id", p_void), ("lane_meta", p_void), ("group_len", p_void),
         ("group_block", p_void), ("group_start", p_void), ("n_groups", i32), ("nch", i32),
+        ("group_ctx", p_void),
     ]
 
 
@@ -108,6 +109,7 @@ _SIGNATURES = {
                            p_void, p_void, p_void],
     "mpm_scatter_sorted": [C.POINTER(StoreView), p_void, p_void, p_void, p_void, p_void, p_void,
                            p_void, i32, p_void, f64, C.POINTER(StoreView), p_void],
+    "mpm_build_group_ctx": [C.POINTER(StoreView), C.POINTER(TableView), p_void],
     "mpm_clear": [p_void, p_void, i32, i32, i32, C.POINTER(Guard), p_void],
     "mpm_status_reset": [p_void, C.POINTER(Guard), p_void],
     "mpm_p2g": [C.POINTER(StoreView), C.POINTER(TableView), p_void, p_void,

@@ -545,6 +545,28 @@ __global__ void fill_i32_kernel(int *p, int n, int v)
     if (i < n) p[i] = v;
 }
 
+// One 128-byte context line per lane group (mpm_store_view.group_ctx): the neighbour row of the
+// group's block as node indices, the block origin, the group length and the block index.
+__global__ void __launch_bounds__(256) group_ctx_kernel(const int *__restrict__ group_len,
+                                                        const int *__restrict__ group_block, int n_groups,
+                                                        const int4 *__restrict__ origin,
+                                                        const int *__restrict__ neighbor,
+                                                        int *__restrict__ ctx)
+{
+    const int g = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    const int lane = threadIdx.x & 31;
+    if (g >= n_groups) return;
+    const int b = group_block[g];
+    int v;
+    if (lane < 27) v = neighbor[b * 27 + lane] * 64;
+    else if (lane == 27) v = origin[b].x;
+    else if (lane == 28) v = origin[b].y;
+    else if (lane == 29) v = origin[b].z;
+    else if (lane == 30) v = group_len[g];
+    else v = b;
+    ctx[g * 32 + lane] = v;
+}
+
 }  // namespace mpm
 
 using namespace mpm;
@@ -692,6 +714,17 @@ int mpm_scatter_sorted(const mpm_store_view *old_store, const int32_t *src_slot,
         (const int4 *)table_origin, inv_dx, new_store->data, (long long *)new_store->orig_id,
         new_store->lane_meta, new_store->group_len, new_store->group_block, new_store->group_start, G);
     return check_launch("mpm_scatter_sorted", 1);
+}
+
+int mpm_build_group_ctx(const mpm_store_view *store, const mpm_table_view *table, void *stream_)
+{
+    if (!store || !table || !store->group_ctx) return MPM_ERR_REJECTED_INPUT;
+    const int G = store->n_groups;
+    if (G <= 0) return MPM_OK;
+    group_ctx_kernel<<<nblk((int64_t)G * 32, 256), 256, 0, (cudaStream_t)stream_>>>(
+        store->group_len, store->group_block, G, (const int4 *)table->origin, table->neighbor,
+        store->group_ctx);
+    return check_launch("mpm_build_group_ctx", 1);
 }
 
 int mpm_gather_state(const mpm_store_view *store, float *flat, int64_t *ids, void *stream_)

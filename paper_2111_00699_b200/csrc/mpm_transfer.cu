@@ -22,6 +22,7 @@ struct TransferArgs {
     uint16_t *meta;
     const int *group_len;
     const int *group_block;
+    const int *group_ctx;
     int n_groups;
     int nch;
     const int4 *origin;
@@ -288,6 +289,8 @@ __device__ __forceinline__ void scatter27(float4 *__restrict__ raw, const int *n
 #pragma unroll
             for (int k = 0; k < 3; ++k) {
                 const float w = wxy * wz[k];
+                // issued before the shuffles so that its shared-memory latency overlaps them
+                const int node = nrow[rxy + rz[k]] + sxy + sz[k];
                 acc_t c0, c1, c2, c3;
                 if (DET) {
                     c0 = (acc_t)__float2ll_rn((w * mm) * MPM_MASS_SCALE);
@@ -320,7 +323,6 @@ __device__ __forceinline__ void scatter27(float4 *__restrict__ raw, const int *n
                 MPM_SEG_STEP(16, f16)
 #undef MPM_SEG_STEP
                 if (leader) {
-                    const int node = nrow[rxy + rz[k]] + sxy + sz[k];
                     if (DET) red_add_det((long long *)raw + (size_t)node * 4, (long long)c0, (long long)c1,
                                          (long long)c2, (long long)c3);
                     else red_add_v4(&raw[node], (float)c0, (float)c1, (float)c2, (float)c3);
@@ -345,17 +347,29 @@ template <int MAT, bool GATHER, bool SCATTER, bool DET>
 __global__ void __launch_bounds__(TW * 32, MPM_MINBLOCKS) transfer_kernel(const TransferArgs a)
 {
     if (guarded_out(a.guard)) return;
-    __shared__ int s_nrow[TW][28];
+    __shared__ int s_nrow[TW][32];
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int g = blockIdx.x * TW + warp;
     const unsigned FULL = 0xffffffffu;
     if (g >= a.n_groups) return;     // warps are independent: no CTA-wide barrier below
 
-    const int len = a.group_len[g];
-    const int block = a.group_block[g];
-    const int4 org = a.origin[block];
-    if (lane < 27) s_nrow[warp][lane] = a.neighbor[block * 27 + lane] * 64;   // node index of slot 0
-    __syncwarp();
+    // group context: neighbour row (as node indices of slot 0), block origin, group length.  One
+    // 128-byte line per group written at the rebuild (mpm_build_group_ctx) -- every load of the
+    // prologue depends on g alone; without it, the dependent chain through the block table.
+    int len;
+    int4 org;
+    if (a.group_ctx) {
+        s_nrow[warp][lane] = __ldg(&a.group_ctx[g * 32 + lane]);
+        __syncwarp();
+        org.x = s_nrow[warp][27]; org.y = s_nrow[warp][28]; org.z = s_nrow[warp][29]; org.w = 0;
+        len = s_nrow[warp][30];
+    } else {
+        len = a.group_len[g];
+        const int block = a.group_block[g];
+        org = a.origin[block];
+        if (lane < 27) s_nrow[warp][lane] = a.neighbor[block * 27 + lane] * 64;
+        __syncwarp();
+    }
     const int *nrow = s_nrow[warp];
 
     float *gd = a.data + (size_t)g * a.nch * 32 + lane;
@@ -363,7 +377,7 @@ __global__ void __launch_bounds__(TW * 32, MPM_MINBLOCKS) transfer_kernel(const 
     bool active = lane < len && !(meta & MPM_LANE_QUARANTINED);
     float m = active ? gd[CH_MASS * 32] : 0.0f;
     active = active && (m > 0.0f);
-    int key = meta & 0x3ff;
+    int key = min(meta & 0x3ff, 999);     // three digits 0..9: every address below stays inside nrow
 
     float px = 0.f, py = 0.f, pz = 0.f, vx = 0.f, vy = 0.f, vz = 0.f;
     float C[9];
@@ -574,6 +588,7 @@ static int fill_args(TransferArgs &a, const mpm_store_view *store, const mpm_tab
     a.meta = store->lane_meta;
     a.group_len = store->group_len;
     a.group_block = store->group_block;
+    a.group_ctx = store->group_ctx;
     a.n_groups = store->n_groups;
     a.nch = store->nch;
     a.origin = (const int4 *)table->origin;

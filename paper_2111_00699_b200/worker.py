@@ -74,6 +74,7 @@ class CudaParticleStore:
         self._group_len = mk(torch.int32)
         self._group_block = mk(torch.int32)
         self._group_start = mk(torch.int32)
+        self._group_ctx = mk(torch.int32, (LW,))
         self.cur = 0
         self.n_groups = 0
         self.count = 0
@@ -88,13 +89,14 @@ class CudaParticleStore:
         k = self.cur if which is None else which
         return StoreView(self._data[k].ptr, self._orig_id[k].ptr, self._lane_meta[k].ptr,
                          self._group_len[k].ptr, self._group_block[k].ptr,
-                         self._group_start[k].ptr, self.n_groups if k == self.cur else 0, self.nch)
+                         self._group_start[k].ptr, self.n_groups if k == self.cur else 0, self.nch,
+                         self._group_ctx[k].ptr)
 
     @property
     def realloc_count(self) -> int:
         return sum(b.realloc_count for pair in (self._data, self._orig_id, self._lane_meta,
                                                 self._group_len, self._group_block,
-                                                self._group_start) for b in pair)
+                                                self._group_start, self._group_ctx) for b in pair)
 
     # -- population (particles.py:309-334) --
     def default_deformation(self, n):
@@ -980,16 +982,19 @@ class CudaWorker:
         # new particle store (other half of the double buffer)
         nxt = 1 - st.cur
         for bufs in (st._data, st._orig_id, st._lane_meta, st._group_len, st._group_block,
-                     st._group_start):
+                     st._group_start, st._group_ctx):
             bufs[nxt].resize(G, keep=False)
         new = StoreView(st._data[nxt].ptr, st._orig_id[nxt].ptr, st._lane_meta[nxt].ptr,
                         st._group_len[nxt].ptr, st._group_block[nxt].ptr, st._group_start[nxt].ptr,
-                        G, st.nch)
+                        G, st.nch, st._group_ctx[nxt].ptr)
         self._call("mpm_scatter_sorted", C.byref(old), src_slot.ptr, self._sptr(0),
                    staged.data_ptr() if n_staged else None,
                    staged_ids.data_ptr() if n_staged else None, perm.ptr, bin_start.ptr, bgf.ptr,
                    n_g, tb._origin.ptr, float(self.params.dx), C.byref(new), stream)
         st.cur, st.n_groups, st.count = nxt, G, n
+        if G:
+            tv = tb.view()
+            self._call("mpm_build_group_ctx", C.byref(new), C.byref(tv), stream)
         self.last_perm = perm.data[:n]
         self.last_gidx = gidx.data[:n]
         # nodal buffers (pipeline.py:996-1006): vel and raw[par] start from zero; the other
