@@ -49,6 +49,15 @@ struct TransferArgs {
 #ifndef MPM_LATE_F
 #define MPM_LATE_F 1
 #endif
+#ifndef MPM_ROLL_J
+#define MPM_ROLL_J 0      // 1: scatter loops rolled over x and y (three nodes per trip)
+#endif
+#ifndef MPM_ONE_DEPTH
+#define MPM_ONE_DEPTH 1   // 1: no separate instantiation for warps whose runs are all <= 2 lanes
+#endif
+#ifndef MPM_RUNCAP
+#define MPM_RUNCAP 4      // power of two; 32 = one reduction per (subgroup, node) whatever the run length
+#endif
 constexpr int TW = MPM_TW;   // warps (groups) per CTA
 
 __device__ __forceinline__ void red_add_v4(float4 *addr, float a, float b, float c, float d)
@@ -279,13 +288,23 @@ __device__ __forceinline__ void scatter27(float4 *__restrict__ raw, const int *n
         const float wxi = mm > 0.0f ? quad_weight_at(fx, i) : 0.0f;   // inactive lanes contribute zeros
         const float dpx = ((float)i - fx) * dx;
         const float X0 = mm * vx + Q[0] * dpx, X1 = mm * vy + Q[3] * dpx, X2 = mm * vz + Q[6] * dpx;
+#if MPM_ROLL_J
+#pragma unroll 1
+#else
 #pragma unroll
+#endif
         for (int j = 0; j < 3; ++j) {
             const float dpy = ((float)j - fy) * dx;
+#if MPM_ROLL_J
+            const float wxy = wxi * quad_weight_at(fy, j);
+            const int rxy = rx + ((ky + j) >> 2) * 3;
+            const int sxy = sx + slot_bits<1>(ky + j);
+#else
             const float wxy = wxi * wy[j];
-            const float XY0 = X0 + Q[1] * dpy, XY1 = X1 + Q[4] * dpy, XY2 = X2 + Q[7] * dpy;
             const int rxy = rx + ry[j];
             const int sxy = sx + sy[j];
+#endif
+            const float XY0 = X0 + Q[1] * dpy, XY1 = X1 + Q[4] * dpy, XY2 = X2 + Q[7] * dpy;
 #pragma unroll
             for (int k = 0; k < 3; ++k) {
                 const float w = wxy * wz[k];
@@ -546,8 +565,22 @@ __global__ void __launch_bounds__(TW * 32, MPM_MINBLOCKS) transfer_kernel(const 
         // runs of consecutive active lanes with equal keys
         const unsigned act = __ballot_sync(FULL, active);
         const int prev_key = __shfl_up_sync(FULL, key, 1);
-        const bool head = !active || lane == 0 || prev_key != key || !((act >> (lane - 1)) & 1u);
-        const unsigned heads = __ballot_sync(FULL, head);
+        bool head = !active || lane == 0 || prev_key != key || !((act >> (lane - 1)) & 1u);
+        const unsigned run_heads = __ballot_sync(FULL, head);      // the reference's subgroups
+        unsigned heads = run_heads;
+#if MPM_RUNCAP < 32
+        {
+            // A run longer than MPM_RUNCAP lanes is reduced in pieces of MPM_RUNCAP, each with its
+            // own leader: the reduction depth of the whole warp is bounded by log2(MPM_RUNCAP)
+            // instead of being set by its longest run (just after a rebuild runs average 7 lanes),
+            // at the price of one more vector reduction per node and extra piece.  Counters keep
+            // the reference's meaning (runs, not pieces).
+            const unsigned below = run_heads & ((2u << lane) - 1u);
+            const int run_first = 31 - __clz(below);
+            head = head || (((lane - run_first) & (MPM_RUNCAP - 1)) == 0);
+            heads = __ballot_sync(FULL, head);
+        }
+#endif
         const unsigned above = lane == 31 ? 0u : (heads & ~((2u << lane) - 1u));
         const int reach = (above ? (__ffs(above) - 2) : 31) - lane;
         const int maxd = __reduce_max_sync(FULL, reach);
@@ -560,15 +593,21 @@ __global__ void __launch_bounds__(TW * 32, MPM_MINBLOCKS) transfer_kernel(const 
             const float mm = active ? m : 0.0f;
             const bool leader = head && active;
             if (DET) scatter27<5, true>((float4 *)a.raw, nrow, kx, ky, kz, fx, fy, fz, a.dx, mm, vx, vy, vz, Q, reach, maxd, leader);
+#if !MPM_ONE_DEPTH
             else if (maxd < 2) scatter27<1, false>(a.raw, nrow, kx, ky, kz, fx, fy, fz, a.dx, mm, vx, vy, vz, Q, reach, maxd, leader);
-            else if (maxd < 4) scatter27<2, false>(a.raw, nrow, kx, ky, kz, fx, fy, fz, a.dx, mm, vx, vy, vz, Q, reach, maxd, leader);
-            else if (maxd < 8) scatter27<3, false>(a.raw, nrow, kx, ky, kz, fx, fy, fz, a.dx, mm, vx, vy, vz, Q, reach, maxd, leader);
+#endif
+            else if (MPM_RUNCAP <= 4 || maxd < 4) scatter27<2, false>(a.raw, nrow, kx, ky, kz, fx, fy, fz, a.dx, mm, vx, vy, vz, Q, reach, maxd, leader);
+#if MPM_RUNCAP > 4
+            else if (MPM_RUNCAP <= 8 || maxd < 8) scatter27<3, false>(a.raw, nrow, kx, ky, kz, fx, fy, fz, a.dx, mm, vx, vy, vz, Q, reach, maxd, leader);
+#endif
+#if MPM_RUNCAP > 8
             else scatter27<5, false>(a.raw, nrow, kx, ky, kz, fx, fy, fz, a.dx, mm, vx, vy, vz, Q, reach, maxd, leader);
+#endif
             unsigned nbmask = leader ? block_mask27(kx, ky, kz) : 0u;
             nbmask = __reduce_or_sync(FULL, nbmask);
             if (lane < 27 && ((nbmask >> lane) & 1u)) a.touched[nrow[lane] >> 6] = 1;
             if (a.count_stats && lane == 0) {
-                const int runs = __popc(heads & act);
+                const int runs = __popc(run_heads & act);
                 atomicAdd(&a.status->counters[MPM_C_SUBGROUPS], (unsigned long long)runs);
                 atomicAdd(&a.status->counters[MPM_C_ACCUM], (unsigned long long)runs * 27ull);
             }
