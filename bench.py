@@ -213,7 +213,7 @@ def run_ours(args):
             return DistWorker(DistRuntime(dev, initial_vmax=vmax0), W.params, W.material, W.boundary,
                               opts, device=dev, count_stats=False)
         return CudaWorker(0, SharedRuntime(1, initial_vmax=vmax0), W.params, W.material, W.boundary,
-                          opts, device=dev, count_stats=False, fuse_clear=True)
+                          opts, device=dev, count_stats=False, fuse_clear=True, lazy_flush=True)
 
     def barrier():
         if world > 1:

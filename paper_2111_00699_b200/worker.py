@@ -83,6 +83,7 @@ class CudaParticleStore:
         self._next_id = 0
         self._pin = {}
         self._table = None   # set by the worker: group_origin comes from the block table
+        self._before_read = None   # set by the worker: completes a lazily pending gather
 
     # -- views for the C ABI --
     def view(self, which=None) -> StoreView:
@@ -238,6 +239,8 @@ class CudaParticleStore:
 
     # -- readback (lazy D2H views in the reference's layout / dtype) --
     def _g(self, bufs):
+        if self._before_read is not None:
+            self._before_read()
         return bufs[self.cur].data[:self.n_groups]
 
     @property
@@ -277,6 +280,8 @@ class CudaParticleStore:
 
     def state_with_ids(self):
         """All stored lanes (quarantined included) in (group, lane) order: flat f64 [n, nch], ids."""
+        if self._before_read is not None:
+            self._before_read()
         n = self.count
         flat = torch.zeros((max(n, 1), self.nch), dtype=torch.float32, device=self.device)
         ids = torch.zeros(max(n, 1), dtype=torch.int64, device=self.device)
@@ -289,6 +294,8 @@ class CudaParticleStore:
     def positions_with_ids(self, dtype=np.float64):
         """particles.py:466-475: positions of every stored particle (quarantined included) and
         their ids, in (group, lane) order."""
+        if self._before_read is not None:
+            self._before_read()
         n = self.count
         if not n:
             return np.zeros((0, 3), dtype=dtype), np.zeros(0, dtype=np.int64)
@@ -308,6 +315,8 @@ class CudaParticleStore:
         return hpos.numpy().astype(dtype), hids.numpy().copy()
 
     def _aggregates(self):
+        if self._before_read is not None:
+            self._before_read()
         out = torch.zeros(5, dtype=torch.float64, device=self.device)
         v = self.view()
         check(_capi.lib().mpm_particle_aggregates(C.byref(v), out.data_ptr(), _stream_ptr()),
@@ -435,7 +444,8 @@ class CudaWorker:
 
     def __init__(self, wid, runtime, params: SimParams, material: Material,
                  boundary: BoundaryBox | None, options: PipelineOptions | None = None,
-                 device=None, count_stats: bool = True, fuse_clear: bool = False):
+                 device=None, count_stats: bool = True, fuse_clear: bool = False,
+                 lazy_flush: bool = False):
         _capi.require_device()
         self.lib = _capi.lib()
         self.device = torch.device(device if device is not None else "cuda:0")
@@ -478,6 +488,7 @@ class CudaWorker:
         self._vel_dt = params.dt
         self._global_step = 0
         self._pending_gather = False
+        self._flushing = False
         self._pending_full_clear_parity = -1
         self._published_codes = (None, 0)
         self._peer_map = [None] * runtime.n_workers
@@ -490,6 +501,12 @@ class CudaWorker:
         self.frame_dts = []
         self.count_stats = bool(count_stats)
         self.fuse_clear = bool(fuse_clear)
+        # lazy_flush: a frame may end with the fused transfer's gather still pending (the reference
+        # flushes it at every frame end, pipeline.py:877-880, because its harness reads positions
+        # there).  The flush then happens on the first access to the particle store, so what a
+        # caller observes is unchanged, and back-to-back frames stay fused across the boundary.
+        self.lazy_flush = bool(lazy_flush)
+        self.store._before_read = self._ensure_flushed
         self.last_perm = None
         self.last_gidx = None
         self._scratch = {}
@@ -660,7 +677,7 @@ class CudaWorker:
                     self.run_step(self._global_step)
                     self._frame_steps += 1
                     self.frame_dts.append(self.dt)
-            if self._pending_gather:
+            if self._pending_gather and not self.lazy_flush:
                 self._flush_gather()
 
     def _run_frame_pipelined(self):
@@ -723,7 +740,7 @@ class CudaWorker:
         finally:
             self._defer = False
             self._guard = None
-        if self._pending_gather:
+        if self._pending_gather and not self.lazy_flush:
             self._flush_gather()
 
     # -- batched steady state (fixed dt): mpm_enqueue_steps ------------------------------------
@@ -828,7 +845,7 @@ class CudaWorker:
                     next_step = self._global_step
                     self._guard_word.fill_(_INT_MAX)
                     break
-        if self._pending_gather:
+        if self._pending_gather and not self.lazy_flush:
             self._flush_gather()
 
     def _snapshot(self):
@@ -1091,6 +1108,16 @@ class CudaWorker:
         self._call("mpm_g2p", C.byref(sv), C.byref(tv), self.grid._vel.ptr, self._vel_old_ptr(),
                    C.byref(self._params()), self._status_ptr(slot), self._gref(), stream)
         self._after_gather(slot, step)
+
+    def _ensure_flushed(self):
+        """Called by the particle store before anything reads or writes particle state."""
+        if self._pending_gather and self.lazy_flush and not self._flushing:
+            self._flushing = True
+            try:
+                with torch.cuda.device(self.device):
+                    self._flush_gather()
+            finally:
+                self._flushing = False
 
     def _flush_gather(self):
         guard, defer = self._guard, self._defer
