@@ -209,7 +209,7 @@ def run_ours(args):
             if halo == "peer":
                 from paper_2111_00699_b200.peer import PeerDistWorker, PeerRuntime
                 return PeerDistWorker(PeerRuntime(dev, initial_vmax=vmax0), W.params, W.material,
-                                      W.boundary, opts, device=dev, count_stats=False)
+                                      W.boundary, opts, device=dev, count_stats=False, lazy_flush=True)
             return DistWorker(DistRuntime(dev, initial_vmax=vmax0), W.params, W.material, W.boundary,
                               opts, device=dev, count_stats=False)
         return CudaWorker(0, SharedRuntime(1, initial_vmax=vmax0), W.params, W.material, W.boundary,

@@ -27,6 +27,11 @@ clears raw[par] at step s + 2, after its grid update of step s + 1 has waited fo
 signal of step s + 1, which those peers issue after their own grid update of step s -- the
 read of raw[par] at step s is therefore complete.
 
+With `lazy_flush=True` (worker.py) a frame may end with the fused gather pending; the next
+frame then starts device-paced as well (no per-frame host collective).  Reading the particle
+store completes the gather and makes the next frame start with a collective step, so store
+reads must be SPMD (every rank or none).
+
 The same sequence of steps and rebuilds as the reference results (tests/dist_check.py compares
 against the reference's two-worker dump).  CFL-auto frames need the global max speed on the host
 every step and use collective (host-paced) steps throughout.
@@ -92,6 +97,7 @@ class PeerDistWorker(DistWorker):
         self.collective_steps = 0
         self.device_paced_steps = 0
         self.batched_steps = 0
+        self._need_collective = True   # first step ever; after that only when some rank asks for it
         self.batch_steps = 4          # steps per mpm_enqueue_steps call (0 = one guarded step per call)
 
     # -- exported memory -------------------------------------------------------------------
@@ -348,7 +354,11 @@ class PeerDistWorker(DistWorker):
             else:
                 self.dt = self.params.dt
                 inflight = []
-                collective = True          # first step of a frame: agree on pending rebuilds
+                # The first step of a frame is collective (agree on rebuilds the frame-end flush may
+                # have asked for) -- unless lazy_flush left the gather pending and nothing read the
+                # store since: then the frame boundary is invisible to the device-paced pipeline.
+                # Store reads (which flush) must be SPMD: every rank or none.
+                collective = self._need_collective or not (self.lazy_flush and self._pending_gather)
                 while self._frame_steps < spf:
                     if collective:
                         collective = self._collective_step()
@@ -377,7 +387,8 @@ class PeerDistWorker(DistWorker):
                             self._restore(inflight[0][2])
                             self.speculative_discards += len(inflight)
                         inflight, collective = [], True
-            if self._pending_gather:
+            self._need_collective = collective
+            if self._pending_gather and not self.lazy_flush:
                 self._flush_gather()
 
     def _run_frame_collective_cfl(self):

@@ -43,7 +43,7 @@ def main():
     if halo == "peer":
         rt = PeerRuntime(dev, initial_vmax=vmax0)
         w = PeerDistWorker(rt, params, material, boundary, PipelineOptions(transfer=transfer), device=dev,
-                           wait_timeout_ms=20000)
+                           wait_timeout_ms=20000, lazy_flush=os.environ.get("MPM_LAZY", "0") == "1")
         w.batch_steps = int(os.environ.get("MPM_PEER_BATCH", "4"))   # 0: one guarded step per host call
     else:
         rt = DistRuntime(dev, initial_vmax=vmax0)

@@ -11,12 +11,12 @@ pytestmark = pytest.mark.gpu
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 
 
-def _run(world, transfer, halo="sendrecv", mode="steps", batch=4):
+def _run(world, transfer, halo="sendrecv", mode="steps", batch=4, lazy=0):
     with socket.socket() as s:
         s.bind(("127.0.0.1", 0))
         port = s.getsockname()[1]
     env = dict(os.environ, MPM_DIST_BACKEND="gloo", MPM_TRANSFER=transfer, MPM_HALO=halo, MPM_MODE=mode,
-               MPM_PEER_BATCH=str(batch))
+               MPM_PEER_BATCH=str(batch), MPM_LAZY=str(lazy))
     cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={world}",
            "--master-addr", "127.0.0.1", "--master-port", str(port),
            os.path.join(ROOT, "tests", "dist_check.py")]
@@ -51,3 +51,8 @@ def test_peer_mapped_three_ranks_device_paced_frames_fused():
 
 def test_peer_mapped_two_ranks_one_guarded_step_per_host_call():
     _run(2, "g2p2g", halo="peer", mode="frames", batch=0)
+
+
+def test_peer_mapped_frames_without_a_per_frame_collective():
+    """lazy_flush: the second frame starts device-paced (no host collective at the frame boundary)."""
+    _run(2, "g2p2g", halo="peer", mode="frames", lazy=1)
