@@ -287,8 +287,9 @@ def run_ours(args):
     if not args.no_e2e:
         w2 = fresh_worker()
         k_e2e = max(2, min(args.steps, 4))
-        for it in range(1 + k_e2e):
-            if it == 1:
+        E2E_WARM = 3      # untimed: the second worker's buffers, pinned staging and the allocator settle
+        for it in range(E2E_WARM + k_e2e):
+            if it == E2E_WARM:
                 barrier()
                 t0 = time.perf_counter()
             w2.replace_particles(pin_pos, pin_vel, W.particle_mass, pin_ids)
