@@ -375,6 +375,13 @@ __global__ void __launch_bounds__(TW * 32, MPM_MINBLOCKS) transfer_kernel(const 
     // group context: neighbour row (as node indices of slot 0), block origin, group length.  One
     // 128-byte line per group written at the rebuild (mpm_build_group_ctx) -- every load of the
     // prologue depends on g alone; without it, the dependent chain through the block table.
+    // Every prologue load is issued before the first use of any of them: context line, lane
+    // meta, mass and position cost ONE trip to memory instead of three dependent ones (rows are
+    // 32 lanes wide whatever the group length, and the rebuild zeroes the padding lanes).
+    float *gd = a.data + (size_t)g * a.nch * 32 + lane;
+    uint16_t meta = a.meta[g * 32 + lane];
+    float m = gd[CH_MASS * 32];
+    float px = gd[(CH_POS + 0) * 32], py = gd[(CH_POS + 1) * 32], pz = gd[(CH_POS + 2) * 32];
     int len;
     int4 org;
     if (a.group_ctx) {
@@ -391,14 +398,11 @@ __global__ void __launch_bounds__(TW * 32, MPM_MINBLOCKS) transfer_kernel(const 
     }
     const int *nrow = s_nrow[warp];
 
-    float *gd = a.data + (size_t)g * a.nch * 32 + lane;
-    uint16_t meta = a.meta[g * 32 + lane];
-    bool active = lane < len && !(meta & MPM_LANE_QUARANTINED);
-    float m = active ? gd[CH_MASS * 32] : 0.0f;
-    active = active && (m > 0.0f);
+    bool active = lane < len && !(meta & MPM_LANE_QUARANTINED) && (m > 0.0f);
+    if (!active) { m = 0.0f; px = py = pz = 0.0f; }
     int key = min(meta & 0x3ff, 999);     // three digits 0..9: every address below stays inside nrow
 
-    float px = 0.f, py = 0.f, pz = 0.f, vx = 0.f, vy = 0.f, vz = 0.f;
+    float vx = 0.f, vy = 0.f, vz = 0.f;
     float C[9];
     float F[9];   // F (elastic kinds) or F[0] = J (fluid)
     float tau[9]; // plastic kinds: stress of the projected state, produced by the gather
@@ -408,10 +412,7 @@ __global__ void __launch_bounds__(TW * 32, MPM_MINBLOCKS) transfer_kernel(const 
     unsigned vmax_bits = 0;
     // the deformation state is loaded after the 27-node gather (MPM_LATE_F): nine registers less
     // across the gather loop
-    if (active) {
-        px = gd[(CH_POS + 0) * 32]; py = gd[(CH_POS + 1) * 32]; pz = gd[(CH_POS + 2) * 32];
-        if (!(GATHER && MPM_LATE_F)) load_deformation<MAT>(gd, F, plastic);
-    }
+    if (active && !(GATHER && MPM_LATE_F)) load_deformation<MAT>(gd, F, plastic);
 
     // =========================== gather (pipeline.py:400-600) ===========================
     if (GATHER) {

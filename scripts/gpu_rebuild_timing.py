@@ -5,7 +5,7 @@ import numpy as np, torch
 import bench
 from paper_2111_00699_b200 import PipelineOptions, SharedRuntime
 from paper_2111_00699_b200.worker import CudaWorker
-W = bench.build_world("snow_fc")
+W = bench.build_world(sys.argv[1] if len(sys.argv) > 1 else "snow_fc")
 n = len(W.positions)
 w = CudaWorker(0, SharedRuntime(1, 150.0), W.params, W.material, W.boundary,
                PipelineOptions(transfer="g2p2g", fused_threshold=1 << 62), count_stats=False, fuse_clear=True)
