@@ -1,6 +1,7 @@
 """Static SASS statistics per kernel of libmpm_b200.so: python scripts/sass_stats.py [filter]"""
 import collections, re, subprocess, sys
-so = "paper_2111_00699_b200/libmpm_b200.so"
+import os
+so = os.environ.get("SO", "paper_2111_00699_b200/libmpm_b200.so")
 out = subprocess.run(["cuobjdump", "-sass", so], capture_output=True, text=True).stdout
 flt = sys.argv[1] if len(sys.argv) > 1 else "transfer_kernel"
 cur, stats = None, {}
