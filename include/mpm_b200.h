@@ -129,6 +129,9 @@ const char *mpm_version(void);
 const char *mpm_last_error(void);       /* text of the last CUDA error seen by this thread */
 int mpm_device_arch(void);              /* 100 for sm_100 */
 unsigned long long mpm_launch_count(void);  /* kernels launched by this library so far (process-wide) */
+/* device alias of page-locked host memory (cudaHostGetDevicePointer), NULL when it is not mapped:
+ * the address kernels store status blocks to (mpm_status_publish, mpm_grid_params.publish_*) */
+void *mpm_host_alias(void *pinned_host);
 
 /* ---- rebuild-mapping: Worker._rebuild (pipeline.py:958-1015) ------------------------ */
 
@@ -260,6 +263,16 @@ typedef struct mpm_grid_params {
     int32_t reserved1;
     const int32_t *wait_flags[MPM_MAX_PEERS];    /* peers' step words (written by mpm_signal_step) */
     int32_t *wait_error;                         /* local device word */
+    /* Status publication without the copy engine (all optional, NULL = off): after the step
+     * barrier CTA 0 stores *publish_src to *publish_dst and *publish_guard_src to
+     * *publish_guard_dst, both device aliases of pinned host memory (cudaHostGetDevicePointer).
+     * A kernel -> copy -> kernel chain costs a copy-engine round trip (~20 us) per step; these
+     * 60 bytes ride on the update kernel instead.  A guarded-out launch still publishes the guard
+     * word (the host tells a skipped step by guard < step). */
+    const mpm_step_status *publish_src;
+    mpm_step_status *publish_dst;
+    const int32_t *publish_guard_src;
+    int32_t *publish_guard_dst;
 } mpm_grid_params;
 int mpm_grid_update(float *raw, uint8_t *touched, float *vel, float *vel_old,
                     const mpm_table_view *table, const mpm_grid_params *params,
@@ -293,13 +306,20 @@ int mpm_g2p2g(const mpm_store_view *store, const mpm_table_view *table, const fl
 /* Reset zone_violation and vmax2_bits of a status block before a gather (the reference
  * passes a fresh out_stats = zeros(2) per call, pipeline.py:1090). */
 int mpm_status_reset(mpm_step_status *status, const mpm_guard *guard, void *stream);
+/* Store *src (and *guard_src, optional) to mapped pinned host memory from a one-warp kernel: the
+ * readback of out_stats (pipeline.py:1102-1104) in stream order without the copy engine.  Not
+ * guarded: a skipped step still reports where the guard stood. */
+int mpm_status_publish(const mpm_step_status *src, mpm_step_status *dst_mapped, const int32_t *guard_src,
+                       int32_t *guard_dst_mapped, void *stream);
 
 /* Batched enqueue of n_steps guarded no-rebuild substeps of ONE worker (the inner loop of
  * Worker.run_frame, pipeline.py:872-876, issued from C: small scenes are bound by launch
  * overhead, not by the kernels).  Step s uses raw/touched[s & 1] and status slot s % ring; the
- * slot is copied to `status_host` (pinned) and `events[slot]` (cudaEvent_t handles owned by the
- * caller) is recorded after the copy.  Fused: g2p2g -> copy -> grid update.  Split: [clear] ->
- * p2g -> grid update -> g2p -> copy.  Every kernel carries the guard {guard_word, s}. */
+ * slot is stored to `status_host` (pinned, written through its device alias by the grid update
+ * (fused) or by mpm_status_publish (split); cudaMemcpyAsync when the memory is not mapped) and
+ * `events[slot]` (cudaEvent_t handles owned by the caller) is recorded after it.  Fused: g2p2g ->
+ * grid update (+ publication).  Split: [clear] -> p2g -> grid update -> g2p -> publication.
+ * Every kernel carries the guard {guard_word, s}. */
 #define MPM_MAX_STATUS_RING 32
 typedef struct mpm_step_plan {
     mpm_store_view store;

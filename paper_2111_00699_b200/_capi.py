@@ -59,6 +59,8 @@ class GridParams(C.Structure):
         ("peer_map", p_void * MPM_MAX_PEERS),
         ("n_wait", i32), ("wait_value", i32), ("wait_timeout_ms", i32), ("reserved1", i32),
         ("wait_flags", p_void * MPM_MAX_PEERS), ("wait_error", p_void),
+        ("publish_src", p_void), ("publish_dst", p_void), ("publish_guard_src", p_void),
+        ("publish_guard_dst", p_void),
     ]
 
 
@@ -112,6 +114,7 @@ _SIGNATURES = {
     "mpm_build_group_ctx": [C.POINTER(StoreView), C.POINTER(TableView), p_void],
     "mpm_clear": [p_void, p_void, i32, i32, i32, C.POINTER(Guard), p_void],
     "mpm_status_reset": [p_void, C.POINTER(Guard), p_void],
+    "mpm_status_publish": [p_void, p_void, p_void, p_void, p_void],
     "mpm_p2g": [C.POINTER(StoreView), C.POINTER(TableView), p_void, p_void,
                 C.POINTER(TransferParams), p_void, C.POINTER(Guard), p_void],
     "mpm_grid_update": [p_void, p_void, p_void, p_void, C.POINTER(TableView),
@@ -133,9 +136,10 @@ _SIGNATURES = {
     "mpm_last_error": [],
     "mpm_device_arch": [],
     "mpm_launch_count": [],
+    "mpm_host_alias": [p_void],
 }
 _RESTYPES = {"mpm_version": C.c_char_p, "mpm_last_error": C.c_char_p,
-             "mpm_launch_count": C.c_ulonglong}
+             "mpm_launch_count": C.c_ulonglong, "mpm_host_alias": C.c_void_p}
 
 EXPORTED_SYMBOLS = tuple(_SIGNATURES)
 

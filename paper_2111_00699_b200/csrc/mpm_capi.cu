@@ -47,4 +47,14 @@ int mpm_device_arch(void)
     return major * 10 + minor;
 }
 
+void *mpm_host_alias(void *pinned_host)
+{
+    void *dev = nullptr;
+    if (!pinned_host || cudaHostGetDevicePointer(&dev, pinned_host, 0) != cudaSuccess) {
+        cudaGetLastError();
+        return nullptr;
+    }
+    return dev;
+}
+
 }  // extern "C"

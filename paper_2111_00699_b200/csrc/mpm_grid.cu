@@ -59,7 +59,23 @@ struct GridArgs {
     int n_wait, wait_value, wait_timeout_ms;
     const int *wait_flags[MPM_MAX_PEERS];
     int *wait_error;
+    // status publication to mapped host memory (mpm_grid_params.publish_*)
+    const mpm_step_status *publish_src;
+    mpm_step_status *publish_dst;
+    const int *publish_guard_src;
+    int *publish_guard_dst;
 };
+
+// 56-byte status block (+ guard word) to mapped pinned host memory: lanes 0..6 one 8-byte word each
+__device__ __forceinline__ void publish_status(const mpm_step_status *src, mpm_step_status *dst,
+                                               const int *guard_src, int *guard_dst, int lane)
+{
+    static_assert(sizeof(mpm_step_status) % 8 == 0, "status block is copied in 8-byte words");
+    if (dst && lane < (int)(sizeof(mpm_step_status) / 8))
+        ((volatile unsigned long long *)dst)[lane] = ((const volatile unsigned long long *)src)[lane];
+    if (guard_dst && lane == 31) *(volatile int *)guard_dst = *(const volatile int *)guard_src;
+    __threadfence_system();
+}
 
 __device__ __forceinline__ int ld_acquire_sys(const int *p)
 {
@@ -76,7 +92,12 @@ __device__ __forceinline__ unsigned long long global_timer_ns()
 
 __global__ void __launch_bounds__(256) grid_update_kernel(const GridArgs a)
 {
-    if (guarded_out(a.guard)) return;
+    if (guarded_out(a.guard)) {
+        // a skipped step still tells the host where the guard stood
+        if (a.publish_guard_dst && blockIdx.x == 0 && threadIdx.x == 31)
+            publish_status(nullptr, nullptr, a.publish_guard_src, a.publish_guard_dst, 31);
+        return;
+    }
     if (a.reset_status && blockIdx.x == 0 && threadIdx.x == 0) {
         // fresh out_stats for the gather that follows this update in stream order
         a.reset_status->zone_violation = 0;
@@ -115,6 +136,9 @@ __global__ void __launch_bounds__(256) grid_update_kernel(const GridArgs a)
             __syncthreads();
         }
     }
+    // after the barrier: a guard raised by a peer during this step has landed
+    if ((a.publish_dst || a.publish_guard_dst) && blockIdx.x == 0 && threadIdx.x < 32)
+        publish_status(a.publish_src, a.publish_dst, a.publish_guard_src, a.publish_guard_dst, threadIdx.x);
     if (hit && a.block_filter) {
         // 1: only blocks no peer holds (can run while the halo rows are in flight), 2: the rest
         bool shared = false;
@@ -294,6 +318,12 @@ __global__ void wait_step_kernel(const WaitArgs a, const DevGuard guard)
     }
 }
 
+__global__ void status_publish_kernel(const mpm_step_status *src, mpm_step_status *dst, const int *guard_src,
+                                      int *guard_dst)
+{
+    publish_status(src, dst, guard_src, guard_dst, threadIdx.x);
+}
+
 __global__ void status_reset_kernel(mpm_step_status *status, const DevGuard guard)
 {
     if (guarded_out(guard)) return;
@@ -321,6 +351,15 @@ int mpm_status_reset(mpm_step_status *status, const mpm_guard *guard, void *stre
 {
     status_reset_kernel<<<1, 1, 0, (cudaStream_t)stream>>>(status, make_guard(guard));
     return check_launch("mpm_status_reset", 1);
+}
+
+int mpm_status_publish(const mpm_step_status *src, mpm_step_status *dst_mapped, const int32_t *guard_src,
+                       int32_t *guard_dst_mapped, void *stream)
+{
+    if ((dst_mapped && !src) || (guard_dst_mapped && !guard_src)) return MPM_ERR_REJECTED_INPUT;
+    if (!dst_mapped && !guard_dst_mapped) return MPM_OK;
+    status_publish_kernel<<<1, 32, 0, (cudaStream_t)stream>>>(src, dst_mapped, guard_src, guard_dst_mapped);
+    return check_launch("mpm_status_publish", 1);
 }
 
 int mpm_grid_update(float *raw, uint8_t *touched, float *vel, float *vel_old,
@@ -367,6 +406,12 @@ int mpm_grid_update(float *raw, uint8_t *touched, float *vel, float *vel_old,
     a.wait_timeout_ms = p->wait_timeout_ms > 0 ? p->wait_timeout_ms : 10000;
     for (int k = 0; k < MPM_MAX_PEERS; ++k) a.wait_flags[k] = k < p->n_wait ? p->wait_flags[k] : nullptr;
     a.wait_error = p->wait_error;
+    if ((p->publish_dst && !p->publish_src) || (p->publish_guard_dst && !p->publish_guard_src))
+        return MPM_ERR_REJECTED_INPUT;
+    a.publish_src = p->publish_src;
+    a.publish_dst = p->publish_dst;
+    a.publish_guard_src = p->publish_guard_src;
+    a.publish_guard_dst = p->publish_guard_dst;
     grid_update_kernel<<<(a.count + 3) / 4, 256, 0, (cudaStream_t)stream>>>(a);
     return check_launch("mpm_grid_update", 1);
 }

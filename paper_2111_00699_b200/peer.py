@@ -88,6 +88,7 @@ class PeerDistWorker(DistWorker):
             # the replicated guard word lives in memory the peers can reach
             self._guard_word = self._mailbox[MB_GUARD:MB_GUARD + 1]
             self._guard_host = torch.full((_RING,), _INT_MAX, dtype=torch.int32).pin_memory()
+            self._guard_alias = self.lib.mpm_host_alias(self._guard_host.data_ptr())
         self.wait_timeout_ms = int(wait_timeout_ms)
         self.depth = max(1, int(depth))
         self._peer_mem = None
@@ -213,8 +214,13 @@ class PeerDistWorker(DistWorker):
         self._vel_dt = self.dt
 
     def _after_gather(self, slot, step):
-        self._status_host[slot].copy_(self._status[slot], non_blocking=True)
-        self._guard_host[slot:slot + 1].copy_(self._guard_word, non_blocking=True)
+        if self._status_alias and self._guard_alias:
+            self._call("mpm_status_publish", self._status_ptr(slot),
+                       self._status_alias + slot * _capi.STATUS_BYTES, self._guard_word.data_ptr(),
+                       self._guard_alias + 4 * slot, _stream_ptr())
+        else:
+            self._status_host[slot].copy_(self._status[slot], non_blocking=True)
+            self._guard_host[slot:slot + 1].copy_(self._guard_word, non_blocking=True)
         self._status_events[slot].record()
         if self._defer:
             self._unconsumed = (slot, step)

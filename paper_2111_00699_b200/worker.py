@@ -472,6 +472,10 @@ class CudaWorker:
                                        device=self.device)
             self._status_host = torch.zeros((_RING, _capi.STATUS_BYTES // 8),
                                             dtype=torch.int64).pin_memory()
+            # device alias of the host ring: status blocks are stored to it by kernels
+            # (mpm_status_publish / the grid update), not copied -- a kernel -> copy -> kernel chain
+            # idles the device for a copy-engine round trip per step
+            self._status_alias = self.lib.mpm_host_alias(self._status_host.data_ptr())
             self._status_events = [torch.cuda.Event() for _ in range(_RING)]
             self._time_events = [torch.cuda.Event(enable_timing=True) for _ in range(2 * _BATCH * 2)]
             for ev in self._status_events + self._time_events:
@@ -1090,7 +1094,11 @@ class CudaWorker:
         return slot
 
     def _after_gather(self, slot, step):
-        self._status_host[slot].copy_(self._status[slot], non_blocking=True)
+        if self._status_alias:
+            self._call("mpm_status_publish", self._status_ptr(slot),
+                       self._status_alias + slot * _capi.STATUS_BYTES, None, None, _stream_ptr())
+        else:
+            self._status_host[slot].copy_(self._status[slot], non_blocking=True)
         self._status_events[slot].record()
         if self._defer:
             self._unconsumed = (slot, step)
