@@ -111,8 +111,8 @@ __global__ void __launch_bounds__(256) grid_update_kernel(const GridArgs a)
         // their rows are read.  Only CTAs that own a block shared with a peer wait (and CTA 0, so
         // that the kernel as a whole -- hence everything after it in the stream -- is ordered
         // after every peer's signal and after any guard the peers raised).
-        __shared__ int s_wait;
-        if (threadIdx.x == 0) s_wait = blockIdx.x == 0;
+        __shared__ int s_wait, s_void;
+        if (threadIdx.x == 0) { s_wait = blockIdx.x == 0; s_void = 0; }
         __syncthreads();
         if (hit && slot == 0) {
             bool shared = false;
@@ -126,6 +126,14 @@ __global__ void __launch_bounds__(256) grid_update_kernel(const GridArgs a)
                 const unsigned long long t0 = global_timer_ns();
                 const unsigned long long limit = (unsigned long long)a.wait_timeout_ms * 1000000ull;
                 while (ld_acquire_sys(flag) < a.wait_value) {
+                    // Split transfers gather AFTER this barrier: a peer whose gather of step s left
+                    // its free zone raises the guard while this rank may already be waiting in step
+                    // s + 1 for a signal the peer will never send (its step s + 1 is guarded out).
+                    // The raise reaches this rank's word too: the step is void, stop waiting.
+                    if (a.guard.word && ld_acquire_sys(a.guard.word) < a.guard.step) {
+                        s_void = 1;
+                        break;
+                    }
                     if (global_timer_ns() - t0 > limit) {
                         if (a.wait_error) atomicExch(a.wait_error, 1);
                         break;
@@ -134,6 +142,11 @@ __global__ void __launch_bounds__(256) grid_update_kernel(const GridArgs a)
                 }
             }
             __syncthreads();
+            if (s_void) {
+                if (a.publish_guard_dst && blockIdx.x == 0 && threadIdx.x == 31)
+                    publish_status(nullptr, nullptr, a.publish_guard_src, a.publish_guard_dst, 31);
+                return;
+            }
         }
     }
     // after the barrier: a guard raised by a peer during this step has landed
@@ -309,6 +322,7 @@ __global__ void wait_step_kernel(const WaitArgs a, const DevGuard guard)
         const unsigned long long t0 = global_timer_ns();
         const unsigned long long limit = (unsigned long long)a.wait_timeout_ms * 1000000ull;
         while (ld_acquire_sys(flag) < a.wait_value) {
+            if (guard.word && ld_acquire_sys(guard.word) < guard.step) break;   // void step (see grid_update_kernel)
             if (global_timer_ns() - t0 > limit) {
                 if (a.wait_error) atomicExch(a.wait_error, 1);
                 break;

@@ -248,46 +248,14 @@ __device__ __forceinline__ void sand_principal(const float *e, const PlasticPara
     for (int k = 0; k < 3; ++k) d[k] = 2.0f * p.mu * e[k] + p.lam * tr;
 }
 
-// Return mapping of the trial elastic deformation (in place), plastic scalar update, and the
-// stress of the projected state.  MAT: 2 snow, 3 sand.
+// Return mapping on the singular values s of the trial elastic deformation: projected values sc,
+// plastic scalar update, principal Kirchhoff stresses d of the projected state.  Elementwise in
+// s, so neither the order nor (for sand, which takes |s|) the sign convention of the
+// decomposition matters.  MAT: 2 snow, 3 sand.
 template <int MAT>
-__device__ __forceinline__ void plastic_project(float *f, float &plastic, const PlasticParams &p, float *tau)
+__device__ __forceinline__ void plastic_return(const float *s, float &plastic, const PlasticParams &p,
+                                               float *sc, float *d)
 {
-    if (MAT == MPM_MAT_SNOW) {
-        // Elastic fast path: when every singular value lies inside the yield interval nothing is
-        // clamped and the projection is the identity.  Gershgorin discs of the symmetric
-        // stretch S = R^T F (R from the Newton polar factor) bound the singular values without
-        // an SVD; the stress is then the fixed-corotated form with hardened moduli.
-        float r[9];
-        const float J = det3(f);
-        if (polar_rotation(f, J, r)) {
-            const float s00 = r[0] * f[0] + r[3] * f[3] + r[6] * f[6];
-            const float s11 = r[1] * f[1] + r[4] * f[4] + r[7] * f[7];
-            const float s22 = r[2] * f[2] + r[5] * f[5] + r[8] * f[8];
-            const float s01 = fabsf(r[0] * f[1] + r[3] * f[4] + r[6] * f[7]);
-            const float s02 = fabsf(r[0] * f[2] + r[3] * f[5] + r[6] * f[8]);
-            const float s12 = fabsf(r[1] * f[2] + r[4] * f[5] + r[7] * f[8]);
-            const float lo = fminf(fminf(s00 - s01 - s02, s11 - s01 - s12), s22 - s02 - s12);
-            const float hi = fmaxf(fmaxf(s00 + s01 + s02, s11 + s01 + s12), s22 + s02 + s12);
-            if (lo >= 1.0f - p.theta_c && hi <= 1.0f + p.theta_s) {
-                plastic = fminf(plastic > 0.1f ? plastic : 0.1f, 10.0f);
-                const float h = expf(p.hardening * (1.0f - plastic));
-                const float two_mu = 2.0f * p.mu * h, diag = p.lam * h * (J - 1.0f) * J;
-#pragma unroll
-                for (int a = 0; a < 3; ++a)
-#pragma unroll
-                    for (int b = 0; b < 3; ++b) {
-                        const float acc = two_mu * ((f[3 * a] - r[3 * a]) * f[3 * b] +
-                                                    (f[3 * a + 1] - r[3 * a + 1]) * f[3 * b + 1] +
-                                                    (f[3 * a + 2] - r[3 * a + 2]) * f[3 * b + 2]);
-                        tau[3 * a + b] = (a == b) ? acc + diag : acc;
-                    }
-                return;
-            }
-        }
-    }
-    float u[9], s[3], v[9], sc[3], d[3];
-    svd3(f, u, s, v);
     if (MAT == MPM_MAT_SNOW) {
         const float num = s[0] * s[1] * s[2];
         float den = 1.0f;
@@ -321,6 +289,115 @@ __device__ __forceinline__ void plastic_project(float *f, float &plastic, const 
         for (int k = 0; k < 3; ++k) sc[k] = expf(e[k]);
         sand_principal(e, p, d);
     }
+}
+
+// General route: Jacobi SVD of F itself (reflections, near-singular states).  Out of line: only
+// states the Newton polar iteration refuses (J <= 0.02) come here.
+template <int MAT>
+__device__ __noinline__ void plastic_project_svd(float *f, float &plastic, const PlasticParams &p, float *tau)
+{
+    float u[9], s[3], v[9], sc[3], d[3];
+    svd3(f, u, s, v);
+    plastic_return<MAT>(s, plastic, p, sc, d);
+    rebuild_from_svd(u, sc, v, f);
+    tau_from_principal(u, d, tau);
+}
+
+// One rotation of the cyclic Jacobi eigen-solver of a symmetric 3x3 matrix (Rutishauser's update:
+// a_pp -= t a_pq, a_qq += t a_pq).  No pivot search and no branch: every lane of the warp walks
+// the same three rotations per sweep; an already negligible a_pq gets the identity (t = 0, which
+// also absorbs the 0/0 of a_pp == a_qq, a_pq == 0).
+template <int P, int Q>
+__device__ __forceinline__ void sym_rotate(float &app, float &aqq, float &apq, float &arp, float &arq,
+                                           float *v, float eps)
+{
+    const float theta = __fdividef(aqq - app, 2.0f * apq);
+    float t = copysignf(__fdividef(1.0f, fabsf(theta) + sqrtf(fmaf(theta, theta, 1.0f))), theta);
+    t = fabsf(apq) > eps ? t : 0.0f;
+    const float c = rsqrtf(fmaf(t, t, 1.0f)), s = t * c;
+    app = fmaf(-t, apq, app);
+    aqq = fmaf(t, apq, aqq);
+    apq = t != 0.0f ? 0.0f : apq;
+    const float rp = arp, rq = arq;
+    arp = c * rp - s * rq;
+    arq = s * rp + c * rq;
+#pragma unroll
+    for (int k = 0; k < 3; ++k) {
+        const float vp = v[3 * k + P], vq = v[3 * k + Q];
+        v[3 * k + P] = c * vp - s * vq;
+        v[3 * k + Q] = s * vp + c * vq;
+    }
+}
+
+// S = V diag(lam) V^T for symmetric S (upper triangle given), V orthogonal, eigenvalues unordered.
+__device__ __forceinline__ void sym_eig3(float a00, float a11, float a22, float a01, float a02, float a12,
+                                         float *lam, float *v)
+{
+    v[0] = 1.f; v[1] = 0.f; v[2] = 0.f; v[3] = 0.f; v[4] = 1.f; v[5] = 0.f; v[6] = 0.f; v[7] = 0.f; v[8] = 1.f;
+    const float scale = fabsf(a00) + fabsf(a11) + fabsf(a22);
+    const float tol = 2e-8f * scale + 1e-37f, eps = 1e-9f * scale + 1e-38f;
+#pragma unroll 1
+    for (int sweep = 0; sweep < 6; ++sweep) {
+        if (fmaxf(fmaxf(fabsf(a01), fabsf(a02)), fabsf(a12)) <= tol) break;
+        sym_rotate<0, 1>(a00, a11, a01, a02, a12, v, eps);
+        sym_rotate<0, 2>(a00, a22, a02, a01, a12, v, eps);
+        sym_rotate<1, 2>(a11, a22, a12, a01, a02, v, eps);
+    }
+    lam[0] = a00; lam[1] = a11; lam[2] = a22;
+}
+
+// Return mapping of the trial elastic deformation (in place), plastic scalar update, and the
+// stress of the projected state.  With the polar factor F = R S at hand (Newton iteration, also
+// what the fixed-corotated stress uses) the SVD is the eigen-decomposition of the symmetric
+// stretch: S = R^T F = V diag(s) V^T, U = R V.  Working on S instead of F^T F does not square the
+// condition number, and S is positive definite, so there is no reflection / sign handling.
+template <int MAT>
+__device__ __forceinline__ void plastic_project(float *f, float &plastic, const PlasticParams &p, float *tau)
+{
+    float r[9];
+    const float J = det3(f);
+    if (!polar_rotation(f, J, r)) {
+        plastic_project_svd<MAT>(f, plastic, p, tau);
+        return;
+    }
+    const float s00 = r[0] * f[0] + r[3] * f[3] + r[6] * f[6];
+    const float s11 = r[1] * f[1] + r[4] * f[4] + r[7] * f[7];
+    const float s22 = r[2] * f[2] + r[5] * f[5] + r[8] * f[8];
+    // S is symmetric up to the residual of the polar iteration: average the two triangles
+    const float s01 = 0.5f * (r[0] * f[1] + r[3] * f[4] + r[6] * f[7] + r[1] * f[0] + r[4] * f[3] + r[7] * f[6]);
+    const float s02 = 0.5f * (r[0] * f[2] + r[3] * f[5] + r[6] * f[8] + r[2] * f[0] + r[5] * f[3] + r[8] * f[6]);
+    const float s12 = 0.5f * (r[1] * f[2] + r[4] * f[5] + r[7] * f[8] + r[2] * f[1] + r[5] * f[4] + r[8] * f[7]);
+    if (MAT == MPM_MAT_SNOW) {
+        // Elastic fast path: when every singular value lies inside the yield interval nothing is
+        // clamped and the projection is the identity.  Gershgorin discs of S bound them without
+        // an eigen-solve; the stress is then the fixed-corotated form with hardened moduli.
+        const float o01 = fabsf(s01), o02 = fabsf(s02), o12 = fabsf(s12);
+        const float lo = fminf(fminf(s00 - o01 - o02, s11 - o01 - o12), s22 - o02 - o12);
+        const float hi = fmaxf(fmaxf(s00 + o01 + o02, s11 + o01 + o12), s22 + o02 + o12);
+        if (lo >= 1.0f - p.theta_c && hi <= 1.0f + p.theta_s) {
+            plastic = fminf(plastic > 0.1f ? plastic : 0.1f, 10.0f);
+            const float h = expf(p.hardening * (1.0f - plastic));
+            const float two_mu = 2.0f * p.mu * h, diag = p.lam * h * (J - 1.0f) * J;
+#pragma unroll
+            for (int a = 0; a < 3; ++a)
+#pragma unroll
+                for (int b = 0; b < 3; ++b) {
+                    const float acc = two_mu * ((f[3 * a] - r[3 * a]) * f[3 * b] +
+                                                (f[3 * a + 1] - r[3 * a + 1]) * f[3 * b + 1] +
+                                                (f[3 * a + 2] - r[3 * a + 2]) * f[3 * b + 2]);
+                    tau[3 * a + b] = (a == b) ? acc + diag : acc;
+                }
+            return;
+        }
+    }
+    float lam[3], v[9], u[9], sc[3], d[3];
+    sym_eig3(s00, s11, s22, s01, s02, s12, lam, v);
+#pragma unroll
+    for (int a = 0; a < 3; ++a)
+#pragma unroll
+        for (int b = 0; b < 3; ++b)
+            u[3 * a + b] = r[3 * a] * v[b] + r[3 * a + 1] * v[3 + b] + r[3 * a + 2] * v[6 + b];
+    plastic_return<MAT>(lam, plastic, p, sc, d);
     rebuild_from_svd(u, sc, v, f);
     tau_from_principal(u, d, tau);
 }

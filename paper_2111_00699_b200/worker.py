@@ -818,9 +818,16 @@ class CudaWorker:
                 enq += n
             if not pending:
                 # rebuild step, first fused step after a rebuild, pending full clear: one plain step
+                # (its gather's status is read after the whole step is enqueued)
                 self._guard = None
-                self._defer = False
-                self.run_step(self._global_step)
+                self._defer, self._unconsumed = True, None
+                try:
+                    self.run_step(self._global_step)
+                finally:
+                    self._defer = False
+                if self._unconsumed is not None:
+                    self._consume(*self._unconsumed)
+                    self._unconsumed = None
                 self._frame_steps += 1
                 self.frame_dts.append(self.dt)
                 enq = self._frame_steps
@@ -873,9 +880,12 @@ class CudaWorker:
             self.flags.rebuild_needed = True
         rebuilt = False
         if self.flags.rebuild_needed:
+            flushed = None
             if self._pending_gather:
-                self._flush_gather()
-            self._rebuild(step, par)
+                # the flush's status block is read at the rebuild's first host sync, not before
+                # its first kernels are enqueued (one device idle gap less per rebuild)
+                flushed = self._flush_gather(defer=True)
+            self._rebuild(step, par, flushed)
             rebuilt = True
         else:
             self._clear(par)
@@ -918,7 +928,7 @@ class CudaWorker:
             return False
         return True
 
-    def _rebuild(self, step, par):
+    def _rebuild(self, step, par, flushed=None):
         """Worker._rebuild (pipeline.py:958-1015) on the device; two host syncs (block count,
         then pblock + group counts) -- the paper's CPU-GPU sync points."""
         lib, st, tb, gr = self.lib, self.store, self.table, self.grid
@@ -952,6 +962,9 @@ class CudaWorker:
                        tb._hvals.ptr, tb._hfirst.ptr, cap, pslot.ptr, flag.ptr, scan.ptr, gidx.ptr,
                        gcodes.ptr, self._sptr(3), self._sptr(4), stream)
             sc = self._read_scalars()
+            if flushed is not None:
+                self._consume(*flushed)      # the gather flushed just before this rebuild
+                flushed = None
             n, bad, n_g, overflow = int(sc[1]), int(sc[2]), int(sc[3]), int(sc[4])
             if bad != _INT_MAX:
                 raise SpatialDomainError(
@@ -1127,14 +1140,19 @@ class CudaWorker:
             finally:
                 self._flushing = False
 
-    def _flush_gather(self):
-        guard, defer = self._guard, self._defer
-        self._guard, self._defer = None, False      # a flush is always read back at once
+    def _flush_gather(self, defer=False):
+        """Complete a pending fused gather.  Its status block is read back at once, or (defer)
+        handed to the caller as (slot, step) to be consumed at its next host sync."""
+        guard, was_defer, unconsumed = self._guard, self._defer, self._unconsumed
+        self._guard, self._defer = None, bool(defer)
+        self._unconsumed = None
         try:
             self._run_g2p(self._global_step)
+            flushed = self._unconsumed
         finally:
-            self._guard, self._defer = guard, defer
+            self._guard, self._defer, self._unconsumed = guard, was_defer, unconsumed
         self._pending_gather = False
+        return flushed
 
     def _run_g2p2g(self, step, par):
         st = self.store
