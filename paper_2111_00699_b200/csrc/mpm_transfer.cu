@@ -60,6 +60,11 @@ struct TransferArgs {
 #endif
 constexpr int TW = MPM_TW;   // warps (groups) per CTA
 
+__device__ __forceinline__ void prefetch_l1(const void *p)
+{
+    asm volatile("prefetch.global.L1 [%0];" ::"l"(p));
+}
+
 __device__ __forceinline__ void red_add_v4(float4 *addr, float a, float b, float c, float d)
 {
     atomicAdd(addr, make_float4(a, b, c, d));   // RED.E.ADD.F32x4 on sm_90+
@@ -382,6 +387,19 @@ __global__ void __launch_bounds__(TW * 32, MPM_MINBLOCKS) transfer_kernel(const 
     uint16_t meta = a.meta[g * 32 + lane];
     float m = gd[CH_MASS * 32];
     float px = gd[(CH_POS + 0) * 32], py = gd[(CH_POS + 1) * 32], pz = gd[(CH_POS + 2) * 32];
+    // the running max |v|^2 is only a filter for the atomicMax at the end of the gather: an early
+    // (possibly stale, never too large) copy saves a dependent trip to L2 there
+    unsigned vmax_seen = 0;
+    if (GATHER && lane == 0) vmax_seen = *((volatile unsigned *)&a.status->vmax2_bits);
+#if MPM_LATE_F
+    if (GATHER) {
+        // the deformation rows are read after the 27-node gather (register budget); asking L1 for
+        // them now makes that read a hit
+#pragma unroll
+        for (int r = 0; r < (MAT == MPM_MAT_FLUID ? 1 : 9); ++r) prefetch_l1(gd + (CH_DEF + r) * 32);
+        if (MAT >= MPM_MAT_SNOW) prefetch_l1(gd + CH_PLASTIC * 32);
+    }
+#endif
     int len;
     int4 org;
     if (a.group_ctx) {
@@ -511,8 +529,7 @@ __global__ void __launch_bounds__(TW * 32, MPM_MINBLOCKS) transfer_kernel(const 
         }
         // max |v|^2 of the warp -> one conditional atomicMax (pipeline.py:576-578)
         vmax_bits = __reduce_max_sync(FULL, vmax_bits);
-        if (lane == 0 && vmax_bits > *((volatile unsigned *)&a.status->vmax2_bits))
-            atomicMax(&a.status->vmax2_bits, vmax_bits);
+        if (lane == 0 && vmax_bits > vmax_seen) atomicMax(&a.status->vmax2_bits, vmax_bits);
     } else if (SCATTER) {
         if (active) {
             vx = gd[(CH_VEL + 0) * 32]; vy = gd[(CH_VEL + 1) * 32]; vz = gd[(CH_VEL + 2) * 32];
