@@ -341,9 +341,9 @@ def run_ours(args):
 
 # dram__bytes_read.sum + dram__bytes_write.sum of the dominant kernel, per launch, from the
 # committed `ncu --set full` capture of the fused kernel on the 1.37 M scene
-# (profiles/r1_g_fused_snow_v3_metrics.csv: 95.7 MB read + 40.4 MB write; r1_g_fused_snow_fc_v3: 89.7 + 39.9);
+# (profiles/r1_i_fused_snow_v4_metrics.csv: 96.4 MB read + 55.7 MB write; r1_i_fused_snow_fc_v4: 89.7 + 39.4);
 # only quoted for those scenes
-TRAFFIC_NCU = {"snow": 136.1e6, "snow_fc": 129.6e6}
+TRAFFIC_NCU = {"snow": 152.1e6, "snow_fc": 129.1e6}
 
 
 def run_fountain(args):
