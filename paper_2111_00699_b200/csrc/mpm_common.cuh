@@ -108,6 +108,49 @@ inline DevGuard make_guard(const mpm_guard *g)
     return d;
 }
 
+// ---- programmatic dependent launch (sm_90+) -------------------------------------------
+// The steady-state step is a chain transfer -> grid update -> transfer -> ... on one stream.  A
+// kernel launched with the programmatic-serialization attribute may have its CTAs resident
+// while the tail of the previous kernel drains; they block in pdl_wait() until that kernel has
+// completed and its writes are visible, so the launch latency between dependent kernels
+// (2-4 us each, two per step) is off the critical path.  Every kernel of the chain calls
+// pdl_wait() before it touches memory (the guard word included) and pdl_launch_dependents()
+// right after it.  Kernels launched the ordinary way are unaffected (full serialisation).
+#ifndef MPM_PDL
+#define MPM_PDL 1
+#endif
+__device__ __forceinline__ void pdl_wait()
+{
+#if MPM_PDL
+    asm volatile("griddepcontrol.wait;" ::: "memory");
+#endif
+}
+__device__ __forceinline__ void pdl_launch_dependents()
+{
+#if MPM_PDL
+    asm volatile("griddepcontrol.launch_dependents;");
+#endif
+}
+template <typename... KArgs, typename... Args>
+inline void launch_chained(void (*kernel)(KArgs...), int grid, int block, cudaStream_t stream, Args &&...args)
+{
+#if MPM_PDL
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3((unsigned)grid);
+    cfg.blockDim = dim3((unsigned)block);
+    cfg.dynamicSmemBytes = 0;
+    cfg.stream = stream;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    cudaLaunchKernelEx(&cfg, kernel, static_cast<KArgs>(args)...);
+#else
+    kernel<<<grid, block, 0, stream>>>(static_cast<KArgs>(args)...);
+#endif
+}
+
 // exclusive scan of int32 (three kernels, no library): out may alias in; total (device) optional
 void exclusive_scan_i32(const int32_t *in, int32_t *out, int32_t n, int32_t *block_sums,
                         int32_t *total, cudaStream_t stream);

@@ -92,6 +92,8 @@ __device__ __forceinline__ unsigned long long global_timer_ns()
 
 __global__ void __launch_bounds__(256) grid_update_kernel(const GridArgs a)
 {
+    pdl_wait();
+    pdl_launch_dependents();
     if (guarded_out(a.guard)) {
         // a skipped step still tells the host where the guard stood
         if (a.publish_guard_dst && blockIdx.x == 0 && threadIdx.x == 31)
@@ -426,7 +428,7 @@ int mpm_grid_update(float *raw, uint8_t *touched, float *vel, float *vel_old,
     a.publish_dst = p->publish_dst;
     a.publish_guard_src = p->publish_guard_src;
     a.publish_guard_dst = p->publish_guard_dst;
-    grid_update_kernel<<<(a.count + 3) / 4, 256, 0, (cudaStream_t)stream>>>(a);
+    launch_chained(grid_update_kernel, (a.count + 3) / 4, 256, (cudaStream_t)stream, a);
     return check_launch("mpm_grid_update", 1);
 }
 

@@ -370,6 +370,8 @@ __device__ __forceinline__ void load_deformation(const float *gd, float *F, floa
 template <int MAT, bool GATHER, bool SCATTER, bool DET>
 __global__ void __launch_bounds__(TW * 32, MPM_MINBLOCKS) transfer_kernel(const TransferArgs a)
 {
+    pdl_wait();
+    pdl_launch_dependents();
     if (guarded_out(a.guard)) return;
     __shared__ int s_nrow[TW][32];
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -684,10 +686,10 @@ static int launch_transfer(const TransferArgs &a, int mat, cudaStream_t stream)
         // fixed-point accumulation exists for the reference's own material kinds
         switch (mat) {
         case MPM_MAT_FLUID:
-            transfer_kernel<MPM_MAT_FLUID, GATHER, SCATTER, true><<<grid, TW * 32, 0, stream>>>(a);
+            launch_chained(transfer_kernel<MPM_MAT_FLUID, GATHER, SCATTER, true>, grid, TW * 32, stream, a);
             return MPM_OK;
         case MPM_MAT_FIXED_COROTATED:
-            transfer_kernel<MPM_MAT_FIXED_COROTATED, GATHER, SCATTER, true><<<grid, TW * 32, 0, stream>>>(a);
+            launch_chained(transfer_kernel<MPM_MAT_FIXED_COROTATED, GATHER, SCATTER, true>, grid, TW * 32, stream, a);
             return MPM_OK;
         default:
             return MPM_ERR_CONFIG;
@@ -695,16 +697,16 @@ static int launch_transfer(const TransferArgs &a, int mat, cudaStream_t stream)
     }
     switch (mat) {
     case MPM_MAT_FLUID:
-        transfer_kernel<MPM_MAT_FLUID, GATHER, SCATTER, false><<<grid, TW * 32, 0, stream>>>(a);
+        launch_chained(transfer_kernel<MPM_MAT_FLUID, GATHER, SCATTER, false>, grid, TW * 32, stream, a);
         break;
     case MPM_MAT_FIXED_COROTATED:
-        transfer_kernel<MPM_MAT_FIXED_COROTATED, GATHER, SCATTER, false><<<grid, TW * 32, 0, stream>>>(a);
+        launch_chained(transfer_kernel<MPM_MAT_FIXED_COROTATED, GATHER, SCATTER, false>, grid, TW * 32, stream, a);
         break;
     case MPM_MAT_SNOW:
-        transfer_kernel<MPM_MAT_SNOW, GATHER, SCATTER, false><<<grid, TW * 32, 0, stream>>>(a);
+        launch_chained(transfer_kernel<MPM_MAT_SNOW, GATHER, SCATTER, false>, grid, TW * 32, stream, a);
         break;
     case MPM_MAT_SAND:
-        transfer_kernel<MPM_MAT_SAND, GATHER, SCATTER, false><<<grid, TW * 32, 0, stream>>>(a);
+        launch_chained(transfer_kernel<MPM_MAT_SAND, GATHER, SCATTER, false>, grid, TW * 32, stream, a);
         break;
     default:
         return MPM_ERR_CONFIG;

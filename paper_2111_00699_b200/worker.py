@@ -799,15 +799,16 @@ class CudaWorker:
                 n = min(self.batch_steps, spf - enq)
                 plan = self._step_plan()
                 tev = None
+                for k in range(2 * n):
+                    plan.time_events[k] = None
                 if self.time_kernels:
+                    # the FIRST step of a batch is timed: an event between two kernels of the chain
+                    # serialises them fully (no programmatic dependent launch across it), so the
+                    # other steps run exactly as they do untimed
                     tev = tbase
-                    for k in range(n):
-                        plan.time_events[2 * k] = self._time_events[2 * (tbase + k)].cuda_event
-                        plan.time_events[2 * k + 1] = self._time_events[2 * (tbase + k) + 1].cuda_event
+                    plan.time_events[0] = self._time_events[2 * tbase].cuda_event
+                    plan.time_events[1] = self._time_events[2 * tbase + 1].cuda_event
                     tbase = (tbase + _BATCH) % (2 * _BATCH)
-                else:
-                    for k in range(2 * n):
-                        plan.time_events[k] = None
                 # the first step of a batch gathers with the dt of the last grid update done
                 plan.transfer.dt_gather = float(self._vel_dt if not pending else self.dt)
                 self.kernel_calls += 1
@@ -838,10 +839,10 @@ class CudaWorker:
                 step = first + k
                 self._slot_clean[step % _RING] = False
                 self._consume(step % _RING, step)
-                if tev is not None:
+                if tev is not None and k == 0:
                     name = "mpm_g2p2g" if self.options.transfer == "g2p2g" else "mpm_p2g"
-                    self.kernel_events.append((name, self._time_events[2 * (tev + k)],
-                                               self._time_events[2 * (tev + k) + 1]))
+                    self.kernel_events.append((name, self._time_events[2 * tev],
+                                               self._time_events[2 * tev + 1]))
                 # step `step` itself ran to completion (the guard only stops LATER steps)
                 self._global_step = step + 1
                 self._vel_dt = self.dt
