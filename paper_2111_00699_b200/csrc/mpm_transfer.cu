@@ -49,6 +49,9 @@ struct TransferArgs {
 #ifndef MPM_LATE_F
 #define MPM_LATE_F 1
 #endif
+#ifndef MPM_PREFETCH_F
+#define MPM_PREFETCH_F 1  // deformation rows asked of L1 in the prologue (they are read after the node gather)
+#endif
 #ifndef MPM_ROLL_J
 #define MPM_ROLL_J 0      // 1: scatter loops rolled over x and y (three nodes per trip)
 #endif
@@ -393,7 +396,7 @@ __global__ void __launch_bounds__(TW * 32, MPM_MINBLOCKS) transfer_kernel(const 
     // (possibly stale, never too large) copy saves a dependent trip to L2 there
     unsigned vmax_seen = 0;
     if (GATHER && lane == 0) vmax_seen = *((volatile unsigned *)&a.status->vmax2_bits);
-#if MPM_LATE_F
+#if MPM_LATE_F && MPM_PREFETCH_F
     if (GATHER) {
         // the deformation rows are read after the 27-node gather (register budget); asking L1 for
         // them now makes that read a hit
