@@ -282,3 +282,57 @@ def test_pinned_tensor_upload_and_zero_copy_readback(rng):
     # same inputs, same kernels; float atomics may reorder sums between two runs
     assert np.allclose(pa, pb, rtol=0, atol=1e-5)
     assert np.allclose(wa.store.data, wb.store.data, rtol=1e-4, atol=1e-4)
+
+
+def test_status_block_published_to_mapped_host_memory():
+    """mpm_status_publish / mpm_host_alias: the read of out_stats after a gather
+    (pipeline.py:1102-1104) is a store to pinned host memory by a kernel, in stream order."""
+    import ctypes as C
+    import torch
+    from paper_2111_00699_b200 import _capi
+    lib = _capi.lib()
+    words = _capi.STATUS_BYTES // 8
+    dev = torch.arange(1, 1 + 2 * words, dtype=torch.int64, device="cuda").reshape(2, words)
+    host = torch.zeros((2, words), dtype=torch.int64).pin_memory()
+    guard = torch.tensor([17], dtype=torch.int32, device="cuda")
+    guard_host = torch.zeros(2, dtype=torch.int32).pin_memory()
+    alias, galias = lib.mpm_host_alias(host.data_ptr()), lib.mpm_host_alias(guard_host.data_ptr())
+    assert alias and galias
+    stream = torch.cuda.current_stream().cuda_stream
+    _capi.check(lib.mpm_status_publish(dev[1].data_ptr(), alias + _capi.STATUS_BYTES, guard.data_ptr(),
+                                       galias + 4, stream))
+    torch.cuda.synchronize()
+    assert host[0].abs().sum() == 0 and torch.equal(host[1], dev[1].cpu())
+    assert guard_host.tolist() == [0, 17]
+    # pageable memory has no device alias; inconsistent arguments are rejected
+    assert not lib.mpm_host_alias(torch.zeros(8).data_ptr())
+    assert lib.mpm_status_publish(None, alias, None, None, stream) == -1
+    assert lib.mpm_status_publish(None, None, None, None, stream) == 0
+
+
+@pytest.mark.parametrize("transfer", ["g2p2g", "split"])
+def test_batched_frames_report_every_step(transfer):
+    """Frames enqueued from C (status stored by the grid update / the publish kernel, kernels
+    chained with programmatic dependent launch) against the same frames stepped one host call
+    at a time: same rebuild steps, same max speed per step, same particles."""
+    from parity_util import block_scene
+    dx = 25.0 / 64.0
+    pos, vel = block_scene(8, 3, dx)
+    kw = dict(params=SimParams(dx=dx, dt=(1 / 48) / 36), boundary=BoundaryBox((8 * dx,) * 3, (40 * dx,) * 3),
+              mass=2.0 * dx ** 3 / 8, transfer=transfer)
+    wa, wb = _mk(pos, vel, **kw), _mk(pos, vel, **kw)
+    wb.pipelined = False
+    vmax = {0: [], 1: []}
+    for k, w in enumerate((wa, wb)):
+        pub = w.runtime.publish_vmax
+        w.runtime.publish_vmax = lambda slot, wid, v, k=k, pub=pub: (vmax[k].append(v), pub(slot, wid, v))[1]
+    for _ in range(2):
+        wa.run_frame()
+        wb.run_frame()
+    assert wa.kernel_calls < wb.kernel_calls          # wa really went through mpm_enqueue_steps
+    assert wa.rebuild_steps == wb.rebuild_steps and len(wa.rebuild_steps) >= 3
+    assert len(vmax[0]) == len(vmax[1])
+    assert np.allclose(vmax[0], vmax[1], rtol=1e-4, atol=1e-6)
+    pa, ia = wa.store.positions_with_ids()
+    pb, ib = wb.store.positions_with_ids()
+    assert np.array_equal(ia, ib) and np.allclose(pa, pb, rtol=0, atol=2e-5)
