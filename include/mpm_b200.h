@@ -132,6 +132,13 @@ unsigned long long mpm_launch_count(void);  /* kernels launched by this library 
 /* device alias of page-locked host memory (cudaHostGetDevicePointer), NULL when it is not mapped:
  * the address kernels store status blocks to (mpm_status_publish, mpm_grid_params.publish_*) */
 void *mpm_host_alias(void *pinned_host);
+/* Map a device allocation exported by another process (64-byte cudaIpcMemHandle_t) into the
+ * current device's context, enabling peer access to the exporting GPU when it is another device
+ * (cudaIpcMemLazyEnablePeerAccess): the rows a worker reads from its peers (pipeline.py:1172-1188)
+ * are then plain device pointers, NVLink loads on an NVSwitch node.  *base_out is the base of the
+ * exporter's allocation; one open per (process, handle). */
+int mpm_ipc_open(const void *handle64, void **base_out);
+int mpm_ipc_close(void *base);
 
 /* ---- rebuild-mapping: Worker._rebuild (pipeline.py:958-1015) ------------------------ */
 

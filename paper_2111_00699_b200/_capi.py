@@ -137,6 +137,8 @@ _SIGNATURES = {
     "mpm_device_arch": [],
     "mpm_launch_count": [],
     "mpm_host_alias": [p_void],
+    "mpm_ipc_open": [C.c_char_p, C.POINTER(p_void)],
+    "mpm_ipc_close": [p_void],
 }
 _RESTYPES = {"mpm_version": C.c_char_p, "mpm_last_error": C.c_char_p,
              "mpm_launch_count": C.c_ulonglong, "mpm_host_alias": C.c_void_p}

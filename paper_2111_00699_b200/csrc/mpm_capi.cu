@@ -57,4 +57,36 @@ void *mpm_host_alias(void *pinned_host)
     return dev;
 }
 
+// Peer memory: a buffer exported by another process (cudaIpcGetMemHandle through torch's
+// storage sharing) is opened in THIS process's current-device context.  With
+// cudaIpcMemLazyEnablePeerAccess the driver enables peer access between the current device and
+// the exporting device, so the mapping is valid for kernels of the current device -- over NVLink
+// when the exporter is another GPU of the node.
+int mpm_ipc_open(const void *handle64, void **base_out)
+{
+    if (!handle64 || !base_out) return MPM_ERR_REJECTED_INPUT;
+    cudaIpcMemHandle_t h;
+    static_assert(sizeof(h) == 64, "CUDA IPC memory handles are 64 bytes");
+    memcpy(&h, handle64, sizeof h);
+    cudaError_t e = cudaIpcOpenMemHandle(base_out, h, cudaIpcMemLazyEnablePeerAccess);
+    if (e != cudaSuccess) {
+        cudaGetLastError();
+        mpm::set_last_error("mpm_ipc_open", e);
+        return MPM_ERR_RESOURCE;
+    }
+    return MPM_OK;
+}
+
+int mpm_ipc_close(void *base)
+{
+    if (!base) return MPM_OK;
+    cudaError_t e = cudaIpcCloseMemHandle(base);
+    if (e != cudaSuccess) {
+        cudaGetLastError();
+        mpm::set_last_error("mpm_ipc_close", e);
+        return MPM_ERR_RESOURCE;
+    }
+    return MPM_OK;
+}
+
 }  // extern "C"

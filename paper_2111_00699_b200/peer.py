@@ -46,7 +46,7 @@ import torch.distributed as dist
 
 from . import _capi
 from .dist import DistRuntime, DistWorker
-from .errors import BarrierTimeoutError, ContractViolationError
+from .errors import BarrierTimeoutError, ContractViolationError, ResourceError
 from .memory import DeviceBuffer
 from .worker import _INT_MAX, _RING, _stream_ptr
 
@@ -63,19 +63,65 @@ class PeerRuntime(DistRuntime):
         self.all_gather_i64([0])
 
     def exchange_tensors(self, named: dict):
-        """Collective.  Returns one dict per rank with tensors aliasing THAT rank's device memory
-        (this rank's own entry holds the tensors passed in)."""
-        from torch.multiprocessing.reductions import reduce_tensor
-        payload = {k: reduce_tensor(t) for k, t in named.items()}
+        """Collective.  Returns one dict per rank of objects with .data_ptr() addressing THAT
+        rank's device memory from this rank's device (this rank's own entry holds the tensors
+        passed in).
+
+        The exporter's side is torch's storage sharing (cudaIpcGetMemHandle of the caching
+        allocator's block + the offset inside it); the importer opens the handle itself
+        (mpm_ipc_open) in ITS OWN device context with lazy peer access.  torch's own rebuild
+        (torch.multiprocessing.reductions) maps the block in a context of the exporting device,
+        which is what a tensor living "on cuda:q" needs, but not what a kernel running on this
+        rank's GPU needs: that takes a mapping (and peer access) in this rank's context."""
+        payload = {}
+        for k, t in named.items():
+            st = t.untyped_storage()
+            _, handle, _, block_offset = st._share_cuda_()[:4]
+            handle = bytes(handle)
+            if len(handle) in (65, 66):
+                # recent caching allocators prefix the 64-byte cudaIpcMemHandle_t with [a version
+                # byte and] a type tag: 'c' = cudaMalloc block; expandable segments ('e') are
+                # shared as file descriptors
+                if handle[-65:-64] != b"c":
+                    raise ResourceError("peer-mapped halo rows need cudaMalloc-backed torch blocks "
+                                        "(PYTORCH_CUDA_ALLOC_CONF=expandable_segments must be off)")
+                handle = handle[-64:]
+            if len(handle) != 64:
+                raise ResourceError(f"unexpected CUDA IPC handle of {len(handle)} bytes")
+            payload[k] = (handle, int(block_offset) + t.storage_offset() * t.element_size(),
+                          t.numel() * t.element_size())
         gathered = [None] * self.n_workers
         dist.all_gather_object(gathered, payload, group=self.group)
+        lib = _capi.lib()
         out = []
         for q, pl in enumerate(gathered):
             if q == self.wid:
                 out.append(dict(named))
-            else:
-                out.append({k: fn(*args) for k, (fn, args) in pl.items()})
+                continue
+            mem = {}
+            for k, (handle, offset, nbytes) in pl.items():
+                base = self._ipc_open.get((q, handle))
+                if base is None:
+                    ptr = C.c_void_p()
+                    _capi.check(lib.mpm_ipc_open(handle, C.byref(ptr)), "mpm_ipc_open")
+                    base = self._ipc_open[(q, handle)] = int(ptr.value)
+                mem[k] = MappedMemory(base + offset, nbytes)
+            out.append(mem)
         return out
+
+    _ipc_open: dict = {}     # (rank, handle) -> base address in this process; process-wide, never closed
+                             # while the group lives (the exporter's caching allocator keeps its blocks)
+
+
+class MappedMemory:
+    """A peer's buffer as seen from this rank's device."""
+    __slots__ = ("ptr", "nbytes")
+
+    def __init__(self, ptr: int, nbytes: int):
+        self.ptr, self.nbytes = int(ptr), int(nbytes)
+
+    def data_ptr(self) -> int:
+        return self.ptr
 
 
 class PeerDistWorker(DistWorker):

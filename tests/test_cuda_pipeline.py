@@ -326,11 +326,12 @@ def test_batched_frames_report_every_step(transfer):
     for k, w in enumerate((wa, wb)):
         pub = w.runtime.publish_vmax
         w.runtime.publish_vmax = lambda slot, wid, v, k=k, pub=pub: (vmax[k].append(v), pub(slot, wid, v))[1]
-    for _ in range(2):
+    for _ in range(3):
         wa.run_frame()
         wb.run_frame()
     assert wa.kernel_calls < wb.kernel_calls          # wa really went through mpm_enqueue_steps
-    assert wa.rebuild_steps == wb.rebuild_steps and len(wa.rebuild_steps) >= 3
+    assert wa.rebuild_steps == wb.rebuild_steps, (wa.rebuild_steps, wb.rebuild_steps)
+    assert len(wa.rebuild_steps) >= 3, wa.rebuild_steps
     assert len(vmax[0]) == len(vmax[1])
     assert np.allclose(vmax[0], vmax[1], rtol=1e-4, atol=1e-6)
     pa, ia = wa.store.positions_with_ids()
