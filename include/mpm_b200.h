@@ -50,7 +50,8 @@ enum mpm_status {
     MPM_ERR_MODE_CONFLICT = -5,      /* ModeConflictError    */
     MPM_ERR_DEGENERATE = -6,         /* DegenerateStateError */
     MPM_ERR_CONFIG = -7,             /* ConfigError          */
-    MPM_ERR_BARRIER_TIMEOUT = -8     /* BarrierTimeoutError  */
+    MPM_ERR_BARRIER_TIMEOUT = -8,    /* BarrierTimeoutError  */
+    MPM_NEED_CAPACITY = 1            /* mpm_rebuild: a caller-owned buffer is too small (not an error) */
 };
 
 enum mpm_material_kind {             /* domain.py:26-28 (+ two plastic kinds) */
@@ -201,6 +202,57 @@ int mpm_scatter_sorted(const mpm_store_view *old_store, const int32_t *src_slot,
                        const int32_t *bin_start, const int32_t *block_group_first, int32_t n_gblocks,
                        const int32_t *table_origin, double dx, const mpm_store_view *new_store,
                        void *stream);
+
+/* Worker._rebuild (pipeline.py:958-1015) in one call: compact_live -> particle_codes ->
+ * hash_insert_blocks -> [host sync: block count] -> dilate_and_link -> sort_and_group -> [host
+ * sync: pblock and group counts] -> scatter_sorted -> build_group_ctx -> vel rows zeroed, raw
+ * rows of this parity cleared.  Same kernels, same results as the separate calls; what it
+ * removes is the interpreter between them (the device idles while the host prepares the next
+ * call after each sync).  Every buffer is the caller's and is described with its capacity; when
+ * a count outgrows one the call returns MPM_NEED_CAPACITY with the sizes it needs in the result
+ * (the old store has not been touched) and the caller grows the buffers and calls again.
+ * MPM_ERR_SPATIAL_DOMAIN: result.bad_particle / result.bad_block say which (particles.py:54-57,
+ * grid.py:372-377). */
+typedef struct mpm_rebuild_plan {
+    mpm_store_view old_store;          /* current store (read only) */
+    mpm_store_view new_store;          /* other half of the double buffer, room for cap_groups groups */
+    int32_t cap_groups;
+    int32_t n_staged;                  /* staged appends: flat [n_staged][nch] + ids, or 0 */
+    const float *staged;
+    const int64_t *staged_ids;
+    int32_t n_upper;                   /* particles of the old store + n_staged */
+    int32_t cap_gblocks;               /* bounds neighbor [*][27], qslot 27x, qflag 54x, bin_start 64x + 1, bgf + 1 */
+    double dx;
+    /* scratch (ScratchPool, memory.py:72-114) */
+    int32_t *glive;                    /* old n_groups + 1 */
+    int32_t *src_slot, *pslot, *flag, *gidx, *tmp_perm, *perm;   /* n_upper each */
+    int64_t *codes, *gcodes;           /* n_upper each */
+    int32_t *scan;                     /* n_upper / 16 + 1024 */
+    int32_t *qslot, *qflag, *bin_start, *bgf;
+    /* block table (BlockTable, grid.py:325-386) */
+    int64_t *hkeys;
+    int32_t *hvals, *hfirst;
+    int32_t hash_cap;                  /* power of two; load factor kept below 1/8 */
+    int32_t cap_table;                 /* capacity of table_codes / table_origin (>= 27 n_gblocks needed) */
+    int64_t *table_codes;
+    int32_t *table_origin;
+    int32_t *table_neighbor;
+    /* nodal buffers reset by the rebuild (pipeline.py:996-1006) */
+    float *vel;                        /* [cap_nodes][64] float4 */
+    float *raw_par;                    /* rows of this step's parity, node_bytes per node */
+    uint8_t *touched_par;
+    int32_t cap_nodes;
+    int32_t node_bytes;                /* 16, or 32 in deterministic mode */
+    int32_t *scalars_dev;              /* 16 device words */
+    int32_t *scalars_host;             /* 16 pinned host words */
+} mpm_rebuild_plan;
+typedef struct mpm_rebuild_result {
+    int32_t n, n_gblocks, count, n_groups;
+    int32_t bad_particle, bad_block;   /* INT32_MAX = none */
+    int32_t need_hash, need_gblocks, need_table, need_groups, need_nodes;   /* 0 = fits */
+    int32_t reserved;
+} mpm_rebuild_result;
+int mpm_rebuild(const mpm_rebuild_plan *plan, mpm_rebuild_result *result, void *stream);
 
 /* ---- substep: Worker.run_step (pipeline.py:905-940) ---------------------------------
  *

@@ -92,6 +92,28 @@ class StepPlan(C.Structure):
     ]
 
 
+class RebuildPlan(C.Structure):
+    _fields_ = [
+        ("old_store", StoreView), ("new_store", StoreView), ("cap_groups", i32), ("n_staged", i32),
+        ("staged", p_void), ("staged_ids", p_void), ("n_upper", i32), ("cap_gblocks", i32), ("dx", f64),
+        ("glive", p_void), ("src_slot", p_void), ("pslot", p_void), ("flag", p_void), ("gidx", p_void),
+        ("tmp_perm", p_void), ("perm", p_void), ("codes", p_void), ("gcodes", p_void), ("scan", p_void),
+        ("qslot", p_void), ("qflag", p_void), ("bin_start", p_void), ("bgf", p_void),
+        ("hkeys", p_void), ("hvals", p_void), ("hfirst", p_void), ("hash_cap", i32), ("cap_table", i32),
+        ("table_codes", p_void), ("table_origin", p_void), ("table_neighbor", p_void),
+        ("vel", p_void), ("raw_par", p_void), ("touched_par", p_void), ("cap_nodes", i32),
+        ("node_bytes", i32), ("scalars_dev", p_void), ("scalars_host", p_void),
+    ]
+
+
+class RebuildResult(C.Structure):
+    _fields_ = [(k, i32) for k in ("n", "n_gblocks", "count", "n_groups", "bad_particle", "bad_block",
+                                   "need_hash", "need_gblocks", "need_table", "need_groups",
+                                   "need_nodes", "reserved")]
+
+
+NEED_CAPACITY = 1
+
 _STATUS_TO_ERROR = {
     -1: E.RejectedInputError, -2: E.SpatialDomainError, -3: E.ResourceError,
     -4: E.ContractViolationError, -5: E.ModeConflictError, -6: E.DegenerateStateError,
@@ -112,6 +134,7 @@ _SIGNATURES = {
     "mpm_scatter_sorted": [C.POINTER(StoreView), p_void, p_void, p_void, p_void, p_void, p_void,
                            p_void, i32, p_void, f64, C.POINTER(StoreView), p_void],
     "mpm_build_group_ctx": [C.POINTER(StoreView), C.POINTER(TableView), p_void],
+    "mpm_rebuild": [C.POINTER(RebuildPlan), C.POINTER(RebuildResult), p_void],
     "mpm_clear": [p_void, p_void, i32, i32, i32, C.POINTER(Guard), p_void],
     "mpm_status_reset": [p_void, C.POINTER(Guard), p_void],
     "mpm_status_publish": [p_void, p_void, p_void, p_void, p_void],

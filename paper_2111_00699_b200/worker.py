@@ -930,120 +930,112 @@ class CudaWorker:
         return True
 
     def _rebuild(self, step, par, flushed=None):
-        """Worker._rebuild (pipeline.py:958-1015) on the device; two host syncs (block count,
-        then pblock + group counts) -- the paper's CPU-GPU sync points."""
+        """Worker._rebuild (pipeline.py:958-1015) on the device: one call (mpm_rebuild) that issues
+        every rebuild kernel and takes the two host syncs of the paper's rebuild (block count,
+        then pblock + group counts) in C.  Buffers stay Python's: they are sized
+        here from the counts of the previous rebuild (4x growth rule, so a steady state never
+        reallocates) and the call reports what it needs when a count outgrew one."""
         lib, st, tb, gr = self.lib, self.store, self.table, self.grid
         stream = _stream_ptr()
         t_rebuild = time.perf_counter()
         staged, staged_ids, n_staged = st.take_staged()
         n_upper = st.count + n_staged
-        old = st.view()
-        S = self._scratch_i32
-        src_slot = S("src_slot", n_upper)
-        scan = S("scan", n_upper // 16 + 1024)   # block sums of the largest scan (n_g*64+1 bins)
-        codes = self._scratch_i64("codes", n_upper)
-        # scalars: 0 n_live, 1 n_total, 2 bad_index, 3 n_gblocks, 4 overflow, 5 count, 6 bad_block,
-        #          7 n_groups
-        glive = S("glive", st.n_groups + 1)
-        self._call("mpm_compact_live", C.byref(old), 1, glive.ptr, src_slot.ptr, self._sptr(0),
-                   scan.ptr, stream)
-        self._call("mpm_particle_codes", C.byref(old), src_slot.ptr, self._sptr(0),
-                   staged.data_ptr() if n_staged else None, n_staged, n_upper, float(self.params.dx),
-                   codes.ptr, self._sptr(1), self._sptr(2), stream)
-        pslot, flag, gidx = S("pslot", n_upper), S("flag", n_upper), S("gidx", n_upper)
-        gcodes = self._scratch_i64("gcodes", n_upper)
+        S, S64 = self._scratch_i32, self._scratch_i64
+        nxt = 1 - st.cur
+        new_bufs = [b[nxt] for b in (st._data, st._orig_id, st._lane_meta, st._group_len, st._group_block,
+                                     st._group_start, st._group_ctx)]
+        # requests: the counts of the last rebuild (a first guess for the very first one)
+        want_g = max(tb.n_gblocks, 1)
+        want_groups = max(st.n_groups, n_upper // 32 + 1)
+        want_nodes = max(tb.count, 1)
         # hash capacity: load factor < 1/8 against the pblock count seen last time, or a
-        # conservative first guess; an overflow doubles it and retries
+        # conservative first guess; an overflow quadruples it and retries
         cap = max(tb.hash_cap, _pow2_at_least(8 * max(tb.count, 1)), 1 << 12)
         if tb.count == 0:
             cap = max(cap, _pow2_at_least(max(n_upper // 2, 1)))
+        plan, res = _capi.RebuildPlan(), _capi.RebuildResult()
+        plan.old_store = st.view()
+        plan.n_staged, plan.n_upper = n_staged, n_upper
+        plan.staged = staged.data_ptr() if n_staged else None
+        plan.staged_ids = staged_ids.data_ptr() if n_staged else None
+        plan.dx = float(self.params.dx)
+        plan.glive = S("glive", st.n_groups + 1).ptr
+        for tag in ("src_slot", "pslot", "flag", "gidx", "tmp_perm", "perm"):
+            setattr(plan, tag, S(tag, n_upper).ptr)
+        plan.codes, plan.gcodes = S64("codes", n_upper).ptr, S64("gcodes", n_upper).ptr
+        plan.scan = S("scan", n_upper // 16 + 1024).ptr      # block sums of the largest scan
+        plan.node_bytes = self._node_bytes
+        plan.scalars_dev, plan.scalars_host = self._scalars.data_ptr(), self._scalars_host.data_ptr()
         while True:
+            # block-indexed scratch and tables; codes/origin/touched sized for the worst case of the
+            # dilation, 27 n_g (they are small)
+            qslot, qflag = S("qslot", 27 * want_g), S("qflag", 2 * 27 * want_g)
+            bin_start, bgf = S("bin_start", want_g * 64 + 1), S("bgf", want_g + 1)
             tb.ensure_hash(cap)
-            self._call("mpm_hash_insert_blocks", codes.ptr, self._sptr(1), n_upper, tb._hkeys.ptr,
-                       tb._hvals.ptr, tb._hfirst.ptr, cap, pslot.ptr, flag.ptr, scan.ptr, gidx.ptr,
-                       gcodes.ptr, self._sptr(3), self._sptr(4), stream)
-            sc = self._read_scalars()
+            tb._codes.ensure_capacity(27 * want_g, keep=False)
+            tb._origin.ensure_capacity(27 * want_g, keep=False)
+            tb._neighbor.ensure_capacity(want_g, keep=False)
+            for k in (0, 1):
+                tb._touched[k].len = min(tb._touched[k].len, tb.count)
+                tb._touched[k].ensure_capacity(27 * want_g, keep=True)
+            for buf in new_bufs:
+                buf.ensure_capacity(want_groups, keep=False)
+            gr._vel.ensure_capacity(want_nodes, keep=False)
+            gr._raw[par].ensure_capacity(want_nodes, keep=False)
+            plan.qslot, plan.qflag, plan.bin_start, plan.bgf = qslot.ptr, qflag.ptr, bin_start.ptr, bgf.ptr
+            plan.cap_gblocks = min(tb._neighbor.capacity, qslot.capacity // 27, qflag.capacity // 54,
+                                   (bin_start.capacity - 1) // 64, bgf.capacity - 1)
+            plan.hkeys, plan.hvals, plan.hfirst = tb._hkeys.ptr, tb._hvals.ptr, tb._hfirst.ptr
+            plan.hash_cap = cap
+            plan.cap_table = min(tb._codes.capacity, tb._origin.capacity, tb._touched[0].capacity,
+                                 tb._touched[1].capacity)
+            plan.table_codes, plan.table_origin = tb._codes.ptr, tb._origin.ptr
+            plan.table_neighbor = tb._neighbor.ptr
+            plan.new_store = StoreView(*(b.ptr for b in new_bufs[:6]), 0, st.nch, new_bufs[6].ptr)
+            plan.cap_groups = min(b.capacity for b in new_bufs)
+            plan.vel, plan.raw_par = gr._vel.ptr, gr._raw[par].ptr
+            plan.touched_par = tb._touched[par].ptr
+            plan.cap_nodes = min(gr._vel.capacity, gr._raw[par].capacity)
+            self.kernel_calls += 1
+            rc = lib.mpm_rebuild(C.byref(plan), C.byref(res), stream)
             if flushed is not None:
                 self._consume(*flushed)      # the gather flushed just before this rebuild
                 flushed = None
-            n, bad, n_g, overflow = int(sc[1]), int(sc[2]), int(sc[3]), int(sc[4])
-            if bad != _INT_MAX:
+            if rc == _capi.NEED_CAPACITY:
+                if res.need_hash:
+                    cap *= 4
+                want_g = max(want_g, res.need_gblocks, (res.need_table + 26) // 27)
+                want_groups = max(want_groups, res.need_groups)
+                want_nodes = max(want_nodes, res.need_nodes)
+                continue
+            if rc == -2 and res.bad_particle != _INT_MAX:
                 raise SpatialDomainError(
-                    f"worker {self.wid}: particle {bad} of the rebuild input lies outside the "
-                    f"encodable domain [0, 2^21) cells")
-            if not overflow and 8 * n_g <= cap:
-                break
-            cap *= 4
-        # 27-dilation; codes/origin/touched sized for the worst case 27 n_g (they are small)
-        pcap = max(27 * n_g, 1)
-        tb._codes.ensure_capacity(pcap, keep=False)
-        tb._origin.ensure_capacity(pcap, keep=False)
-        tb._neighbor.ensure_capacity(max(n_g, 1), keep=False)
-        for k in (0, 1):
-            tb._touched[k].len = min(tb._touched[k].len, tb.count)
-            tb._touched[k].ensure_capacity(pcap, keep=True)
-        qslot, qflag = S("qslot", 27 * n_g), S("qflag", 2 * 27 * n_g)
-        pcap_eff = min(tb._codes.capacity, tb._origin.capacity)
-        while True:
-            self._call("mpm_dilate_and_link", gcodes.ptr, n_g, tb._hkeys.ptr, tb._hvals.ptr,
-                       tb._hfirst.ptr, cap, qslot.ptr, qflag.ptr, scan.ptr, tb._codes.ptr,
-                       tb._origin.ptr, tb._neighbor.ptr, pcap_eff, self._sptr(5), self._sptr(6),
-                       self._sptr(4), stream)
-            bin_start = S("bin_start", n_g * 64 + 1)
-            tmp_perm, perm = S("tmp_perm", n_upper), S("perm", n_upper)
-            bgf = S("bgf", n_g + 1)
-            self._call("mpm_sort_and_group", codes.ptr, gidx.ptr, self._sptr(1), n_upper, n_g,
-                       bin_start.ptr, tmp_perm.ptr, perm.ptr, bgf.ptr, scan.ptr, self._sptr(7),
-                       stream)
-            sc = self._read_scalars()
-            overflow, count, bad_block, G = int(sc[4]), int(sc[5]), int(sc[6]), int(sc[7])
-            if bad_block != _INT_MAX:
-                code = int(gcodes.data[bad_block].item())
+                    f"worker {self.wid}: particle {res.bad_particle} of the rebuild input lies outside "
+                    f"the encodable domain [0, 2^21) cells")
+            if rc == -2 and res.bad_block != _INT_MAX:
+                code = int(self._scratch["gcodes"].data[res.bad_block].item())
                 x, y, z = _decode(code)
                 raise SpatialDomainError(
                     f"block ({x - CELL_BIAS // 4}, {y - CELL_BIAS // 4}, {z - CELL_BIAS // 4}) "
                     f"touches the domain boundary; scenes must leave a one-block margin")
-            if overflow != 1:
-                break
-            # hash too small for the halo: rebuild the gblock part in a larger table
-            cap *= 4
-            tb.ensure_hash(cap)
-            self._call("mpm_hash_insert_blocks", codes.ptr, self._sptr(1), n_upper, tb._hkeys.ptr,
-                       tb._hvals.ptr, tb._hfirst.ptr, cap, pslot.ptr, flag.ptr, scan.ptr, gidx.ptr,
-                       gcodes.ptr, self._sptr(3), self._sptr(4), stream)
-        tb.n_gblocks, prev_count, tb.count = n_g, tb.count, count
+            check(rc, "mpm_rebuild")
+            break
+        n, n_g, count, G = res.n, res.n_gblocks, res.count, res.n_groups
+        tb.n_gblocks, tb.count = n_g, count
         tb._codes.len = tb._origin.len = count
         tb._neighbor.len = n_g
-        # new particle store (other half of the double buffer)
-        nxt = 1 - st.cur
-        for bufs in (st._data, st._orig_id, st._lane_meta, st._group_len, st._group_block,
-                     st._group_start, st._group_ctx):
-            bufs[nxt].resize(G, keep=False)
-        new = StoreView(st._data[nxt].ptr, st._orig_id[nxt].ptr, st._lane_meta[nxt].ptr,
-                        st._group_len[nxt].ptr, st._group_block[nxt].ptr, st._group_start[nxt].ptr,
-                        G, st.nch, st._group_ctx[nxt].ptr)
-        self._call("mpm_scatter_sorted", C.byref(old), src_slot.ptr, self._sptr(0),
-                   staged.data_ptr() if n_staged else None,
-                   staged_ids.data_ptr() if n_staged else None, perm.ptr, bin_start.ptr, bgf.ptr,
-                   n_g, tb._origin.ptr, float(self.params.dx), C.byref(new), stream)
+        for buf in new_bufs:
+            buf.len = G
         st.cur, st.n_groups, st.count = nxt, G, n
-        if G:
-            tv = tb.view()
-            self._call("mpm_build_group_ctx", C.byref(new), C.byref(tv), stream)
-        self.last_perm = perm.data[:n]
-        self.last_gidx = gidx.data[:n]
-        # nodal buffers (pipeline.py:996-1006): vel and raw[par] start from zero; the other
+        self.last_perm = self._scratch["perm"].data[:n]
+        self.last_gidx = self._scratch["gidx"].data[:n]
+        # nodal buffers (pipeline.py:996-1006): vel and raw[par] were zeroed by the call; the other
         # parity keeps whatever it held and is cleared in full at its next use
-        gr._vel.resize(count, keep=False)
-        gr._raw[par].resize(count, keep=False)
+        gr._vel.len = gr._raw[par].len = count
         gr._raw[1 - par].resize(count, keep=False)
         if gr._vel_old is not None:
             gr._vel_old.resize(count, keep=False)
         gr.count = count
-        gr._vel.data[:count].zero_()
-        if count:
-            self._call("mpm_clear", gr._raw[par].ptr, tb._touched[par].ptr, count, 1, self._node_bytes,
-                       None, stream)
         for k in (0, 1):
             tb._touched[k].len = count
         self._pending_full_clear_parity = 1 - par
