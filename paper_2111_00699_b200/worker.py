@@ -476,6 +476,7 @@ class CudaWorker:
             # (mpm_status_publish / the grid update), not copied -- a kernel -> copy -> kernel chain
             # idles the device for a copy-engine round trip per step
             self._status_alias = self.lib.mpm_host_alias(self._status_host.data_ptr())
+            self._status_views = None
             self._status_events = [torch.cuda.Event() for _ in range(_RING)]
             self._time_events = [torch.cuda.Event(enable_timing=True) for _ in range(2 * _BATCH * 2)]
             for ev in self._status_events + self._time_events:
@@ -1165,15 +1166,19 @@ class CudaWorker:
         max speed -> vmax ring (pipeline.py:1102-1104), addressing counter -> exception
         (pipeline.py:1233-1238)."""
         self._status_events[slot].synchronize()
-        raw = self._status_host[slot].numpy()
-        head = raw[:1].view(np.uint32)
-        if head[0]:
+        views = self._status_views
+        if views is None:
+            # numpy views of the pinned ring, made once: this runs for every substep
+            raw = self._status_host.numpy()
+            views = self._status_views = (raw, raw.view(np.uint32), raw.view(np.float32))
+        raw, u32, f32 = views
+        if u32[slot, 0]:
             self.flags.rebuild_needed = True
-        vmax2 = float(head[1:2].view(np.float32)[0])
+        vmax2 = float(f32[slot, 1])
         self.runtime.publish_vmax(step % 3, self.wid, math.sqrt(max(vmax2, 0.0)))
-        if raw[1 + C_ADDRESS_ERR]:
+        if raw[slot, 1 + C_ADDRESS_ERR]:
             raise ContractViolationError(
-                f"worker {self.wid}: {int(raw[1 + C_ADDRESS_ERR])} stencil accesses left the "
+                f"worker {self.wid}: {int(raw[slot, 1 + C_ADDRESS_ERR])} stencil accesses left the "
                 f"27-neighbor pblock set")
 
     def _check_addressing(self):
