@@ -141,6 +141,16 @@ void *mpm_host_alias(void *pinned_host);
 int mpm_ipc_open(const void *handle64, void **base_out);
 int mpm_ipc_close(void *base);
 
+/* Host rendezvous of the ranks of ONE node over a shared-memory segment mapped by the caller
+ * (zero-filled, >= mpm_shm_bytes(n_ranks) long): the SpinBarrier + shared Python state of the
+ * reference's SharedRuntime (multiworker.py:27-107) for one process per GPU.  Every rank passes
+ * n_values (<= MPM_SHM_MAX_VALUES) integers and receives out[n_ranks][n_values]; the call is a
+ * full barrier.  MPM_ERR_BARRIER_TIMEOUT after timeout_ms (multiworker.py:66-69). */
+#define MPM_SHM_MAX_VALUES 15
+int64_t mpm_shm_bytes(int32_t n_ranks);
+int mpm_shm_allgather_i64(void *base, int32_t n_ranks, int32_t rank, const int64_t *values, int32_t n_values,
+                          int64_t *out, int32_t timeout_ms);
+
 /* ---- rebuild-mapping: Worker._rebuild (pipeline.py:958-1015) ------------------------ */
 
 /* Compaction of the live lanes of the old store into rebuild input order

@@ -113,6 +113,7 @@ class RebuildResult(C.Structure):
 
 
 NEED_CAPACITY = 1
+SHM_MAX_VALUES = 15
 
 _STATUS_TO_ERROR = {
     -1: E.RejectedInputError, -2: E.SpatialDomainError, -3: E.ResourceError,
@@ -162,9 +163,11 @@ _SIGNATURES = {
     "mpm_host_alias": [p_void],
     "mpm_ipc_open": [C.c_char_p, C.POINTER(p_void)],
     "mpm_ipc_close": [p_void],
+    "mpm_shm_bytes": [i32],
+    "mpm_shm_allgather_i64": [p_void, i32, i32, p_void, i32, p_void, i32],
 }
 _RESTYPES = {"mpm_version": C.c_char_p, "mpm_last_error": C.c_char_p,
-             "mpm_launch_count": C.c_ulonglong, "mpm_host_alias": C.c_void_p}
+             "mpm_launch_count": C.c_ulonglong, "mpm_host_alias": C.c_void_p, "mpm_shm_bytes": C.c_int64}
 
 EXPORTED_SYMBOLS = tuple(_SIGNATURES)
 

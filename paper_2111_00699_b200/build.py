@@ -13,7 +13,7 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 CSRC = os.path.join(HERE, "csrc")
 OUT = os.path.join(HERE, "libmpm_b200.so")
 SOURCES = ["mpm_capi.cu", "mpm_rebuild.cu", "mpm_rebuild_plan.cu", "mpm_grid.cu", "mpm_transfer.cu",
-           "mpm_steps.cu"]
+           "mpm_steps.cu", "mpm_shm.cu"]
 HEADERS = ["mpm_common.cuh", "mpm_math.cuh", os.path.join("..", "..", "include", "mpm_b200.h")]
 NVCC_FLAGS = ["-gencode", "arch=compute_100a,code=sm_100a", "-O3", "-lineinfo", "-std=c++17",
               "-Xcompiler", "-fPIC"]

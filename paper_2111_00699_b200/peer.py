@@ -59,6 +59,57 @@ SKIPPED, DONE, RAISED = 0, 1, 2
 class PeerRuntime(DistRuntime):
     """DistRuntime + mapping of the other ranks' device buffers into this process."""
 
+    def __init__(self, device, initial_vmax: float = 0.0, group=None, host_timeout_ms: int = 120000):
+        super().__init__(device, initial_vmax, group)
+        self.host_timeout_ms = int(host_timeout_ms)
+        self._shm = self._shm_base = None
+        self._setup_shm()
+
+    def _setup_shm(self):
+        """Map one zero-filled segment under /dev/shm into every rank (all ranks of a PeerRuntime
+        share a host: they map each other's device memory).  Rank 0 creates the file and unlinks
+        it once everybody has it open, so nothing outlives the processes.  Without /dev/shm the
+        small collectives stay on torch.distributed."""
+        import mmap
+        import os
+        import uuid
+        lib = _capi.lib()
+        size = int(lib.mpm_shm_bytes(self.n_workers))
+        path = [None]
+        if self.wid == 0 and os.path.isdir("/dev/shm"):
+            path[0] = f"/dev/shm/mpm_b200_{os.getpid()}_{uuid.uuid4().hex}"
+            with open(path[0], "wb") as f:
+                f.truncate(size)
+        dist.broadcast_object_list(path, src=0, group=self.group)
+        mm = None
+        if path[0] is not None:
+            try:
+                fd = os.open(path[0], os.O_RDWR)
+                try:
+                    mm = mmap.mmap(fd, size)
+                finally:
+                    os.close(fd)
+            except OSError:
+                mm = None
+        ok = super().all_gather_i64([int(mm is not None)])[:, 0].all()     # also: everybody has it open
+        if self.wid == 0 and path[0] is not None:
+            os.unlink(path[0])
+        if ok:
+            self._shm = mm
+            self._shm_base = C.addressof(C.c_char.from_buffer(mm))
+
+    def all_gather_i64(self, values) -> np.ndarray:
+        """[n_workers, len(values)] on the host, through the shared segment (a full barrier)."""
+        if self._shm_base is None or len(values) > _capi.SHM_MAX_VALUES:
+            return super().all_gather_i64(values)
+        n = len(values)
+        mine = (C.c_int64 * max(n, 1))(*[int(v) for v in values])
+        out = np.empty((self.n_workers, n), dtype=np.int64)
+        _capi.check(_capi.lib().mpm_shm_allgather_i64(self._shm_base, self.n_workers, self.wid, mine, n,
+                                                      out.ctypes.data, self.host_timeout_ms),
+                    "mpm_shm_allgather_i64")
+        return out
+
     def host_barrier(self):
         self.all_gather_i64([0])
 
@@ -152,7 +203,7 @@ class PeerDistWorker(DistWorker):
         gr, tb = self.grid, self.table
         named = {"raw0": gr._raw[0].data, "raw1": gr._raw[1].data,
                  "touched0": tb._touched[0].data, "touched1": tb._touched[1].data,
-                 "mailbox": self._mailbox}
+                 "codes": tb._codes.data, "mailbox": self._mailbox}
         # a rank without blocks has nothing to map; peers never dereference its rows (count 0)
         return {k: (t if t.numel() else self._mailbox) for k, t in named.items()}
 
@@ -197,8 +248,9 @@ class PeerDistWorker(DistWorker):
         self._peer_counts = list(counts)
         if not any_rebuilt:
             return
-        mine = tb._codes.data[:tb.count]
-        lists = rt.all_gather_codes(mine, counts)
+        # The peers' block-code lists are read where they lie (their tables are mapped like their
+        # rows): every rank has passed the second host sync of its rebuild before it reached the
+        # step_info exchange above, so the lists are complete in memory.
         stream = _stream_ptr()
         for q in range(rt.n_workers):
             if q == rt.wid:
@@ -210,8 +262,7 @@ class PeerDistWorker(DistWorker):
             if m is None:
                 m = self._peer_map[q] = DeviceBuffer(torch.int32, (), self.device)
             m.resize(tb.count, keep=False)
-            codes_q = lists[q].contiguous()
-            self._call("mpm_tag_shared", codes_q.data_ptr(), int(counts[q]), tb._hkeys.ptr,
+            self._call("mpm_tag_shared", self._peer_mem[q]["codes"].data_ptr(), int(counts[q]), tb._hkeys.ptr,
                        tb._hvals.ptr, tb.hash_cap, m.ptr, tb.count, stream)
 
     def _fill_peers(self, gp, par=None, plan=None):

@@ -189,3 +189,52 @@ def test_oracle_populations_meet_on_the_grid():
     t = 30 * W.params.dt
     snow_pz = co.workers[0].store.total_momentum()[2]
     assert snow_pz < 1.2 * (-981.0 * t) * m0[0]      # pushed by the sand, not only by gravity
+
+
+def _shm_rank(path, n_ranks, rank, rounds, queue):
+    import ctypes as C
+    import mmap
+    import numpy as np
+    from paper_2111_00699_b200 import _capi
+    lib = _capi.lib()
+    with open(path, "r+b") as f:
+        mm = mmap.mmap(f.fileno(), int(lib.mpm_shm_bytes(n_ranks)))
+    base = C.addressof(C.c_char.from_buffer(mm))
+    ok = True
+    for r in range(rounds):
+        vals = (C.c_int64 * 3)(rank, r, 1000 * rank + r)
+        out = np.empty((n_ranks, 3), dtype=np.int64)
+        rc = lib.mpm_shm_allgather_i64(base, n_ranks, rank, vals, 3, out.ctypes.data, 20000)
+        ok = ok and rc == 0 and all(tuple(out[q]) == (q, r, 1000 * q + r) for q in range(n_ranks))
+    queue.put((rank, ok))
+
+
+def test_shared_memory_rendezvous_of_three_processes(tmp_path):
+    """mpm_shm_allgather_i64: the host barrier + integer exchange of the peer runtime's collective
+    steps (SpinBarrier / SharedRuntime of multiworker.py:27-107 across processes), no GPU needed."""
+    import multiprocessing as mp
+    from paper_2111_00699_b200 import _capi
+    n, rounds = 3, 200
+    path = tmp_path / "segment"
+    path.write_bytes(b"\0" * int(_capi.lib().mpm_shm_bytes(n)))
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    procs = [ctx.Process(target=_shm_rank, args=(str(path), n, r, rounds, q)) for r in range(n)]
+    for p in procs:
+        p.start()
+    results = sorted(q.get(timeout=120) for _ in procs)
+    for p in procs:
+        p.join(timeout=60)
+    assert results == [(r, True) for r in range(n)]
+    # a rank that waits alone runs into the timeout (multiworker.py:66-69)
+    import ctypes as C
+    import mmap
+    import numpy as np
+    lib = _capi.lib()
+    path.write_bytes(b"\0" * int(lib.mpm_shm_bytes(2)))
+    with open(path, "r+b") as f:
+        mm = mmap.mmap(f.fileno(), int(lib.mpm_shm_bytes(2)))
+    out = np.empty((2, 1), dtype=np.int64)
+    rc = lib.mpm_shm_allgather_i64(C.addressof(C.c_char.from_buffer(mm)), 2, 0, (C.c_int64 * 1)(7), 1,
+                                   out.ctypes.data, 50)
+    assert rc == -8
