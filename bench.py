@@ -296,13 +296,20 @@ def run_ours(args):
         w2 = fresh_worker()
         k_e2e = max(2, min(args.steps, 4))
         E2E_WARM = 3      # untimed: the second worker's buffers, pinned staging and the allocator settle
+        pending = None
         for it in range(E2E_WARM + k_e2e):
             if it == E2E_WARM:
                 barrier()
                 t0 = time.perf_counter()
             w2.replace_particles(pin_pos, pin_vel, W.particle_mass, pin_ids)
             w2.run_frame()
-            out_pos, out_ids = w2.store.positions_with_ids(dtype=None)   # pinned readback buffers
+            # the snapshot of this frame travels to pinned host memory while the next frame's
+            # inputs are uploaded; every step's result is on the host before the clock stops
+            handle = w2.store.positions_with_ids_async()
+            if pending is not None:
+                out_pos, out_ids = pending.wait()
+            pending = handle
+        out_pos, out_ids = pending.wait()
         barrier()
         dt_e2e = max_over_ranks((time.perf_counter() - t0) / k_e2e)
         e2e = {"value": round(n * spf / dt_e2e / 1e6, 2), "unit": UNIT,
@@ -310,7 +317,7 @@ def run_ours(args):
                "d2h_bytes_per_step": int(out_pos.nbytes + out_ids.nbytes),
                "ms_per_step": round(dt_e2e * 1e3, 3), "steps": k_e2e,
                "api": "CudaWorker.replace_particles(pinned x, v, ids) + run_frame() + "
-                      "store.positions_with_ids() into pinned buffers; every step re-seeds the scene's "
+                      "store.positions_with_ids_async() into pinned buffers (waited for one step later); every step re-seeds the scene's "
                       "initial state from the host, so it times the scene's first frame (fewer rebuilds "
                       "and less yielding than the frames `value` is taken over)"}
 

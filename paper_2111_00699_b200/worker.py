@@ -314,6 +314,43 @@ class CudaParticleStore:
             return hpos.numpy(), hids.numpy()
         return hpos.numpy().astype(dtype), hids.numpy().copy()
 
+    def positions_with_ids_async(self):
+        """positions_with_ids(dtype=None) without the host wait: the snapshot is gathered on the
+        compute stream into one of two device buffers and copied to pinned host memory on a copy
+        stream, so the transfer overlaps whatever the caller enqueues next (the upload and the
+        first substeps of the following frame).  Returns a PendingReadback; .wait() gives the
+        (positions float32 [n, 3], ids int64 [n]) views, valid until the second next call."""
+        if self._before_read is not None:
+            self._before_read()
+        n = self.count
+        k = self._rb_parity = 1 - getattr(self, "_rb_parity", 1)
+        if not hasattr(self, "_rb_stream"):
+            self._rb_stream = torch.cuda.Stream(device=self.device)
+            self._rb_done = [None, None]
+            self._rb_dev = [None, None]
+        main = torch.cuda.current_stream()
+        if self._rb_done[k] is not None:
+            main.wait_event(self._rb_done[k])      # the copy that last used these buffers
+        dev = self._rb_dev[k]
+        if dev is None or dev[0].shape[0] < n:
+            dev = self._rb_dev[k] = (torch.empty((max(n, 1), 3), dtype=torch.float32, device=self.device),
+                                     torch.empty(max(n, 1), dtype=torch.int64, device=self.device))
+        hpos = self._pinned(f"out_pos{k}", (n, 3), torch.float32)
+        hids = self._pinned(f"out_ids{k}", (n,), torch.int64)
+        if n:
+            v = self.view()
+            check(_capi.lib().mpm_gather_positions(C.byref(v), dev[0].data_ptr(), dev[1].data_ptr(),
+                                                   _stream_ptr()), "mpm_gather_positions")
+            gathered = torch.cuda.Event()
+            gathered.record(main)
+            self._rb_stream.wait_event(gathered)
+            with torch.cuda.stream(self._rb_stream):
+                hpos.copy_(dev[0][:n], non_blocking=True)
+                hids.copy_(dev[1][:n], non_blocking=True)
+        done = self._rb_done[k] = torch.cuda.Event()
+        done.record(self._rb_stream)
+        return PendingReadback(done, hpos, hids)
+
     def _aggregates(self):
         if self._before_read is not None:
             self._before_read()
@@ -331,6 +368,17 @@ class CudaParticleStore:
 
     def kinetic_energy(self) -> float:
         return float(self._aggregates()[4])
+
+
+class PendingReadback:
+    """A snapshot on its way to pinned host memory (CudaParticleStore.positions_with_ids_async)."""
+
+    def __init__(self, done, hpos, hids):
+        self._done, self._hpos, self._hids = done, hpos, hids
+
+    def wait(self):
+        self._done.synchronize()
+        return self._hpos.numpy(), self._hids.numpy()
 
 
 # --------------------------------------------------------------------------------------

@@ -337,3 +337,21 @@ def test_batched_frames_report_every_step(transfer):
     pa, ia = wa.store.positions_with_ids()
     pb, ib = wb.store.positions_with_ids()
     assert np.array_equal(ia, ib) and np.allclose(pa, pb, rtol=0, atol=2e-5)
+
+
+def test_asynchronous_snapshot_readback(rng):
+    """positions_with_ids_async: same snapshot as the blocking call, two readbacks in flight."""
+    pos = rng.uniform(6.0, 10.0, (500, 3))
+    vel = rng.normal(0, 10, (500, 3))
+    w = _mk(pos, vel, params=SimParams(dx=0.5, dt=1e-4), mass=0.5)
+    handles, expect = [], []
+    for s in range(3):
+        w.run_step(s)
+        handles.append(w.store.positions_with_ids_async())
+        if s < 2:
+            continue                     # first two handles are left pending over the next steps
+    expect = w.store.positions_with_ids(dtype=None)
+    p2, i2 = handles[2].wait()
+    assert np.array_equal(i2, expect[1]) and np.array_equal(p2, expect[0])
+    p1, i1 = handles[1].wait()           # the other buffer pair: the state one step earlier
+    assert np.array_equal(np.sort(i1), np.sort(i2)) and not np.array_equal(p1, p2)
