@@ -55,6 +55,8 @@ __device__ __forceinline__ int block_exclusive_scan(int v, int *total)
 
 __global__ void __launch_bounds__(SCAN_THREADS) scan_reduce_kernel(const int *in, int n, int *block_sums)
 {
+    pdl_wait();
+    pdl_launch_dependents();
     const int base = blockIdx.x * SCAN_TILE + threadIdx.x * SCAN_ITEMS;
     int s = 0;
 #pragma unroll
@@ -67,6 +69,8 @@ __global__ void __launch_bounds__(SCAN_THREADS) scan_reduce_kernel(const int *in
 
 __global__ void __launch_bounds__(1024) scan_blocksums_kernel(int *block_sums, int nb, int *total_out)
 {
+    pdl_wait();
+    pdl_launch_dependents();
     __shared__ int carry;
     if (threadIdx.x == 0) carry = 0;
     __syncthreads();
@@ -90,6 +94,8 @@ __global__ void __launch_bounds__(1024) scan_blocksums_kernel(int *block_sums, i
 __global__ void __launch_bounds__(SCAN_THREADS) scan_apply_kernel(const int *in, int *out, int n,
                                                                   const int *block_sums)
 {
+    pdl_wait();
+    pdl_launch_dependents();
     const int base = blockIdx.x * SCAN_TILE + threadIdx.x * SCAN_ITEMS;
     int v[SCAN_ITEMS];
     int s = 0;
@@ -115,9 +121,9 @@ void exclusive_scan_i32(const int32_t *in, int32_t *out, int32_t n, int32_t *blo
         return;
     }
     const int nb = (n + SCAN_TILE - 1) / SCAN_TILE;
-    scan_reduce_kernel<<<nb, SCAN_THREADS, 0, stream>>>(in, n, block_sums);
-    scan_blocksums_kernel<<<1, 1024, 0, stream>>>(block_sums, nb, total);
-    scan_apply_kernel<<<nb, SCAN_THREADS, 0, stream>>>(in, out, n, block_sums);
+    launch_chained(scan_reduce_kernel, nb, SCAN_THREADS, stream, in, n, block_sums);
+    launch_chained(scan_blocksums_kernel, 1, 1024, stream, block_sums, nb, total);
+    launch_chained(scan_apply_kernel, nb, SCAN_THREADS, stream, in, out, n, block_sums);
 }
 
 // ===================================================================================
@@ -128,6 +134,8 @@ __global__ void __launch_bounds__(256) live_count_kernel(const uint16_t *__restr
                                                          int n_groups, int drop_q,
                                                          int *__restrict__ group_live)
 {
+    pdl_wait();
+    pdl_launch_dependents();
     const int g = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
     const int lane = threadIdx.x & 31;
     if (g >= n_groups) return;
@@ -144,6 +152,8 @@ __global__ void __launch_bounds__(256) live_write_kernel(const uint16_t *__restr
                                                          const int *__restrict__ group_base,
                                                          int *__restrict__ src_slot)
 {
+    pdl_wait();
+    pdl_launch_dependents();
     const int g = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
     const int lane = threadIdx.x & 31;
     if (g >= n_groups) return;
@@ -167,6 +177,8 @@ __global__ void __launch_bounds__(256) particle_codes_kernel(
     const int *__restrict__ n_live_dev, const float *__restrict__ staged, int n_staged, int n_upper,
     double dx, long long *__restrict__ codes, int *__restrict__ bad_index)
 {
+    pdl_wait();
+    pdl_launch_dependents();
     const int i = blockIdx.x * blockDim.x + threadIdx.x;
     const int n_live = n_live_dev ? *n_live_dev : 0;
     const int n = n_live + n_staged;
@@ -202,6 +214,8 @@ __global__ void __launch_bounds__(256) particle_codes_kernel(
 // ===================================================================================
 __global__ void hash_clear_kernel(long long *hkeys, int *hvals, int *hfirst, int cap)
 {
+    pdl_wait();
+    pdl_launch_dependents();
     const int i = blockIdx.x * blockDim.x + threadIdx.x;
     if (i < cap) {
         hkeys[i] = MPM_EMPTY_KEY;
@@ -245,6 +259,8 @@ __global__ void __launch_bounds__(256) block_insert_kernel(const long long *__re
                                                            int mask, int *__restrict__ pslot,
                                                            int *overflow)
 {
+    pdl_wait();
+    pdl_launch_dependents();
     const int i = blockIdx.x * blockDim.x + threadIdx.x;
     if (i >= n_upper) return;
     if (i >= *n_dev) { pslot[i] = -1; return; }
@@ -260,6 +276,8 @@ __global__ void __launch_bounds__(256) first_flag_kernel(const int *__restrict__
                                                          const int *__restrict__ hvals, int n_upper,
                                                          int only_unassigned, int *__restrict__ flag)
 {
+    pdl_wait();
+    pdl_launch_dependents();
     const int i = blockIdx.x * blockDim.x + threadIdx.x;
     if (i >= n_upper) return;
     const int slot = pslot[i];
@@ -274,6 +292,8 @@ __global__ void __launch_bounds__(256) block_assign_kernel(const long long *__re
                                                            const int *__restrict__ rank, int n_upper,
                                                            int *hvals, long long *__restrict__ gcodes)
 {
+    pdl_wait();
+    pdl_launch_dependents();
     const int i = blockIdx.x * blockDim.x + threadIdx.x;
     if (i >= n_upper) return;
     const int slot = pslot[i];
@@ -288,6 +308,8 @@ __global__ void __launch_bounds__(256) gidx_kernel(const int *__restrict__ pslot
                                                    const int *__restrict__ hvals, int n_upper,
                                                    int *__restrict__ gidx)
 {
+    pdl_wait();
+    pdl_launch_dependents();
     const int i = blockIdx.x * blockDim.x + threadIdx.x;
     if (i >= n_upper) return;
     const int slot = pslot[i];
@@ -303,6 +325,8 @@ __global__ void __launch_bounds__(256) dilate_insert_kernel(const long long *__r
                                                             int shift, int mask, int *__restrict__ qslot,
                                                             int *bad_block, int *overflow)
 {
+    pdl_wait();
+    pdl_launch_dependents();
     const int q = blockIdx.x * blockDim.x + threadIdx.x;
     if (q >= n_g * 27) return;
     const int g = q / 27, s = q - g * 27;
@@ -331,6 +355,8 @@ __global__ void __launch_bounds__(256) dilate_assign_kernel(const int *__restric
                                                             int *hvals, long long *__restrict__ codes,
                                                             int *overflow)
 {
+    pdl_wait();
+    pdl_launch_dependents();
     const int q = blockIdx.x * blockDim.x + threadIdx.x;
     if (q >= n_q) return;
     if (!flag[q]) return;
@@ -345,6 +371,8 @@ __global__ void __launch_bounds__(256) dilate_link_kernel(const int *__restrict_
                                                           const int *__restrict__ hvals, int n_q,
                                                           int *__restrict__ neighbor)
 {
+    pdl_wait();
+    pdl_launch_dependents();
     const int q = blockIdx.x * blockDim.x + threadIdx.x;
     if (q >= n_q) return;
     const int slot = qslot[q];
@@ -354,6 +382,8 @@ __global__ void __launch_bounds__(256) dilate_link_kernel(const int *__restrict_
 __global__ void __launch_bounds__(256) gblock_codes_kernel(const long long *__restrict__ gcodes,
                                                            int n_g, long long *__restrict__ codes)
 {
+    pdl_wait();
+    pdl_launch_dependents();
     const int g = blockIdx.x * blockDim.x + threadIdx.x;
     if (g < n_g) codes[g] = gcodes[g];
 }
@@ -362,6 +392,8 @@ __global__ void __launch_bounds__(256) block_origin_kernel(const long long *__re
                                                            const int *__restrict__ count_dev,
                                                            int pblock_cap, int4 *__restrict__ origin)
 {
+    pdl_wait();
+    pdl_launch_dependents();
     const int b = blockIdx.x * blockDim.x + threadIdx.x;
     if (b >= pblock_cap || b >= *count_dev) return;
     const unsigned long long code = (unsigned long long)codes[b];
@@ -371,6 +403,8 @@ __global__ void __launch_bounds__(256) block_origin_kernel(const long long *__re
 
 __global__ void add_scalar_kernel(int *dst, const int *a, int b)
 {
+    pdl_wait();
+    pdl_launch_dependents();
     *dst = *a + b;
 }
 
@@ -382,6 +416,8 @@ __global__ void __launch_bounds__(256) hist_kernel(const long long *__restrict__
                                                    const int *__restrict__ n_dev, int n_upper,
                                                    int *bins, int *__restrict__ ticket)
 {
+    pdl_wait();
+    pdl_launch_dependents();
     const int i = blockIdx.x * blockDim.x + threadIdx.x;
     if (i >= n_upper || i >= *n_dev) return;
     const int key = (gidx[i] << 6) | (int)(codes[i] & 63);
@@ -395,6 +431,8 @@ __global__ void __launch_bounds__(256) place_kernel(const long long *__restrict_
                                                     const int *__restrict__ ticket,
                                                     int *__restrict__ tmp_perm)
 {
+    pdl_wait();
+    pdl_launch_dependents();
     const int i = blockIdx.x * blockDim.x + threadIdx.x;
     if (i >= n_upper || i >= *n_dev) return;
     const int key = (gidx[i] << 6) | (int)(codes[i] & 63);
@@ -409,6 +447,8 @@ __global__ void __launch_bounds__(256) stable_rank_kernel(const long long *__res
                                                           const int *__restrict__ tmp_perm,
                                                           int *__restrict__ perm)
 {
+    pdl_wait();
+    pdl_launch_dependents();
     const int j = blockIdx.x * blockDim.x + threadIdx.x;
     if (j >= n_upper || j >= *n_dev) return;
     const int i = tmp_perm[j];
@@ -422,6 +462,8 @@ __global__ void __launch_bounds__(256) stable_rank_kernel(const long long *__res
 __global__ void __launch_bounds__(256) block_groups_kernel(const int *__restrict__ bin_start, int n_g,
                                                            int *__restrict__ ngroups)
 {
+    pdl_wait();
+    pdl_launch_dependents();
     const int b = blockIdx.x * blockDim.x + threadIdx.x;
     if (b >= n_g) return;
     const int c = bin_start[(b + 1) * 64] - bin_start[b * 64];
@@ -443,6 +485,8 @@ __global__ void __launch_bounds__(256) scatter_sorted_kernel(
     uint16_t *__restrict__ new_meta, int *__restrict__ group_len, int *__restrict__ group_block,
     int *__restrict__ group_start, int n_groups)
 {
+    pdl_wait();
+    pdl_launch_dependents();
     const int g = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
     const int lane = threadIdx.x & 31;
     if (g >= n_groups) return;
@@ -501,6 +545,8 @@ __global__ void __launch_bounds__(256) gather_state_kernel(const float *__restri
                                                            int n_groups, float *__restrict__ flat,
                                                            long long *__restrict__ out_ids)
 {
+    pdl_wait();
+    pdl_launch_dependents();
     const int g = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
     const int lane = threadIdx.x & 31;
     if (g >= n_groups || lane >= group_len[g]) return;
@@ -517,6 +563,8 @@ __global__ void __launch_bounds__(256) gather_positions_kernel(const float *__re
                                                                int n_groups, float *__restrict__ pos,
                                                                long long *__restrict__ out_ids)
 {
+    pdl_wait();
+    pdl_launch_dependents();
     const int g = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
     const int lane = threadIdx.x & 31;
     if (g >= n_groups || lane >= group_len[g]) return;
@@ -533,6 +581,8 @@ __global__ void __launch_bounds__(256) tag_shared_kernel(const long long *__rest
                                                          const int *__restrict__ hvals, int shift,
                                                          int mask, int *__restrict__ peer_map)
 {
+    pdl_wait();
+    pdl_launch_dependents();
     const int q = blockIdx.x * blockDim.x + threadIdx.x;
     if (q >= n_peer) return;
     const int slot = hash_find(hkeys, shift, mask, peer_codes[q]);
@@ -541,6 +591,8 @@ __global__ void __launch_bounds__(256) tag_shared_kernel(const long long *__rest
 
 __global__ void fill_i32_kernel(int *p, int n, int v)
 {
+    pdl_wait();
+    pdl_launch_dependents();
     const int i = blockIdx.x * blockDim.x + threadIdx.x;
     if (i < n) p[i] = v;
 }
@@ -553,6 +605,8 @@ __global__ void __launch_bounds__(256) group_ctx_kernel(const int *__restrict__ 
                                                         const int *__restrict__ neighbor,
                                                         int *__restrict__ ctx)
 {
+    pdl_wait();
+    pdl_launch_dependents();
     const int g = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
     const int lane = threadIdx.x & 31;
     if (g >= n_groups) return;
@@ -584,10 +638,10 @@ int mpm_compact_live(const mpm_store_view *store, int drop_quarantined, int32_t 
         cudaMemsetAsync(n_live, 0, sizeof(int32_t), stream);
         return check_launch("mpm_compact_live", 5);
     }
-    live_count_kernel<<<nblk((int64_t)G * 32, 256), 256, 0, stream>>>(
+    launch_chained(live_count_kernel, nblk((int64_t)G * 32, 256), 256, stream, 
         store->lane_meta, store->group_len, G, drop_quarantined, group_live_scratch);
     exclusive_scan_i32(group_live_scratch, group_live_scratch, G, scan_scratch, n_live, stream);
-    live_write_kernel<<<nblk((int64_t)G * 32, 256), 256, 0, stream>>>(
+    launch_chained(live_write_kernel, nblk((int64_t)G * 32, 256), 256, stream, 
         store->lane_meta, store->group_len, G, drop_quarantined, group_live_scratch, src_slot);
     return check_launch("mpm_compact_live", 5);
 }
@@ -598,11 +652,11 @@ int mpm_particle_codes(const mpm_store_view *store, const int32_t *src_slot, con
 {
     cudaStream_t stream = (cudaStream_t)stream_;
     if (!(dx > 0.0)) return MPM_ERR_REJECTED_INPUT;
-    fill_i32_kernel<<<1, 32, 0, stream>>>(bad_index, 1, MPM_INT_MAX);
-    if (n_live_dev) add_scalar_kernel<<<1, 1, 0, stream>>>(n_total, n_live_dev, n_staged);
-    else fill_i32_kernel<<<1, 32, 0, stream>>>(n_total, 1, n_staged);
+    launch_chained(fill_i32_kernel, 1, 32, stream, bad_index, 1, MPM_INT_MAX);
+    if (n_live_dev) launch_chained(add_scalar_kernel, 1, 1, stream, n_total, n_live_dev, n_staged);
+    else launch_chained(fill_i32_kernel, 1, 32, stream, n_total, 1, n_staged);
     if (n_upper > 0)
-        particle_codes_kernel<<<nblk(n_upper, 256), 256, 0, stream>>>(
+        launch_chained(particle_codes_kernel, nblk(n_upper, 256), 256, stream, 
             store->data, store->nch, src_slot, n_live_dev, staged, n_staged, n_upper, dx,
             (long long *)codes, bad_index);
     return check_launch("mpm_particle_codes", 3);
@@ -617,20 +671,20 @@ int mpm_hash_insert_blocks(const int64_t *codes, const int32_t *n_dev, int32_t n
     cudaStream_t stream = (cudaStream_t)stream_;
     if (hash_cap <= 0 || (hash_cap & (hash_cap - 1))) return MPM_ERR_REJECTED_INPUT;
     const int shift = hash_shift_for(hash_cap), mask = hash_cap - 1;
-    hash_clear_kernel<<<nblk(hash_cap, 256), 256, 0, stream>>>((long long *)hkeys, hvals, hfirst, hash_cap);
+    launch_chained(hash_clear_kernel, nblk(hash_cap, 256), 256, stream, (long long *)hkeys, hvals, hfirst, hash_cap);
     cudaMemsetAsync(overflow, 0, sizeof(int32_t), stream);
     if (n_upper <= 0) {
         cudaMemsetAsync(n_gblocks, 0, sizeof(int32_t), stream);
         return check_launch("mpm_hash_insert_blocks", 8);
     }
     const int nb = nblk(n_upper, 256);
-    block_insert_kernel<<<nb, 256, 0, stream>>>((const long long *)codes, n_dev, n_upper,
+    launch_chained(block_insert_kernel, nb, 256, stream, (const long long *)codes, n_dev, n_upper,
                                                 (long long *)hkeys, hfirst, shift, mask, pslot, overflow);
-    first_flag_kernel<<<nb, 256, 0, stream>>>(pslot, hfirst, hvals, n_upper, 0, flag_scratch);
+    launch_chained(first_flag_kernel, nb, 256, stream, pslot, hfirst, hvals, n_upper, 0, flag_scratch);
     exclusive_scan_i32(flag_scratch, flag_scratch, n_upper, scan_scratch, n_gblocks, stream);
-    block_assign_kernel<<<nb, 256, 0, stream>>>((const long long *)codes, pslot, hfirst, flag_scratch,
+    launch_chained(block_assign_kernel, nb, 256, stream, (const long long *)codes, pslot, hfirst, flag_scratch,
                                                 n_upper, hvals, (long long *)gcodes);
-    gidx_kernel<<<nb, 256, 0, stream>>>(pslot, hvals, n_upper, gidx);
+    launch_chained(gidx_kernel, nb, 256, stream, pslot, hvals, n_upper, gidx);
     return check_launch("mpm_hash_insert_blocks", 8);
 }
 
@@ -643,7 +697,7 @@ int mpm_dilate_and_link(const int64_t *gcodes, int32_t n_g, int64_t *hkeys, int3
     cudaStream_t stream = (cudaStream_t)stream_;
     if (hash_cap <= 0 || (hash_cap & (hash_cap - 1))) return MPM_ERR_REJECTED_INPUT;
     const int shift = hash_shift_for(hash_cap), mask = hash_cap - 1;
-    fill_i32_kernel<<<1, 32, 0, stream>>>(bad_block, 1, MPM_INT_MAX);
+    launch_chained(fill_i32_kernel, 1, 32, stream, bad_block, 1, MPM_INT_MAX);
     if (n_g <= 0) {
         cudaMemsetAsync(count, 0, sizeof(int32_t), stream);
         return check_launch("mpm_dilate_and_link", 11);
@@ -653,20 +707,20 @@ int mpm_dilate_and_link(const int64_t *gcodes, int32_t n_g, int64_t *hkeys, int3
     const int nb = nblk(n_q, 256);
     // hfirst of the halo slots must start at INT_MAX: gblock slots already hold particle indices,
     // but those are never compared again (their hvals >= 0).
-    dilate_insert_kernel<<<nb, 256, 0, stream>>>((const long long *)gcodes, n_g, (long long *)hkeys,
+    launch_chained(dilate_insert_kernel, nb, 256, stream, (const long long *)gcodes, n_g, (long long *)hkeys,
                                                  hvals, hfirst, shift, mask, qslot, bad_block, overflow);
-    first_flag_kernel<<<nb, 256, 0, stream>>>(qslot, hfirst, hvals, n_q, 1, flag_scratch);
+    launch_chained(first_flag_kernel, nb, 256, stream, qslot, hfirst, hvals, n_q, 1, flag_scratch);
     // keep the flags: the scan result goes to a second array (flag_scratch + n_q)
     int32_t *rank = flag_scratch + n_q;
     exclusive_scan_i32(flag_scratch, rank, n_q, scan_scratch, count, stream);
-    gblock_codes_kernel<<<nblk(n_g, 256), 256, 0, stream>>>((const long long *)gcodes, n_g,
+    launch_chained(gblock_codes_kernel, nblk(n_g, 256), 256, stream, (const long long *)gcodes, n_g,
                                                             (long long *)codes);
-    dilate_assign_kernel<<<nb, 256, 0, stream>>>(qslot, flag_scratch, rank, n_q, n_g, pblock_cap,
+    launch_chained(dilate_assign_kernel, nb, 256, stream, qslot, flag_scratch, rank, n_q, n_g, pblock_cap,
                                                  (const long long *)hkeys, hvals, (long long *)codes,
                                                  overflow);
-    dilate_link_kernel<<<nb, 256, 0, stream>>>(qslot, hvals, n_q, neighbor);
-    add_scalar_kernel<<<1, 1, 0, stream>>>(count, count, n_g);
-    block_origin_kernel<<<nblk(pblock_cap, 256), 256, 0, stream>>>((const long long *)codes, count,
+    launch_chained(dilate_link_kernel, nb, 256, stream, qslot, hvals, n_q, neighbor);
+    launch_chained(add_scalar_kernel, 1, 1, stream, count, count, n_g);
+    launch_chained(block_origin_kernel, nblk(pblock_cap, 256), 256, stream, (const long long *)codes, count,
                                                                    pblock_cap, (int4 *)origin);
     return check_launch("mpm_dilate_and_link", 11);
 }
@@ -685,13 +739,13 @@ int mpm_sort_and_group(const int64_t *codes, const int32_t *gidx, const int32_t 
     const int nb = nblk(n_upper, 256);
     // tickets live in `perm` until the final ranking overwrites it
     cudaMemsetAsync(bin_start, 0, sizeof(int32_t) * (size_t)(n_bins + 1), stream);
-    hist_kernel<<<nb, 256, 0, stream>>>((const long long *)codes, gidx, n_dev, n_upper, bin_start, perm);
+    launch_chained(hist_kernel, nb, 256, stream, (const long long *)codes, gidx, n_dev, n_upper, bin_start, perm);
     exclusive_scan_i32(bin_start, bin_start, n_bins + 1, scan_scratch, nullptr, stream);
-    place_kernel<<<nb, 256, 0, stream>>>((const long long *)codes, gidx, n_dev, n_upper, bin_start,
+    launch_chained(place_kernel, nb, 256, stream, (const long long *)codes, gidx, n_dev, n_upper, bin_start,
                                          perm, tmp_perm);
-    stable_rank_kernel<<<nb, 256, 0, stream>>>((const long long *)codes, gidx, n_dev, n_upper,
+    launch_chained(stable_rank_kernel, nb, 256, stream, (const long long *)codes, gidx, n_dev, n_upper,
                                                bin_start, tmp_perm, perm);
-    block_groups_kernel<<<nblk(n_g, 256), 256, 0, stream>>>(bin_start, n_g, block_group_first);
+    launch_chained(block_groups_kernel, nblk(n_g, 256), 256, stream, bin_start, n_g, block_group_first);
     // n_g+1 entries so that block_group_first[n_g] = n_groups
     cudaMemsetAsync(block_group_first + n_g, 0, sizeof(int32_t), stream);
     exclusive_scan_i32(block_group_first, block_group_first, n_g + 1, scan_scratch, n_groups, stream);
@@ -708,7 +762,7 @@ int mpm_scatter_sorted(const mpm_store_view *old_store, const int32_t *src_slot,
     const int G = new_store->n_groups;
     if (G <= 0) return MPM_OK;
     const double inv_dx = 1.0 / dx;
-    scatter_sorted_kernel<<<nblk((int64_t)G * 32, 256), 256, 0, stream>>>(
+    launch_chained(scatter_sorted_kernel, nblk((int64_t)G * 32, 256), 256, stream, 
         old_store->data, (const long long *)old_store->orig_id, new_store->nch, src_slot, n_live_dev,
         staged, (const long long *)staged_ids, perm, bin_start, block_group_first, n_g,
         (const int4 *)table_origin, inv_dx, new_store->data, (long long *)new_store->orig_id,
@@ -721,7 +775,7 @@ int mpm_build_group_ctx(const mpm_store_view *store, const mpm_table_view *table
     if (!store || !table || !store->group_ctx) return MPM_ERR_REJECTED_INPUT;
     const int G = store->n_groups;
     if (G <= 0) return MPM_OK;
-    group_ctx_kernel<<<nblk((int64_t)G * 32, 256), 256, 0, (cudaStream_t)stream_>>>(
+    launch_chained(group_ctx_kernel, nblk((int64_t)G * 32, 256), 256, (cudaStream_t)stream_, 
         store->group_len, store->group_block, G, (const int4 *)table->origin, table->neighbor,
         store->group_ctx);
     return check_launch("mpm_build_group_ctx", 1);
@@ -732,7 +786,7 @@ int mpm_gather_state(const mpm_store_view *store, float *flat, int64_t *ids, voi
     cudaStream_t stream = (cudaStream_t)stream_;
     const int G = store->n_groups;
     if (G <= 0) return MPM_OK;
-    gather_state_kernel<<<nblk((int64_t)G * 32, 256), 256, 0, stream>>>(
+    launch_chained(gather_state_kernel, nblk((int64_t)G * 32, 256), 256, stream, 
         store->data, (const long long *)store->orig_id, store->nch, store->group_len,
         store->group_start, G, flat, (long long *)ids);
     return check_launch("mpm_gather_state", 1);
@@ -743,7 +797,7 @@ int mpm_gather_positions(const mpm_store_view *store, float *pos, int64_t *ids, 
     cudaStream_t stream = (cudaStream_t)stream_;
     const int G = store->n_groups;
     if (G <= 0) return MPM_OK;
-    gather_positions_kernel<<<nblk((int64_t)G * 32, 256), 256, 0, stream>>>(
+    launch_chained(gather_positions_kernel, nblk((int64_t)G * 32, 256), 256, stream, 
         store->data, (const long long *)store->orig_id, store->nch, store->group_len,
         store->group_start, G, pos, (long long *)ids);
     return check_launch("mpm_gather_positions", 1);
@@ -756,9 +810,9 @@ int mpm_tag_shared(const int64_t *peer_codes, int32_t n_peer_codes, const int64_
     cudaStream_t stream = (cudaStream_t)stream_;
     if (hash_cap <= 0 || (hash_cap & (hash_cap - 1))) return MPM_ERR_REJECTED_INPUT;
     if (local_count > 0)
-        fill_i32_kernel<<<nblk(local_count, 256), 256, 0, stream>>>(peer_map, local_count, -1);
+        launch_chained(fill_i32_kernel, nblk(local_count, 256), 256, stream, peer_map, local_count, -1);
     if (n_peer_codes > 0)
-        tag_shared_kernel<<<nblk(n_peer_codes, 256), 256, 0, stream>>>(
+        launch_chained(tag_shared_kernel, nblk(n_peer_codes, 256), 256, stream, 
             (const long long *)peer_codes, n_peer_codes, (const long long *)hkeys, hvals,
             hash_shift_for(hash_cap), hash_cap - 1, peer_map);
     return check_launch("mpm_tag_shared", 2);
