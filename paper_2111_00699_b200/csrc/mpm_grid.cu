@@ -23,6 +23,8 @@ struct PeerSet {
 __global__ void __launch_bounds__(256) clear_kernel(float4 *raw, uint8_t *touched, int count, int full,
                                                     int vec_per_node, const DevGuard guard)
 {
+    pdl_wait();
+    pdl_launch_dependents();
     if (guarded_out(guard)) return;
     const int b = blockIdx.x * 4 + (threadIdx.x >> 6);
     const int slot = threadIdx.x & 63;
@@ -244,6 +246,8 @@ __global__ void __launch_bounds__(256) particle_aggregates_kernel(const float *_
                                                                   const int *__restrict__ group_len,
                                                                   int n_groups, double *out5)
 {
+    pdl_wait();
+    pdl_launch_dependents();
     const int g = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
     const int lane = threadIdx.x & 31;
     double m = 0, mx = 0, my = 0, mz = 0, ke = 0;
@@ -267,6 +271,8 @@ __global__ void __launch_bounds__(256) grid_aggregates_kernel(const float4 *__re
                                                               const uint8_t *__restrict__ touched,
                                                               int count, int det, double *out4)
 {
+    pdl_wait();
+    pdl_launch_dependents();
     const int b = blockIdx.x * 4 + (threadIdx.x >> 6);
     const int slot = threadIdx.x & 63;
     const int lane = threadIdx.x & 31;
@@ -294,6 +300,8 @@ __global__ void __launch_bounds__(256) pack_halo_kernel(const float4 *__restrict
                                                         const int *__restrict__ send_idx, int n,
                                                         float4 *__restrict__ out)
 {
+    pdl_wait();
+    pdl_launch_dependents();
     const int i = blockIdx.x * 4 + (threadIdx.x >> 6);
     const int slot = threadIdx.x & 63;
     if (i >= n) return;
@@ -303,6 +311,8 @@ __global__ void __launch_bounds__(256) pack_halo_kernel(const float4 *__restrict
 
 __global__ void signal_step_kernel(int *word, int value, const DevGuard guard)
 {
+    pdl_wait();
+    pdl_launch_dependents();
     if (guarded_out(guard)) return;
     // everything enqueued before this kernel on the stream has completed; make it visible to the
     // peers before the word they poll changes
@@ -318,6 +328,8 @@ struct WaitArgs {
 // the step barrier alone (a rank whose block table is empty has no grid update to hang it on)
 __global__ void wait_step_kernel(const WaitArgs a, const DevGuard guard)
 {
+    pdl_wait();
+    pdl_launch_dependents();
     if (guarded_out(guard)) return;
     if (threadIdx.x < a.n_wait) {
         const int *flag = a.wait_flags[threadIdx.x];
@@ -337,11 +349,15 @@ __global__ void wait_step_kernel(const WaitArgs a, const DevGuard guard)
 __global__ void status_publish_kernel(const mpm_step_status *src, mpm_step_status *dst, const int *guard_src,
                                       int *guard_dst)
 {
+    pdl_wait();
+    pdl_launch_dependents();
     publish_status(src, dst, guard_src, guard_dst, threadIdx.x);
 }
 
 __global__ void status_reset_kernel(mpm_step_status *status, const DevGuard guard)
 {
+    pdl_wait();
+    pdl_launch_dependents();
     if (guarded_out(guard)) return;
     status->zone_violation = 0;
     status->vmax2_bits = 0;
@@ -358,14 +374,14 @@ int mpm_clear(float *raw, uint8_t *touched, int32_t count, int full, int32_t nod
 {
     if (count <= 0) return MPM_OK;
     if (node_bytes != 16 && node_bytes != 32) return MPM_ERR_REJECTED_INPUT;
-    clear_kernel<<<(count + 3) / 4, 256, 0, (cudaStream_t)stream>>>((float4 *)raw, touched, count, full,
+    launch_chained(clear_kernel, (count + 3) / 4, 256, (cudaStream_t)stream, (float4 *)raw, touched, count, full,
                                                                     node_bytes / 16, make_guard(guard));
     return check_launch("mpm_clear", 1);
 }
 
 int mpm_status_reset(mpm_step_status *status, const mpm_guard *guard, void *stream)
 {
-    status_reset_kernel<<<1, 1, 0, (cudaStream_t)stream>>>(status, make_guard(guard));
+    launch_chained(status_reset_kernel, 1, 1, (cudaStream_t)stream, status, make_guard(guard));
     return check_launch("mpm_status_reset", 1);
 }
 
@@ -374,7 +390,7 @@ int mpm_status_publish(const mpm_step_status *src, mpm_step_status *dst_mapped, 
 {
     if ((dst_mapped && !src) || (guard_dst_mapped && !guard_src)) return MPM_ERR_REJECTED_INPUT;
     if (!dst_mapped && !guard_dst_mapped) return MPM_OK;
-    status_publish_kernel<<<1, 32, 0, (cudaStream_t)stream>>>(src, dst_mapped, guard_src, guard_dst_mapped);
+    launch_chained(status_publish_kernel, 1, 32, (cudaStream_t)stream, src, dst_mapped, guard_src, guard_dst_mapped);
     return check_launch("mpm_status_publish", 1);
 }
 
@@ -435,7 +451,7 @@ int mpm_grid_update(float *raw, uint8_t *touched, float *vel, float *vel_old,
 int mpm_signal_step(int32_t *word, int32_t value, const mpm_guard *guard, void *stream)
 {
     if (!word) return MPM_ERR_REJECTED_INPUT;
-    signal_step_kernel<<<1, 1, 0, (cudaStream_t)stream>>>(word, value, make_guard(guard));
+    launch_chained(signal_step_kernel, 1, 1, (cudaStream_t)stream, word, value, make_guard(guard));
     return check_launch("mpm_signal_step", 1);
 }
 
@@ -449,7 +465,7 @@ int mpm_wait_step(const mpm_grid_params *p, const mpm_guard *guard, void *stream
     a.wait_timeout_ms = p->wait_timeout_ms > 0 ? p->wait_timeout_ms : 10000;
     for (int k = 0; k < MPM_MAX_PEERS; ++k) a.wait_flags[k] = k < p->n_wait ? p->wait_flags[k] : nullptr;
     a.wait_error = p->wait_error;
-    wait_step_kernel<<<1, 32, 0, (cudaStream_t)stream>>>(a, make_guard(guard));
+    launch_chained(wait_step_kernel, 1, 32, (cudaStream_t)stream, a, make_guard(guard));
     return check_launch("mpm_wait_step", 1);
 }
 
@@ -457,7 +473,7 @@ int mpm_pack_halo(const float *raw, const uint8_t *touched, const int32_t *send_
                   float *out_rows, void *stream)
 {
     if (n <= 0) return MPM_OK;
-    pack_halo_kernel<<<(n + 3) / 4, 256, 0, (cudaStream_t)stream>>>((const float4 *)raw, touched, send_idx, n,
+    launch_chained(pack_halo_kernel, (n + 3) / 4, 256, (cudaStream_t)stream, (const float4 *)raw, touched, send_idx, n,
                                                                     (float4 *)out_rows);
     return check_launch("mpm_pack_halo", 1);
 }
@@ -468,7 +484,7 @@ int mpm_particle_aggregates(const mpm_store_view *store, double *out5, void *str
     cudaMemsetAsync(out5, 0, 5 * sizeof(double), stream);
     const int G = store->n_groups;
     if (G > 0)
-        particle_aggregates_kernel<<<(int)(((int64_t)G * 32 + 255) / 256), 256, 0, stream>>>(
+        launch_chained(particle_aggregates_kernel, (int)(((int64_t)G * 32 + 255) / 256), 256, stream, 
             store->data, store->nch, store->group_len, G, out5);
     return check_launch("mpm_particle_aggregates", 1);
 }
@@ -479,7 +495,7 @@ int mpm_grid_aggregates(const float *raw, const uint8_t *touched, int32_t count,
     cudaStream_t stream = (cudaStream_t)stream_;
     cudaMemsetAsync(out4, 0, 4 * sizeof(double), stream);
     if (count > 0)
-        grid_aggregates_kernel<<<(count + 3) / 4, 256, 0, stream>>>((const float4 *)raw, touched, count,
+        launch_chained(grid_aggregates_kernel, (count + 3) / 4, 256, stream, (const float4 *)raw, touched, count,
                                                                   deterministic, out4);
     return check_launch("mpm_grid_aggregates", 1);
 }
