@@ -261,7 +261,7 @@ def run_ours(args):
     all_kernel_ms = {}
     for name, a, b in w.kernel_events:
         all_kernel_ms[name] = all_kernel_ms.get(name, 0.0) + a.elapsed_time(b)
-    # Steps enqueued in batches from C time the first launch of each batch only (an event between
+    # Steps enqueued in batches from C time ONE launch per batch, at a rotating position (an event between
     # two kernels of the chain would serialise what programmatic dependent launch overlaps); the
     # dominant kernel's total is its mean duration x its launches in the region: every substep
     # except, for the fused transfer, the rebuild steps (those run the split P2G).

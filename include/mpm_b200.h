@@ -255,12 +255,21 @@ typedef struct mpm_rebuild_plan {
     int32_t node_bytes;                /* 16, or 32 in deterministic mode */
     int32_t *scalars_dev;              /* 16 device words */
     int32_t *scalars_host;             /* 16 pinned host words */
+    /* Optional rest of the rebuild step for a single worker (p2g_params NULL = none): the
+     * scatter of the step (pipeline.py:924-926, always split P2G on a rebuild step) and its grid
+     * update (pipeline.py:933) are issued right behind the rebuild kernels, so the device does
+     * not wait for the host's bookkeeping of the new tables.  Declared later in this header. */
+    const struct mpm_transfer_params *p2g_params;
+    struct mpm_step_status *p2g_status;
+    const struct mpm_grid_params *grid_params;
+    struct mpm_step_status *grid_reset_status;
+    float *vel_old;                    /* FLIP only */
 } mpm_rebuild_plan;
 typedef struct mpm_rebuild_result {
     int32_t n, n_gblocks, count, n_groups;
     int32_t bad_particle, bad_block;   /* INT32_MAX = none */
     int32_t need_hash, need_gblocks, need_table, need_groups, need_nodes;   /* 0 = fits */
-    int32_t reserved;
+    int32_t tail_done;                 /* 1: the P2G and the grid update of the step were issued */
 } mpm_rebuild_result;
 int mpm_rebuild(const mpm_rebuild_plan *plan, mpm_rebuild_result *result, void *stream);
 
@@ -420,6 +429,10 @@ typedef struct mpm_step_plan {
     const uint8_t *peer_touched[2][MPM_MAX_PEERS];
     void *time_events[2 * MPM_MAX_STATUS_RING]; /* optional (NULL): cudaEvent_t pairs recorded around the
                                           dominant transfer kernel (g2p2g / p2g) of step first+k */
+    int32_t full_clear_first;          /* 1: the first step of the batch clears its raw parity in full
+                                          before scattering -- the first use of the parity a rebuild
+                                          left untouched (pipeline.py:1002-1006, 1022-1037) */
+    int32_t reserved3;
 } mpm_step_plan;
 int mpm_enqueue_steps(const mpm_step_plan *plan, int32_t first_step, int32_t n_steps, void *stream);
 

@@ -89,6 +89,7 @@ class StepPlan(C.Structure):
         ("signal_word", p_void), ("guard_host", p_void),
         ("peer_raw", (p_void * MPM_MAX_PEERS) * 2), ("peer_touched", (p_void * MPM_MAX_PEERS) * 2),
         ("time_events", p_void * (2 * MAX_STATUS_RING)),
+        ("full_clear_first", i32), ("reserved3", i32),
     ]
 
 
@@ -103,13 +104,15 @@ class RebuildPlan(C.Structure):
         ("table_codes", p_void), ("table_origin", p_void), ("table_neighbor", p_void),
         ("vel", p_void), ("raw_par", p_void), ("touched_par", p_void), ("cap_nodes", i32),
         ("node_bytes", i32), ("scalars_dev", p_void), ("scalars_host", p_void),
+        ("p2g_params", p_void), ("p2g_status", p_void), ("grid_params", p_void),
+        ("grid_reset_status", p_void), ("vel_old", p_void),
     ]
 
 
 class RebuildResult(C.Structure):
     _fields_ = [(k, i32) for k in ("n", "n_gblocks", "count", "n_groups", "bad_particle", "bad_block",
                                    "need_hash", "need_gblocks", "need_table", "need_groups",
-                                   "need_nodes", "reserved")]
+                                   "need_nodes", "tail_done")]
 
 
 NEED_CAPACITY = 1

@@ -106,5 +106,23 @@ extern "C" int mpm_rebuild(const mpm_rebuild_plan *p, mpm_rebuild_result *r, voi
         rc = mpm_clear(p->raw_par, p->touched_par, r->count, 1, p->node_bytes, nullptr, stream);
         if (rc != MPM_OK) return rc;
     }
+    if (p->p2g_params && p->grid_params && r->count > 0) {
+        // the rest of the rebuild step: P2G of the new store, then reduce + update
+        mpm_table_view tv;
+        memset(&tv, 0, sizeof tv);
+        tv.codes = p->table_codes;
+        tv.origin = p->table_origin;
+        tv.neighbor = p->table_neighbor;
+        tv.count = r->count;
+        tv.n_gblocks = n_g;
+        if (r->n_groups > 0) {
+            rc = mpm_p2g(&ns, &tv, p->raw_par, p->touched_par, p->p2g_params, p->p2g_status, nullptr, stream);
+            if (rc != MPM_OK) return rc;
+        }
+        rc = mpm_grid_update(p->raw_par, p->touched_par, p->vel, p->vel_old, &tv, p->grid_params,
+                             p->grid_reset_status, nullptr, stream);
+        if (rc != MPM_OK) return rc;
+        r->tail_done = 1;
+    }
     return mpm::check_launch("mpm_rebuild", 0);
 }

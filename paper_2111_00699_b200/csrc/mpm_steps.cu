@@ -50,7 +50,13 @@ extern "C" int mpm_enqueue_steps(const mpm_step_plan *p, int32_t first_step, int
         int rc;
         // after the first step of a batch the gather dt is the batch's own dt (pipeline.py:1230)
         if (k > 0) tp.dt_gather = tp.dt;
-        if (!gp.fuse_clear) {
+        if (k == 0 && p->full_clear_first) {
+            // first use of the parity the last rebuild left untouched: every row, not only the
+            // touched ones (pipeline.py:1022-1037)
+            rc = mpm_clear(p->raw[par], p->touched[par], p->table.count, 1, gp.deterministic ? 32 : 16, &guard,
+                           stream);
+            if (rc != MPM_OK) return rc;
+        } else if (!gp.fuse_clear) {
             // Worker._clear (pipeline.py:1022-1037): rows of this parity touched two steps ago
             rc = mpm_clear(p->raw[par], p->touched[par], p->table.count, 0, gp.deterministic ? 32 : 16, &guard,
                            stream);

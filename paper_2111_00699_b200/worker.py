@@ -565,6 +565,8 @@ class CudaWorker:
         self._scratch = {}
         self._scratch_allocs = 0
         self.kernel_calls = 0
+        self._tail_done = False
+        self._time_rot = 0
         self.time_kernels = False     # bench: CUDA events around the step kernels
         self.pipelined = True         # run_frame enqueues step s+1 before reading step s's flag
         self.batch_steps = _BATCH     # fixed-dt frames: steps per mpm_enqueue_steps call (0 = off)
@@ -797,9 +799,16 @@ class CudaWorker:
             self._flush_gather()
 
     # -- batched steady state (fixed dt): mpm_enqueue_steps ------------------------------------
-    def _can_batch(self):
-        if self.flags.rebuild_needed or self._pending_full_clear_parity != -1:
+    def _can_batch(self, next_step=None):
+        if self.flags.rebuild_needed:
             return False
+        if self._pending_full_clear_parity != -1:
+            # the first batch after a rebuild clears the parity the rebuild left untouched itself
+            # (mpm_step_plan.full_clear_first); callers that do not say which step comes next
+            # (peer.py) take the plain step
+            if next_step is None or next_step != self._global_step or \
+                    self._pending_full_clear_parity != (next_step & 1):
+                return False
         if not self.store.n_groups or self.store.staged_count:
             return False
         if self.options.transfer == "g2p2g":
@@ -844,19 +853,25 @@ class CudaWorker:
         next_step = self._global_step
         tbase = 0
         while self._frame_steps < spf:
-            while len(pending) < 2 and enq < spf and self._can_batch():
+            while len(pending) < 2 and enq < spf and self._can_batch(next_step):
                 n = min(self.batch_steps, spf - enq)
                 plan = self._step_plan()
+                plan.full_clear_first = int(self._pending_full_clear_parity != -1)
+                self._pending_full_clear_parity = -1
                 tev = None
                 for k in range(2 * n):
                     plan.time_events[k] = None
                 if self.time_kernels:
-                    # the FIRST step of a batch is timed: an event between two kernels of the chain
+                    # ONE step of a batch is timed: an event between two kernels of the chain
                     # serialises them fully (no programmatic dependent launch across it), so the
-                    # other steps run exactly as they do untimed
-                    tev = tbase
-                    plan.time_events[0] = self._time_events[2 * tbase].cuda_event
-                    plan.time_events[1] = self._time_events[2 * tbase + 1].cuda_event
+                    # other steps run exactly as they do untimed.  Its position rotates from batch
+                    # to batch: the first step after a rebuild (freshly sorted lanes, cold L2) must
+                    # not be over-represented in the mean.
+                    tk = self._time_rot % n
+                    self._time_rot += 1
+                    tev = (tbase, tk)
+                    plan.time_events[2 * tk] = self._time_events[2 * tbase].cuda_event
+                    plan.time_events[2 * tk + 1] = self._time_events[2 * tbase + 1].cuda_event
                     tbase = (tbase + _BATCH) % (2 * _BATCH)
                 # the first step of a batch gathers with the dt of the last grid update done
                 plan.transfer.dt_gather = float(self._vel_dt if not pending else self.dt)
@@ -888,10 +903,10 @@ class CudaWorker:
                 step = first + k
                 self._slot_clean[step % _RING] = False
                 self._consume(step % _RING, step)
-                if tev is not None and k == 0:
+                if tev is not None and k == tev[1]:
                     name = "mpm_g2p2g" if self.options.transfer == "g2p2g" else "mpm_p2g"
-                    self.kernel_events.append((name, self._time_events[2 * tev],
-                                               self._time_events[2 * tev + 1]))
+                    self.kernel_events.append((name, self._time_events[2 * tev[0]],
+                                               self._time_events[2 * tev[0] + 1]))
                 # step `step` itself ran to completion (the guard only stops LATER steps)
                 self._global_step = step + 1
                 self._vel_dt = self.dt
@@ -935,13 +950,15 @@ class CudaWorker:
                 # the flush's status block is read at the rebuild's first host sync, not before
                 # its first kernels are enqueued (one device idle gap less per rebuild)
                 flushed = self._flush_gather(defer=True)
-            self._rebuild(step, par, flushed)
+            self._rebuild(step, par, flushed, tail=self._rebuild_tail_ok())
             rebuilt = True
         else:
             self._clear(par)
         fused_now = self._fused_active()
         self.flags.fused_mode = fused_now
-        if fused_now and self._pending_gather:
+        if self._tail_done:
+            pass        # mpm_rebuild issued the P2G (and the grid update) of this step itself
+        elif fused_now and self._pending_gather:
             self._run_g2p2g(step, par)
         else:
             if self._pending_gather:
@@ -978,7 +995,17 @@ class CudaWorker:
             return False
         return True
 
-    def _rebuild(self, step, par, flushed=None):
+    def _rebuild_tail_ok(self):
+        """A single worker lets mpm_rebuild issue the rest of the rebuild step (P2G, grid update)
+        behind the rebuild kernels; workers with peers publish / meet / re-tag in between."""
+        cls = type(self)
+        return (self.runtime.n_workers == 1 and self._guard is None
+                and cls._publish is CudaWorker._publish
+                and cls._reduce_and_update is CudaWorker._reduce_and_update
+                and cls._run_p2g is CudaWorker._run_p2g
+                and not self.options.collect_conservation and not self.params.flip_blend > 0.0)
+
+    def _rebuild(self, step, par, flushed=None, tail=False):
         """Worker._rebuild (pipeline.py:958-1015) on the device: one call (mpm_rebuild) that issues
         every rebuild kernel and takes the two host syncs of the paper's rebuild (block count,
         then pblock + group counts) in C.  Buffers stay Python's: they are sized
@@ -1015,6 +1042,16 @@ class CudaWorker:
         plan.scan = S("scan", n_upper // 16 + 1024).ptr      # block sums of the largest scan
         plan.node_bytes = self._node_bytes
         plan.scalars_dev, plan.scalars_host = self._scalars.data_ptr(), self._scalars_host.data_ptr()
+        if tail:
+            # rest of the step (step_pre_barrier / step_post_barrier): P2G into status slot `step`,
+            # grid update that also zeroes the status block of the gather following it
+            tp, gp = self._params(), self._grid_params()
+            gp.fuse_clear = int(self.fuse_clear)
+            reset_slot = (step + 1 if self._fused_active() else step) % _RING
+            plan.p2g_params, plan.grid_params = C.addressof(tp), C.addressof(gp)
+            plan.p2g_status = self._status_ptr(step % _RING)
+            plan.grid_reset_status = self._status_ptr(reset_slot)
+            self._tail_reset_slot = reset_slot
         while True:
             # block-indexed scratch and tables; codes/origin/touched sized for the worst case of the
             # dilation, 27 n_g (they are small)
@@ -1087,6 +1124,7 @@ class CudaWorker:
         gr.count = count
         for k in (0, 1):
             tb._touched[k].len = count
+        self._tail_done = bool(res.tail_done)
         self._pending_full_clear_parity = 1 - par
         self._plan = None             # buffers may have moved: the batched-step plan is rebuilt
         self._published_codes = (tb._codes, count)
@@ -1266,6 +1304,12 @@ class CudaWorker:
         """pipeline.py:1166-1231 in one kernel: reduce over peers, finalize, boundary."""
         if step is None:
             step = self._global_step
+        if self._tail_done:
+            # issued by mpm_rebuild behind the P2G of this (rebuild) step
+            self._tail_done = False
+            self._slot_clean[self._tail_reset_slot] = True     # the slot that update zeroed
+            self._vel_dt = self.dt
+            return
         tb, gr = self.table, self.grid
         count = tb.count
         stream = _stream_ptr()
