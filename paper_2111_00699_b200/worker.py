@@ -624,14 +624,6 @@ class CudaWorker:
         self._scratch_allocs += buf.realloc_count - before
         return buf
 
-    def _read_scalars(self):
-        self._scalars_host.copy_(self._scalars, non_blocking=True)
-        torch.cuda.current_stream().synchronize()
-        return self._scalars_host.numpy()
-
-    def _sptr(self, k):
-        return self._scalars.data_ptr() + 4 * k
-
     @property
     def counters(self):
         host = self._status.cpu().numpy()
