@@ -203,6 +203,15 @@ def run_ours(args):
     pin_ids = torch.from_numpy(np.ascontiguousarray(part, dtype=np.int64)).pin_memory()
 
     halo = os.environ.get("MPM_HALO", "peer")   # peer: rows read in place over NVLink (peer.py); sendrecv: NCCL
+    if world > 1 and halo == "peer":
+        # peer memory must really be reachable from every rank's device; if not (no P2P between two
+        # of the GPUs, IPC disabled in the container) the literal send/recv protocol still runs
+        from paper_2111_00699_b200.peer import PeerRuntime
+        if not PeerRuntime(dev, initial_vmax=vmax0).probe():
+            halo = "sendrecv"
+            if rank == 0:
+                print("peer-mapped memory is not available on this box: halo rows over send/recv",
+                      file=sys.stderr, flush=True)
 
     def fresh_worker():
         if world > 1:

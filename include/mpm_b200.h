@@ -140,6 +140,8 @@ void *mpm_host_alias(void *pinned_host);
  * exporter's allocation; one open per (process, handle). */
 int mpm_ipc_open(const void *handle64, void **base_out);
 int mpm_ipc_close(void *base);
+/* *out_host = *dev_ptr (blocking): probe of a mapping opened with mpm_ipc_open. */
+int mpm_peek_i32(const int32_t *dev_ptr, int32_t *out_host);
 
 /* Host rendezvous of the ranks of ONE node over a shared-memory segment mapped by the caller
  * (zero-filled, >= mpm_shm_bytes(n_ranks) long): the SpinBarrier + shared Python state of the

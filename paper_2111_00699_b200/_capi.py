@@ -166,6 +166,7 @@ _SIGNATURES = {
     "mpm_host_alias": [p_void],
     "mpm_ipc_open": [C.c_char_p, C.POINTER(p_void)],
     "mpm_ipc_close": [p_void],
+    "mpm_peek_i32": [p_void, p_void],
     "mpm_shm_bytes": [i32],
     "mpm_shm_allgather_i64": [p_void, i32, i32, p_void, i32, p_void, i32],
 }

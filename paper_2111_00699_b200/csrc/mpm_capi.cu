@@ -77,6 +77,20 @@ int mpm_ipc_open(const void *handle64, void **base_out)
     return MPM_OK;
 }
 
+// One word read back from a device pointer (blocking): the probe a rank uses to check that a
+// peer mapping really is reachable from its device before it relies on it.
+int mpm_peek_i32(const int32_t *dev_ptr, int32_t *out_host)
+{
+    if (!dev_ptr || !out_host) return MPM_ERR_REJECTED_INPUT;
+    cudaError_t e = cudaMemcpy(out_host, dev_ptr, sizeof(int32_t), cudaMemcpyDeviceToHost);
+    if (e != cudaSuccess) {
+        cudaGetLastError();
+        mpm::set_last_error("mpm_peek_i32", e);
+        return MPM_ERR_RESOURCE;
+    }
+    return MPM_OK;
+}
+
 int mpm_ipc_close(void *base)
 {
     if (!base) return MPM_OK;

@@ -113,6 +113,28 @@ class PeerRuntime(DistRuntime):
     def host_barrier(self):
         self.all_gather_i64([0])
 
+    def probe(self) -> bool:
+        """Collective.  True when every rank can map every other rank's device memory and read
+        it from its own device (CUDA IPC + peer access): what PeerDistWorker relies on.  A caller
+        falls back to the send/recv transport (dist.py) when this says no."""
+        mine = torch.full((16,), self.wid + 1, dtype=torch.int32, device=self.device)
+        torch.cuda.synchronize(self.device)
+        ok = 1
+        try:
+            mem = self.exchange_tensors({"probe": mine})
+        except Exception:
+            mem, ok = None, 0
+        if mem is not None:
+            lib = _capi.lib()
+            for q, m in enumerate(mem):
+                if q == self.wid:
+                    continue
+                word = C.c_int32(0)
+                if lib.mpm_peek_i32(m["probe"].data_ptr(), C.byref(word)) != 0 or word.value != q + 1:
+                    ok = 0
+        self._probe_keepalive = mine
+        return bool(DistRuntime.all_gather_i64(self, [ok])[:, 0].all())
+
     def exchange_tensors(self, named: dict):
         """Collective.  Returns one dict per rank of objects with .data_ptr() addressing THAT
         rank's device memory from this rank's device (this rank's own entry holds the tensors
@@ -124,6 +146,34 @@ class PeerRuntime(DistRuntime):
         (torch.multiprocessing.reductions) maps the block in a context of the exporting device,
         which is what a tensor living "on cuda:q" needs, but not what a kernel running on this
         rank's GPU needs: that takes a mapping (and peer access) in this rank's context."""
+        try:
+            payload = self._export_payload(named)
+        except Exception as exc:            # stay in step with the other ranks: fail after the collective
+            payload, failure = None, exc
+        gathered = [None] * self.n_workers
+        dist.all_gather_object(gathered, payload, group=self.group)
+        if any(pl is None for pl in gathered):
+            raise ResourceError("a rank could not export its device buffers over CUDA IPC"
+                                + (f": {failure}" if payload is None else ""))
+        lib = _capi.lib()
+        out = []
+        for q, pl in enumerate(gathered):
+            if q == self.wid:
+                out.append(dict(named))
+                continue
+            mem = {}
+            for k, (handle, offset, nbytes) in pl.items():
+                base = self._ipc_open.get((q, handle))
+                if base is None:
+                    ptr = C.c_void_p()
+                    _capi.check(lib.mpm_ipc_open(handle, C.byref(ptr)), "mpm_ipc_open")
+                    base = self._ipc_open[(q, handle)] = int(ptr.value)
+                mem[k] = MappedMemory(base + offset, nbytes)
+            out.append(mem)
+        return out
+
+    @staticmethod
+    def _export_payload(named: dict):
         payload = {}
         for k, t in named.items():
             st = t.untyped_storage()
@@ -141,24 +191,7 @@ class PeerRuntime(DistRuntime):
                 raise ResourceError(f"unexpected CUDA IPC handle of {len(handle)} bytes")
             payload[k] = (handle, int(block_offset) + t.storage_offset() * t.element_size(),
                           t.numel() * t.element_size())
-        gathered = [None] * self.n_workers
-        dist.all_gather_object(gathered, payload, group=self.group)
-        lib = _capi.lib()
-        out = []
-        for q, pl in enumerate(gathered):
-            if q == self.wid:
-                out.append(dict(named))
-                continue
-            mem = {}
-            for k, (handle, offset, nbytes) in pl.items():
-                base = self._ipc_open.get((q, handle))
-                if base is None:
-                    ptr = C.c_void_p()
-                    _capi.check(lib.mpm_ipc_open(handle, C.byref(ptr)), "mpm_ipc_open")
-                    base = self._ipc_open[(q, handle)] = int(ptr.value)
-                mem[k] = MappedMemory(base + offset, nbytes)
-            out.append(mem)
-        return out
+        return payload
 
     _ipc_open: dict = {}     # (rank, handle) -> base address in this process; process-wide, never closed
                              # while the group lives (the exporter's caching allocator keeps its blocks)
