@@ -155,6 +155,12 @@ int mpm_shm_allgather_i64(void *base, int32_t n_ranks, int32_t rank, const int64
 
 /* ---- rebuild-mapping: Worker._rebuild (pipeline.py:958-1015) ------------------------ */
 
+/* Staged particles (ParticleStore.stage_append, particles.py:309-334) as the flat channel rows the
+ * rebuild reads: flat[i][nch] from compact pos[n][3], vel[n][3] and mass[n] (or mass_scalar when
+ * mass is NULL), with the defaults F = I (J = 1), C = 0, plastic scalar at rest. */
+int mpm_stage_particles(const float *pos, const float *vel, const float *mass, float mass_scalar, int32_t n,
+                        int32_t nch, int32_t mat_kind, float *flat, void *stream);
+
 /* Compaction of the live lanes of the old store into rebuild input order
  * (ParticleStore.gather_flat, particles.py:336-358; _gather_live, particles.py:177-188):
  * group-major, lane-minor, quarantined lanes dropped (drop_quarantined=1) or kept.

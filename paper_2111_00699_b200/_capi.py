@@ -126,6 +126,7 @@ _STATUS_TO_ERROR = {
 
 # name -> argtypes; every function returns int (mpm_status) unless listed in _RESTYPES
 _SIGNATURES = {
+    "mpm_stage_particles": [p_void, p_void, p_void, C.c_float, i32, i32, i32, p_void, p_void],
     "mpm_compact_live": [C.POINTER(StoreView), i32, p_void, p_void, p_void, p_void, p_void],
     "mpm_particle_codes": [C.POINTER(StoreView), p_void, p_void, p_void, i32, i32, f64, p_void,
                            p_void, p_void, p_void],

@@ -627,7 +627,43 @@ using namespace mpm;
 
 static inline int nblk(int64_t n, int t) { return (int)((n + t - 1) / t); }
 
+// Flat channel rows [n][nch] of staged particles from compact x, v, m (ParticleStore.stage_append
+// defaults, particles.py:309-334): F = I (J = 1 for the fluid), C = 0, plastic scalar at rest.
+// One thread per (particle, channel): coalesced stores of the 100-byte rows.
+__global__ void __launch_bounds__(256) stage_particles_kernel(const float *__restrict__ pos,
+                                                              const float *__restrict__ vel,
+                                                              const float *__restrict__ mass, float mass_scalar,
+                                                              long long n_elems, int nch, int mat_kind,
+                                                              float *__restrict__ flat)
+{
+    pdl_wait();
+    pdl_launch_dependents();
+    const long long e = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+    if (e >= n_elems) return;
+    const long long i = e / nch;
+    const int c = (int)(e - i * nch);
+    float v = 0.0f;
+    if (c < CH_VEL) v = pos[i * 3 + c];
+    else if (c < CH_C) v = vel[i * 3 + (c - CH_VEL)];
+    else if (c == CH_MASS) v = mass ? mass[i] : mass_scalar;
+    else if (c == CH_DEF) v = 1.0f;
+    else if (mat_kind != MPM_MAT_FLUID && (c == CH_DEF + 4 || c == CH_DEF + 8)) v = 1.0f;
+    else if (c == CH_PLASTIC && mat_kind == MPM_MAT_SNOW) v = 1.0f;
+    flat[e] = v;
+}
+
 extern "C" {
+
+int mpm_stage_particles(const float *pos, const float *vel, const float *mass, float mass_scalar, int32_t n,
+                        int32_t nch, int32_t mat_kind, float *flat, void *stream_)
+{
+    if (n <= 0) return MPM_OK;
+    if (!pos || !vel || !flat || nch <= CH_DEF) return MPM_ERR_REJECTED_INPUT;
+    const long long n_elems = (long long)n * nch;
+    launch_chained(stage_particles_kernel, nblk(n_elems, 256), 256, (cudaStream_t)stream_, pos, vel, mass,
+                   mass_scalar, n_elems, nch, mat_kind, flat);
+    return check_launch("mpm_stage_particles", 1);
+}
 
 int mpm_compact_live(const mpm_store_view *store, int drop_quarantined, int32_t *group_live_scratch,
                      int32_t *src_slot, int32_t *n_live, int32_t *scan_scratch, void *stream_)

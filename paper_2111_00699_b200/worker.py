@@ -183,24 +183,29 @@ class CudaParticleStore:
         dev = self.device
         if all(isinstance(e[0], torch.Tensor) for e in self._staged):
             # tensors (ideally pinned): straight H2D copies into the flat rows
-            flat = torch.zeros((n, self.nch), dtype=torch.float32, device=dev)
+            # the rows are laid out by one kernel per staged batch (mpm_stage_particles)
+            flat = torch.empty((n, self.nch), dtype=torch.float32, device=dev)
             dids = torch.empty(n, dtype=torch.int64, device=dev)
+            lib, stream = _capi.lib(), _stream_ptr()
             o = 0
             for tp, tv, tm, _, _, ti in self._staged:
                 k = tp.shape[0]
-                flat[o:o + k, CH_POS:CH_POS + 3] = tp.to(dev, non_blocking=True)
-                flat[o:o + k, CH_VEL:CH_VEL + 3] = tv.to(dev, non_blocking=True)
+                dpos, dvel = tp.to(dev, non_blocking=True), tv.to(dev, non_blocking=True)
+                dmass, scalar = None, 0.0
                 if isinstance(tm, torch.Tensor):
-                    flat[o:o + k, CH_MASS] = tm.to(dev, torch.float32, non_blocking=True)
+                    dmass = tm.to(dev, torch.float32, non_blocking=True).contiguous()
                 elif tm.ndim:
-                    flat[o:o + k, CH_MASS] = torch.from_numpy(np.broadcast_to(tm, (k,)).copy()).to(dev)
+                    dmass = torch.from_numpy(np.ascontiguousarray(np.broadcast_to(tm, (k,)))).to(dev)
                 else:
-                    flat[o:o + k, CH_MASS] = float(tm)
+                    scalar = float(tm)
+                check(lib.mpm_stage_particles(dpos.data_ptr(), dvel.data_ptr(),
+                                              dmass.data_ptr() if dmass is not None else None, scalar, k,
+                                              self.nch, self.kind, flat.data_ptr() + 4 * o * self.nch, stream),
+                      "mpm_stage_particles")
                 dids[o:o + k] = ti.to(dev, non_blocking=True)
                 o += k
             self._staged.clear()
             self.staged_count = 0
-            self._default_state(flat)
             return flat, dids, n
         self._staged = [tuple(x.numpy() if isinstance(x, torch.Tensor) else x for x in e)
                         for e in self._staged]
