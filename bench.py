@@ -389,9 +389,9 @@ def run_ours(args):
 
 # dram__bytes_read.sum + dram__bytes_write.sum of the dominant kernel, per launch, from the
 # committed `ncu --set full` capture of the fused kernel on the 1.37 M scene
-# (profiles/r1_i_fused_snow_v4_metrics.csv: 96.4 MB read + 55.7 MB write; r1_i_fused_snow_fc_v4: 89.7 + 39.4);
+# (profiles/r1_l_fused_snow_final_metrics.csv: 96.5 MB read + 52.7 MB write; r1_l_fused_snow_fc_final: 89.8 + 40.8);
 # only quoted for those scenes
-TRAFFIC_NCU = {"snow": 152.1e6, "snow_fc": 129.1e6}
+TRAFFIC_NCU = {"snow": 149.2e6, "snow_fc": 130.5e6}
 
 
 def run_fountain(args):
