@@ -57,7 +57,7 @@ def build_halo_lists(peer_map: torch.Tensor):
 class DistRuntime:
     """SharedRuntime (multiworker.py:73-107) across processes."""
 
-    def __init__(self, device, initial_vmax: float = 0.0, group=None):
+    def __init__(self, device, initial_vmax: float = 0.0, group=None, host_timeout_ms: int = 120000):
         self.group = group
         self.n_workers = dist.get_world_size(group)
         self.wid = dist.get_rank(group)
@@ -68,13 +68,68 @@ class DistRuntime:
         self._vmax = np.full((3, self.n_workers), float(initial_vmax))
         self._local_vmax = {}
         self.peer_counts = [0] * self.n_workers
+        self.host_timeout_ms = int(host_timeout_ms)
+        self._shm = self._shm_base = None
+        self._setup_shm()
+
+    def _setup_shm(self):
+        """Map one zero-filled segment under /dev/shm into every rank when all of them run on one
+        host (one process per GPU of a box): the step barrier and the few integers per rank that
+        go with it then cost microseconds (mpm_shm_allgather_i64) instead of a library collective
+        (kernel launch + device round trip + stream sync with NCCL).  Rank 0 creates the file and
+        unlinks it once everybody has it open, so nothing outlives the processes.  Ranks on
+        different hosts, no /dev/shm, or MPM_SHM=0: the small collectives stay on
+        torch.distributed."""
+        import mmap
+        import os
+        import socket
+        import uuid
+        hosts = [None] * self.n_workers
+        dist.all_gather_object(hosts, socket.gethostname(), group=self.group)
+        one_host = len(set(hosts)) == 1 and os.environ.get("MPM_SHM", "1") != "0"
+        lib = _capi.lib()
+        size = int(lib.mpm_shm_bytes(self.n_workers))
+        path = [None]
+        if self.wid == 0 and one_host and os.path.isdir("/dev/shm"):
+            path[0] = f"/dev/shm/mpm_b200_{os.getpid()}_{uuid.uuid4().hex}"
+            with open(path[0], "wb") as f:
+                f.truncate(size)
+        dist.broadcast_object_list(path, src=0, group=self.group)
+        mm = None
+        if path[0] is not None:
+            try:
+                fd = os.open(path[0], os.O_RDWR)
+                try:
+                    mm = mmap.mmap(fd, size)
+                finally:
+                    os.close(fd)
+            except OSError:
+                mm = None
+        ok = self._all_gather_i64_dist([int(mm is not None)])[:, 0].all()     # also: everybody has it open
+        if self.wid == 0 and path[0] is not None:
+            os.unlink(path[0])
+        if ok:
+            self._shm = mm
+            self._shm_base = C.addressof(C.c_char.from_buffer(mm))
 
     # -- transport helpers ----------------------------------------------------------------
     def _wire(self, t: torch.Tensor) -> torch.Tensor:
         return t.cpu() if self.stage_on_host else t
 
     def all_gather_i64(self, values) -> np.ndarray:
-        """One small all_gather: [n_workers, len(values)] on the host."""
+        """One small all_gather, [n_workers, len(values)] on the host, and a full barrier: through
+        the shared segment when there is one."""
+        if self._shm_base is None or len(values) > _capi.SHM_MAX_VALUES:
+            return self._all_gather_i64_dist(values)
+        n = len(values)
+        mine = (C.c_int64 * max(n, 1))(*[int(v) for v in values])
+        out = np.empty((self.n_workers, n), dtype=np.int64)
+        _capi.check(_capi.lib().mpm_shm_allgather_i64(self._shm_base, self.n_workers, self.wid, mine, n,
+                                                      out.ctypes.data, self.host_timeout_ms),
+                    "mpm_shm_allgather_i64")
+        return out
+
+    def _all_gather_i64_dist(self, values) -> np.ndarray:
         dev = torch.device("cpu") if (self.stage_on_host or self.device.type == "cpu") else self.device
         mine = torch.tensor(values, dtype=torch.int64, device=dev)
         out = torch.empty((self.n_workers, len(values)), dtype=torch.int64, device=dev)

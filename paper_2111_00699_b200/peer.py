@@ -59,57 +59,6 @@ SKIPPED, DONE, RAISED = 0, 1, 2
 class PeerRuntime(DistRuntime):
     """DistRuntime + mapping of the other ranks' device buffers into this process."""
 
-    def __init__(self, device, initial_vmax: float = 0.0, group=None, host_timeout_ms: int = 120000):
-        super().__init__(device, initial_vmax, group)
-        self.host_timeout_ms = int(host_timeout_ms)
-        self._shm = self._shm_base = None
-        self._setup_shm()
-
-    def _setup_shm(self):
-        """Map one zero-filled segment under /dev/shm into every rank (all ranks of a PeerRuntime
-        share a host: they map each other's device memory).  Rank 0 creates the file and unlinks
-        it once everybody has it open, so nothing outlives the processes.  Without /dev/shm the
-        small collectives stay on torch.distributed."""
-        import mmap
-        import os
-        import uuid
-        lib = _capi.lib()
-        size = int(lib.mpm_shm_bytes(self.n_workers))
-        path = [None]
-        if self.wid == 0 and os.path.isdir("/dev/shm"):
-            path[0] = f"/dev/shm/mpm_b200_{os.getpid()}_{uuid.uuid4().hex}"
-            with open(path[0], "wb") as f:
-                f.truncate(size)
-        dist.broadcast_object_list(path, src=0, group=self.group)
-        mm = None
-        if path[0] is not None:
-            try:
-                fd = os.open(path[0], os.O_RDWR)
-                try:
-                    mm = mmap.mmap(fd, size)
-                finally:
-                    os.close(fd)
-            except OSError:
-                mm = None
-        ok = super().all_gather_i64([int(mm is not None)])[:, 0].all()     # also: everybody has it open
-        if self.wid == 0 and path[0] is not None:
-            os.unlink(path[0])
-        if ok:
-            self._shm = mm
-            self._shm_base = C.addressof(C.c_char.from_buffer(mm))
-
-    def all_gather_i64(self, values) -> np.ndarray:
-        """[n_workers, len(values)] on the host, through the shared segment (a full barrier)."""
-        if self._shm_base is None or len(values) > _capi.SHM_MAX_VALUES:
-            return super().all_gather_i64(values)
-        n = len(values)
-        mine = (C.c_int64 * max(n, 1))(*[int(v) for v in values])
-        out = np.empty((self.n_workers, n), dtype=np.int64)
-        _capi.check(_capi.lib().mpm_shm_allgather_i64(self._shm_base, self.n_workers, self.wid, mine, n,
-                                                      out.ctypes.data, self.host_timeout_ms),
-                    "mpm_shm_allgather_i64")
-        return out
-
     def host_barrier(self):
         self.all_gather_i64([0])
 
@@ -133,7 +82,7 @@ class PeerRuntime(DistRuntime):
                 if lib.mpm_peek_i32(m["probe"].data_ptr(), C.byref(word)) != 0 or word.value != q + 1:
                     ok = 0
         self._probe_keepalive = mine
-        return bool(DistRuntime.all_gather_i64(self, [ok])[:, 0].all())
+        return bool(self.all_gather_i64([ok])[:, 0].all())
 
     def exchange_tensors(self, named: dict):
         """Collective.  Returns one dict per rank of objects with .data_ptr() addressing THAT
