@@ -388,3 +388,34 @@ def test_lazy_flush_defers_the_frame_end_gather_until_the_store_is_read():
     # flush the full one: the rebuild cadence may differ by a step, the particles may not
     assert abs(len(wa.rebuild_steps) - len(wb.rebuild_steps)) <= 1
     assert wb.store.total_mass() == pytest.approx(wa.store.total_mass(), rel=1e-7)
+
+
+def test_sparse_world_one_particle_per_block_grows_the_hash_table():
+    """Edge case of the rebuild: 2 500 particles, each alone in its own gblock (ragged groups of
+    one lane, 27-block halos that overlap), so the block count outgrows the first hash capacity
+    (mpm_rebuild answers MPM_NEED_CAPACITY, the table is re-inserted at four times the size) and
+    every capacity bound of the plan is exercised.  Tables, groups and keys bit-exact against the
+    oracle; one substep within the fp32 bars."""
+    from paper_2111_00699_b200 import Material, SimParams
+    rng = np.random.default_rng(7)
+    dx = 0.5
+    lattice = np.stack(np.meshgrid(np.arange(25), np.arange(10), np.arange(10), indexing="ij"), -1).reshape(-1, 3)
+    pos = ((lattice * 8 + 16) + rng.uniform(0.6, 3.4, lattice.shape)) * dx      # 8-cell pitch: own 4-cell block
+    pos = pos.astype(np.float32).astype(np.float64)
+    vel = rng.normal(0.0, 20.0, pos.shape).astype(np.float32).astype(np.float64)
+    material = Material.fixed_corotated(2.0, 1.0e5, 0.3)
+    params = SimParams(dx=dx, dt=1e-4)
+    wc = U.cuda_worker(pos, vel, 0.25, material, params, None, transfer="split")
+    wo = U.oracle_worker(pos, vel, 0.25, material, params, None, transfer="split")
+    wc.run_step(0)
+    wo.run_step(0)
+    assert wc.table.n_gblocks == len(pos) == wo.table.n_gblocks
+    assert wc.table.hash_cap >= 8 * len(pos)            # grown past the initial 4096 entries
+    assert np.array_equal(wc.table.codes, wo.table.codes[:wo.table.count])
+    assert np.array_equal(wc.table.neighbor, wo.table.neighbor[:wo.table.n_gblocks])
+    assert np.array_equal(wc.store.orig_id, wo.store.orig_id[:wo.store.n_groups])
+    assert np.array_equal(wc.store.group_len, wo.store.group_len[:wo.store.n_groups])
+    assert np.array_equal(wc.store.lane_key, wo.store.lane_key[:wo.store.n_groups])
+    edge = float(pos.max() - pos.min())
+    ex, ev, ef, _ = U.particle_errors(U.state_by_id(wc), U.state_by_id(wo), edge, 9)
+    assert ex <= U.X_RTOL and ev <= U.V_RTOL and ef <= U.F_ATOL, (ex, ev, ef)
