@@ -2,7 +2,7 @@
 kernels are launched from C but belong to this process, so they are all seen): busy time per
 kernel, idle gaps of the device and what surrounds them.
 
-    python scripts/gpu_timeline.py [scene] [frames]     (on a GPU box)
+    python scripts/gpu_timeline.py [scene] [frames] [N rank]     (on a GPU box; N rank = one slab of N)
 """
 import collections, json, os, sys, tempfile
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
@@ -15,6 +15,11 @@ from paper_2111_00699_b200.worker import CudaWorker
 scene = sys.argv[1] if len(sys.argv) > 1 else "snow"
 frames = int(sys.argv[2]) if len(sys.argv) > 2 else 4
 W = bench.build_world(scene)
+if len(sys.argv) > 4:
+    # one rank's slab of the scene run alone: python scripts/gpu_timeline.py snow 4 8 0
+    from paper_2111_00699_b200 import partition_particles
+    part = partition_particles(W.positions, int(sys.argv[3]))[int(sys.argv[4])]
+    W.positions, W.velocities = W.positions[part], W.velocities[part]
 n = len(W.positions)
 w = CudaWorker(0, SharedRuntime(1, 150.0), W.params, W.material, W.boundary,
                PipelineOptions(transfer="g2p2g", fused_threshold=1 << 62), count_stats=False,
