@@ -155,6 +155,9 @@ int mpm_shm_allgather_i64(void *base, int32_t n_ranks, int32_t rank, const int64
 
 /* ---- rebuild-mapping: Worker._rebuild (pipeline.py:958-1015) ------------------------ */
 
+/* dst[0..n) = value (device words: guard words, flags). */
+int mpm_fill_i32(int32_t *dst, int32_t n, int32_t value, void *stream);
+
 /* Staged particles (ParticleStore.stage_append, particles.py:309-334) as the flat channel rows the
  * rebuild reads: flat[i][nch] from compact pos[n][3], vel[n][3] and mass[n] (or mass_scalar when
  * mass is NULL), with the defaults F = I (J = 1), C = 0, plastic scalar at rest. */
@@ -272,6 +275,8 @@ typedef struct mpm_rebuild_plan {
     const struct mpm_grid_params *grid_params;
     struct mpm_step_status *grid_reset_status;
     float *vel_old;                    /* FLIP only */
+    int32_t *guard_word;               /* optional: reset to INT32_MAX first (the guard of the speculative
+                                          launches that asked for this rebuild, see mpm_guard) */
 } mpm_rebuild_plan;
 typedef struct mpm_rebuild_result {
     int32_t n, n_gblocks, count, n_groups;

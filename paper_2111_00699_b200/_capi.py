@@ -105,7 +105,7 @@ class RebuildPlan(C.Structure):
         ("vel", p_void), ("raw_par", p_void), ("touched_par", p_void), ("cap_nodes", i32),
         ("node_bytes", i32), ("scalars_dev", p_void), ("scalars_host", p_void),
         ("p2g_params", p_void), ("p2g_status", p_void), ("grid_params", p_void),
-        ("grid_reset_status", p_void), ("vel_old", p_void),
+        ("grid_reset_status", p_void), ("vel_old", p_void), ("guard_word", p_void),
     ]
 
 
@@ -126,6 +126,7 @@ _STATUS_TO_ERROR = {
 
 # name -> argtypes; every function returns int (mpm_status) unless listed in _RESTYPES
 _SIGNATURES = {
+    "mpm_fill_i32": [p_void, i32, i32, p_void],
     "mpm_stage_particles": [p_void, p_void, p_void, C.c_float, i32, i32, i32, p_void, p_void],
     "mpm_compact_live": [C.POINTER(StoreView), i32, p_void, p_void, p_void, p_void, p_void],
     "mpm_particle_codes": [C.POINTER(StoreView), p_void, p_void, p_void, i32, i32, f64, p_void,

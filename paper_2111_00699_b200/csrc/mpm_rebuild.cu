@@ -654,6 +654,14 @@ __global__ void __launch_bounds__(256) stage_particles_kernel(const float *__res
 
 extern "C" {
 
+int mpm_fill_i32(int32_t *dst, int32_t n, int32_t value, void *stream_)
+{
+    if (n <= 0) return MPM_OK;
+    if (!dst) return MPM_ERR_REJECTED_INPUT;
+    launch_chained(fill_i32_kernel, nblk(n, 256), 256, (cudaStream_t)stream_, dst, n, value);
+    return check_launch("mpm_fill_i32", 1);
+}
+
 int mpm_stage_particles(const float *pos, const float *vel, const float *mass, float mass_scalar, int32_t n,
                         int32_t nch, int32_t mat_kind, float *flat, void *stream_)
 {

@@ -38,6 +38,10 @@ extern "C" int mpm_rebuild(const mpm_rebuild_plan *p, mpm_rebuild_result *r, voi
     const float *staged = p->n_staged ? p->staged : nullptr;
     const int64_t *staged_ids = p->n_staged ? p->staged_ids : nullptr;
     int rc;
+    if (p->guard_word) {
+        rc = mpm_fill_i32(p->guard_word, 1, MPM_INT_MAX, stream);
+        if (rc != MPM_OK) return rc;
+    }
 
     // ---- particles -> codes -> gblocks (first sync: block count) ----------------------------
     rc = mpm_compact_live(&p->old_store, 1, p->glive, p->src_slot, S + 0, p->scan, stream);

@@ -320,7 +320,7 @@ class PeerDistWorker(DistWorker):
         torch.cuda.current_stream().synchronize()     # none of my kernels / remote atomics in flight
         self._check_wait_error()
         rt.host_barrier()                             # ... nor anybody else's
-        self._guard_word.fill_(_INT_MAX)
+        self._call("mpm_fill_i32", self._guard_word.data_ptr(), 1, _INT_MAX, _stream_ptr())
         torch.cuda.current_stream().synchronize()
         rt.host_barrier()                             # every copy of the guard is reset
         step = self._global_step

@@ -576,6 +576,8 @@ class CudaWorker:
         self.pipelined = True         # run_frame enqueues step s+1 before reading step s's flag
         self.batch_steps = _BATCH     # fixed-dt frames: steps per mpm_enqueue_steps call (0 = off)
         self._plan = None
+        self._plan_stale = True
+        self._guard_reset_in_rebuild = False
         self.speculative_discards = 0
         self.kernel_events = []
         self._frame_event_start = 0
@@ -778,7 +780,7 @@ class CudaWorker:
                     if self.flags.rebuild_needed:
                         # the step just enqueued was skipped on the device: undo it on the host
                         self._restore(snap)
-                        self._guard_word.fill_(_INT_MAX)
+                        self._call("mpm_fill_i32", self._guard_word.data_ptr(), 1, _INT_MAX, _stream_ptr())
                         self.speculative_discards += 1
                         continue
                 inflight = cur
@@ -788,7 +790,7 @@ class CudaWorker:
             if inflight is not None:
                 self._consume(*inflight)
                 if self.flags.rebuild_needed:
-                    self._guard_word.fill_(_INT_MAX)
+                    self._call("mpm_fill_i32", self._guard_word.data_ptr(), 1, _INT_MAX, _stream_ptr())
         finally:
             self._defer = False
             self._guard = None
@@ -814,14 +816,19 @@ class CudaWorker:
 
     def _step_plan(self):
         plan = self._plan
-        if plan is None:
-            plan = self._plan = _capi.StepPlan()
+        if plan is None or self._plan_stale:
+            # buffers may have moved at the last rebuild: the views are refreshed, the rest is static
             st, tb, gr = self.store, self.table, self.grid
+            if plan is None:
+                plan = _capi.StepPlan()
             plan.store, plan.table = st.view(), tb.view()
             for k in (0, 1):
                 plan.raw[k], plan.touched[k] = gr._raw[k].ptr, tb._touched[k].ptr
             plan.vel = gr._vel.ptr
             plan.vel_old = self._vel_old_ptr()
+            self._plan_stale = False
+        if self._plan is None:
+            self._plan = plan
             plan.fused = int(self.options.transfer == "g2p2g")
             plan.status_ring = _RING
             plan.status_dev = self._status.data_ptr()
@@ -916,7 +923,12 @@ class CudaWorker:
                     pending = []
                     enq = self._frame_steps
                     next_step = self._global_step
-                    self._guard_word.fill_(_INT_MAX)
+                    if self._rebuild_tail_ok_static():
+                        # nothing guarded is enqueued before the rebuild this flag asks for, and
+                        # mpm_rebuild resets the word itself (one launch and its gap less)
+                        self._guard_reset_in_rebuild = True
+                    else:
+                        self._call("mpm_fill_i32", self._guard_word.data_ptr(), 1, _INT_MAX, _stream_ptr())
                     break
         if self._pending_gather and not self.lazy_flush:
             self._flush_gather()
@@ -992,15 +1004,18 @@ class CudaWorker:
             return False
         return True
 
-    def _rebuild_tail_ok(self):
-        """A single worker lets mpm_rebuild issue the rest of the rebuild step (P2G, grid update)
-        behind the rebuild kernels; workers with peers publish / meet / re-tag in between."""
+    def _rebuild_tail_ok_static(self):
         cls = type(self)
-        return (self.runtime.n_workers == 1 and self._guard is None
+        return (self.runtime.n_workers == 1
                 and cls._publish is CudaWorker._publish
                 and cls._reduce_and_update is CudaWorker._reduce_and_update
                 and cls._run_p2g is CudaWorker._run_p2g
                 and not self.options.collect_conservation and not self.params.flip_blend > 0.0)
+
+    def _rebuild_tail_ok(self):
+        """A single worker lets mpm_rebuild issue the rest of the rebuild step (P2G, grid update)
+        behind the rebuild kernels; workers with peers publish / meet / re-tag in between."""
+        return self._guard is None and self._rebuild_tail_ok_static()
 
     def _rebuild(self, step, par, flushed=None, tail=False):
         """Worker._rebuild (pipeline.py:958-1015) on the device: one call (mpm_rebuild) that issues
@@ -1039,6 +1054,9 @@ class CudaWorker:
         plan.scan = S("scan", n_upper // 16 + 1024).ptr      # block sums of the largest scan
         plan.node_bytes = self._node_bytes
         plan.scalars_dev, plan.scalars_host = self._scalars.data_ptr(), self._scalars_host.data_ptr()
+        if self._guard_reset_in_rebuild:
+            plan.guard_word = self._guard_word.data_ptr()
+            self._guard_reset_in_rebuild = False
         if tail:
             # rest of the step (step_pre_barrier / step_post_barrier): P2G into status slot `step`,
             # grid update that also zeroes the status block of the gather following it
@@ -1123,7 +1141,7 @@ class CudaWorker:
             tb._touched[k].len = count
         self._tail_done = bool(res.tail_done)
         self._pending_full_clear_parity = 1 - par
-        self._plan = None             # buffers may have moved: the batched-step plan is rebuilt
+        self._plan_stale = True       # buffers may have moved: the batched-step plan refreshes its views
         self._published_codes = (tb._codes, count)
         self.flags.rebuild_needed = False
         self.flags.steps_since_rebuild = 0
