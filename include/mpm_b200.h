@@ -207,11 +207,14 @@ int mpm_dilate_and_link(const int64_t *gcodes, int32_t n_gblocks, int64_t *hkeys
 /* ParticleStore.histogram_sort part 1 (particles.py:360-399; _counting_sort_perm :66-80,
  * _build_groups :152-173): stable counting sort by key=(gidx<<6)|(code&63) and the lane
  * group structure.  perm[j] = input index of sorted position j.  bin_start has
- * n_gblocks*64+1 entries.  *n_groups (device) = group count. */
+ * n_gblocks*64+1 entries.  *n_groups (device) = group count.  Members of a (block, cell) bin rank
+ * themselves by input index; bins with more than 1024 members (particles piled into one cell)
+ * are ranked from a bitmap over the input order instead, linear in the bin size:
+ * large_scratch (n_upper words) and large_list (n_upper / 1024 + 2 words) are its scratch. */
 int mpm_sort_and_group(const int64_t *codes, const int32_t *gidx, const int32_t *n_dev, int32_t n_upper,
                        int32_t n_gblocks, int32_t *bin_start, int32_t *tmp_perm, int32_t *perm,
                        int32_t *block_group_first, int32_t *scan_scratch, int32_t *n_groups,
-                       void *stream);
+                       int32_t *large_scratch, int32_t *large_list, void *stream);
 
 /* ParticleStore.histogram_sort part 2 (_scatter_sorted particles.py:192-199) fused with
  * set_group_origins + _recompute_lane_keys (particles.py:235-261, 453): permutes all

@@ -447,9 +447,15 @@ typedef struct {
  *   F_E = U S' V^T, Jp <- clamp(Jp * prod(S) / prod(S'), 0.1, 10);
  *   stress = fixed-corotated on F_E with mu, lam scaled by exp(hardening * (1 - Jp)).
  * Sand (Klar et al. 2016, Drucker-Prager): e = log|S|, tr = sum e, dev = e - tr/3;
- *   tr > 0 or |dev| == 0 -> S' = I (and the plastic scalar accumulates tr);
+ *   tr > 0 -> S' = I (tip of the cone; the plastic scalar accumulates tr);
  *   dg = |dev| + (3 lam + 2 mu) / (2 mu) * tr * alpha; dg <= 0 -> S' = S;
- *   else S' = exp(e - dg dev / |dev|).  Stress = U (2 mu e' + lam tr(e') I) U^T, e' = log S'. */
+ *   else S' = exp(e - dg dev / |dev|).  Stress = U (2 mu e' + lam tr(e') I) U^T, e' = log S'.
+ *   (Klar's Algorithm 2 sends |dev| == 0 to the tip before it evaluates dg; for tr <= 0 that makes
+ *   the map discontinuous at isotropic compression, which lies INSIDE the cone: dg = (..) tr alpha
+ *   <= 0.  Here |dev| == 0, tr <= 0 falls under dg <= 0, so the projection is continuous and a
+ *   float32 evaluation can be held to it; dg > 0 with tr <= 0 implies |dev| > 0.)
+ * Pinned against numpy's LAPACK SVD + the published closed forms: tests/golden/make_plastic_golden.py,
+ * tests/golden/plastic.npz, tests/test_oracle_golden.py::test_plastic_models_against_numpy_pin. */
 void orc_snow_project(double *F, double *Jp, double theta_c, double theta_s)
 {
     double u[9], s[3], v[9], sc[3];
@@ -483,7 +489,7 @@ void orc_sand_project(double *F, double *vc, double mu, double lam, double alpha
     double tr = e[0] + e[1] + e[2];
     double d0 = e[0] - tr / 3.0, d1 = e[1] - tr / 3.0, d2 = e[2] - tr / 3.0;
     double dn = sqrt(d0 * d0 + d1 * d1 + d2 * d2);
-    if (tr > 0.0 || dn == 0.0) {
+    if (tr > 0.0) {
         sc[0] = sc[1] = sc[2] = 1.0;
         *vc += tr;
     } else {

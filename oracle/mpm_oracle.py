@@ -168,6 +168,36 @@ def corotated_tau(F, mu, lam):
     return t.reshape(3, 3), bool(clamped)
 
 
+def snow_project(F, Jp, theta_c, theta_s):
+    """Return mapping of the snow model (orc_snow_project): projected F_E and updated J_P."""
+    F = np.array(F, dtype=np.float64).reshape(9)
+    jp = C.c_double(float(Jp))
+    lib().orc_snow_project(_p(F), C.byref(jp), _d(theta_c), _d(theta_s))
+    return F.reshape(3, 3), float(jp.value)
+
+
+def snow_tau(FE, Jp, mu, lam, hardening):
+    """Stress of a projected snow state as scatter_prep evaluates it: fixed-corotated with
+    moduli hardened by exp(xi (1 - J_P))."""
+    h = float(np.exp(hardening * (1.0 - Jp)))
+    return corotated_tau(FE, mu * h, lam * h)[0]
+
+
+def sand_project(F, vc, mu, lam, alpha):
+    """Drucker-Prager return mapping (orc_sand_project): projected F_E, volume-correction scalar."""
+    F = np.array(F, dtype=np.float64).reshape(9)
+    v = C.c_double(float(vc))
+    lib().orc_sand_project(_p(F), C.byref(v), _d(mu), _d(lam), _d(alpha))
+    return F.reshape(3, 3), float(v.value)
+
+
+def sand_tau(F, mu, lam):
+    F = np.ascontiguousarray(F, dtype=np.float64).reshape(9)
+    t = np.empty(9)
+    lib().orc_sand_tau(_p(F), _d(mu), _d(lam), _p(t))
+    return t.reshape(3, 3)
+
+
 def fluid_tau(J, kappa, gamma, clamp_tension=False):
     return float(lib().orc_fluid_tau(float(J), float(kappa), float(gamma), int(bool(clamp_tension))))
 

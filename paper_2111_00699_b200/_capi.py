@@ -136,7 +136,7 @@ _SIGNATURES = {
     "mpm_dilate_and_link": [p_void, i32, p_void, p_void, p_void, i32, p_void, p_void, p_void,
                             p_void, p_void, p_void, i32, p_void, p_void, p_void, p_void],
     "mpm_sort_and_group": [p_void, p_void, p_void, i32, i32, p_void, p_void, p_void, p_void,
-                           p_void, p_void, p_void],
+                           p_void, p_void, p_void, p_void, p_void],
     "mpm_scatter_sorted": [C.POINTER(StoreView), p_void, p_void, p_void, p_void, p_void, p_void,
                            p_void, i32, p_void, f64, C.POINTER(StoreView), p_void],
     "mpm_build_group_ctx": [C.POINTER(StoreView), C.POINTER(TableView), p_void],

@@ -87,15 +87,26 @@ struct DevGuard {
     int *peer_words[MPM_MAX_PEERS];
 };
 // raise the guard: this rank's word and, with peer-mapped memory, every peer's (system scope)
+// A word that peers update over NVLink (atomicMin_system) is updated with system scope by its
+// owner too: atomics of different scopes on one address are not atomic with respect to each other
+// (a lost minimum would leave the word above the true first bad step).
 __device__ __forceinline__ void guard_raise(const DevGuard &g)
 {
     if (!g.word) return;
-    atomicMin(g.word, g.step);
-    for (int p = 0; p < g.n_peers; ++p) atomicMin_system(g.peer_words[p], g.step);
+    if (g.n_peers > 0) {
+        atomicMin_system(g.word, g.step);
+        for (int p = 0; p < g.n_peers; ++p) atomicMin_system(g.peer_words[p], g.step);
+    } else {
+        atomicMin(g.word, g.step);
+    }
 }
 __device__ __forceinline__ bool guarded_out(const DevGuard &g)
 {
-    return g.word != nullptr && *((volatile const int *)g.word) < g.step;
+    if (g.word == nullptr) return false;
+    int v;
+    if (g.n_peers > 0) asm volatile("ld.relaxed.sys.global.s32 %0, [%1];" : "=r"(v) : "l"(g.word) : "memory");
+    else v = *((volatile const int *)g.word);
+    return v < g.step;
 }
 inline DevGuard make_guard(const mpm_guard *g)
 {

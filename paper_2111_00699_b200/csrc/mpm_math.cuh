@@ -275,7 +275,7 @@ __device__ __forceinline__ void plastic_return(const float *s, float &plastic, c
         const float tr = e[0] + e[1] + e[2];
         const float d0 = e[0] - tr * (1.0f / 3.0f), d1 = e[1] - tr * (1.0f / 3.0f), d2 = e[2] - tr * (1.0f / 3.0f);
         const float dn = sqrtf(d0 * d0 + d1 * d1 + d2 * d2);
-        if (tr > 0.0f || dn == 0.0f) {
+        if (tr > 0.0f) {   // tip of the cone; dg > 0 below implies dn > 0 (see orc_sand_project)
             e[0] = e[1] = e[2] = 0.0f;
             plastic += tr;
         } else {

@@ -439,13 +439,20 @@ __global__ void __launch_bounds__(256) place_kernel(const long long *__restrict_
     tmp_perm[bin_start[key] + ticket[i]] = i;
 }
 
-// rank the members of each bin by input index: the order a stable sort yields
+// rank the members of each bin by input index: the order a stable sort yields.  A bin holds the
+// particles of one cell (8-27 normally): every member counts the members with a smaller index.
+// That loop is quadratic in the bin size, so bins above MPM_LARGE_BIN members (particles piled
+// into one cell) are only listed here and ranked by large_bin_rank_kernel, whose
+// cost is linear in the bin size.
+#ifndef MPM_LARGE_BIN
+#define MPM_LARGE_BIN 1024
+#endif
 __global__ void __launch_bounds__(256) stable_rank_kernel(const long long *__restrict__ codes,
                                                           const int *__restrict__ gidx,
                                                           const int *__restrict__ n_dev, int n_upper,
                                                           const int *__restrict__ bin_start,
                                                           const int *__restrict__ tmp_perm,
-                                                          int *__restrict__ perm)
+                                                          int *__restrict__ perm, int *large_list)
 {
     pdl_wait();
     pdl_launch_dependents();
@@ -454,9 +461,68 @@ __global__ void __launch_bounds__(256) stable_rank_kernel(const long long *__res
     const int i = tmp_perm[j];
     const int key = (gidx[i] << 6) | (int)(codes[i] & 63);
     const int s = bin_start[key], e = bin_start[key + 1];
+    if (e - s > MPM_LARGE_BIN) {
+        // large_list[0] = number of large bins, then their keys (at most n / MPM_LARGE_BIN of them)
+        if (j == s) large_list[1 + atomicAdd(&large_list[0], 1)] = key;
+        return;
+    }
     int rank = 0;
     for (int t = s; t < e; ++t) rank += tmp_perm[t] < i;
     perm[s + rank] = i;
+}
+
+// Stable order of a LARGE bin without comparing its members with each other: the members are a
+// subset of the input indices [0, n), so their sorted order is the order of the set bits of a
+// bitmap over the input.  One CTA per large bin: clear n/32 words, set one bit per member,
+// exclusive scan of the word popcounts, emit.  O(n/32 + members) per large bin, and there are at
+// most n / MPM_LARGE_BIN such bins.  `scratch` holds 2 * words per CTA (bitmap, prefix).
+constexpr int LARGE_BIN_CTAS = 8;
+__global__ void __launch_bounds__(1024) large_bin_rank_kernel(const int *__restrict__ bin_start,
+                                                              const int *__restrict__ tmp_perm,
+                                                              int *__restrict__ perm,
+                                                              const int *__restrict__ large_list,
+                                                              unsigned *scratch, int words)
+{
+    pdl_wait();
+    pdl_launch_dependents();
+    const int n_large = large_list[0];
+    if (n_large == 0) return;
+    __shared__ int carry;
+    unsigned *bits = scratch + (size_t)blockIdx.x * 2 * words;
+    int *pre = (int *)(bits + words);
+    const int tid = threadIdx.x;
+    for (int k = blockIdx.x; k < n_large; k += gridDim.x) {
+        const int key = large_list[1 + k];
+        const int s = bin_start[key], e = bin_start[key + 1];
+        for (int w = tid; w < words; w += 1024) bits[w] = 0u;
+        if (tid == 0) carry = 0;
+        __syncthreads();
+        for (int t = s + tid; t < e; t += 1024) {
+            const int i = tmp_perm[t];
+            atomicOr(&bits[i >> 5], 1u << (i & 31));
+        }
+        __syncthreads();
+        for (int base = 0; base < words; base += 1024) {
+            const int w = base + tid;
+            const int v = w < words ? __popc(bits[w]) : 0;
+            int total;
+            const int excl = block_exclusive_scan(v, &total);
+            const int c = carry;
+            if (w < words) pre[w] = excl + c;
+            __syncthreads();
+            if (tid == 0) carry = c + total;
+            __syncthreads();
+        }
+        for (int w = tid; w < words; w += 1024) {
+            unsigned m = bits[w];
+            int r = s + pre[w];
+            while (m) {
+                perm[r++] = w * 32 + (__ffs(m) - 1);
+                m &= m - 1;
+            }
+        }
+        __syncthreads();
+    }
 }
 
 __global__ void __launch_bounds__(256) block_groups_kernel(const int *__restrict__ bin_start, int n_g,
@@ -475,8 +541,13 @@ __global__ void __launch_bounds__(256) block_groups_kernel(const int *__restrict
 // ===================================================================================
 __device__ __forceinline__ int clamp09(long long v) { return v < 0 ? 0 : (v > 9 ? 9 : (int)v); }
 
+// NCH is a template parameter so that the channel loop unrolls: the NCH loads of a lane (one per
+// 128-byte channel row of its source group) are all in flight before the first store, instead of
+// one dependent load-store pair at a time (the kernel is latency-bound, not DRAM-bound: its DRAM
+// traffic is already the algorithmic 2 x NCH x 4 bytes per particle).
+template <int NCH>
 __global__ void __launch_bounds__(256) scatter_sorted_kernel(
-    const float *__restrict__ old_data, const long long *__restrict__ old_ids, int nch,
+    const float *__restrict__ old_data, const long long *__restrict__ old_ids,
     const int *__restrict__ src_slot, const int *__restrict__ n_live_dev,
     const float *__restrict__ staged, const long long *__restrict__ staged_ids,
     const int *__restrict__ perm, const int *__restrict__ bin_start,
@@ -505,39 +576,47 @@ __global__ void __launch_bounds__(256) scatter_sorted_kernel(
         group_block[g] = b;
         group_start[g] = first;
     }
-    float *dst = new_data + (size_t)g * nch * 32 + lane;
+    float *dst = new_data + (size_t)g * NCH * 32 + lane;
+    float v[NCH];
+    long long id = 0;
+    uint16_t key = 0;
     if (lane >= len) {
-        for (int c = 0; c < nch; ++c) dst[c * 32] = 0.0f;
-        new_ids[g * 32 + lane] = 0;
-        new_meta[g * 32 + lane] = 0;
-        return;
-    }
-    const int i = perm[first + lane];
-    const int n_live = n_live_dev ? *n_live_dev : 0;
-    float px, py, pz;
-    if (i < n_live) {
-        const int slot = src_slot[i];
-        const float *src = old_data + (size_t)(slot >> 5) * nch * 32 + (slot & 31);
-        for (int c = 0; c < nch; ++c) dst[c * 32] = src[c * 32];
-        px = src[0]; py = src[32]; pz = src[64];
-        new_ids[g * 32 + lane] = old_ids[slot];
+#pragma unroll
+        for (int c = 0; c < NCH; ++c) v[c] = 0.0f;
     } else {
-        const float *src = staged + (size_t)(i - n_live) * nch;
-        for (int c = 0; c < nch; ++c) dst[c * 32] = src[c];
-        px = src[0]; py = src[1]; pz = src[2];
-        new_ids[g * 32 + lane] = staged_ids[i - n_live];
+        const int i = perm[first + lane];
+        const int n_live = n_live_dev ? *n_live_dev : 0;
+        if (i < n_live) {
+            const int slot = src_slot[i];
+            const float *src = old_data + (size_t)(slot >> 5) * NCH * 32 + (slot & 31);
+#pragma unroll
+            for (int c = 0; c < NCH; ++c) v[c] = src[c * 32];
+            id = old_ids[slot];
+        } else {
+            const float *src = staged + (size_t)(i - n_live) * NCH;
+#pragma unroll
+            for (int c = 0; c < NCH; ++c) v[c] = src[c];
+            id = staged_ids[i - n_live];
+        }
+        // lane key: float64 floor(p * inv_dx - 0.5) + bias - (origin - 4), clamped (particles.py:235-261)
+        const int4 org = table_origin[b];
+        const int kx = clamp09((long long)floor(__dsub_rn(__dmul_rn((double)v[CH_POS + 0], inv_dx), 0.5)) + MPM_CELL_BIAS - (org.x - 4));
+        const int ky = clamp09((long long)floor(__dsub_rn(__dmul_rn((double)v[CH_POS + 1], inv_dx), 0.5)) + MPM_CELL_BIAS - (org.y - 4));
+        const int kz = clamp09((long long)floor(__dsub_rn(__dmul_rn((double)v[CH_POS + 2], inv_dx), 0.5)) + MPM_CELL_BIAS - (org.z - 4));
+        key = (uint16_t)(kx + 10 * (ky + 10 * kz));
     }
-    // lane key: float64 floor(p * inv_dx - 0.5) + bias - (origin - 4), clamped (particles.py:235-261)
-    const int4 org = table_origin[b];
-    const int kx = clamp09((long long)floor(__dsub_rn(__dmul_rn((double)px, inv_dx), 0.5)) + MPM_CELL_BIAS - (org.x - 4));
-    const int ky = clamp09((long long)floor(__dsub_rn(__dmul_rn((double)py, inv_dx), 0.5)) + MPM_CELL_BIAS - (org.y - 4));
-    const int kz = clamp09((long long)floor(__dsub_rn(__dmul_rn((double)pz, inv_dx), 0.5)) + MPM_CELL_BIAS - (org.z - 4));
-    new_meta[g * 32 + lane] = (uint16_t)(kx + 10 * (ky + 10 * kz));
+#pragma unroll
+    for (int c = 0; c < NCH; ++c) dst[c * 32] = v[c];
+    new_ids[g * 32 + lane] = id;
+    new_meta[g * 32 + lane] = key;
 }
 
 // ===================================================================================
 // readback helpers
 // ===================================================================================
+// flat[group_start + lane][nch]: the rows of one group are contiguous in the output, so the warp
+// transposes its [nch][32] tile through shared memory and writes len * nch consecutive floats.
+#define MPM_MAX_NCH 26
 __global__ void __launch_bounds__(256) gather_state_kernel(const float *__restrict__ data,
                                                            const long long *__restrict__ ids, int nch,
                                                            const int *__restrict__ group_len,
@@ -547,13 +626,18 @@ __global__ void __launch_bounds__(256) gather_state_kernel(const float *__restri
 {
     pdl_wait();
     pdl_launch_dependents();
+    __shared__ float tile[8][32 * MPM_MAX_NCH];
     const int g = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
-    const int lane = threadIdx.x & 31;
-    if (g >= n_groups || lane >= group_len[g]) return;
-    const size_t j = (size_t)group_start[g] + lane;
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    if (g >= n_groups) return;
+    const int len = group_len[g];
+    const size_t j0 = (size_t)group_start[g];
     const float *src = data + (size_t)g * nch * 32 + lane;
-    for (int c = 0; c < nch; ++c) flat[j * nch + c] = src[c * 32];
-    out_ids[j] = ids[g * 32 + lane];
+    for (int c = 0; c < nch; ++c) tile[warp][lane * nch + c] = src[c * 32];
+    __syncwarp();
+    float *dst = flat + j0 * nch;
+    for (int k = lane; k < len * nch; k += 32) dst[k] = tile[warp][k];
+    if (lane < len) out_ids[j0 + lane] = ids[g * 32 + lane];
 }
 
 __global__ void __launch_bounds__(256) gather_positions_kernel(const float *__restrict__ data,
@@ -772,12 +856,12 @@ int mpm_dilate_and_link(const int64_t *gcodes, int32_t n_g, int64_t *hkeys, int3
 int mpm_sort_and_group(const int64_t *codes, const int32_t *gidx, const int32_t *n_dev, int32_t n_upper,
                        int32_t n_g, int32_t *bin_start, int32_t *tmp_perm, int32_t *perm,
                        int32_t *block_group_first, int32_t *scan_scratch, int32_t *n_groups,
-                       void *stream_)
+                       int32_t *large_scratch, int32_t *large_list, void *stream_)
 {
     cudaStream_t stream = (cudaStream_t)stream_;
     if (n_g <= 0 || n_upper <= 0) {
         cudaMemsetAsync(n_groups, 0, sizeof(int32_t), stream);
-        return check_launch("mpm_sort_and_group", 13);
+        return check_launch("mpm_sort_and_group", 14);
     }
     const int n_bins = n_g * 64;
     const int nb = nblk(n_upper, 256);
@@ -787,13 +871,20 @@ int mpm_sort_and_group(const int64_t *codes, const int32_t *gidx, const int32_t 
     exclusive_scan_i32(bin_start, bin_start, n_bins + 1, scan_scratch, nullptr, stream);
     launch_chained(place_kernel, nb, 256, stream, (const long long *)codes, gidx, n_dev, n_upper, bin_start,
                                          perm, tmp_perm);
+    if (!large_scratch || !large_list) return MPM_ERR_REJECTED_INPUT;
+    cudaMemsetAsync(large_list, 0, sizeof(int32_t), stream);
     launch_chained(stable_rank_kernel, nb, 256, stream, (const long long *)codes, gidx, n_dev, n_upper,
-                                               bin_start, tmp_perm, perm);
+                                               bin_start, tmp_perm, perm, large_list);
+    // bins above MPM_LARGE_BIN members (none in an ordinary scene: the kernel returns at once);
+    // 2 * ceil(n/32) words per CTA fit n_upper words for every n that can hold a large bin
+    if (n_upper > MPM_LARGE_BIN)
+        launch_chained(large_bin_rank_kernel, LARGE_BIN_CTAS, 1024, stream, bin_start, tmp_perm, perm, large_list,
+                       (unsigned *)large_scratch, (n_upper + 31) / 32);
     launch_chained(block_groups_kernel, nblk(n_g, 256), 256, stream, bin_start, n_g, block_group_first);
     // n_g+1 entries so that block_group_first[n_g] = n_groups
     cudaMemsetAsync(block_group_first + n_g, 0, sizeof(int32_t), stream);
     exclusive_scan_i32(block_group_first, block_group_first, n_g + 1, scan_scratch, n_groups, stream);
-    return check_launch("mpm_sort_and_group", 13);
+    return check_launch("mpm_sort_and_group", 14);
 }
 
 int mpm_scatter_sorted(const mpm_store_view *old_store, const int32_t *src_slot, const int32_t *n_live_dev,
@@ -806,11 +897,20 @@ int mpm_scatter_sorted(const mpm_store_view *old_store, const int32_t *src_slot,
     const int G = new_store->n_groups;
     if (G <= 0) return MPM_OK;
     const double inv_dx = 1.0 / dx;
-    launch_chained(scatter_sorted_kernel, nblk((int64_t)G * 32, 256), 256, stream, 
-        old_store->data, (const long long *)old_store->orig_id, new_store->nch, src_slot, n_live_dev,
-        staged, (const long long *)staged_ids, perm, bin_start, block_group_first, n_g,
-        (const int4 *)table_origin, inv_dx, new_store->data, (long long *)new_store->orig_id,
-        new_store->lane_meta, new_store->group_len, new_store->group_block, new_store->group_start, G);
+#define MPM_SCATTER_SORTED(NCH)                                                                              \
+    launch_chained(scatter_sorted_kernel<NCH>, nblk((int64_t)G * 32, 256), 256, stream, old_store->data,    \
+                   (const long long *)old_store->orig_id, src_slot, n_live_dev, staged,                     \
+                   (const long long *)staged_ids, perm, bin_start, block_group_first, n_g,                  \
+                   (const int4 *)table_origin, inv_dx, new_store->data, (long long *)new_store->orig_id,    \
+                   new_store->lane_meta, new_store->group_len, new_store->group_block,                      \
+                   new_store->group_start, G)
+    switch (new_store->nch) {
+    case 17: MPM_SCATTER_SORTED(17); break;
+    case 25: MPM_SCATTER_SORTED(25); break;
+    case 26: MPM_SCATTER_SORTED(26); break;
+    default: return MPM_ERR_CONFIG;
+    }
+#undef MPM_SCATTER_SORTED
     return check_launch("mpm_scatter_sorted", 1);
 }
 
@@ -830,6 +930,7 @@ int mpm_gather_state(const mpm_store_view *store, float *flat, int64_t *ids, voi
     cudaStream_t stream = (cudaStream_t)stream_;
     const int G = store->n_groups;
     if (G <= 0) return MPM_OK;
+    if (store->nch > MPM_MAX_NCH) return MPM_ERR_CONFIG;
     launch_chained(gather_state_kernel, nblk((int64_t)G * 32, 256), 256, stream, 
         store->data, (const long long *)store->orig_id, store->nch, store->group_len,
         store->group_start, G, flat, (long long *)ids);

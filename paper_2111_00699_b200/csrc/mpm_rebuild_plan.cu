@@ -70,7 +70,7 @@ extern "C" int mpm_rebuild(const mpm_rebuild_plan *p, mpm_rebuild_result *r, voi
                              S + 5, S + 6, S + 4, stream);
     if (rc != MPM_OK) return rc;
     rc = mpm_sort_and_group(p->codes, p->gidx, S + 1, p->n_upper, n_g, p->bin_start, p->tmp_perm, p->perm,
-                            p->bgf, p->scan, S + 7, stream);
+                            p->bgf, p->scan, S + 7, p->pslot, p->flag, stream);   // pslot / flag are free by now
     if (rc != MPM_OK) return rc;
     rc = read_scalars(p, stream);
     if (rc != MPM_OK) return rc;

@@ -87,13 +87,15 @@ class RunConfig:
     flip_blend: float = 0.0
     fused_threshold: int = 100_000
     collect_conservation: bool = False
+    barrier_timeout: float = 10.0     # seconds (reference bench.py RunConfig): the device-side step
+                                      # barrier of peer-mapped runs takes it as its wait timeout
     device: str = "cuda:0"
     profile_phases: bool = False      # CUDA events around the step kernels (CSV phase columns)
 
     def __post_init__(self):
         if self.scene not in SCENES:
             raise ConfigError(f"scene must be one of {SCENES}, got {self.scene!r}")
-        for name in ("l", "ppc", "steps_per_frame", "workers"):
+        for name in ("l", "ppc", "steps_per_frame", "workers", "lane_width"):
             if getattr(self, name) < 1:
                 raise ConfigError(f"{name} must be positive, got {getattr(self, name)}")
         if self.frames < 0:
@@ -133,7 +135,19 @@ def build_scene(cfg: RunConfig) -> scenes.World:
                                   poisson=cfg.poisson, gravity_z=cfg.gravity_z, gap_cells=cfg.gap_cells,
                                   drop_cells=cfg.drop_cells, flip_blend=cfg.flip_blend)
     if cfg.scene == "snow":
-        return scenes.snow(l=cfg.l, boxes=cfg.boxes, ppc=cfg.ppc, seed=cfg.seed)
+        # the snow scene has its own cell width / frame / substep defaults (configs[2]); a config
+        # that sets them away from RunConfig's sand-blocks defaults is taken at its word
+        d = RunConfig()
+        kw = {}
+        if cfg.dx != d.dx:
+            kw["dx"] = cfg.dx
+        if cfg.steps_per_frame != d.steps_per_frame:
+            kw["steps_per_frame"] = cfg.steps_per_frame
+        if cfg.frame_dt != d.frame_dt:
+            kw["frame_dt"] = cfg.frame_dt
+        if cfg.init_speed != d.init_speed:
+            kw["init_speed"] = cfg.init_speed
+        return scenes.snow(l=cfg.l, boxes=cfg.boxes, ppc=cfg.ppc, seed=cfg.seed, **kw)
     if cfg.scene == "fountain_lite":
         return scenes.fountain(dx=cfg.dx, seed=cfg.seed, frame_dt=cfg.frame_dt, cfl=cfg.cfl,
                                radius=cfg.fountain_radius, emit_speed=cfg.emit_speed,
@@ -178,6 +192,7 @@ class RunResult:
     conservation: list
     counters: np.ndarray
     snapshot_paths: list = field(default_factory=list)
+    effective_transfer: str = "split"     # what the workers ran (g2p2g falls back above fused_threshold)
 
     @property
     def mean_steps_between_rebuilds(self) -> float:
@@ -290,7 +305,8 @@ def run(cfg: RunConfig, params_override: SimParams | None = None) -> RunResult:
     mean_ms = float(np.mean([r.ms_total for r in rows])) if rows else 0.0
     return RunResult(rows=rows, workers=workers, mean_ms_per_frame=mean_ms, rebuild_gaps=gaps,
                      particle_count=sum(w.store.count for w in workers), conservation=conservation,
-                     counters=counters, snapshot_paths=snapshot_paths)
+                     counters=counters, snapshot_paths=snapshot_paths,
+                     effective_transfer=workers[0].effective_transfer if workers else cfg.transfer)
 
 
 def run_efficiency(cfg: RunConfig, max_workers: int, warmup: bool = True):

@@ -321,6 +321,14 @@ class PeerDistWorker(DistWorker):
         self._check_wait_error()
         rt.host_barrier()                             # ... nor anybody else's
         self._call("mpm_fill_i32", self._guard_word.data_ptr(), 1, _INT_MAX, _stream_ptr())
+        # The step word too: with split transfers a fast rank may have signalled a step that a
+        # slower peer's late guard then voided (its clear / P2G of step s + 1 ran and stored
+        # s + 2 before the peer's G2P of step s raised the guard).  Left in place, that stale
+        # value would satisfy the peers' wait of the RE-RUN step while this rank's new scatter is
+        # still in flight.  Everything is drained here, so the word goes back to "steps below
+        # _global_step are complete".
+        self._call("mpm_fill_i32", self._mailbox.data_ptr() + 4 * MB_STEP, 1, self._global_step,
+                   _stream_ptr())
         torch.cuda.current_stream().synchronize()
         rt.host_barrier()                             # every copy of the guard is reset
         step = self._global_step

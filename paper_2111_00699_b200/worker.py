@@ -15,6 +15,7 @@ Host/device protocol of one substep (pipeline.py:905-940):
 from __future__ import annotations
 
 import ctypes as C
+import logging
 import math
 import time
 
@@ -29,6 +30,8 @@ from .errors import (ConfigError, ContractViolationError, ModeConflictError, Rej
 from .memory import DeviceBuffer
 from .options import (C_ADDRESS_ERR, FREE_ZONE_HI_CELLS, FREE_ZONE_LO_CELLS, FUSED_MARGIN_CELLS,
                       N_COUNTERS, BoundaryBox, PipelineOptions, StepFlags)
+
+log = logging.getLogger(__name__)
 
 CELL_BIAS = 64
 CH_POS, CH_VEL, CH_C, CH_MASS, CH_DEF, CH_PLASTIC = 0, 3, 6, 15, 16, 25
@@ -558,6 +561,7 @@ class CudaWorker:
         self._peer_map = [None] * runtime.n_workers
         self._peer_states = None
         self._fused_now = False
+        self._fused_fallback_logged = False
         self._phase_ms = {k: 0.0 for k in _PHASES}
         self._frame_steps = 0
         self._frame_rebuilds = 0
@@ -1007,8 +1011,22 @@ class CudaWorker:
         if self.store.staged_count:
             return False
         if self.store.count >= self.options.fused_threshold:
+            # pipeline.py:948-954: the fallback is announced once per worker
+            if not self._fused_fallback_logged:
+                log.info("worker %d: %d particles exceed the fused-transfer threshold of %d; "
+                         "using split transfers", self.wid, self.store.count,
+                         self.options.fused_threshold)
+                self._fused_fallback_logged = True
             return False
         return True
+
+    @property
+    def effective_transfer(self) -> str:
+        """The transfer arm the worker is actually running ("g2p2g" falls back to "split" above
+        PipelineOptions.fused_threshold particles and while appends are staged)."""
+        if self.options.transfer != "g2p2g" or self.store.count >= self.options.fused_threshold:
+            return "split"
+        return "g2p2g"
 
     def _rebuild_tail_ok_static(self):
         cls = type(self)

@@ -129,3 +129,185 @@ def test_two_workers_equal_one_at_full_size(world):
     ex, ev, ef, _ = U.particle_errors(states[1], states[0], edge, 9)
     print("full size, 2 workers vs 1: x %.2e v %.2e F %.2e" % (ex, ev, ef))
     assert ex <= U.X_RTOL_RUN and ev <= U.V_RTOL_RUN and ef <= U.F_ATOL_RUN
+
+
+# ---- the HEADLINE configuration: snow plasticity at 1 372 000 particles ---------------------------
+# bench.py times transfer_kernel<SNOW, gather, scatter>; the model is pinned by tests/golden/plastic.npz
+# (numpy LAPACK SVD + the published closed forms) through the oracle.  Two substeps from the scene's
+# initial state exercise no yielding (the boxes are still falling), so the comparison starts from a
+# state taken two frames into the run, when the snow has hit the floor and a good share of the
+# particles is on the yield surface.
+def _seed_full_state(w, flat, ids, oracle):
+    part = O.partition_particles(flat[:, 0:3], 1)[0]
+    f = flat[part]
+    w.store.stage_append(f[:, 0:3], f[:, 3:6], f[:, 15], deformation=f[:, 16:26], affine=f[:, 6:15],
+                         ids=ids[part])
+    if oracle:
+        w.rebuild_needed = True
+    else:
+        w.flags.rebuild_needed = True
+
+
+@pytest.fixture(scope="module")
+def plastic_midrun():
+    from paper_2111_00699_b200 import scenes
+    W = scenes.snow(plastic=True)
+    f32r = lambda a: np.asarray(a, dtype=np.float64).astype(np.float32).astype(np.float64)
+    W.positions, W.velocities = f32r(W.positions), f32r(W.velocities)
+    w = _worker(W, transfer="g2p2g")
+    for _ in range(2):
+        w.run_frame()
+    flat, ids = w.store.state_with_ids()
+    assert len(ids) == 1372000 and np.isfinite(flat).all()
+    yielded = float((flat[:, 25] != 1.0).mean())
+    print("snow, two frames in: %.1f %% of the particles have yielded, J_P in [%.3f, %.3f]"
+          % (100 * yielded, flat[:, 25].min(), flat[:, 25].max()))
+    assert yielded > 0.02
+    return W, flat, ids
+
+
+def _pair_from_state(W, flat, ids, transfer):
+    from oracle import mpm_oracle as Or
+    from paper_2111_00699_b200 import PipelineOptions, SharedRuntime
+    from paper_2111_00699_b200.worker import CudaWorker
+    opts = dict(transfer=transfer, fused_threshold=1 << 62)
+    vmax = float(np.linalg.norm(flat[:, 3:6], axis=1).max())
+    wc = CudaWorker(0, SharedRuntime(1, initial_vmax=vmax), W.params, W.material, W.boundary,
+                    PipelineOptions(**opts))
+    wo = Or.OracleWorker(0, Or.OracleRuntime(1, vmax), W.params, W.material, W.boundary,
+                         PipelineOptions(**opts))
+    _seed_full_state(wc, flat, ids, oracle=False)
+    _seed_full_state(wo, flat, ids, oracle=True)
+    return wc, wo
+
+
+from oracle import mpm_oracle as O  # noqa: E402
+
+
+@pytest.mark.parametrize("transfer,steps", [("split", 2), ("g2p2g", 3)])
+def test_plastic_substeps_against_the_oracle_at_full_size(plastic_midrun, transfer, steps):
+    """split: rebuild + 2 substeps; g2p2g: rebuild step + 2 fused steps + flush (the kernel the
+    bench times).  Structures bit-exact, x / v / F at the one-substep bars, J_P <= 1e-5."""
+    W, flat, ids = plastic_midrun
+    wc, wo = _pair_from_state(W, flat, ids, transfer)
+    for s in range(steps):
+        wc.run_step(s)
+        wo.run_step(s)
+    if wc._pending_gather:
+        wc._flush_gather()
+        wo._flush_gather()
+    G = wo.store.n_groups
+    assert wc.table.count == wo.table.count and wc.store.n_groups == G
+    assert np.array_equal(wc.table.codes, wo.table.codes[:wo.table.count])
+    assert np.array_equal(wc.store.orig_id, wo.store.orig_id[:G])
+    assert np.array_equal(wc.store.group_block, wo.store.group_block[:G])
+    sc, so = U.state_by_id(wc), U.state_by_id(wo)
+    edge = float(W.positions.max() - W.positions.min())
+    ex, ev, ef, _ = U.particle_errors(sc, so, edge, 9)
+    ej = np.abs(sc[:, 25] - so[:, 25]).max()
+    moved = float((so[:, 25] != flat[np.argsort(ids, kind="stable"), 25]).mean())
+    print("full size snow plasticity, %s x%d: x %.2e v %.2e F %.2e J_P %.2e; %.1f %% yielded in these steps"
+          % (transfer, steps, ex, ev, ef, ej, 100 * moved))
+    assert ex <= U.X_RTOL and ev <= U.V_RTOL and ef <= U.F_ATOL and ej <= 1e-5
+    assert moved > 0.005      # the return mapping was exercised in the compared steps
+
+
+# ---- the other named sizes: 64 000 (whole frame) and 389 344 (one substep) ------------------------
+def test_whole_frame_of_the_64k_scene_against_the_oracle():
+    """configs[0], the reference's own scene (sand_blocks l=20 boxes=1: 64 000 particles, 36 substeps
+    of 5.787e-4 s, -150 cm/s): one whole fused frame through run_frame (batched, speculative) vs the
+    oracle's frame; same rebuild steps, x / v / F at the short-run bars."""
+    from paper_2111_00699_b200 import scenes
+    W = scenes.sand_blocks(l=20, boxes=1)
+    f32r = lambda a: np.asarray(a, dtype=np.float64).astype(np.float32).astype(np.float64)
+    W.positions, W.velocities = f32r(W.positions), f32r(W.velocities)
+    assert len(W.positions) == 64000
+    for transfer in ("g2p2g", "split"):
+        wc = _worker(W, transfer=transfer)
+        wo = U.oracle_worker(W.positions, W.velocities, W.particle_mass, W.material, W.params, W.boundary,
+                             transfer=transfer, fused_threshold=1 << 62)
+        wc.run_frame()
+        wo.run_frame()
+        assert wc._global_step == wo._global_step == 36
+        assert wc.rebuild_steps == wo.rebuild_steps and len(wc.rebuild_steps) >= 3
+        edge = float(W.positions.max() - W.positions.min())
+        ex, ev, ef, _ = U.particle_errors(U.state_by_id(wc), U.state_by_id(wo), edge, 9)
+        print("64 K scene, one frame (%s): x %.2e v %.2e F %.2e, rebuilds at %s"
+              % (transfer, ex, ev, ef, wc.rebuild_steps))
+        assert ex <= U.X_RTOL_RUN and ev <= U.V_RTOL_RUN and ef <= U.F_ATOL_RUN
+        assert wc.store.total_mass() == pytest.approx(64000 * W.particle_mass, rel=1e-6)
+
+
+def test_one_substep_of_the_389k_scene_against_the_oracle():
+    """configs[3] sweep point (sand_blocks l=23 boxes=4: 389 344 particles): rebuild + 2 substeps."""
+    from paper_2111_00699_b200 import scenes
+    W = scenes.sand_blocks(l=23, boxes=4)
+    f32r = lambda a: np.asarray(a, dtype=np.float64).astype(np.float32).astype(np.float64)
+    W.positions, W.velocities = f32r(W.positions), f32r(W.velocities)
+    assert len(W.positions) == 389344
+    wc = _worker(W, transfer="split")
+    wo = U.oracle_worker(W.positions, W.velocities, W.particle_mass, W.material, W.params, W.boundary,
+                         transfer="split", fused_threshold=1 << 62)
+    for s in range(2):
+        wc.run_step(s)
+        wo.run_step(s)
+    G = wo.store.n_groups
+    assert np.array_equal(wc.table.codes, wo.table.codes[:wo.table.count])
+    assert np.array_equal(wc.table.neighbor, wo.table.neighbor[:wo.table.n_gblocks])
+    assert np.array_equal(wc.store.orig_id, wo.store.orig_id[:G])
+    assert np.array_equal(wc.store.lane_key, wo.store.lane_key[:G])
+    errs = U.grid_errors(wc.grid.vel, wo.grid.vel[:wo.table.count])
+    edge = float(W.positions.max() - W.positions.min())
+    ex, ev, ef, _ = U.particle_errors(U.state_by_id(wc), U.state_by_id(wo), edge, 9)
+    print("389 K scene, 2 substeps: grid vel", ["%.1e" % e for e in errs], "x %.2e v %.2e F %.2e" % (ex, ev, ef))
+    assert max(errs) <= U.GRID_RTOL and ex <= U.X_RTOL and ev <= U.V_RTOL and ef <= U.F_ATOL
+
+
+# ---- pile-up: 10 000 particles in ONE cell next to an ordinary block ------------------------------
+def test_pile_up_in_one_cell_sorts_stably_in_bounded_time():
+    """SURVEY 7.4 #3 / PAPER.md:284: a dense cell.  The stable counting sort must still return the
+    sequential algorithm's permutation (particles.py:66-80) -- orig_id per (group, lane) bit-exact
+    against the oracle -- and a rebuild must not degenerate (the bin holds 10^4 members: the rank of a
+    member of a large bin comes from a bitmap of the bin over the input order, linear in bin size)."""
+    import time
+    import torch
+    from paper_2111_00699_b200 import BoundaryBox, Material, SimParams
+    dx = 0.5
+    rng = np.random.default_rng(77)
+    pile = (np.array([20.0, 20.0, 20.0]) + rng.random((10000, 3))) * dx
+    block, _ = U.block_scene(6, 3, dx, origin_cells=(14, 14, 14))
+    pos = np.concatenate([pile, block])
+    pos = pos[rng.permutation(len(pos))]
+    f32r = lambda a: np.asarray(a, dtype=np.float64).astype(np.float32).astype(np.float64)
+    pos = f32r(pos)
+    vel = np.zeros_like(pos)
+    material = Material.fixed_corotated(2.0, 1.0e5, 0.3)
+    params = SimParams(dx=dx, dt=1e-4)
+    boundary = BoundaryBox((2.0,) * 3, (30.0,) * 3, mode="slip")
+    wc = U.cuda_worker(pos, vel, 1e-3, material, params, boundary, transfer="split")
+    wo = U.oracle_worker(pos, vel, 1e-3, material, params, boundary, transfer="split")
+    for s in range(2):
+        wc.run_step(s)
+        wo.run_step(s)
+    G = wo.store.n_groups
+    assert wc.store.n_groups == G
+    assert np.array_equal(wc.store.orig_id, wo.store.orig_id[:G])
+    assert np.array_equal(wc.store.group_len, wo.store.group_len[:G])
+    assert np.array_equal(wc.store.lane_key, wo.store.lane_key[:G])
+    assert int(wc.store.group_len.sum()) == len(pos)
+    errs = U.grid_errors(wc.grid.vel, wo.grid.vel[:wo.table.count])
+    ex, ev, ef, _ = U.particle_errors(U.state_by_id(wc), U.state_by_id(wo), 13.0, 9)
+    print("pile-up: grid", ["%.1e" % e for e in errs], "x %.2e v %.2e F %.2e" % (ex, ev, ef))
+    assert errs[0] <= 1e-5 and ex <= U.X_RTOL and ev <= 1e-4 and ef <= 1e-4
+    assert wc.store.total_mass() == pytest.approx(len(pos) * 1e-3, rel=1e-6)
+    # bounded time: the rebuild of the piled-up store (buffers sized, kernels warm)
+    wc._rebuild(2, 0)
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    wc._rebuild(3, 1)
+    torch.cuda.synchronize()
+    ms = (time.perf_counter() - t0) * 1e3
+    print("pile-up rebuild: %.2f ms" % ms)
+    assert ms < 20.0
+    assert np.array_equal(np.sort(wc.store.orig_id[np.arange(32)[None, :] < wc.store.group_len[:, None]]),
+                          np.arange(len(pos)))

@@ -247,6 +247,59 @@ def test_plastic_models_against_float64_definition(kind, transfer):
     assert (so[:, 25] != (1.0 if kind == "snow" else 0.0)).any()
 
 
+@pytest.mark.parametrize("kind", ["snow", "sand"])
+def test_plastic_projection_against_numpy_pin(kind):
+    """The CUDA return mappings held to tests/golden/plastic.npz (numpy LAPACK SVD + the published
+    closed forms, tests/golden/make_plastic_golden.py) directly: every golden F is planted in a
+    particle, the grid velocity is painted zero (C = 0, so the gather's trial state is F itself)
+    and one G2P projects it.  fp32 bars: F_E 2e-5 (5e-4 for the nearly singular states, whose
+    small singular value the clamp replaces), J_P 1e-4 relative, volume scalar 1e-5."""
+    from conftest import golden
+    from paper_2111_00699_b200 import BoundaryBox, Material, SimParams
+    g = golden("plastic.npz")
+    F, tag = g["F"], g["tag"]
+    n = len(F)
+    dx = 0.5
+    rng = np.random.default_rng(5)
+    pos = rng.uniform(7.0, 9.0, (n, 3))
+    E = 1.0e5
+    if kind == "snow":
+        material = Material.snow(2.0, E, 0.3, theta_c=float(g["theta_c"]), theta_s=float(g["theta_s"]),
+                                 hardening=float(g["xi"]))
+        plastic0, ref_F, ref_p = g["Jp"], g["snow_FE"], g["snow_Jp"]
+    else:
+        material = Material.sand(2.0, E, 0.3)
+        plastic0, ref_F, ref_p = g["vc"], g["sand_FE"], g["sand_vc"]
+    assert abs(material.mu - float(g["mu"])) <= 1e-12 * material.mu and abs(material.lam - float(g["lam"])) <= 1e-12 * material.lam
+    params = SimParams(dx=dx, dt=1e-4, gravity=(0.0, 0.0, 0.0))
+    w = U.cuda_worker(pos, np.zeros_like(pos), 1.0, material, params, None, transfer="split")
+    w.run_step(0)
+    d = w.store.data
+    ids = w.store.orig_id
+    live = np.arange(32)[None, :] < w.store.group_len[:, None]
+    gi, li = np.nonzero(live)
+    k = ids[gi, li]
+    for r in range(9):
+        d[gi, 16 + r, li] = F[k].reshape(n, 9)[:, r]
+    d[gi, 25, li] = plastic0[k]
+    w.store.set_data(d)
+    w.grid.set_vel(np.zeros((w.table.count, 4, 64)))
+    w._vel_dt = params.dt
+    w._run_g2p(1)
+    out = w.store.data
+    got_F = np.stack([out[gi, 16 + r, li] for r in range(9)], axis=-1).reshape(-1, 3, 3)
+    got_p = out[gi, 25, li]
+    eF = np.abs(got_F - ref_F[k]).reshape(n, -1).max(axis=1)
+    scale = np.maximum(np.abs(ref_p[k]), 1.0 if kind == "sand" else 1e-30)
+    ep = np.abs(got_p - ref_p[k]) / scale
+    for t in np.unique(tag):
+        m = tag[k] == t
+        print(kind, "tag", int(t), "F_E %.2e plastic %.2e" % (eF[m].max(), ep[m].max()))
+    bar_F = np.where(tag[k] == 2, 5e-4, 2e-5)
+    assert (eF <= bar_F).all(), (eF.max(), int(np.argmax(eF / bar_F)))
+    assert (ep <= (1e-4 if kind == "snow" else 1e-5)).all(), ep.max()
+
+
 def test_fountain_frames_with_emission_against_oracle():
     """configs[1] in miniature: per-frame emission (append_particles forces a rebuild per frame,
     pipeline.py:837-850), weakly compressible fluid, CFL-auto dt (pipeline.py:858-871)."""

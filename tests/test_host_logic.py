@@ -238,3 +238,17 @@ def test_shared_memory_rendezvous_of_three_processes(tmp_path):
     rc = lib.mpm_shm_allgather_i64(C.addressof(C.c_char.from_buffer(mm)), 2, 0, (C.c_int64 * 1)(7), 1,
                                    out.ctypes.data, 50)
     assert rc == -8
+
+
+def test_run_config_accepts_the_reference_fields():
+    """A reference RunConfig dump (bench.py:62-100 of the reference, barrier_timeout included)
+    loads unchanged; lane_width is range-checked with the other counts."""
+    from paper_2111_00699_b200.errors import ConfigError
+    from paper_2111_00699_b200.harness import RunConfig
+    cfg = RunConfig.from_dict({"scene": "sand_blocks", "l": 12, "boxes": 4, "workers": 2,
+                               "barrier_timeout": 3.5, "transfer": "g2p2g"})
+    assert cfg.barrier_timeout == 3.5
+    with pytest.raises(ConfigError):
+        RunConfig(lane_width=0)
+    with pytest.raises(ConfigError):
+        RunConfig.from_dict({"no_such_field": 1})
