@@ -224,7 +224,7 @@ class CudaParticleStore:
             hvel[o:o + k].copy_(torch.from_numpy(vel))
             hids[o:o + k].copy_(torch.from_numpy(ids))
             if mass.ndim:
-                hmass[o:o + k].copy_(torch.from_numpy(mass))
+                hmass[o:o + k].copy_(torch.from_numpy(np.ascontiguousarray(mass).copy() if not mass.flags.writeable else mass))
             else:
                 hmass[o:o + k].fill_(float(mass))
             if defo is not None or aff is not None:
