@@ -41,12 +41,20 @@ def parse_args():
     ap.add_argument("--transfer", default="g2p2g", choices=["split", "g2p2g"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-pinned-variant", action="store_true",
+                    help="snow only: skip the fixed-corotated (reference-pinned) run of the same scene")
     ap.add_argument("--ref-substeps", type=int, default=2,
                     help="substeps per step of the reference arm (bounded sample)")
     return ap.parse_args()
 
 
 def build_world(scene):
+    W = _build_world(scene)
+    W.tag = scene
+    return W
+
+
+def _build_world(scene):
     from paper_2111_00699_b200 import scenes
     if scene == "snow":
         return scenes.snow(plastic=SNOW_PLASTIC)
@@ -102,28 +110,36 @@ class ClockSampler:
             self.proc = None
 
     def stop(self):
+        """Ends the sampling; returns the summary of the window marked with mark_begin / mark_end."""
         if self.proc is None:
-            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+            self.lines = None
+            return self.window(self.t0, self.t1)
         self.proc.terminate()
         try:
             out, _ = self.proc.communicate(timeout=5)
         except subprocess.TimeoutExpired:
             self.proc.kill()
             out, _ = self.proc.communicate()
+        self.lines = out.strip().splitlines()
+        return self.window(self.t0, self.t1)
+
+    def window(self, t0, t1):
+        """Clocks / throttle reasons of the samples taken in [t0, t1] (50 ms of slack either side)."""
+        if getattr(self, "lines", None) is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
         sm, smax, power, reasons = [], [], [], set()
         names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
         import datetime
-        for line in out.strip().splitlines():
+        for line in self.lines:
             f = [x.strip() for x in line.split(",")]
             if len(f) < 9:
                 continue
-            if self.t0 is not None and self.t1 is not None:
-                # keep the samples taken inside the timed region (50 ms of slack either side)
+            if t0 is not None and t1 is not None:
                 try:
                     ts = datetime.datetime.strptime(f[0], "%Y/%m/%d %H:%M:%S.%f").timestamp()
                 except ValueError:
                     continue
-                if ts < self.t0 - 0.05 or ts > self.t1 + 0.05:
+                if ts < t0 - 0.05 or ts > t1 + 0.05:
                     continue
             try:
                 sm.append(float(f[1])); smax.append(float(f[2])); power.append(float(f[3]))
@@ -182,47 +198,19 @@ def run_ours(args):
             dist.init_process_group("nccl", device_id=dev)
         else:
             dist.init_process_group(backend)
-    W = build_world(args.scene)
-    n = len(W.positions)
-    spf = W.params.steps_per_frame
-    opts = PipelineOptions(transfer=args.transfer, fused_threshold=1 << 62)
     lib = _capi.lib()
-    vmax0 = float(np.abs(W.velocities).max())
-
-    if world > 1:
-        from paper_2111_00699_b200.dist import DistRuntime, DistWorker
-        from paper_2111_00699_b200 import partition_particles
-        part = partition_particles(W.positions, world)[rank]
-    else:
-        part = np.arange(n, dtype=np.int64)
-    my_pos = np.ascontiguousarray(W.positions[part], dtype=np.float32)
-    my_vel = np.ascontiguousarray(W.velocities[part], dtype=np.float32)
-    # end-to-end inputs live in pinned host memory (allocated once, outside the timed region)
-    pin_pos = torch.from_numpy(my_pos).pin_memory()
-    pin_vel = torch.from_numpy(my_vel).pin_memory()
-    pin_ids = torch.from_numpy(np.ascontiguousarray(part, dtype=np.int64)).pin_memory()
+    opts = PipelineOptions(transfer=args.transfer, fused_threshold=1 << 62)
 
     halo = os.environ.get("MPM_HALO", "peer")   # peer: rows read in place over NVLink (peer.py); sendrecv: NCCL
     if world > 1 and halo == "peer":
         # peer memory must really be reachable from every rank's device; if not (no P2P between two
         # of the GPUs, IPC disabled in the container) the literal send/recv protocol still runs
         from paper_2111_00699_b200.peer import PeerRuntime
-        if not PeerRuntime(dev, initial_vmax=vmax0).probe():
+        if not PeerRuntime(dev, initial_vmax=150.0).probe():
             halo = "sendrecv"
             if rank == 0:
                 print("peer-mapped memory is not available on this box: halo rows over send/recv",
                       file=sys.stderr, flush=True)
-
-    def fresh_worker():
-        if world > 1:
-            if halo == "peer":
-                from paper_2111_00699_b200.peer import PeerDistWorker, PeerRuntime
-                return PeerDistWorker(PeerRuntime(dev, initial_vmax=vmax0), W.params, W.material,
-                                      W.boundary, opts, device=dev, count_stats=False, lazy_flush=True)
-            return DistWorker(DistRuntime(dev, initial_vmax=vmax0), W.params, W.material, W.boundary,
-                              opts, device=dev, count_stats=False)
-        return CudaWorker(0, SharedRuntime(1, initial_vmax=vmax0), W.params, W.material, W.boundary,
-                          opts, device=dev, count_stats=False, fuse_clear=True, lazy_flush=True)
 
     def barrier():
         if world > 1:
@@ -239,69 +227,144 @@ def run_ours(args):
     sampler = ClockSampler(local)
     if rank == 0:
         sampler.start()           # nvidia-smi needs a moment to start: launch it before the warm-up
-    w = fresh_worker()
-    w.seed_particles(my_pos, my_vel, W.particle_mass, ids=part)
-    for _ in range(args.warmup):
-        w.run_frame()
-    barrier()
-    w.time_kernels = True
-    w.kernel_events.clear()
-    l0 = lib.mpm_launch_count()
-    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    reb0 = len(w.rebuild_steps)
-    barrier()
-    sampler.mark_begin()
-    e0.record()
-    for _ in range(args.steps):
-        w.run_frame()
-    e1.record()
-    barrier()
-    sampler.mark_end()
-    total_ms = max_over_ranks(e0.elapsed_time(e1))
-    launches = int(lib.mpm_launch_count() - l0)
-    clocks = sampler.stop() if rank == 0 else None
-    rebuilds = len(w.rebuild_steps) - reb0
-    ms_per_step = total_ms / args.steps
-    value = n * spf * args.steps / (total_ms * 1e-3) / 1e6
-    # dominant kernel: average launch duration from CUDA events on the launching stream
-    w.time_kernels = False
-    dom = "mpm_g2p2g" if args.transfer == "g2p2g" else "mpm_p2g"
-    durs = [a.elapsed_time(b) for name, a, b in w.kernel_events if name == dom]
-    all_kernel_ms = {}
-    for name, a, b in w.kernel_events:
-        all_kernel_ms[name] = all_kernel_ms.get(name, 0.0) + a.elapsed_time(b)
-    # Steps enqueued in batches from C time ONE launch per batch, at a rotating position (an event between
-    # two kernels of the chain would serialise what programmatic dependent launch overlaps); the
-    # dominant kernel's total is its mean duration x its launches in the region: every substep
-    # except, for the fused transfer, the rebuild steps (those run the split P2G).
-    n_dom = spf * args.steps - (rebuilds if dom == "mpm_g2p2g" else 0)
-    if durs:
-        all_kernel_ms[dom] = float(np.mean(durs)) * n_dom
-    # touched pblocks of one substep (flags survive when the clear is not fused into the update)
-    w.fuse_clear, w.pipelined = False, False
-    step = w._global_step
-    w.dt = W.params.dt
-    w.run_step(step)
-    touched = int(w.table._touched[step & 1].data[:w.table.count].sum().item())
-    n_local = len(part)
-    peak, peak_src = measured_peak_gbs()
-    roofline = None
-    if durs:
-        avg_ms = float(np.mean(durs))
-        abytes = algorithmic_bytes(int(W.material.kind), args.transfer, n_local, touched)
-        achieved = abytes / (avg_ms * 1e-3) / 1e9
-        roofline = {"bound": "hbm", "kernel": dom, "achieved": round(achieved, 1), "peak": peak,
-                    "unit": "GB/s", "frac": round(achieved / peak, 4),
-                    "traffic": TRAFFIC_NCU.get(args.scene) if (world == 1 and args.transfer == "g2p2g") else None,
-                    "peak_source": peak_src, "avg_launch_ms": round(avg_ms, 4),
-                    "algorithmic_bytes_per_launch": int(abytes), "launches_timed": len(durs),
-                    "launches_in_region": int(n_dom),
-                    "kernel_share_of_step": round(avg_ms * n_dom / total_ms, 3),
-                    "kernel_ms_per_step": {k: round(v / args.steps, 4) for k, v in all_kernel_ms.items()}}
+
+    def make_arm(W):
+        """Everything one workload needs: its slab of the particles and a worker factory."""
+        n = len(W.positions)
+        vmax0 = float(np.abs(W.velocities).max())
+        if world > 1:
+            from paper_2111_00699_b200 import partition_particles
+            part = partition_particles(W.positions, world)[rank]
+        else:
+            part = np.arange(n, dtype=np.int64)
+        my_pos = np.ascontiguousarray(W.positions[part], dtype=np.float32)
+        my_vel = np.ascontiguousarray(W.velocities[part], dtype=np.float32)
+
+        def fresh_worker():
+            if world > 1:
+                from paper_2111_00699_b200.dist import DistRuntime, DistWorker
+                if halo == "peer":
+                    from paper_2111_00699_b200.peer import PeerDistWorker, PeerRuntime
+                    return PeerDistWorker(PeerRuntime(dev, initial_vmax=vmax0), W.params, W.material,
+                                          W.boundary, opts, device=dev, count_stats=False, lazy_flush=True)
+                return DistWorker(DistRuntime(dev, initial_vmax=vmax0), W.params, W.material, W.boundary,
+                                  opts, device=dev, count_stats=False)
+            return CudaWorker(0, SharedRuntime(1, initial_vmax=vmax0), W.params, W.material, W.boundary,
+                              opts, device=dev, count_stats=False, fuse_clear=True, lazy_flush=True)
+        return n, part, my_pos, my_vel, fresh_worker
+
+    def resident(W, steps, warmup):
+        """`value` leg: K frames with the particle state resident in HBM, CUDA events on the launching
+        stream, max over ranks; roofline of the dominant kernel from events inside the same region."""
+        n, part, my_pos, my_vel, fresh_worker = make_arm(W)
+        spf = W.params.steps_per_frame
+        w = fresh_worker()
+        w.seed_particles(my_pos, my_vel, W.particle_mass, ids=part)
+        for _ in range(warmup):
+            w.run_frame()
+        barrier()
+        w.time_kernels = True
+        w.kernel_events.clear()
+        l0 = lib.mpm_launch_count()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        reb0 = len(w.rebuild_steps)
+        barrier()
+        t_begin = time.time()
+        e0.record()
+        for _ in range(steps):
+            w.run_frame()
+        e1.record()
+        barrier()
+        t_end = time.time()
+        total_ms = max_over_ranks(e0.elapsed_time(e1))
+        launches = int(lib.mpm_launch_count() - l0)
+        rebuilds = len(w.rebuild_steps) - reb0
+        ms_per_step = total_ms / steps
+        value = n * spf * steps / (total_ms * 1e-3) / 1e6
+        # dominant kernel: average launch duration from CUDA events on the launching stream
+        w.time_kernels = False
+        dom = "mpm_g2p2g" if args.transfer == "g2p2g" else "mpm_p2g"
+        durs = [a.elapsed_time(b) for name, a, b in w.kernel_events if name == dom]
+        all_kernel_ms = {}
+        for name, a, b in w.kernel_events:
+            all_kernel_ms[name] = all_kernel_ms.get(name, 0.0) + a.elapsed_time(b)
+        # Steps enqueued in batches from C time ONE launch per batch, at a rotating position (an event between
+        # two kernels of the chain would serialise what programmatic dependent launch overlaps); the
+        # dominant kernel's total is its mean duration x its launches in the region: every substep
+        # except, for the fused transfer, the rebuild steps (those run the split P2G).
+        n_dom = spf * steps - (rebuilds if dom == "mpm_g2p2g" else 0)
+        if durs:
+            all_kernel_ms[dom] = float(np.mean(durs)) * n_dom
+        # touched pblocks of one substep (flags survive when the clear is not fused into the update)
+        w.fuse_clear, w.pipelined = False, False
+        step = w._global_step
+        w.dt = W.params.dt
+        w.run_step(step)
+        touched = int(w.table._touched[step & 1].data[:w.table.count].sum().item())
+        n_local = len(part)
+        peak, peak_src = measured_peak_gbs()
+        roofline = None
+        if durs:
+            avg_ms = float(np.mean(durs))
+            abytes = algorithmic_bytes(int(W.material.kind), args.transfer, n_local, touched)
+            achieved = abytes / (avg_ms * 1e-3) / 1e9
+            traffic = TRAFFIC_NCU.get(W.tag) if (world == 1 and args.transfer == "g2p2g") else None
+            roofline = {"bound": "hbm", "kernel": dom, "achieved": round(achieved, 1), "peak": peak,
+                        "unit": "GB/s", "frac": round(achieved / peak, 4),
+                        "traffic": traffic[0] if traffic else None,
+                        "traffic_source": traffic[1] if traffic else None,
+                        "peak_source": peak_src, "avg_launch_ms": round(avg_ms, 4),
+                        "algorithmic_bytes_per_launch": int(abytes), "launches_timed": len(durs),
+                        "launches_in_region": int(n_dom),
+                        "kernel_share_of_step": round(avg_ms * n_dom / total_ms, 3),
+                        "kernel_ms_per_step": {k: round(v / steps, 4) for k, v in all_kernel_ms.items()}}
+        config = {"workload": W.name, "particles": n, "substeps_per_step": spf,
+                  "step": "one frame", "dx": W.params.dx, "dt": W.params.dt,
+                  "transfer": args.transfer, "material": W.material.kind.name,
+                  "parallelism": (f"{world} spatial slabs, halo rows read in place over NVLink peer memory, "
+                                  "device-side step barrier" if halo == "peer" else
+                                  f"{world} spatial slabs, halo rows over NCCL send/recv") if world > 1
+                  else "1 GPU", "rank0_particles": n_local,
+                  "pblocks": int(w.table.count), "groups": int(w.store.n_groups),
+                  "rebuilds_in_timed_region": rebuilds, "touched_pblocks": touched,
+                  "speculative_steps_discarded": int(w.speculative_discards),
+                  # a frame ends with the fused gather pending; it completes on the first access to the
+                  # particle store (the reference flushes at every frame end, pipeline.py:877-880)
+                  "lazy_flush": bool(getattr(w, "lazy_flush", False)),
+                  "fuse_clear": world == 1,
+                  "l2_policy": "inputs larger than L2: "
+                               f"{n_local * w.store.nch * 4 / 1e6:.0f} MB particle state per GPU "
+                               "streamed every substep (L2 126 MB)"}
+        return {"value": round(value, 2), "ms_per_step": round(ms_per_step, 4), "roofline": roofline,
+                "config": config, "launches": launches, "window": (t_begin, t_end)}
+
+    W = build_world(args.scene)
+    main_arm = resident(W, args.steps, args.warmup)
+    n = len(W.positions)
+    spf = W.params.steps_per_frame
+
+    # The headline scene runs the snow plasticity model, pinned by numpy's SVD + the published closed
+    # forms (tests/golden/plastic.npz) but absent from the reference package; the SAME particle set
+    # with the reference's own fixed-corotated material is timed next to it, same K and W.
+    pinned = None
+    if args.scene == "snow" and not args.no_pinned_variant:
+        Wfc = build_world("snow_fc")
+        arm = resident(Wfc, args.steps, args.warmup)
+        pinned = {"workload": Wfc.name, "value": arm["value"], "unit": UNIT, "ms_per_step": arm["ms_per_step"],
+                  "material": Wfc.material.kind.name,
+                  "roofline_frac": arm["roofline"]["frac"] if arm["roofline"] else None,
+                  "avg_launch_ms": arm["roofline"]["avg_launch_ms"] if arm["roofline"] else None,
+                  "rebuilds_in_timed_region": arm["config"]["rebuilds_in_timed_region"]}
 
     # end to end through the public API with host buffers
     e2e = None
     if not args.no_e2e:
+        _, part, my_pos, my_vel, fresh_worker = make_arm(W)
+        n_local = len(part)
+        # end-to-end inputs live in pinned host memory (allocated once, outside the timed region)
+        pin_pos = torch.from_numpy(my_pos).pin_memory()
+        pin_vel = torch.from_numpy(my_vel).pin_memory()
+        pin_ids = torch.from_numpy(np.ascontiguousarray(part, dtype=np.int64)).pin_memory()
         w2 = fresh_worker()
         k_e2e = max(2, min(args.steps, 4))
         E2E_WARM = 3      # untimed: the second worker's buffers, pinned staging and the allocator settle
@@ -354,33 +417,30 @@ def run_ours(args):
                       "initial state from the host, so it times the scene's first frame (fewer rebuilds "
                       "and less yielding than the frames `value` is taken over)"}
 
+    clocks = None
+    if rank == 0:
+        sampler.mark_begin(); sampler.mark_end()
+        sampler.stop()
+        clocks = sampler.window(*main_arm["window"])
+        if pinned is not None:
+            pinned["clocks"] = sampler.window(*arm["window"])
+
     cpu = None
     if not args.no_cpu_baseline and rank == 0 and world == 1:
         cpu = cpu_baseline(W, substeps=2, threads=1)
 
     if rank == 0:
         line = {
-            "metric": METRIC, "value": round(value, 2), "unit": UNIT, "n_gpus": world,
-            "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(ms_per_step, 4),
+            "metric": METRIC, "value": main_arm["value"], "unit": UNIT, "n_gpus": world,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": main_arm["ms_per_step"],
             "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f32",
-            "data": "synthetic",
-            "config": {"workload": W.name, "particles": n, "substeps_per_step": spf,
-                       "step": "one frame", "dx": W.params.dx, "dt": W.params.dt,
-                       "transfer": args.transfer, "material": W.material.kind.name,
-                       "parallelism": (f"{world} spatial slabs, halo rows read in place over NVLink peer memory, "
-                                       "device-side step barrier" if halo == "peer" else
-                                       f"{world} spatial slabs, halo rows over NCCL send/recv") if world > 1
-                       else "1 GPU", "rank0_particles": n_local,
-                       "pblocks": int(w.table.count), "groups": int(w.store.n_groups),
-                       "rebuilds_in_timed_region": rebuilds, "touched_pblocks": touched,
-                       "speculative_steps_discarded": int(w.speculative_discards),
-                       "l2_policy": "inputs larger than L2: "
-                                    f"{n_local * w.store.nch * 4 / 1e6:.0f} MB particle state per GPU "
-                                    "streamed every substep (L2 126 MB)"},
-            "ms_per_frame": round(ms_per_step, 4),
-            "clocks": clocks, "gpu_launches": launches, "e2e": e2e, "roofline": roofline,
-            "cpu_baseline": cpu,
+            "data": "synthetic", "config": main_arm["config"],
+            "ms_per_frame": main_arm["ms_per_step"],
+            "clocks": clocks, "gpu_launches": main_arm["launches"], "e2e": e2e,
+            "roofline": main_arm["roofline"], "cpu_baseline": cpu,
         }
+        if pinned is not None:
+            line["reference_pinned_variant"] = pinned
         print(json.dumps(line), flush=True)
     if world > 1:
         dist.barrier()
@@ -391,7 +451,8 @@ def run_ours(args):
 # committed `ncu --set full` capture of the fused kernel on the 1.37 M scene
 # (profiles/r1_l_fused_snow_final_metrics.csv: 96.5 MB read + 52.7 MB write; r1_l_fused_snow_fc_final: 89.8 + 40.8);
 # only quoted for those scenes
-TRAFFIC_NCU = {"snow": 149.2e6, "snow_fc": 130.5e6}
+TRAFFIC_NCU = {"snow": (149.2e6, "profiles/r1_l_fused_snow_final_metrics.csv (ncu --set full, one launch; not measured in this run)"),
+               "snow_fc": (130.5e6, "profiles/r1_l_fused_snow_fc_final_metrics.csv (ncu --set full, one launch; not measured in this run)")}
 
 
 def run_fountain(args):

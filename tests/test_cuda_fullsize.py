@@ -260,10 +260,13 @@ def test_one_substep_of_the_389k_scene_against_the_oracle():
     assert np.array_equal(wc.table.neighbor, wo.table.neighbor[:wo.table.n_gblocks])
     assert np.array_equal(wc.store.orig_id, wo.store.orig_id[:G])
     assert np.array_equal(wc.store.lane_key, wo.store.lane_key[:G])
-    errs = U.grid_errors(wc.grid.vel, wo.grid.vel[:wo.table.count])
+    # nodal mass, and the nodal velocity as a vector (the scene falls along z: the x and y components
+    # are rounding noise in both implementations and have no scale of their own)
+    gc, go = wc.grid.vel, wo.grid.vel[:wo.table.count]
+    errs = [U.rel_err(gc[:, 0, :], go[:, 0, :]), U.rel_err(gc[:, 1:4, :], go[:, 1:4, :])]
     edge = float(W.positions.max() - W.positions.min())
     ex, ev, ef, _ = U.particle_errors(U.state_by_id(wc), U.state_by_id(wo), edge, 9)
-    print("389 K scene, 2 substeps: grid vel", ["%.1e" % e for e in errs], "x %.2e v %.2e F %.2e" % (ex, ev, ef))
+    print("389 K scene, 2 substeps: grid mass %.1e vel %.1e" % tuple(errs), "x %.2e v %.2e F %.2e" % (ex, ev, ef))
     assert max(errs) <= U.GRID_RTOL and ex <= U.X_RTOL and ev <= U.V_RTOL and ef <= U.F_ATOL
 
 
