@@ -40,6 +40,7 @@ extern "C" {
 #define MPM_CELL_BIAS 64      /* grid.py CELL_BIAS */
 #define MPM_N_COUNTERS 6      /* pipeline.py:57-63 */
 #define MPM_LANE_QUARANTINED 0x8000u
+#define MPM_LANE_SUNK 0x4000u        /* removed by a particle sink (always together with QUARANTINED) */
 
 enum mpm_status {
     MPM_OK = 0,
@@ -66,6 +67,24 @@ enum mpm_counter {                   /* pipeline.py:57-63 */
     MPM_C_SVD_CLAMP = 3, MPM_C_ADDRESS_ERR = 4, MPM_C_SUBGROUPS = 5
 };
 
+/* Step clock of CFL-auto frames (Worker.run_frame, pipeline.py:856-871; cfl_dt, domain.py:523-532)
+ * kept in DEVICE memory, so that frames with an adaptive step size are paced by the device like
+ * fixed-dt frames: the host enqueues steps ahead without knowing their dt.
+ *   dt[s & 1]  size of step s.  Written by the grid update of step s - 1 (mpm_grid_params.clock):
+ *              dt_s = min(frame_dt - t, cfl dx / max(vmax_{s-2} + c_sound, 1e-12)), vmax_{s-2} read
+ *              from the status ring (the reference's 3-slot ring with its two-step lag,
+ *              pipeline.py:866, 1104, 1135); by the host for the first step.
+ *   t          frame time elapsed before the newest step that has a dt.
+ * The grid update of the step that completes a frame (t + dt >= frame_dt - 1e-12) sets bit 1 of
+ * that step's status word and raises the guard at its own step: later steps already enqueued are
+ * no-ops, the host re-issues them as the next frame.  All arithmetic is float64, as in the
+ * reference; kernels convert to float32 where they consume dt. */
+typedef struct mpm_step_clock {
+    double dt[2];
+    double t;
+    double reserved;
+} mpm_step_clock;
+
 /* Material + step scalars of the transfer kernels: the scalar tail of
  * _p2g_kernel / _gather_advect / _g2p2g_kernel (pipeline.py:316-320, 400-403, 604-610). */
 typedef struct mpm_transfer_params {
@@ -86,6 +105,19 @@ typedef struct mpm_transfer_params {
     double margin_lo, margin_hi; /* free zone in cells: [origin-margin_lo, origin+4+margin_hi) */
     double theta_c, theta_s, hardening;   /* snow */
     double sand_alpha;       /* sand: sqrt(2/3) 2 sin(phi) / (3 - sin(phi)) */
+    /* CFL-auto frames paced by the device (NULL = dt / dt_gather above): the scatter takes
+     * clock->dt[clock_step & 1], the gather clock->dt[clock_gather_step & 1] (the step whose grid
+     * update produced vel: the same step for a split G2P, the previous one for the fused kernel
+     * and for a flush). */
+    const mpm_step_clock *clock;
+    int32_t clock_step, clock_gather_step;
+    /* Particle sink (not in the reference): a particle whose advected position lies
+     * in the box [sink_lo, sink_hi) is taken out of the simulation by the gather that moved it there:
+     * mass 0, lane flagged MPM_LANE_QUARANTINED | MPM_LANE_SUNK, orig_id -1, status->removed + 1.
+     * Like a quarantined lane it stops scattering at once and is dropped by the next rebuild's
+     * compaction (particles.py:177-188). */
+    int32_t sink_enabled, reserved5;
+    double sink_lo[3], sink_hi[3];
 } mpm_transfer_params;
 
 /* Particle store view: ParticleStore (particles.py:268-287). */
@@ -116,14 +148,19 @@ typedef struct mpm_table_view {
     int32_t n_gblocks;
 } mpm_table_view;
 
-/* Step status block written by the transfer kernels (device memory, 64 bytes):
+/* Step status block written by the transfer kernels and the grid update (device memory, 72 bytes):
  *   out_stats[0] (free-zone violation) and out_stats[1] (max speed^2) of
  *   _gather_advect (pipeline.py:408-409), plus counters[6] (pipeline.py:57-63). */
 typedef struct mpm_step_status {
-    int32_t zone_violation;
+    int32_t zone_violation;          /* bit 0: a particle left its free zone (out_stats[0]);
+                                        bit 1: this step completed a CFL-auto frame (mpm_step_clock) */
     uint32_t vmax2_bits;             /* float bits of max |v|^2 (nonnegative, so uint order = float order) */
     unsigned long long counters[MPM_N_COUNTERS];
+    double dt;                       /* size of the step, when a device clock paces it (else untouched) */
+    unsigned long long removed;      /* particles taken out by the sink (accumulates like the counters) */
 } mpm_step_status;
+#define MPM_STATUS_ZONE 1
+#define MPM_STATUS_FRAME_END 2
 
 /* ---- library ---------------------------------------------------------------------- */
 const char *mpm_version(void);
@@ -367,6 +404,19 @@ typedef struct mpm_grid_params {
     mpm_step_status *publish_dst;
     const int32_t *publish_guard_src;
     int32_t *publish_guard_dst;
+    /* CFL-auto frames paced by the device (clock NULL = dt above).  The update of step clock_step
+     * uses clock->dt[clock_step & 1], then advances the clock (see mpm_step_clock): vmax of step
+     * clock_step - 1 comes from vmax_ring[(clock_step - 1) % vmax_ring_len] (and from the same slot
+     * of every vmax_peer_rings entry: ranks / logical workers that share the frame clock), the
+     * step's dt and the frame-end bit go to *clock_status. */
+    mpm_step_clock *clock;
+    int32_t clock_step;
+    int32_t vmax_ring_len;
+    const mpm_step_status *vmax_ring;
+    mpm_step_status *clock_status;
+    double frame_dt, cfl_dx, c_sound;
+    int32_t n_vmax_peers, reserved4;
+    const mpm_step_status *vmax_peer_rings[MPM_MAX_PEERS];
 } mpm_grid_params;
 int mpm_grid_update(float *raw, uint8_t *touched, float *vel, float *vel_old,
                     const mpm_table_view *table, const mpm_grid_params *params,
@@ -449,6 +499,8 @@ typedef struct mpm_step_plan {
                                           before scattering -- the first use of the parity a rebuild
                                           left untouched (pipeline.py:1002-1006, 1022-1037) */
     int32_t reserved3;
+    /* CFL-auto frames: grid.clock (and frame_dt / cfl_dx / c_sound / vmax rings) set = every kernel
+     * of the batch takes its dt from the device clock; transfer.dt / dt_gather / grid.dt are ignored. */
 } mpm_step_plan;
 int mpm_enqueue_steps(const mpm_step_plan *plan, int32_t first_step, int32_t n_steps, void *stream);
 

@@ -67,7 +67,8 @@ class _TransferParams(C.Structure):
                 ("density", C.c_double), ("dx", C.c_double),
                 ("det", C.c_int64), ("do_lane_sort", C.c_int64),
                 ("theta_c", C.c_double), ("theta_s", C.c_double), ("hardening", C.c_double),
-                ("sand_alpha", C.c_double)]
+                ("sand_alpha", C.c_double),
+                ("sink_enabled", C.c_int64), ("sink_lo", C.c_double * 3), ("sink_hi", C.c_double * 3)]
 
 
 _lib = None
@@ -474,12 +475,15 @@ class OracleStore:
                                           _p(self.lane_key))
 
     def positions_with_ids(self):
-        flat, ids = self._gather_live(include_quarantined=True)
+        flat, ids = self.state_with_ids()
         return flat[:, CH_POS:CH_POS + 3].copy(), ids.copy()
 
     def state_with_ids(self):
-        """All channels of stored particles (incl. quarantined) + ids; oracle-only helper."""
-        return self._gather_live(include_quarantined=True)
+        """All channels of stored particles (incl. quarantined) + ids; oracle-only helper.
+        Lanes emptied by a particle sink (id -1) are skipped."""
+        flat, ids = self._gather_live(include_quarantined=True)
+        keep = ids >= 0
+        return (flat, ids) if keep.all() else (flat[keep], ids[keep])
 
     def total_mass(self):
         return float(self.data[:self.n_groups, CH_MASS, :].sum()) if self.n_groups else 0.0
@@ -587,6 +591,20 @@ class OracleWorker:
             sand_alpha=math.sqrt(2.0 / 3.0) * 2.0 * math.sin(math.radians(getattr(m, "friction_angle", 30.0)))
             / (3.0 - math.sin(math.radians(getattr(m, "friction_angle", 30.0)))))
 
+    # -- particle sink (not in the reference; mirrors CudaWorker.set_sink) --
+    def set_sink(self, min_corner, max_corner):
+        self._tp.sink_enabled = 1
+        for k in range(3):
+            self._tp.sink_lo[k], self._tp.sink_hi[k] = float(min_corner[k]), float(max_corner[k])
+        self.removed_count = getattr(self, "removed_count", 0)
+        self._sunk_pending = False
+
+    def _after_gather_stats(self, stats):
+        if stats[2] > 0.0:
+            self.removed_count += int(stats[2])
+            self._sunk_pending = True
+            self.store.orig_id[:self.store.n_groups][self.store.quarantined[:self.store.n_groups] == 2] = -1
+
     # -- population --
     def seed_particles(self, positions, velocities, masses, ids):
         n = self.store.stage_append(positions, velocities, masses, ids=ids)
@@ -649,6 +667,12 @@ class OracleWorker:
         self.step_post_barrier(step)
 
     def run_frame(self):
+        self._run_frame()
+        if getattr(self, "_sunk_pending", False):
+            self._sunk_pending = False
+            self.rebuild_needed = True
+
+    def _run_frame(self):
         """pipeline.py:856-880 (single worker)."""
         self.frame_steps = 0
         if self.cfl_mode:
@@ -744,7 +768,7 @@ class OracleWorker:
         if not st.n_groups:
             self.runtime.publish_vmax(step % 3, self.wid, 0.0)
             return
-        stats = np.zeros(2)
+        stats = np.zeros(3)
         lib().orc_gather_advect(
             _p(st.data), _p(st.lane_key), _p(st.quarantined), _p(st.group_len), _p(st.group_block),
             _p(st.group_origin), _p(self.table.neighbor), _p(self.grid.vel), _p(vel_old),
@@ -754,6 +778,7 @@ class OracleWorker:
         self._check_addressing()
         if stats[0] > 0.0:
             self.rebuild_needed = True
+        self._after_gather_stats(stats)
         self.runtime.publish_vmax(step % 3, self.wid, float(np.sqrt(stats[1])))
 
     def _flush_gather(self):
@@ -765,7 +790,7 @@ class OracleWorker:
         vel_old = self._vel_old_arg()
         if not st.n_groups:
             return
-        stats = np.zeros(2)
+        stats = np.zeros(3)
         lib().orc_g2p2g(
             _p(st.data), _p(st.lane_key), _p(st.quarantined), _p(st.group_len), _p(st.group_block),
             _p(st.group_origin), _i(st.n_groups), _p(self.table.neighbor), _p(self.grid.vel),
@@ -776,6 +801,7 @@ class OracleWorker:
         self._check_addressing()
         if stats[0] > 0.0:
             self.rebuild_needed = True
+        self._after_gather_stats(stats)
         self.runtime.publish_vmax(step % 3, self.wid, float(np.sqrt(stats[1])))
 
     def _post_barrier(self, par):

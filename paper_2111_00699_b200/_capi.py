@@ -18,6 +18,7 @@ LIB_PATH = os.environ.get("MPM_B200_LIB", os.path.join(_HERE, "libmpm_b200.so"))
 MPM_MAX_PEERS = 15
 N_COUNTERS = 6
 LANE_QUARANTINED = 0x8000
+LANE_SUNK = 0x4000
 
 p_void = C.c_void_p
 i32 = C.c_int32
@@ -32,6 +33,8 @@ class TransferParams(C.Structure):
         ("density", f64), ("dx", f64), ("dt", f64), ("dt_gather", f64), ("flip_blend", f64),
         ("margin_lo", f64), ("margin_hi", f64),
         ("theta_c", f64), ("theta_s", f64), ("hardening", f64), ("sand_alpha", f64),
+        ("clock", p_void), ("clock_step", i32), ("clock_gather_step", i32),
+        ("sink_enabled", i32), ("reserved5", i32), ("sink_lo", f64 * 3), ("sink_hi", f64 * 3),
     ]
 
 
@@ -61,6 +64,9 @@ class GridParams(C.Structure):
         ("wait_flags", p_void * MPM_MAX_PEERS), ("wait_error", p_void),
         ("publish_src", p_void), ("publish_dst", p_void), ("publish_guard_src", p_void),
         ("publish_guard_dst", p_void),
+        ("clock", p_void), ("clock_step", i32), ("vmax_ring_len", i32), ("vmax_ring", p_void),
+        ("clock_status", p_void), ("frame_dt", f64), ("cfl_dx", f64), ("c_sound", f64),
+        ("n_vmax_peers", i32), ("reserved4", i32), ("vmax_peer_rings", p_void * MPM_MAX_PEERS),
     ]
 
 
@@ -71,7 +77,14 @@ class Guard(C.Structure):
 
 class StepStatus(C.Structure):
     _fields_ = [("zone_violation", i32), ("vmax2_bits", C.c_uint32),
-                ("counters", C.c_ulonglong * N_COUNTERS)]
+                ("counters", C.c_ulonglong * N_COUNTERS), ("dt", f64), ("removed", C.c_ulonglong)]
+
+
+class StepClock(C.Structure):
+    _fields_ = [("dt", f64 * 2), ("t", f64), ("reserved", f64)]
+
+
+STATUS_ZONE, STATUS_FRAME_END = 1, 2
 
 
 STATUS_BYTES = C.sizeof(StepStatus)

@@ -66,7 +66,46 @@ struct GridArgs {
     mpm_step_status *publish_dst;
     const int *publish_guard_src;
     int *publish_guard_dst;
+    // device step clock of CFL-auto frames (mpm_grid_params.clock)
+    mpm_step_clock *clock;
+    int clock_step, vmax_ring_len, n_vmax_peers;
+    const mpm_step_status *vmax_ring;
+    mpm_step_status *clock_status;
+    double frame_dt, cfl_dx, c_sound;
+    const mpm_step_status *vmax_peer_rings[MPM_MAX_PEERS];
 };
+
+// Worker.run_frame's CFL loop (pipeline.py:856-871) for ONE step, on the device: account for step
+// s = clock_step, decide whether it completed the frame, and set the size of step s + 1 from the
+// max speed of step s - 1 (the reference's two-step lag, pipeline.py:866).  float64 like the
+// reference; one thread.
+__device__ __forceinline__ void advance_clock(const GridArgs &a)
+{
+    const int s = a.clock_step;
+    const double dt_s = a.clock->dt[s & 1];
+    double t = a.clock->t + dt_s;
+    const bool frame_end = !(t < a.frame_dt - 1e-12);
+    if (frame_end) t = 0.0;
+    const int slot = (s - 1 + a.vmax_ring_len) % a.vmax_ring_len;
+    unsigned bits = *(volatile const unsigned *)&a.vmax_ring[slot].vmax2_bits;
+    for (int p = 0; p < a.n_vmax_peers; ++p) {
+        unsigned o;
+        asm volatile("ld.relaxed.sys.global.u32 %0, [%1];" : "=r"(o) : "l"(&a.vmax_peer_rings[p][slot].vmax2_bits) : "memory");
+        bits = o > bits ? o : bits;          // nonnegative floats: unsigned order = float order
+    }
+    const double vmax = sqrt((double)__uint_as_float(bits));
+    const double speed = vmax + a.c_sound;
+    double dt_next = a.cfl_dx / (speed > 1e-12 ? speed : 1e-12);
+    const double remaining = a.frame_dt - t;
+    if (remaining < dt_next) dt_next = remaining;
+    a.clock->dt[(s + 1) & 1] = dt_next;
+    a.clock->t = t;
+    if (a.clock_status) {
+        a.clock_status->dt = dt_s;
+        if (frame_end) atomicOr(&a.clock_status->zone_violation, MPM_STATUS_FRAME_END);
+    }
+    if (frame_end) guard_raise(a.guard);     // steps enqueued beyond the frame are void
+}
 
 // 56-byte status block (+ guard word) to mapped pinned host memory: lanes 0..6 one 8-byte word each
 __device__ __forceinline__ void publish_status(const mpm_step_status *src, mpm_step_status *dst,
@@ -153,6 +192,16 @@ __global__ void __launch_bounds__(256) grid_update_kernel(const GridArgs a)
             }
         }
     }
+    float dt = a.dt;
+    if (a.clock) {
+        dt = (float)__ldcg(&a.clock->dt[a.clock_step & 1]);
+        if (blockIdx.x == 0 && threadIdx.x < 32) {
+            // entry (s + 1) & 1 is written, entry s & 1 (read by every CTA) is not
+            if (threadIdx.x == 0) advance_clock(a);
+            __threadfence();
+            __syncwarp();
+        }
+    }
     // after the barrier: a guard raised by a peer during this step has landed
     if ((a.publish_dst || a.publish_guard_dst) && blockIdx.x == 0 && threadIdx.x < 32)
         publish_status(a.publish_src, a.publish_dst, a.publish_guard_src, a.publish_guard_dst, threadIdx.x);
@@ -211,7 +260,7 @@ __global__ void __launch_bounds__(256) grid_update_kernel(const GridArgs a)
         vx = node.y / m; vy = node.z / m; vz = node.w / m;
     }
     if (a.vel_old) a.vel_old[idx] = make_float4(0.f, vx, vy, vz);   // saved before gravity (:692-698)
-    vx += a.dt * a.gx; vy += a.dt * a.gy; vz += a.dt * a.gz;
+    vx += dt * a.gx; vy += dt * a.gy; vz += dt * a.gz;
     if (a.apply_bc) {
         // node world position in float64 so that the inclusive comparisons of
         // pipeline.py:707-718 classify nodes exactly like the reference
@@ -444,6 +493,17 @@ int mpm_grid_update(float *raw, uint8_t *touched, float *vel, float *vel_old,
     a.publish_dst = p->publish_dst;
     a.publish_guard_src = p->publish_guard_src;
     a.publish_guard_dst = p->publish_guard_dst;
+    a.clock = p->clock;
+    a.clock_step = p->clock_step;
+    a.vmax_ring = p->vmax_ring;
+    a.vmax_ring_len = p->vmax_ring_len;
+    a.clock_status = p->clock_status;
+    a.frame_dt = p->frame_dt; a.cfl_dx = p->cfl_dx; a.c_sound = p->c_sound;
+    a.n_vmax_peers = p->clock ? p->n_vmax_peers : 0;
+    if (p->clock && (!p->vmax_ring || p->vmax_ring_len < 3 || !(p->frame_dt > 0.0) ||
+                     a.n_vmax_peers < 0 || a.n_vmax_peers > MPM_MAX_PEERS))
+        return MPM_ERR_REJECTED_INPUT;
+    for (int k = 0; k < MPM_MAX_PEERS; ++k) a.vmax_peer_rings[k] = k < a.n_vmax_peers ? p->vmax_peer_rings[k] : nullptr;
     launch_chained(grid_update_kernel, (a.count + 3) / 4, 256, (cudaStream_t)stream, a);
     return check_launch("mpm_grid_update", 1);
 }

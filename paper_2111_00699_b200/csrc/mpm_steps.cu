@@ -41,6 +41,18 @@ extern "C" int mpm_enqueue_steps(const mpm_step_plan *p, int32_t first_step, int
         guard.n_peer_words = p->n_peer_words;
         for (int q = 0; q < MPM_MAX_PEERS; ++q) guard.peer_words[q] = p->peer_guard_words[q];
         if (gp.n_wait > 0) gp.wait_value = s + 1;
+        if (gp.clock) {
+            // CFL-auto frame: every kernel of the step reads its dt from the device clock; the
+            // update of step s also sets the size of step s + 1 and reports dt_s / the frame end
+            // in the step's status block
+            gp.clock_step = s;
+            gp.clock_status = p->status_dev + slot;
+            tp.clock = gp.clock;
+            tp.clock_step = s;
+            tp.clock_gather_step = s;      // split G2P: the update of the same step
+        } else {
+            tp.clock = nullptr;
+        }
         if (p->signal_word)
             for (int q = 0; q < gp.n_peers; ++q) {
                 gp.peer_raw[q] = p->peer_raw[par][q];
@@ -66,6 +78,7 @@ extern "C" int mpm_enqueue_steps(const mpm_step_plan *p, int32_t first_step, int
             mpm_transfer_params fp = tp;
             fp.margin_lo = p->fused_margin_lo;
             fp.margin_hi = p->fused_margin_hi;
+            fp.clock_gather_step = s - 1;  // the fused gather completes the previous step
             if (p->time_events[2 * k]) cudaEventRecord((cudaEvent_t)p->time_events[2 * k], stream);
             rc = mpm_g2p2g(&p->store, &p->table, p->vel, p->vel_old, p->raw[par], p->touched[par], &fp,
                            st_dev, &guard, stream);

@@ -37,6 +37,14 @@ struct TransferArgs {
     float margin_lo, margin_hi;
     float theta_c, theta_s, hardening, sand_alpha;
     int clamp_tension, count_stats, deterministic;
+    // CFL-auto frames paced by the device: dt of the scatter / gather read from the clock
+    const mpm_step_clock *clock;
+    int clock_step, clock_gather_step;
+    float coeff_per_dt;
+    // particle sink: box in world coordinates, lanes inside it after advection are removed
+    int sink_enabled;
+    float sink_lo[3], sink_hi[3];
+    long long *ids;
     DevGuard guard;
 };
 
@@ -431,6 +439,12 @@ __global__ void __launch_bounds__(TW * 32, MPM_MINBLOCKS) transfer_kernel(const 
     float tau[9]; // plastic kinds: stress of the projected state, produced by the gather
     float plastic = 0.f;
     const PlasticParams pp = {a.mu, a.lam, a.theta_c, a.theta_s, a.hardening, a.sand_alpha};
+    float dt_gather = a.dt_gather, coeff_base = a.coeff_base;
+    if (a.clock) {
+        // adaptive step size kept on the device (mpm_step_clock): two warp-uniform loads
+        if (GATHER) dt_gather = (float)__ldcg(&a.clock->dt[a.clock_gather_step & 1]);
+        if (SCATTER) coeff_base = a.coeff_per_dt * (float)__ldcg(&a.clock->dt[a.clock_step & 1]);
+    }
     int addr_err = 0;
     unsigned vmax_bits = 0;
     // the deformation state is loaded after the 27-node gather (MPM_LATE_F): nine registers less
@@ -468,7 +482,7 @@ __global__ void __launch_bounds__(TW * 32, MPM_MINBLOCKS) transfer_kernel(const 
                     nvy = (1.0f - a.flip) * nvy + a.flip * (ovy + dv[1]);
                     nvz = (1.0f - a.flip) * nvz + a.flip * (ovz + dv[2]);
                 }
-                const float dtg = a.dt_gather;
+                const float dtg = dt_gather;
                 const float npx = px + dtg * nvx, npy = py + dtg * nvy, npz = pz + dtg * nvz;
                 if (!(isfinite(npx) && isfinite(npy) && isfinite(npz) && isfinite(nvx) &&
                       isfinite(nvy) && isfinite(nvz))) {
@@ -518,8 +532,21 @@ __global__ void __launch_bounds__(TW * 32, MPM_MINBLOCKS) transfer_kernel(const 
                     const float zy1 = ((float)(org.y - MPM_CELL_BIAS) + 4.0f + a.margin_hi) * a.dx;
                     const float zz1 = ((float)(org.z - MPM_CELL_BIAS) + 4.0f + a.margin_hi) * a.dx;
                     if (px < zx0 || px >= zx1 || py < zy0 || py >= zy1 || pz < zz0 || pz >= zz1) {
-                        a.status->zone_violation = 1;
+                        // bit 0 of the word (bit 1 belongs to the grid update's frame clock)
+                        if (!(*(volatile int *)&a.status->zone_violation & MPM_STATUS_ZONE))
+                            atomicOr(&a.status->zone_violation, MPM_STATUS_ZONE);
                         guard_raise(a.guard);
+                    }
+                    if (a.sink_enabled && px >= a.sink_lo[0] && px < a.sink_hi[0] && py >= a.sink_lo[1] &&
+                        py < a.sink_hi[1] && pz >= a.sink_lo[2] && pz < a.sink_hi[2]) {
+                        // sink: the lane completes this gather like any other (state stored, free zone,
+                        // max speed) and is then out of the simulation -- no scatter below, dropped by
+                        // the next rebuild's compaction like a quarantined lane
+                        meta |= MPM_LANE_QUARANTINED | MPM_LANE_SUNK;
+                        gd[CH_MASS * 32] = 0.0f;
+                        a.ids[g * 32 + lane] = -1;
+                        atomicAdd(&a.status->removed, 1ull);
+                        active = false;
                     }
                     vmax_bits = __float_as_uint(vx * vx + vy * vy + vz * vz);
                     float tmp;
@@ -528,7 +555,7 @@ __global__ void __launch_bounds__(TW * 32, MPM_MINBLOCKS) transfer_kernel(const 
                     int nkz = (int)stencil_base(pz, a.inv_dx, &tmp) + MPM_CELL_BIAS - (org.z - 4);
                     nkx = min(max(nkx, 0), 9); nky = min(max(nky, 0), 9); nkz = min(max(nkz, 0), 9);
                     key = nkx + 10 * (nky + 10 * nkz);
-                    a.meta[g * 32 + lane] = (uint16_t)key;
+                    a.meta[g * 32 + lane] = (uint16_t)(key | (meta & (MPM_LANE_QUARANTINED | MPM_LANE_SUNK)));
                 }
             }
         }
@@ -557,7 +584,7 @@ __global__ void __launch_bounds__(TW * 32, MPM_MINBLOCKS) transfer_kernel(const 
             }
         }
         if (active) {
-            const float coeff = a.coeff_base * m;
+            const float coeff = coeff_base * m;
             if (MAT == MPM_MAT_FLUID) {
                 float tau;
                 if (F[0] <= 0.0f) {
@@ -667,6 +694,14 @@ static int fill_args(TransferArgs &a, const mpm_store_view *store, const mpm_tab
     a.dt_gather = (float)p->dt_gather;
     a.d_inv = (float)(4.0 * inv_dx * inv_dx);
     a.coeff_base = (float)(-4.0 * p->dt * inv_dx * inv_dx / p->density);
+    a.coeff_per_dt = (float)(-4.0 * inv_dx * inv_dx / p->density);
+    a.clock = p->clock;
+    a.clock_step = p->clock_step;
+    a.clock_gather_step = p->clock_gather_step;
+    a.sink_enabled = p->sink_enabled;
+    for (int k = 0; k < 3; ++k) { a.sink_lo[k] = (float)p->sink_lo[k]; a.sink_hi[k] = (float)p->sink_hi[k]; }
+    a.ids = (long long *)store->orig_id;
+    if (a.sink_enabled && !a.ids) return MPM_ERR_REJECTED_INPUT;
     a.mu = (float)p->mu; a.lam = (float)p->lam; a.kappa = (float)p->kappa; a.gamma = (float)p->gamma;
     a.flip = (float)p->flip_blend;
     a.margin_lo = (float)p->margin_lo; a.margin_hi = (float)p->margin_hi;

@@ -85,6 +85,7 @@ class CudaParticleStore:
         self.staged_count = 0
         self._next_id = 0
         self._pin = {}
+        self.has_sink = False   # set by the worker: sunk lanes (orig_id -1) are skipped by readbacks
         self._table = None   # set by the worker: group_origin comes from the block table
         self._before_read = None   # set by the worker: completes a lazily pending gather
 
@@ -297,7 +298,11 @@ class CudaParticleStore:
             v = self.view()
             check(_capi.lib().mpm_gather_state(C.byref(v), flat.data_ptr(), ids.data_ptr(),
                                                _stream_ptr()), "mpm_gather_state")
-        return flat[:n].to(torch.float64).cpu().numpy(), ids[:n].cpu().numpy()
+        flat, ids = flat[:n].to(torch.float64).cpu().numpy(), ids[:n].cpu().numpy()
+        if self.has_sink:
+            keep = ids >= 0
+            flat, ids = flat[keep], ids[keep]
+        return flat, ids
 
     def positions_with_ids(self, dtype=np.float64):
         """particles.py:466-475: positions of every stored particle (quarantined included) and
@@ -317,6 +322,9 @@ class CudaParticleStore:
         hpos.copy_(pos, non_blocking=True)
         hids.copy_(ids, non_blocking=True)
         torch.cuda.current_stream().synchronize()
+        if self.has_sink:
+            keep = hids.numpy() >= 0
+            return hpos.numpy()[keep].astype(dtype or np.float32), hids.numpy()[keep]
         if dtype is None:
             # zero-copy views of the pinned readback buffers, valid until the next readback
             return hpos.numpy(), hids.numpy()
@@ -547,6 +555,9 @@ class CudaWorker:
             self._guard_word = torch.full((1,), _INT_MAX, dtype=torch.int32, device=self.device)
             self._scalars = torch.zeros(16, dtype=torch.int32, device=self.device)
             self._scalars_host = torch.zeros(16, dtype=torch.int32).pin_memory()
+            # step clock of CFL-auto frames (mpm_step_clock: dt[2], t, reserved), device-resident
+            self._clock = torch.zeros(4, dtype=torch.float64, device=self.device)
+            self._clock_host = torch.zeros(4, dtype=torch.float64).pin_memory()
         self.flags = StepFlags(deterministic_mode=bool(self.options.deterministic))
         self._node_bytes = 32 if self.options.deterministic else 16
         self.conservation = []
@@ -566,6 +577,17 @@ class CudaWorker:
         self._frame_steps = 0
         self._frame_rebuilds = 0
         self.cfl_mode = False
+        # CFL-auto frames paced by the device (mpm_step_clock): the grid update computes the next
+        # step size from the max speed of two steps earlier and ends the frame itself, so adaptive
+        # frames are enqueued ahead like fixed-dt ones.  False = the host computes dt every step.
+        self.device_clock = True
+        self._use_clock = False       # set for the duration of a device-clocked frame
+        self._clock_valid = False     # the device clock holds dt of step _global_step, t = 0
+        self._flushing_gather = False
+        self._last_dt = 0.0
+        self._last_frame_end = False
+        self._removed_seen = [0] * _RING
+        self._sunk_pending = False
         self.frame_dts = []
         self.count_stats = bool(count_stats)
         self.fuse_clear = bool(fuse_clear)
@@ -706,6 +728,30 @@ class CudaWorker:
         self.flags.fused_mode = False
         return self.seed_particles(positions, velocities, masses, ids)
 
+    # -- particle sink (not in the reference) -----------------------------------
+    def set_sink(self, min_corner, max_corner):
+        """Particles whose advected position lies in the box [min_corner, max_corner) leave the
+        simulation: the gather that moved them there zeroes their mass and flags the lane, they stop
+        scattering at once and the next rebuild drops them (a frame in which something sank ends
+        with a rebuild request).  `removed_count` counts them; readbacks skip them."""
+        lo, hi = [float(x) for x in min_corner], [float(x) for x in max_corner]
+        if len(lo) != 3 or len(hi) != 3 or any(not (a < b) for a, b in zip(lo, hi)):
+            raise RejectedInputError(f"sink box needs min < max on three axes, got {lo} / {hi}")
+        self._tp.sink_enabled = 1
+        for k in range(3):
+            self._tp.sink_lo[k], self._tp.sink_hi[k] = lo[k], hi[k]
+        self.store.has_sink = True
+        self._plan_stale = True
+
+    def clear_sink(self):
+        self._tp.sink_enabled = 0
+        self._plan_stale = True
+
+    @property
+    def removed_count(self) -> int:
+        """Particles taken out by the sink so far."""
+        return int(self._status.cpu().numpy()[:, 8].sum())
+
     # -- per frame (pipeline.py:852-880) ------------------------------------------------
     def begin_frame(self):
         self._phase_ms = {k: 0.0 for k in _PHASES}
@@ -715,15 +761,26 @@ class CudaWorker:
         self.frame_dts = []       # step sizes of the current frame, in order
 
     def run_frame(self):
+        self._run_frame()
+        if self._sunk_pending:
+            # lanes emptied by the sink are compacted away by the next rebuild
+            self._sunk_pending = False
+            self.flags.rebuild_needed = True
+
+    def _run_frame(self):
         self.begin_frame()
         if self.pipelined and self.runtime.n_workers == 1 and \
                 self.options.rebuild != "every_step" and not self.options.collect_conservation:
             with torch.cuda.device(self.device):
-                if self.batch_steps > 0 and not self.cfl_mode:
+                if self.cfl_mode and self.device_clock and self.batch_steps > 0:
+                    self._run_frame_batched(cfl=True)
+                elif self.batch_steps > 0 and not self.cfl_mode:
                     self._run_frame_batched()
                 else:
+                    self._clock_valid = False
                     self._run_frame_pipelined()
             return
+        self._clock_valid = False
         with torch.cuda.device(self.device):
             if self.cfl_mode:
                 c_sound = self.material.sound_speed()
@@ -854,92 +911,154 @@ class CudaWorker:
         C.memmove(C.byref(plan.grid), C.byref(gp), C.sizeof(_capi.GridParams))
         return plan
 
-    def _run_frame_batched(self):
-        """Fixed-dt frame with the steady-state steps enqueued in batches from C
-        (mpm_enqueue_steps), two batches in flight.  Same guard protocol as
-        _run_frame_pipelined: a step that raises the rebuild flag turns every later enqueued
-        step into a no-op on the device; the host drops them, rebuilds and carries on from the
-        step after the one that raised the flag -- the reference's sequence of steps."""
+    def _ensure_clock(self):
+        """Device step clock of a CFL-auto frame (mpm_step_clock).  Once a device-clocked frame has
+        run, the clock already holds the size of the next step (its last grid update computed it)
+        and t = 0; it is (re)initialised from the host's vmax ring when steps ran outside it."""
+        if self._clock_valid:
+            return
+        step = self._global_step
+        c_sound = self.material.sound_speed()
+        dt0 = cfl_dt(self.runtime.global_vmax((step - 2) % 3) + c_sound, self.params, self.params.frame_dt)
+        self._clock_host.zero_()
+        self._clock_host[step & 1] = dt0
+        self._clock.copy_(self._clock_host, non_blocking=True)
+        # The update of step `step` reads vmax of step - 1 from the status ring, the one after it
+        # vmax of `step`.  The reference's ring has three slots that keep their last value when a
+        # step publishes nothing (the first step of a fused run has no gather: slot step % 3 still
+        # holds the initial max speed, pipeline.py:866); the same values are planted here.
+        s32 = self._status.view(torch.int32)
+        for k in (step - 1, step):
+            slot = k % _RING
+            v2 = np.float32(self.runtime.global_vmax(k % 3)) ** 2
+            s32[slot, 1] = int(np.float32(v2).view(np.int32))
+            self._slot_clean[slot] = False
+        self._clock_valid = True
+
+    def _publish_clock_status(self, step):
+        """A device-clocked step without a gather of its own (rebuild step of the fused transfer):
+        fetch dt and the frame-end bit the grid update left in the step's status block."""
+        slot = step % _RING
+        if self._status_alias:
+            self._call("mpm_status_publish", self._status_ptr(slot),
+                       self._status_alias + slot * _capi.STATUS_BYTES, None, None, _stream_ptr())
+        else:
+            self._status_host[slot].copy_(self._status[slot], non_blocking=True)
+        self._status_events[slot].record()
+        self._status_events[slot].synchronize()
+        raw = self._status_host.numpy()
+        self._last_dt = float(raw.view(np.float64)[slot, 7])
+        self._last_frame_end = bool(int(raw.view(np.uint32)[slot, 0]) & _capi.STATUS_FRAME_END)
+        self._slot_clean[slot] = False
+
+    def _run_frame_batched(self, cfl=False):
+        """Frame with the steady-state steps enqueued in batches from C (mpm_enqueue_steps), two
+        batches in flight.  Same guard protocol as _run_frame_pipelined: a step that raises the
+        rebuild flag turns every later enqueued step into a no-op on the device; the host drops
+        them, rebuilds and carries on from the step after the one that raised the flag -- the
+        reference's sequence of steps.
+
+        cfl=True (CFL-auto frames, pipeline.py:856-871): the step sizes live on the device
+        (mpm_step_clock).  The host does not know how many steps the frame takes: it keeps
+        enqueueing, reads dt and the frame-end bit from each step's status block, and the grid
+        update of the step that completes the frame voids the steps enqueued beyond it."""
         spf = self.params.steps_per_frame
-        self.dt = self.params.dt
+        if cfl:
+            self._ensure_clock()
+            self._use_clock = True
+        else:
+            self.dt = self.params.dt
         pending = []            # batches in flight: (first_step, n, time-event base or None)
         enq = 0                 # steps of this frame enqueued (confirmed + speculative)
         next_step = self._global_step
         tbase = 0
-        while self._frame_steps < spf:
-            while len(pending) < 2 and enq < spf and self._can_batch(next_step):
-                n = min(self.batch_steps, spf - enq)
-                plan = self._step_plan()
-                plan.full_clear_first = int(self._pending_full_clear_parity != -1)
-                self._pending_full_clear_parity = -1
-                tev = None
-                for k in range(2 * n):
-                    plan.time_events[k] = None
-                if self.time_kernels:
-                    # ONE step of a batch is timed: an event between two kernels of the chain
-                    # serialises them fully (no programmatic dependent launch across it), so the
-                    # other steps run exactly as they do untimed.  Its position rotates from batch
-                    # to batch: the first step after a rebuild (freshly sorted lanes, cold L2) must
-                    # not be over-represented in the mean.
-                    tk = self._time_rot % n
-                    self._time_rot += 1
-                    tev = (tbase, tk)
-                    plan.time_events[2 * tk] = self._time_events[2 * tbase].cuda_event
-                    plan.time_events[2 * tk + 1] = self._time_events[2 * tbase + 1].cuda_event
-                    tbase = (tbase + _BATCH) % (2 * _BATCH)
-                # the first step of a batch gathers with the dt of the last grid update done
-                plan.transfer.dt_gather = float(self._vel_dt if not pending else self.dt)
-                self.kernel_calls += 1
-                check(self.lib.mpm_enqueue_steps(C.byref(plan), next_step, n, _stream_ptr()),
-                      "mpm_enqueue_steps")
-                pending.append((next_step, n, tev))
-                next_step += n
-                enq += n
-            if not pending:
-                # rebuild step, first fused step after a rebuild, pending full clear: one plain step
-                # (its gather's status is read after the whole step is enqueued)
-                self._guard = None
-                self._defer, self._unconsumed = True, None
-                try:
-                    self.run_step(self._global_step)
-                finally:
-                    self._defer = False
-                if self._unconsumed is not None:
-                    self._consume(*self._unconsumed)
-                    self._unconsumed = None
-                self._frame_steps += 1
-                self.frame_dts.append(self.dt)
-                enq = self._frame_steps
-                next_step = self._global_step
-                continue
-            first, n, tev = pending.pop(0)
-            for k in range(n):
-                step = first + k
-                self._slot_clean[step % _RING] = False
-                self._consume(step % _RING, step)
-                if tev is not None and k == tev[1]:
-                    name = "mpm_g2p2g" if self.options.transfer == "g2p2g" else "mpm_p2g"
-                    self.kernel_events.append((name, self._time_events[2 * tev[0]],
-                                               self._time_events[2 * tev[0] + 1]))
-                # step `step` itself ran to completion (the guard only stops LATER steps)
-                self._global_step = step + 1
-                self._vel_dt = self.dt
-                self.flags.steps_since_rebuild += 1
-                self.runtime.generations += 1
-                self._frame_steps += 1
-                self.frame_dts.append(self.dt)
-                if self.flags.rebuild_needed:
-                    self.speculative_discards += (n - 1 - k) + sum(b[1] for b in pending)
-                    pending = []
+        frame_done = False
+        try:
+            while (not frame_done) if cfl else (self._frame_steps < spf):
+                while len(pending) < 2 and (cfl or enq < spf) and self._can_batch(next_step):
+                    n = self.batch_steps if cfl else min(self.batch_steps, spf - enq)
+                    plan = self._step_plan()
+                    plan.full_clear_first = int(self._pending_full_clear_parity != -1)
+                    self._pending_full_clear_parity = -1
+                    tev = None
+                    for k in range(2 * n):
+                        plan.time_events[k] = None
+                    if self.time_kernels:
+                        # ONE step of a batch is timed: an event between two kernels of the chain
+                        # serialises them fully (no programmatic dependent launch across it), so the
+                        # other steps run exactly as they do untimed.  Its position rotates from batch
+                        # to batch: the first step after a rebuild (freshly sorted lanes, cold L2) must
+                        # not be over-represented in the mean.
+                        tk = self._time_rot % n
+                        self._time_rot += 1
+                        tev = (tbase, tk)
+                        plan.time_events[2 * tk] = self._time_events[2 * tbase].cuda_event
+                        plan.time_events[2 * tk + 1] = self._time_events[2 * tbase + 1].cuda_event
+                        tbase = (tbase + _BATCH) % (2 * _BATCH)
+                    # the first step of a batch gathers with the dt of the last grid update done
+                    plan.transfer.dt_gather = float(self._vel_dt if not pending else self.dt)
+                    self.kernel_calls += 1
+                    check(self.lib.mpm_enqueue_steps(C.byref(plan), next_step, n, _stream_ptr()),
+                          "mpm_enqueue_steps")
+                    pending.append((next_step, n, tev))
+                    next_step += n
+                    enq += n
+                if not pending:
+                    # rebuild step, first fused step after a rebuild, pending full clear: one plain step
+                    # (its gather's status is read after the whole step is enqueued)
+                    self._guard = None
+                    self._defer, self._unconsumed = True, None
+                    step = self._global_step
+                    try:
+                        self.run_step(step)
+                    finally:
+                        self._defer = False
+                    if self._unconsumed is not None:
+                        self._consume(*self._unconsumed)
+                        self._unconsumed = None
+                    elif cfl:
+                        self._publish_clock_status(step)
+                    if cfl:
+                        self.dt = self._vel_dt = self._last_dt
+                        frame_done = self._last_frame_end
+                    self._frame_steps += 1
+                    self.frame_dts.append(self.dt)
                     enq = self._frame_steps
                     next_step = self._global_step
-                    if self._rebuild_tail_ok_static():
-                        # nothing guarded is enqueued before the rebuild this flag asks for, and
-                        # mpm_rebuild resets the word itself (one launch and its gap less)
-                        self._guard_reset_in_rebuild = True
-                    else:
-                        self._call("mpm_fill_i32", self._guard_word.data_ptr(), 1, _INT_MAX, _stream_ptr())
-                    break
+                    continue
+                first, n, tev = pending.pop(0)
+                for k in range(n):
+                    step = first + k
+                    self._slot_clean[step % _RING] = False
+                    self._consume(step % _RING, step)
+                    if cfl:
+                        self.dt = self._last_dt
+                        frame_done = self._last_frame_end
+                    if tev is not None and k == tev[1]:
+                        name = "mpm_g2p2g" if self.options.transfer == "g2p2g" else "mpm_p2g"
+                        self.kernel_events.append((name, self._time_events[2 * tev[0]],
+                                                   self._time_events[2 * tev[0] + 1]))
+                    # step `step` itself ran to completion (the guard only stops LATER steps)
+                    self._global_step = step + 1
+                    self._vel_dt = self.dt
+                    self.flags.steps_since_rebuild += 1
+                    self.runtime.generations += 1
+                    self._frame_steps += 1
+                    self.frame_dts.append(self.dt)
+                    if self.flags.rebuild_needed or frame_done:
+                        self.speculative_discards += (n - 1 - k) + sum(b[1] for b in pending)
+                        pending = []
+                        enq = self._frame_steps
+                        next_step = self._global_step
+                        if self.flags.rebuild_needed and self._rebuild_tail_ok_static():
+                            # nothing guarded is enqueued before the rebuild this flag asks for, and
+                            # mpm_rebuild resets the word itself (one launch and its gap less)
+                            self._guard_reset_in_rebuild = True
+                        else:
+                            self._call("mpm_fill_i32", self._guard_word.data_ptr(), 1, _INT_MAX, _stream_ptr())
+                        break
+        finally:
+            self._use_clock = False
         if self._pending_gather and not self.lazy_flush:
             self._flush_gather()
 
@@ -999,6 +1118,8 @@ class CudaWorker:
         self._global_step = step + 1
 
     def run_step(self, step):
+        if not self._use_clock:
+            self._clock_valid = False      # a step with a host-given dt: the device clock is stale
         with torch.cuda.device(self.device):
             self.step_pre_barrier(step)
             self.runtime.barrier_wait(self.wid)
@@ -1084,7 +1205,7 @@ class CudaWorker:
         if tail:
             # rest of the step (step_pre_barrier / step_post_barrier): P2G into status slot `step`,
             # grid update that also zeroes the status block of the gather following it
-            tp, gp = self._params(), self._grid_params()
+            tp, gp = self._params(step=step), self._grid_params(step)
             gp.fuse_clear = int(self.fuse_clear)
             reset_slot = (step + 1 if self._fused_active() else step) % _RING
             plan.p2g_params, plan.grid_params = C.addressof(tp), C.addressof(gp)
@@ -1186,12 +1307,15 @@ class CudaWorker:
         self._call("mpm_clear", self.grid._raw[par].ptr, self.table._touched[par].ptr, count, full,
                    self._node_bytes, self._gref(), _stream_ptr())
 
-    def _params(self, margin_shrink=0.0):
+    def _params(self, margin_shrink=0.0, step=0, gather_step=0):
         tp = self._tp
         tp.dt = float(self.dt)
         tp.dt_gather = float(self._vel_dt)
         tp.margin_lo = FREE_ZONE_LO_CELLS - margin_shrink
         tp.margin_hi = FREE_ZONE_HI_CELLS - 4.0 - margin_shrink
+        # device-clocked CFL frame: dt / dt_gather above are ignored, the kernels read the clock
+        tp.clock = self._clock.data_ptr() if self._use_clock else None
+        tp.clock_step, tp.clock_gather_step = int(step), int(gather_step)
         return tp
 
     def _vel_old_ptr(self):
@@ -1215,7 +1339,7 @@ class CudaWorker:
             return
         sv, tv = st.view(), self.table.view()
         self._call("mpm_p2g", C.byref(sv), C.byref(tv), self.grid._raw[par].ptr,
-                   self.table._touched[par].ptr, C.byref(self._params()),
+                   self.table._touched[par].ptr, C.byref(self._params(step=step)),
                    self._status_ptr(step % _RING), self._gref(), _stream_ptr())
 
     def _gather_slot(self, step, stream):
@@ -1246,7 +1370,8 @@ class CudaWorker:
         stream = _stream_ptr()
         slot = self._gather_slot(step, stream)
         self._call("mpm_g2p", C.byref(sv), C.byref(tv), self.grid._vel.ptr, self._vel_old_ptr(),
-                   C.byref(self._params()), self._status_ptr(slot), self._gref(), stream)
+                   C.byref(self._params(step=step, gather_step=step)), self._status_ptr(slot),
+                   self._gref(), stream)
         self._after_gather(slot, step)
 
     def _ensure_flushed(self):
@@ -1263,13 +1388,16 @@ class CudaWorker:
         """Complete a pending fused gather.  Its status block is read back at once, or (defer)
         handed to the caller as (slot, step) to be consumed at its next host sync."""
         guard, was_defer, unconsumed = self._guard, self._defer, self._unconsumed
+        use_clock = self._use_clock
         self._guard, self._defer = None, bool(defer)
         self._unconsumed = None
+        self._use_clock = False      # the flushed step's dt has been read back: _vel_dt, by value
         try:
             self._run_g2p(self._global_step)
             flushed = self._unconsumed
         finally:
             self._guard, self._defer, self._unconsumed = guard, was_defer, unconsumed
+            self._use_clock = use_clock
         self._pending_gather = False
         return flushed
 
@@ -1282,8 +1410,8 @@ class CudaWorker:
         slot = self._gather_slot(step, stream)
         self._call("mpm_g2p2g", C.byref(sv), C.byref(tv), self.grid._vel.ptr, self._vel_old_ptr(),
                    self.grid._raw[par].ptr, self.table._touched[par].ptr,
-                   C.byref(self._params(FUSED_MARGIN_CELLS)), self._status_ptr(slot), self._gref(),
-                   stream)
+                   C.byref(self._params(FUSED_MARGIN_CELLS, step=step, gather_step=step - 1)),
+                   self._status_ptr(slot), self._gref(), stream)
         self._after_gather(slot, step)
 
     def _consume(self, slot, step):
@@ -1297,8 +1425,17 @@ class CudaWorker:
             raw = self._status_host.numpy()
             views = self._status_views = (raw, raw.view(np.uint32), raw.view(np.float32))
         raw, u32, f32 = views
-        if u32[slot, 0]:
+        word = int(u32[slot, 0])
+        if word & _capi.STATUS_ZONE:
             self.flags.rebuild_needed = True
+        if self._tp.sink_enabled:
+            removed = int(raw[slot, 8])          # accumulates per slot
+            if removed != self._removed_seen[slot]:
+                self._removed_seen[slot] = removed
+                self._sunk_pending = True
+        if self._use_clock:
+            self._last_dt = float(raw.view(np.float64)[slot, 7])
+            self._last_frame_end = bool(word & _capi.STATUS_FRAME_END)
         vmax2 = float(f32[slot, 1])
         self.runtime.publish_vmax(step % 3, self.wid, math.sqrt(max(vmax2, 0.0)))
         if raw[slot, 1 + C_ADDRESS_ERR]:
@@ -1360,7 +1497,7 @@ class CudaWorker:
                 peers.append((s["raw"].ptr, s["touched"].ptr, self._peer_map[q].ptr))
         if self.options.collect_conservation:
             self._collect_conservation(par)
-        gp = self._grid_params()
+        gp = self._grid_params(step)
         gp.fuse_clear = int(self.fuse_clear and self.runtime.n_workers == 1)
         gp.n_peers = len(peers)
         for k, (r, t, m) in enumerate(peers):
@@ -1374,7 +1511,7 @@ class CudaWorker:
             self._slot_clean[nxt] = True
         self._vel_dt = self.dt
 
-    def _grid_params(self):
+    def _grid_params(self, step=None):
         """mpm_grid_params with the per-run constants filled once; dt set per call."""
         gp = self._gp
         if gp is None:
@@ -1394,6 +1531,19 @@ class CudaWorker:
         gp.block_filter = 0
         gp.fuse_clear = 0
         gp.n_peers = 0
+        if self._use_clock:
+            # device-clocked CFL frame (mpm_step_clock): the update advances the clock
+            gp.clock = self._clock.data_ptr()
+            gp.vmax_ring, gp.vmax_ring_len = self._status.data_ptr(), _RING
+            gp.frame_dt = float(self.params.frame_dt)
+            gp.cfl_dx = float(self.params.cfl * self.params.dx)
+            gp.c_sound = float(self.material.sound_speed())
+            gp.n_vmax_peers = 0
+            if step is not None:      # batches: mpm_enqueue_steps sets these per step
+                gp.clock_step = int(step)
+                gp.clock_status = self._status_ptr(int(step) % _RING)
+        else:
+            gp.clock = None
         return gp
 
     def _grid_update_launch(self, gp, tv, par, reset_ptr, stream):

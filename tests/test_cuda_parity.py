@@ -153,13 +153,18 @@ def test_worker_count_invariance():
         _assert_particles(s, states[0], edge, 9, run=True)
 
 
-@pytest.mark.parametrize("pipelined", [False, True])
-def test_cfl_schedule_against_reference_dump(pipelined):
+@pytest.mark.parametrize("mode", ["stepwise", "host_paced", "device_clock"])
+def test_cfl_schedule_against_reference_dump(mode):
+    """CFL-auto frames (pipeline.py:856-871): the reference's dt schedule of two frames.  stepwise =
+    the literal read-flag-then-step loop; host_paced = one guarded step ahead, dt computed by the host;
+    device_clock = dt computed by the grid update on the device (mpm_step_clock), steps enqueued in
+    batches, the frame ended by the device."""
     g = golden("cfl.npz")
     material, params, boundary = fluid_setup(frame_dt=float(g["frame_dt"]), cfl=0.5)
     wc = U.cuda_worker(g["pos"], g["vel"], float(g["mass"]), material, params, boundary)
     wc.cfl_mode = True
-    wc.pipelined = pipelined
+    wc.pipelined = mode != "stepwise"
+    wc.device_clock = mode == "device_clock"
     dts = []
     wc.run_frame()
     dts += wc.frame_dts
@@ -169,6 +174,43 @@ def test_cfl_schedule_against_reference_dump(pipelined):
     assert np.allclose(np.array(dts), g["dts"], rtol=1e-5, atol=0)
     edge = float(g["pos"].max() - g["pos"].min())
     _assert_particles(U.state_by_id(wc), g["state"], edge, 1, run=True)
+
+
+@pytest.mark.parametrize("transfer", ["split", "g2p2g"])
+def test_device_clock_frames_against_the_oracle(transfer):
+    """Device-paced CFL-auto frames on the elastic block (rebuilds inside the frames, fused and split
+    transfers): same number of steps per frame, same dt schedule (1e-5), same rebuild steps and the
+    short-run particle bars against the oracle's host loop; a second worker with the host computing
+    every dt agrees step for step."""
+    g, wc, wo, edge, ndef = _pair("elastic.npz", elastic_setup(), transfer=transfer)
+    _, wh, _, _, _ = _pair("elastic.npz", elastic_setup(), transfer=transfer)
+    wc.cfl_mode = wo.cfl_mode = wh.cfl_mode = True
+    wh.device_clock = False
+    dts_o = []
+    orig = wo.run_step
+
+    def spy(step):
+        dts_o.append(wo.dt)
+        orig(step)
+    wo.run_step = spy
+    dts_c, dts_h, per_frame = [], [], []
+    for _ in range(3):
+        wc.run_frame()
+        wh.run_frame()
+        wo.run_frame()
+        dts_c += wc.frame_dts
+        dts_h += wh.frame_dts
+        per_frame.append(wc.frame_steps)
+    assert len(dts_c) == len(dts_o) == len(dts_h) and len(dts_c) >= 3 * 20
+    assert np.allclose(dts_c, dts_o, rtol=1e-5, atol=0) and np.allclose(dts_h, dts_o, rtol=1e-5, atol=0)
+    for k in range(3):     # every frame adds up to frame_dt
+        lo = sum(per_frame[:k])
+        assert sum(dts_c[lo:lo + per_frame[k]]) == pytest.approx(wc.params.frame_dt, rel=1e-9)
+    assert wc.rebuild_steps == wo.rebuild_steps == wh.rebuild_steps and len(wc.rebuild_steps) >= 3
+    assert wc._global_step == wo._global_step
+    if wc._pending_gather:
+        wc._flush_gather()
+    _assert_particles(U.state_by_id(wc), U.state_by_id(wo), edge, ndef, run=True)
 
 
 def test_aggregate_drift_over_a_frame():
@@ -472,3 +514,46 @@ def test_sparse_world_one_particle_per_block_grows_the_hash_table():
     edge = float(pos.max() - pos.min())
     ex, ev, ef, _ = U.particle_errors(U.state_by_id(wc), U.state_by_id(wo), edge, 9)
     assert ex <= U.X_RTOL and ev <= U.V_RTOL and ef <= U.F_ATOL, (ex, ev, ef)
+
+
+# ---- particle sink (not in the reference: oracle = same rule in float64) --------
+@pytest.mark.parametrize("transfer", ["split", "g2p2g"])
+def test_particle_sink_against_the_oracle(transfer):
+    """A block falls through a sink slab.  Same particles leave (a particle within fp32 resolution of
+    the sink face may leave one step apart), the survivors keep their ids and agree with the oracle
+    at the short-run bars, mass is conserved over survivors, and the rebuild that follows a frame
+    with removals compacts the emptied lanes away."""
+    g, wc, wo, edge, ndef = _pair("elastic.npz", elastic_setup(), transfer=transfer)
+    n = len(g["pos"])
+    z_face = float(np.quantile(g["pos"][:, 2], 0.05)) - 0.55
+    lo, hi = (-1e3, -1e3, -1e3), (1e3, 1e3, z_face)
+    wc.set_sink(lo, hi)
+    wo.set_sink(lo, hi)
+    removed = []
+    for _ in range(2):
+        wc.run_frame()
+        wo.run_frame()
+        removed.append((wc.removed_count, wo.removed_count))
+    print("sink", transfer, "removed (cuda, oracle) per frame:", removed, "of", n)
+    assert 0.1 * n < removed[-1][1] < 0.9 * n                # the scene exercises the sink
+    assert abs(removed[-1][0] - removed[-1][1]) <= 2
+    fc, ic = wc.store.state_with_ids()
+    fo, io = wo.store.state_with_ids()
+    assert (ic >= 0).all() and len(np.unique(ic)) == len(ic)
+    common = np.intersect1d(ic, io)
+    assert len(common) >= max(len(ic), len(io)) - 2
+    # the few particles only one side still holds sit on the sink face
+    for ids, flat in ((ic, fc), (io, fo)):
+        extra = ~np.isin(ids, common)
+        assert (np.abs(flat[extra, 2] - z_face) < 1e-3).all()
+    sc = fc[np.argsort(ic)][np.isin(np.sort(ic), common)]
+    so = fo[np.argsort(io)][np.isin(np.sort(io), common)]
+    _assert_particles(sc, so, edge, ndef, run=True)
+    assert wc.store.total_mass() == pytest.approx(len(ic) * float(g["mass"]), rel=1e-6)
+    assert wc.rebuild_steps == wo.rebuild_steps
+    # the next step rebuilds (a frame with removals asks for it) and the store shrinks
+    assert wc.flags.rebuild_needed and wo.rebuild_needed
+    wc.run_frame()
+    wo.run_frame()
+    assert wc.store.count <= n - removed[-1][0] and wc.store.count == len(wc.store.state_with_ids()[1]) + \
+        (wc.removed_count - removed[-1][0])

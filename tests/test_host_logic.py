@@ -37,15 +37,19 @@ def test_library_exports_every_declared_symbol():
 
 def test_ctypes_structs_match_the_header(tmp_path):
     src = tmp_path / "sizes.c"
-    src.write_text('#include <stdio.h>\n#include "mpm_b200.h"\nint main(void){printf("%zu %zu %zu %zu %zu %zu\\n",'
+    src.write_text('#include <stdio.h>\n#include "mpm_b200.h"\nint main(void){printf("%zu %zu %zu %zu %zu %zu %zu %zu %zu %zu\\n",'
                    'sizeof(mpm_transfer_params),sizeof(mpm_store_view),sizeof(mpm_table_view),'
-                   'sizeof(mpm_step_status),sizeof(mpm_grid_params),sizeof(mpm_guard));return 0;}\n')
+                   'sizeof(mpm_step_status),sizeof(mpm_grid_params),sizeof(mpm_guard),'
+                   'sizeof(mpm_step_plan),sizeof(mpm_rebuild_plan),sizeof(mpm_rebuild_result),'
+                   'sizeof(mpm_step_clock));return 0;}\n')
     exe = tmp_path / "sizes"
     subprocess.check_call(["gcc", "-I", os.path.join(ROOT, "include"), "-o", str(exe), str(src)])
     sizes = [int(x) for x in subprocess.check_output([str(exe)]).split()]
     assert sizes == [ctypes.sizeof(_capi.TransferParams), ctypes.sizeof(_capi.StoreView),
                      ctypes.sizeof(_capi.TableView), ctypes.sizeof(_capi.StepStatus),
-                     ctypes.sizeof(_capi.GridParams), ctypes.sizeof(_capi.Guard)]
+                     ctypes.sizeof(_capi.GridParams), ctypes.sizeof(_capi.Guard),
+                     ctypes.sizeof(_capi.StepPlan), ctypes.sizeof(_capi.RebuildPlan),
+                     ctypes.sizeof(_capi.RebuildResult), ctypes.sizeof(_capi.StepClock)]
 
 
 def test_no_cpu_fallback_without_a_device():
