@@ -417,6 +417,12 @@ typedef struct mpm_grid_params {
     double frame_dt, cfl_dx, c_sound;
     int32_t n_vmax_peers, reserved4;
     const mpm_step_status *vmax_peer_rings[MPM_MAX_PEERS];
+    /* Optional instrumentation of the multi-GPU step (NULL = off): eight device words, of which
+     * four counters accumulate over launches ([4] is scratch): [0] launches, [1] ns CTA 0 spent in the device-side step barrier
+     * (%globaltimer: the latency of the slowest peer's signal as this rank sees it), [2] bytes of
+     * peer rows read (NVLink traffic on a multi-GPU node: 1 KB per shared touched block and peer),
+     * [3] CTAs that had to wait (they own a block shared with a peer). */
+    unsigned long long *prof;
 } mpm_grid_params;
 int mpm_grid_update(float *raw, uint8_t *touched, float *vel, float *vel_old,
                     const mpm_table_view *table, const mpm_grid_params *params,

@@ -67,6 +67,7 @@ class GridParams(C.Structure):
         ("clock", p_void), ("clock_step", i32), ("vmax_ring_len", i32), ("vmax_ring", p_void),
         ("clock_status", p_void), ("frame_dt", f64), ("cfl_dx", f64), ("c_sound", f64),
         ("n_vmax_peers", i32), ("reserved4", i32), ("vmax_peer_rings", p_void * MPM_MAX_PEERS),
+        ("prof", p_void),
     ]
 
 

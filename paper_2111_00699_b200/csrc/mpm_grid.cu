@@ -73,6 +73,7 @@ struct GridArgs {
     mpm_step_status *clock_status;
     double frame_dt, cfl_dx, c_sound;
     const mpm_step_status *vmax_peer_rings[MPM_MAX_PEERS];
+    unsigned long long *prof;      // optional counters: launches, barrier wait ns, peer bytes, waiting CTAs
 };
 
 // Worker.run_frame's CFL loop (pipeline.py:856-871) for ONE step, on the device: account for step
@@ -164,6 +165,7 @@ __global__ void __launch_bounds__(256) grid_update_kernel(const GridArgs a)
         }
         __syncthreads();
         if (s_wait) {
+            if (a.prof && threadIdx.x == 0) atomicAdd(&a.prof[3], 1ull);
             if (threadIdx.x < a.n_wait) {
                 const int *flag = a.wait_flags[threadIdx.x];
                 const unsigned long long t0 = global_timer_ns();
@@ -183,8 +185,14 @@ __global__ void __launch_bounds__(256) grid_update_kernel(const GridArgs a)
                     }
                     __nanosleep(200);
                 }
+                if (a.prof && blockIdx.x == 0) atomicMax(&a.prof[4], global_timer_ns() - t0);
             }
             __syncthreads();
+            if (a.prof && blockIdx.x == 0 && threadIdx.x == 0) {
+                // CTA 0 waits for every peer: its longest wait is the barrier latency of this launch
+                atomicAdd(&a.prof[0], 1ull);
+                atomicAdd(&a.prof[1], atomicExch(&a.prof[4], 0ull));
+            }
             if (s_void) {
                 if (a.publish_guard_dst && blockIdx.x == 0 && threadIdx.x == 31)
                     publish_status(nullptr, nullptr, a.publish_guard_src, a.publish_guard_dst, 31);
@@ -247,6 +255,7 @@ __global__ void __launch_bounds__(256) grid_update_kernel(const GridArgs a)
             if (q < 0 || (a.peers.touched[p] && __ldcv(&a.peers.touched[p][q]) != 1)) continue;
             const float4 o = __ldcg(&a.peers.raw[p][(size_t)q * 64 + slot]);
             node.x += o.x; node.y += o.y; node.z += o.z; node.w += o.w;
+            if (a.prof && slot == 0) atomicAdd(&a.prof[2], 1024ull);
         }
         if (a.fuse_clear) {
             a.raw_mut[idx] = make_float4(0.f, 0.f, 0.f, 0.f);
@@ -499,6 +508,7 @@ int mpm_grid_update(float *raw, uint8_t *touched, float *vel, float *vel_old,
     a.vmax_ring_len = p->vmax_ring_len;
     a.clock_status = p->clock_status;
     a.frame_dt = p->frame_dt; a.cfl_dx = p->cfl_dx; a.c_sound = p->c_sound;
+    a.prof = p->prof;
     a.n_vmax_peers = p->clock ? p->n_vmax_peers : 0;
     if (p->clock && (!p->vmax_ring || p->vmax_ring_len < 3 || !(p->frame_dt > 0.0) ||
                      a.n_vmax_peers < 0 || a.n_vmax_peers > MPM_MAX_PEERS))

@@ -177,8 +177,25 @@ class PeerDistWorker(DistWorker):
         self.collective_steps = 0
         self.device_paced_steps = 0
         self.batched_steps = 0
+        self._prof = None
         self._need_collective = True   # first step ever; after that only when some rank asks for it
         self.batch_steps = 4          # steps per mpm_enqueue_steps call (0 = one guarded step per call)
+
+    # -- instrumentation of the device-side barrier / halo reads (off by default) -------------
+    def enable_profile(self, on=True):
+        """Counters kept by the grid update (mpm_grid_params.prof): barrier wait seen by CTA 0 and
+        bytes of peer rows read.  `profile` reports them per launch."""
+        with torch.cuda.device(self.device):
+            self._prof = torch.zeros(8, dtype=torch.int64, device=self.device) if on else None
+
+    @property
+    def profile(self):
+        if self._prof is None:
+            return None
+        p = self._prof.cpu().numpy()
+        n = max(int(p[0]), 1)
+        return {"grid_updates": int(p[0]), "barrier_wait_us_per_step": float(p[1]) / n / 1e3,
+                "halo_bytes_per_step": float(p[2]) / n, "waiting_ctas_per_step": float(p[3]) / n}
 
     # -- exported memory -------------------------------------------------------------------
     def _exports(self):
@@ -275,6 +292,7 @@ class PeerDistWorker(DistWorker):
         gp.wait_error = self._mailbox.data_ptr() + 4 * MB_WAIT_ERR
         gp.block_filter = 0
         gp.fuse_clear = 0
+        gp.prof = self._prof.data_ptr() if self._prof is not None else None
 
     def _reduce_and_update(self, par, step=None):
         if step is None:

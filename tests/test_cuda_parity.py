@@ -202,7 +202,14 @@ def test_device_clock_frames_against_the_oracle(transfer):
         dts_h += wh.frame_dts
         per_frame.append(wc.frame_steps)
     assert len(dts_c) == len(dts_o) == len(dts_h) and len(dts_c) >= 3 * 20
-    assert np.allclose(dts_c, dts_o, rtol=1e-5, atol=0) and np.allclose(dts_h, dts_o, rtol=1e-5, atol=0)
+    # relative to the typical step: the last step of a frame is the REMAINDER frame_dt - t, a small
+    # difference of sums, so its own size is no scale for its error
+    scale = float(np.median(dts_o))
+    rel_c = np.abs(np.array(dts_c) - np.array(dts_o)) / scale
+    rel_h = np.abs(np.array(dts_h) - np.array(dts_o)) / scale
+    print("dt schedule", transfer, "steps per frame", per_frame, "worst rel diff device %.2e at %d, host %.2e at %d"
+          % (rel_c.max(), rel_c.argmax(), rel_h.max(), rel_h.argmax()), "rebuilds", wc.rebuild_steps)
+    assert rel_c.max() <= 1e-5 and rel_h.max() <= 1e-5
     for k in range(3):     # every frame adds up to frame_dt
         lo = sum(per_frame[:k])
         assert sum(dts_c[lo:lo + per_frame[k]]) == pytest.approx(wc.params.frame_dt, rel=1e-9)
@@ -523,9 +530,18 @@ def test_particle_sink_against_the_oracle(transfer):
     the sink face may leave one step apart), the survivors keep their ids and agree with the oracle
     at the short-run bars, mass is conserved over survivors, and the rebuild that follows a frame
     with removals compacts the emptied lanes away."""
-    g, wc, wo, edge, ndef = _pair("elastic.npz", elastic_setup(), transfer=transfer)
-    n = len(g["pos"])
-    z_face = float(np.quantile(g["pos"][:, 2], 0.05)) - 0.55
+    material, params, boundary = elastic_setup()
+    dx = params.dx
+    pos, vel = U.block_scene(6, 11, dx, origin_cells=(10, 10, 30))     # high above the floor: free fall
+    mass = 2.0 * dx ** 3 / 8
+    g = {"pos": pos, "mass": mass}
+    wc = U.cuda_worker(pos, vel, mass, material, params, boundary, transfer=transfer)
+    wo = U.oracle_worker(pos, vel, mass, material, params, boundary, transfer=transfer)
+    edge, ndef = float(pos.max() - pos.min()), 9
+    n = len(pos)
+    # two frames of fall (150 cm/s + gravity) take the lower half of the block through the face
+    T = 2 * params.frame_dt
+    z_face = float(np.median(pos[:, 2])) - (150.0 * T + 0.5 * 981.0 * T * T)
     lo, hi = (-1e3, -1e3, -1e3), (1e3, 1e3, z_face)
     wc.set_sink(lo, hi)
     wo.set_sink(lo, hi)
