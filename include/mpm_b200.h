@@ -113,9 +113,10 @@ typedef struct mpm_transfer_params {
     int32_t clock_step, clock_gather_step;
     /* Particle sink (not in the reference): a particle whose advected position lies
      * in the box [sink_lo, sink_hi) is taken out of the simulation by the gather that moved it there:
-     * mass 0, lane flagged MPM_LANE_QUARANTINED | MPM_LANE_SUNK, orig_id -1, status->removed + 1.
-     * Like a quarantined lane it stops scattering at once and is dropped by the next rebuild's
-     * compaction (particles.py:177-188). */
+     * position stored, mass 0, lane flagged MPM_LANE_QUARANTINED | MPM_LANE_SUNK, orig_id -1,
+     * status->removed + 1; no deformation update, free-zone test or max-speed contribution.  Like a
+     * quarantined lane it stops scattering at once and is dropped by the next rebuild's compaction
+     * (particles.py:177-188). */
     int32_t sink_enabled, reserved5;
     double sink_lo[3], sink_hi[3];
 } mpm_transfer_params;

@@ -439,7 +439,7 @@ typedef struct {
     /* plastic kinds only (not in the reference) */
     double theta_c, theta_s, hardening, sand_alpha;
     /* particle sink (not in the reference): lanes whose advected position lies in [sink_lo, sink_hi)
-     * complete their gather and are then removed -- mass 0, quarantined = 2, out_stats[2] += 1 */
+     * are removed by the gather that moved them there -- mass 0, quarantined = 2, out_stats[2] += 1 */
     i64 sink_enabled;
     double sink_lo[3], sink_hi[3];
 } OrcTransferParams;
@@ -776,6 +776,17 @@ void orc_gather_advect(double *data, i64 *lane_key, u8 *quarantined, const i32 *
                 counters[C_QUARANTINE] += 1;
                 continue;
             }
+            if (P->sink_enabled && npx >= P->sink_lo[0] && npx < P->sink_hi[0] && npy >= P->sink_lo[1] &&
+                npy < P->sink_hi[1] && npz >= P->sink_lo[2] && npz < P->sink_hi[2]) {
+                /* the particle arrives in the sink box and leaves the simulation: skipped from here
+                 * on like a quarantined lane, dropped at the next rebuild */
+                quarantined[g * LW + l] = 2;
+                dg[(CH_POS + 0) * LW + l] = npx; dg[(CH_POS + 1) * LW + l] = npy;
+                dg[(CH_POS + 2) * LW + l] = npz;
+                dg[CH_MASS * LW + l] = 0.0;
+                out_stats[2] += 1.0;
+                continue;
+            }
             dg[(CH_POS + 0) * LW + l] = npx; dg[(CH_POS + 1) * LW + l] = npy;
             dg[(CH_POS + 2) * LW + l] = npz;
             dg[(CH_VEL + 0) * LW + l] = nvx; dg[(CH_VEL + 1) * LW + l] = nvy;
@@ -811,12 +822,6 @@ void orc_gather_advect(double *data, i64 *lane_key, u8 *quarantined, const i32 *
             i64 ky = clamp09((i64)floor(npy * inv_dx - 0.5) + bias - (oy - 4));
             i64 kz = clamp09((i64)floor(npz * inv_dx - 0.5) + bias - (oz - 4));
             lane_key[g * LW + l] = kx + 10 * (ky + 10 * kz);
-            if (P->sink_enabled && npx >= P->sink_lo[0] && npx < P->sink_hi[0] && npy >= P->sink_lo[1] &&
-                npy < P->sink_hi[1] && npz >= P->sink_lo[2] && npz < P->sink_hi[2]) {
-                quarantined[g * LW + l] = 2;
-                dg[CH_MASS * LW + l] = 0.0;
-                out_stats[2] += 1.0;
-            }
         }
     }
 }

@@ -439,12 +439,7 @@ __global__ void __launch_bounds__(TW * 32, MPM_MINBLOCKS) transfer_kernel(const 
     float tau[9]; // plastic kinds: stress of the projected state, produced by the gather
     float plastic = 0.f;
     const PlasticParams pp = {a.mu, a.lam, a.theta_c, a.theta_s, a.hardening, a.sand_alpha};
-    float dt_gather = a.dt_gather, coeff_base = a.coeff_base;
-    if (a.clock) {
-        // adaptive step size kept on the device (mpm_step_clock): two warp-uniform loads
-        if (GATHER) dt_gather = (float)__ldcg(&a.clock->dt[a.clock_gather_step & 1]);
-        if (SCATTER) coeff_base = a.coeff_per_dt * (float)__ldcg(&a.clock->dt[a.clock_step & 1]);
-    }
+
     int addr_err = 0;
     unsigned vmax_bits = 0;
     // the deformation state is loaded after the 27-node gather (MPM_LATE_F): nine registers less
@@ -482,7 +477,9 @@ __global__ void __launch_bounds__(TW * 32, MPM_MINBLOCKS) transfer_kernel(const 
                     nvy = (1.0f - a.flip) * nvy + a.flip * (ovy + dv[1]);
                     nvz = (1.0f - a.flip) * nvz + a.flip * (ovz + dv[2]);
                 }
-                const float dtg = dt_gather;
+                // adaptive step size kept on the device (mpm_step_clock): a warp-uniform load, at the
+                // point of use (the kernel has no register to carry it across the node gather)
+                const float dtg = a.clock ? (float)__ldcg(&a.clock->dt[a.clock_gather_step & 1]) : a.dt_gather;
                 const float npx = px + dtg * nvx, npy = py + dtg * nvy, npz = pz + dtg * nvz;
                 if (!(isfinite(npx) && isfinite(npy) && isfinite(npz) && isfinite(nvx) &&
                       isfinite(nvy) && isfinite(nvz))) {
@@ -491,6 +488,17 @@ __global__ void __launch_bounds__(TW * 32, MPM_MINBLOCKS) transfer_kernel(const 
                     a.meta[g * 32 + lane] = meta;
                     gd[CH_MASS * 32] = 0.0f;
                     atomicAdd(&a.status->counters[MPM_C_QUARANTINE], 1ull);
+                    active = false;
+                } else if (a.sink_enabled && npx >= a.sink_lo[0] && npx < a.sink_hi[0] && npy >= a.sink_lo[1] &&
+                           npy < a.sink_hi[1] && npz >= a.sink_lo[2] && npz < a.sink_hi[2]) {
+                    // sink: the particle arrives in the sink box and leaves the simulation -- like a
+                    // quarantined lane it is skipped from here on (no deformation update, no free-zone
+                    // test, no scatter) and dropped by the next rebuild's compaction
+                    a.meta[g * 32 + lane] = (uint16_t)(meta | MPM_LANE_QUARANTINED | MPM_LANE_SUNK);
+                    gd[(CH_POS + 0) * 32] = npx; gd[(CH_POS + 1) * 32] = npy; gd[(CH_POS + 2) * 32] = npz;
+                    gd[CH_MASS * 32] = 0.0f;
+                    a.ids[g * 32 + lane] = -1;
+                    atomicAdd(&a.status->removed, 1ull);
                     active = false;
                 } else {
                     px = npx; py = npy; pz = npz; vx = nvx; vy = nvy; vz = nvz;
@@ -537,17 +545,6 @@ __global__ void __launch_bounds__(TW * 32, MPM_MINBLOCKS) transfer_kernel(const 
                             atomicOr(&a.status->zone_violation, MPM_STATUS_ZONE);
                         guard_raise(a.guard);
                     }
-                    if (a.sink_enabled && px >= a.sink_lo[0] && px < a.sink_hi[0] && py >= a.sink_lo[1] &&
-                        py < a.sink_hi[1] && pz >= a.sink_lo[2] && pz < a.sink_hi[2]) {
-                        // sink: the lane completes this gather like any other (state stored, free zone,
-                        // max speed) and is then out of the simulation -- no scatter below, dropped by
-                        // the next rebuild's compaction like a quarantined lane
-                        meta |= MPM_LANE_QUARANTINED | MPM_LANE_SUNK;
-                        gd[CH_MASS * 32] = 0.0f;
-                        a.ids[g * 32 + lane] = -1;
-                        atomicAdd(&a.status->removed, 1ull);
-                        active = false;
-                    }
                     vmax_bits = __float_as_uint(vx * vx + vy * vy + vz * vz);
                     float tmp;
                     int nkx = (int)stencil_base(px, a.inv_dx, &tmp) + MPM_CELL_BIAS - (org.x - 4);
@@ -555,7 +552,7 @@ __global__ void __launch_bounds__(TW * 32, MPM_MINBLOCKS) transfer_kernel(const 
                     int nkz = (int)stencil_base(pz, a.inv_dx, &tmp) + MPM_CELL_BIAS - (org.z - 4);
                     nkx = min(max(nkx, 0), 9); nky = min(max(nky, 0), 9); nkz = min(max(nkz, 0), 9);
                     key = nkx + 10 * (nky + 10 * nkz);
-                    a.meta[g * 32 + lane] = (uint16_t)(key | (meta & (MPM_LANE_QUARANTINED | MPM_LANE_SUNK)));
+                    a.meta[g * 32 + lane] = (uint16_t)key;
                 }
             }
         }
@@ -584,7 +581,8 @@ __global__ void __launch_bounds__(TW * 32, MPM_MINBLOCKS) transfer_kernel(const 
             }
         }
         if (active) {
-            const float coeff = coeff_base * m;
+            const float coeff = (a.clock ? a.coeff_per_dt * (float)__ldcg(&a.clock->dt[a.clock_step & 1])
+                                         : a.coeff_base) * m;
             if (MAT == MPM_MAT_FLUID) {
                 float tau;
                 if (F[0] <= 0.0f) {
