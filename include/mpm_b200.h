@@ -137,6 +137,9 @@ typedef struct mpm_store_view {
      * The transfer kernels read this one line instead of the dependent chain group_block ->
      * origin / neighbor row.  NULL = read the tables. */
     int32_t *group_ctx;
+    /* Optional: the group count lives on the device (a rebuild just produced it and the host has not
+     * read it yet).  n_groups above is then only the launch bound; kernels stop at *n_groups_dev. */
+    const int32_t *n_groups_dev;
 } mpm_store_view;
 
 /* Block table view: BlockTable (grid.py:325-386). */
@@ -147,6 +150,8 @@ typedef struct mpm_table_view {
     uint8_t *touched[2];     /* [count] per parity */
     int32_t count;
     int32_t n_gblocks;
+    /* Optional: pblock count on the device; `count` is then the launch bound (see n_groups_dev). */
+    const int32_t *count_dev;
 } mpm_table_view;
 
 /* Step status block written by the transfer kernels and the grid update (device memory, 72 bytes):
@@ -234,47 +239,56 @@ int mpm_hash_insert_blocks(const int64_t *codes, const int32_t *n_dev, int32_t n
 /* _dilate_and_link (grid.py:282-322) + the tail of BlockTable.rebuild (grid.py:362-386):
  * 27-neighbourhood of every gblock inserted in (gblock, dz, dy, dx) order, new blocks
  * numbered from n_gblocks in order of first appearance; fills codes, origin, neighbor.
+ * The block count is read from the device (*n_gblocks_dev <= gblocks_bound, the launch bound;
+ * flag_scratch holds 2 x 27 x gblocks_bound words): no host round trip between the phases.
  * *count (device) = pblock count; bad_block (device, preset INT32_MAX) = smallest gblock
  * index with a neighbour outside [0, 2^19). */
-int mpm_dilate_and_link(const int64_t *gcodes, int32_t n_gblocks, int64_t *hkeys, int32_t *hvals,
-                        int32_t *hfirst, int32_t hash_cap, int32_t *qslot, int32_t *flag_scratch,
-                        int32_t *scan_scratch, int64_t *codes, int32_t *origin, int32_t *neighbor,
-                        int32_t pblock_cap, int32_t *count, int32_t *bad_block, int32_t *overflow,
-                        void *stream);
+int mpm_dilate_and_link(const int64_t *gcodes, const int32_t *n_gblocks_dev, int32_t gblocks_bound,
+                        int64_t *hkeys, int32_t *hvals, int32_t *hfirst, int32_t hash_cap, int32_t *qslot,
+                        int32_t *flag_scratch, int32_t *scan_scratch, int64_t *codes, int32_t *origin,
+                        int32_t *neighbor, int32_t pblock_cap, int32_t *count, int32_t *bad_block,
+                        int32_t *overflow, void *stream);
 
 /* ParticleStore.histogram_sort part 1 (particles.py:360-399; _counting_sort_perm :66-80,
  * _build_groups :152-173): stable counting sort by key=(gidx<<6)|(code&63) and the lane
  * group structure.  perm[j] = input index of sorted position j.  bin_start has
- * n_gblocks*64+1 entries.  *n_groups (device) = group count.  Members of a (block, cell) bin rank
+ * gblocks_bound*64+1 entries, block_group_first gblocks_bound+1 (block count on the device).  *n_groups (device) = group count.  Members of a (block, cell) bin rank
  * themselves by input index; bins with more than 1024 members (particles piled into one cell)
  * are ranked from a bitmap over the input order instead, linear in the bin size:
  * large_scratch (n_upper words) and large_list (n_upper / 1024 + 2 words) are its scratch. */
 int mpm_sort_and_group(const int64_t *codes, const int32_t *gidx, const int32_t *n_dev, int32_t n_upper,
-                       int32_t n_gblocks, int32_t *bin_start, int32_t *tmp_perm, int32_t *perm,
-                       int32_t *block_group_first, int32_t *scan_scratch, int32_t *n_groups,
+                       const int32_t *n_gblocks_dev, int32_t gblocks_bound, int32_t *bin_start, int32_t *tmp_perm,
+                       int32_t *perm, int32_t *block_group_first, int32_t *scan_scratch, int32_t *n_groups,
                        int32_t *large_scratch, int32_t *large_list, void *stream);
 
 /* ParticleStore.histogram_sort part 2 (_scatter_sorted particles.py:192-199) fused with
  * set_group_origins + _recompute_lane_keys (particles.py:235-261, 453): permutes all
  * channels and ids from the old store / staged arrays into the new store, zero-fills
  * padding lanes, writes group_len/group_block/group_start and the 10-bit lane keys
- * (float64, MULTIPLICATION by 1/dx as in the reference). */
+ * (float64, MULTIPLICATION by 1/dx as in the reference).  new_store->n_groups is the launch
+ * bound, the group and block counts are read from the device. */
 int mpm_scatter_sorted(const mpm_store_view *old_store, const int32_t *src_slot, const int32_t *n_live_dev,
                        const float *staged, const int64_t *staged_ids, const int32_t *perm,
-                       const int32_t *bin_start, const int32_t *block_group_first, int32_t n_gblocks,
+                       const int32_t *bin_start, const int32_t *block_group_first, const int32_t *n_gblocks_dev,
                        const int32_t *table_origin, double dx, const mpm_store_view *new_store,
-                       void *stream);
+                       const int32_t *n_groups_dev, void *stream);
 
-/* Worker._rebuild (pipeline.py:958-1015) in one call: compact_live -> particle_codes ->
- * hash_insert_blocks -> [host sync: block count] -> dilate_and_link -> sort_and_group -> [host
- * sync: pblock and group counts] -> scatter_sorted -> build_group_ctx -> vel rows zeroed, raw
- * rows of this parity cleared.  Same kernels, same results as the separate calls; what it
- * removes is the interpreter between them (the device idles while the host prepares the next
- * call after each sync).  Every buffer is the caller's and is described with its capacity; when
- * a count outgrows one the call returns MPM_NEED_CAPACITY with the sizes it needs in the result
- * (the old store has not been touched) and the caller grows the buffers and calls again.
- * MPM_ERR_SPATIAL_DOMAIN: result.bad_particle / result.bad_block say which (particles.py:54-57,
- * grid.py:372-377). */
+/* Worker._rebuild (pipeline.py:958-1015) in one call, WITHOUT a host round trip inside it:
+ *   compact_live -> particle_codes -> hash_insert_blocks -> dilate_and_link -> sort_and_group ->
+ *   scatter_sorted -> build_group_ctx -> vel rows zeroed, raw rows of this parity cleared
+ *   [-> the rest of the rebuild step -> the first batch of steady steps].
+ * Every count the chain produces (blocks, pblocks, groups) stays on the device: launches are sized
+ * by the caller's capacities and the kernels read the counts where they lie (the paper's rebuild
+ * takes two CPU-GPU sync points for them; at 64 K particles those two waits and the
+ * interpreter around them cost more than the rebuild's kernels).  The scalars are copied to pinned
+ * host memory behind the sort and `done_event` is recorded there; mpm_rebuild_wait blocks on that
+ * event only -- the kernels enqueued behind it keep the device busy meanwhile -- and fills the
+ * result.  Every buffer is the caller's and is described with its capacity.  When a count outgrows
+ * one, the chain aborts ON THE DEVICE: the counts later kernels read are zeroed (they become
+ * no-ops), the guard of the steps enqueued behind the rebuild is lowered below guard_step, and
+ * mpm_rebuild_wait returns MPM_NEED_CAPACITY with the sizes needed (the old store has not been
+ * touched: grow and call again).  MPM_ERR_SPATIAL_DOMAIN: result.bad_particle / result.bad_block
+ * say which (particles.py:54-57, grid.py:372-377). */
 typedef struct mpm_rebuild_plan {
     mpm_store_view old_store;          /* current store (read only) */
     mpm_store_view new_store;          /* other half of the double buffer, room for cap_groups groups */
@@ -317,15 +331,38 @@ typedef struct mpm_rebuild_plan {
     struct mpm_step_status *grid_reset_status;
     float *vel_old;                    /* FLIP only */
     int32_t *guard_word;               /* optional: reset to INT32_MAX first (the guard of the speculative
-                                          launches that asked for this rebuild, see mpm_guard) */
+                                          launches that asked for this rebuild, see mpm_guard); it then
+                                          guards the rest of the step and the next batch at guard_step */
+    int32_t guard_step;                /* step of the rebuild (the tail runs as {guard_word, guard_step}) */
+    int32_t async;                     /* 1: return once everything is enqueued; the caller fetches the
+                                          result with mpm_rebuild_wait.  0: wait before returning */
+    int32_t *large_list;               /* scratch: n_upper / 1024 + 2 words (bins the bitmap ranking takes) */
+    void *done_event;                  /* cudaEvent_t recorded behind the copy of the scalars (async) */
+    /* split transfer: the gather of the rebuild step (pipeline.py:934-938) issued behind its grid
+     * update, its status block stored to status_publish_dst (device alias of pinned memory, or NULL =
+     * the caller copies) and status_event recorded.  g2p_params NULL = the caller runs it. */
+    const struct mpm_transfer_params *g2p_params;
+    struct mpm_step_status *g2p_status;
+    struct mpm_step_status *status_publish_dst;
+    void *status_event;
+    /* The first batch of steady steps (mpm_enqueue_steps) issued right behind the rebuild step, so
+     * that the device does not wait for the host's bookkeeping of the new tables.  The plan's store /
+     * table views are taken from this rebuild (counts on the device); next_steps NULL = none. */
+    const struct mpm_step_plan *next_steps;
+    int32_t next_first_step, next_n_steps;
 } mpm_rebuild_plan;
 typedef struct mpm_rebuild_result {
     int32_t n, n_gblocks, count, n_groups;
     int32_t bad_particle, bad_block;   /* INT32_MAX = none */
     int32_t need_hash, need_gblocks, need_table, need_groups, need_nodes;   /* 0 = fits */
     int32_t tail_done;                 /* 1: the P2G and the grid update of the step were issued */
+    int32_t g2p_done;                  /* 1: ... and the split gather + its status publication */
+    int32_t next_done;                 /* steps of next_steps that were enqueued */
 } mpm_rebuild_result;
 int mpm_rebuild(const mpm_rebuild_plan *plan, mpm_rebuild_result *result, void *stream);
+/* Blocks until the scalars of an async mpm_rebuild are on the host, then fills `result` and returns
+ * the rebuild's status (MPM_OK / MPM_NEED_CAPACITY / MPM_ERR_SPATIAL_DOMAIN). */
+int mpm_rebuild_wait(const mpm_rebuild_plan *plan, mpm_rebuild_result *result);
 
 /* ---- substep: Worker.run_step (pipeline.py:905-940) ---------------------------------
  *

@@ -42,14 +42,14 @@ class StoreView(C.Structure):
     _fields_ = [
         ("data", p_void), ("orig_id", p_void), ("lane_meta", p_void), ("group_len", p_void),
         ("group_block", p_void), ("group_start", p_void), ("n_groups", i32), ("nch", i32),
-        ("group_ctx", p_void),
+        ("group_ctx", p_void), ("n_groups_dev", p_void),
     ]
 
 
 class TableView(C.Structure):
     _fields_ = [
         ("codes", p_void), ("origin", p_void), ("neighbor", p_void), ("touched", p_void * 2),
-        ("count", i32), ("n_gblocks", i32),
+        ("count", i32), ("n_gblocks", i32), ("count_dev", p_void),
     ]
 
 
@@ -120,13 +120,16 @@ class RebuildPlan(C.Structure):
         ("node_bytes", i32), ("scalars_dev", p_void), ("scalars_host", p_void),
         ("p2g_params", p_void), ("p2g_status", p_void), ("grid_params", p_void),
         ("grid_reset_status", p_void), ("vel_old", p_void), ("guard_word", p_void),
+        ("guard_step", i32), ("async_", i32), ("large_list", p_void), ("done_event", p_void),
+        ("g2p_params", p_void), ("g2p_status", p_void), ("status_publish_dst", p_void),
+        ("status_event", p_void), ("next_steps", p_void), ("next_first_step", i32), ("next_n_steps", i32),
     ]
 
 
 class RebuildResult(C.Structure):
     _fields_ = [(k, i32) for k in ("n", "n_gblocks", "count", "n_groups", "bad_particle", "bad_block",
                                    "need_hash", "need_gblocks", "need_table", "need_groups",
-                                   "need_nodes", "tail_done")]
+                                   "need_nodes", "tail_done", "g2p_done", "next_done")]
 
 
 NEED_CAPACITY = 1
@@ -147,14 +150,15 @@ _SIGNATURES = {
                            p_void, p_void, p_void],
     "mpm_hash_insert_blocks": [p_void, p_void, i32, p_void, p_void, p_void, i32, p_void, p_void,
                                p_void, p_void, p_void, p_void, p_void, p_void],
-    "mpm_dilate_and_link": [p_void, i32, p_void, p_void, p_void, i32, p_void, p_void, p_void,
+    "mpm_dilate_and_link": [p_void, p_void, i32, p_void, p_void, p_void, i32, p_void, p_void, p_void,
                             p_void, p_void, p_void, i32, p_void, p_void, p_void, p_void],
-    "mpm_sort_and_group": [p_void, p_void, p_void, i32, i32, p_void, p_void, p_void, p_void,
+    "mpm_sort_and_group": [p_void, p_void, p_void, i32, p_void, i32, p_void, p_void, p_void, p_void,
                            p_void, p_void, p_void, p_void, p_void],
     "mpm_scatter_sorted": [C.POINTER(StoreView), p_void, p_void, p_void, p_void, p_void, p_void,
-                           p_void, i32, p_void, f64, C.POINTER(StoreView), p_void],
+                           p_void, p_void, p_void, f64, C.POINTER(StoreView), p_void, p_void],
     "mpm_build_group_ctx": [C.POINTER(StoreView), C.POINTER(TableView), p_void],
     "mpm_rebuild": [C.POINTER(RebuildPlan), C.POINTER(RebuildResult), p_void],
+    "mpm_rebuild_wait": [C.POINTER(RebuildPlan), C.POINTER(RebuildResult)],
     "mpm_clear": [p_void, p_void, i32, i32, i32, C.POINTER(Guard), p_void],
     "mpm_status_reset": [p_void, C.POINTER(Guard), p_void],
     "mpm_status_publish": [p_void, p_void, p_void, p_void, p_void],

@@ -163,8 +163,10 @@ inline void launch_chained(void (*kernel)(KArgs...), int grid, int block, cudaSt
 }
 
 // exclusive scan of int32 (three kernels, no library): out may alias in; total (device) optional
+// n_dev (optional): the length lives on the device, n = min(n, *n_dev * mul + add); grids are sized by n
 void exclusive_scan_i32(const int32_t *in, int32_t *out, int32_t n, int32_t *block_sums,
-                        int32_t *total, cudaStream_t stream);
+                        int32_t *total, cudaStream_t stream, const int32_t *n_dev = nullptr, int mul = 1,
+                        int add = 0);
 // scratch entries needed by exclusive_scan_i32 for n elements
 inline int32_t scan_scratch_len(int64_t n) { return (int32_t)((n + 1023) / 1024 + 1); }
 

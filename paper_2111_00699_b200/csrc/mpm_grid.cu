@@ -20,12 +20,14 @@ struct PeerSet {
     int n;
 };
 
-__global__ void __launch_bounds__(256) clear_kernel(float4 *raw, uint8_t *touched, int count, int full,
+__global__ void __launch_bounds__(256) clear_kernel(float4 *raw, uint8_t *touched, int count,
+                                                    const int *__restrict__ count_dev, int full,
                                                     int vec_per_node, const DevGuard guard)
 {
     pdl_wait();
     pdl_launch_dependents();
     if (guarded_out(guard)) return;
+    if (count_dev) count = min(count, *count_dev);
     const int b = blockIdx.x * 4 + (threadIdx.x >> 6);
     const int slot = threadIdx.x & 63;
     const bool hit = b < count && (full || touched[b]);
@@ -44,6 +46,7 @@ struct GridArgs {
     float4 *vel_old;
     const int4 *origin;
     int count;
+    const int *count_dev;      // optional: the count on the device (count is then the launch bound)
     PeerSet peers;
     float dt;
     float gx, gy, gz;
@@ -149,7 +152,7 @@ __global__ void __launch_bounds__(256) grid_update_kernel(const GridArgs a)
     }
     const int b = blockIdx.x * 4 + (threadIdx.x >> 6);
     const int slot = threadIdx.x & 63;
-    bool hit = b < a.count && a.touched[b];
+    bool hit = b < a.count && (!a.count_dev || b < __ldg(a.count_dev)) && a.touched[b];
     if (a.n_wait) {
         // Step barrier on the device: the peers' scatter of this step must be complete before
         // their rows are read.  Only CTAs that own a block shared with a peer wait (and CTA 0, so
@@ -432,10 +435,26 @@ int mpm_clear(float *raw, uint8_t *touched, int32_t count, int full, int32_t nod
 {
     if (count <= 0) return MPM_OK;
     if (node_bytes != 16 && node_bytes != 32) return MPM_ERR_REJECTED_INPUT;
-    launch_chained(clear_kernel, (count + 3) / 4, 256, (cudaStream_t)stream, (float4 *)raw, touched, count, full,
-                                                                    node_bytes / 16, make_guard(guard));
+    launch_chained(clear_kernel, (count + 3) / 4, 256, (cudaStream_t)stream, (float4 *)raw, touched, count,
+                   (const int *)nullptr, full, node_bytes / 16, make_guard(guard));
     return check_launch("mpm_clear", 1);
 }
+
+}  // extern "C"
+
+namespace mpm {
+// mpm_clear with the row count on the device (`bound` sizes the launch)
+int clear_rows_dev(float *raw, uint8_t *touched, int32_t bound, const int32_t *count_dev, int full,
+                   int32_t node_bytes, const mpm_guard *guard, cudaStream_t stream)
+{
+    if (bound <= 0) return MPM_OK;
+    launch_chained(clear_kernel, (bound + 3) / 4, 256, stream, (float4 *)raw, touched, bound, count_dev, full,
+                   node_bytes / 16, make_guard(guard));
+    return check_launch("mpm_clear", 1);
+}
+}  // namespace mpm
+
+extern "C" {
 
 int mpm_status_reset(mpm_step_status *status, const mpm_guard *guard, void *stream)
 {
@@ -468,6 +487,7 @@ int mpm_grid_update(float *raw, uint8_t *touched, float *vel, float *vel_old,
     a.vel_old = (float4 *)vel_old;
     a.origin = (const int4 *)table->origin;
     a.count = table->count;
+    a.count_dev = table->count_dev;
     a.peers.n = p->n_peers;
     for (int k = 0; k < p->n_peers; ++k) {
         a.peers.raw[k] = (const float4 *)p->peer_raw[k];

@@ -53,10 +53,25 @@ __device__ __forceinline__ int block_exclusive_scan(int v, int *total)
     return excl;
 }
 
-__global__ void __launch_bounds__(SCAN_THREADS) scan_reduce_kernel(const int *in, int n, int *block_sums)
+// Length of a scan whose size lives on the device: n = min(bound, *n_dev * mul + add) (n_dev NULL:
+// the bound itself).  Grids are sized from the bound, which the host knows; the rebuild never waits
+// for a count in the middle of its kernel chain.
+struct ScanLen {
+    const int *n_dev;
+    int mul, add, bound;
+};
+__device__ __forceinline__ int scan_len(const ScanLen &L)
+{
+    if (!L.n_dev) return L.bound;
+    const long long n = (long long)(*L.n_dev) * L.mul + L.add;
+    return (int)(n < (long long)L.bound ? (n < 0 ? 0 : n) : L.bound);
+}
+
+__global__ void __launch_bounds__(SCAN_THREADS) scan_reduce_kernel(const int *in, ScanLen L, int *block_sums)
 {
     pdl_wait();
     pdl_launch_dependents();
+    const int n = scan_len(L);
     const int base = blockIdx.x * SCAN_TILE + threadIdx.x * SCAN_ITEMS;
     int s = 0;
 #pragma unroll
@@ -91,11 +106,12 @@ __global__ void __launch_bounds__(1024) scan_blocksums_kernel(int *block_sums, i
     }
 }
 
-__global__ void __launch_bounds__(SCAN_THREADS) scan_apply_kernel(const int *in, int *out, int n,
+__global__ void __launch_bounds__(SCAN_THREADS) scan_apply_kernel(const int *in, int *out, ScanLen L,
                                                                   const int *block_sums)
 {
     pdl_wait();
     pdl_launch_dependents();
+    const int n = scan_len(L);
     const int base = blockIdx.x * SCAN_TILE + threadIdx.x * SCAN_ITEMS;
     int v[SCAN_ITEMS];
     int s = 0;
@@ -114,16 +130,17 @@ __global__ void __launch_bounds__(SCAN_THREADS) scan_apply_kernel(const int *in,
 }
 
 void exclusive_scan_i32(const int32_t *in, int32_t *out, int32_t n, int32_t *block_sums,
-                        int32_t *total, cudaStream_t stream)
+                        int32_t *total, cudaStream_t stream, const int32_t *n_dev, int mul, int add)
 {
     if (n <= 0) {
         if (total) cudaMemsetAsync(total, 0, sizeof(int32_t), stream);
         return;
     }
+    const ScanLen L = {n_dev, mul, add, n};
     const int nb = (n + SCAN_TILE - 1) / SCAN_TILE;
-    launch_chained(scan_reduce_kernel, nb, SCAN_THREADS, stream, in, n, block_sums);
+    launch_chained(scan_reduce_kernel, nb, SCAN_THREADS, stream, in, L, block_sums);
     launch_chained(scan_blocksums_kernel, 1, 1024, stream, block_sums, nb, total);
-    launch_chained(scan_apply_kernel, nb, SCAN_THREADS, stream, in, out, n, block_sums);
+    launch_chained(scan_apply_kernel, nb, SCAN_THREADS, stream, in, out, L, block_sums);
 }
 
 // ===================================================================================
@@ -274,12 +291,14 @@ __global__ void __launch_bounds__(256) block_insert_kernel(const long long *__re
 __global__ void __launch_bounds__(256) first_flag_kernel(const int *__restrict__ pslot,
                                                          const int *__restrict__ hfirst,
                                                          const int *__restrict__ hvals, int n_upper,
+                                                         const int *__restrict__ n_dev, int n_mul,
                                                          int only_unassigned, int *__restrict__ flag)
 {
     pdl_wait();
     pdl_launch_dependents();
     const int i = blockIdx.x * blockDim.x + threadIdx.x;
     if (i >= n_upper) return;
+    if (n_dev && i >= *n_dev * n_mul) { flag[i] = 0; return; }   // beyond the live entries: pslot is stale
     const int slot = pslot[i];
     int f = 0;
     if (slot >= 0 && hfirst[slot] == i && (!only_unassigned || hvals[slot] < 0)) f = 1;
@@ -320,7 +339,7 @@ __global__ void __launch_bounds__(256) gidx_kernel(const int *__restrict__ pslot
 // 27-dilation (grid.py:282-322)
 // ===================================================================================
 __global__ void __launch_bounds__(256) dilate_insert_kernel(const long long *__restrict__ gcodes,
-                                                            int n_g, long long *hkeys,
+                                                            const int *__restrict__ n_g_dev, long long *hkeys,
                                                             const int *__restrict__ hvals, int *hfirst,
                                                             int shift, int mask, int *__restrict__ qslot,
                                                             int *bad_block, int *overflow)
@@ -328,6 +347,7 @@ __global__ void __launch_bounds__(256) dilate_insert_kernel(const long long *__r
     pdl_wait();
     pdl_launch_dependents();
     const int q = blockIdx.x * blockDim.x + threadIdx.x;
+    const int n_g = *n_g_dev;
     if (q >= n_g * 27) return;
     const int g = q / 27, s = q - g * 27;
     const int dz = s / 9 - 1, dy = (s / 3) % 3 - 1, dxx = s % 3 - 1;
@@ -347,18 +367,22 @@ __global__ void __launch_bounds__(256) dilate_insert_kernel(const long long *__r
     if (hvals[slot] < 0) atomicMin(&hfirst[slot], q);   // gblock slots keep their index
 }
 
+// also copies the gblock codes to the head of the table (grid.py:362-371: gblocks occupy [0, n_g))
 __global__ void __launch_bounds__(256) dilate_assign_kernel(const int *__restrict__ qslot,
                                                             const int *__restrict__ flag,
-                                                            const int *__restrict__ rank, int n_q,
-                                                            int n_g, int pblock_cap,
+                                                            const int *__restrict__ rank,
+                                                            const int *__restrict__ n_g_dev, int pblock_cap,
                                                             const long long *__restrict__ hkeys,
+                                                            const long long *__restrict__ gcodes,
                                                             int *hvals, long long *__restrict__ codes,
                                                             int *overflow)
 {
     pdl_wait();
     pdl_launch_dependents();
     const int q = blockIdx.x * blockDim.x + threadIdx.x;
-    if (q >= n_q) return;
+    const int n_g = *n_g_dev;
+    if (q < n_g && q < pblock_cap) codes[q] = gcodes[q];
+    if (q >= n_g * 27) return;
     if (!flag[q]) return;
     const int slot = qslot[q];
     const int idx = n_g + rank[q];
@@ -368,24 +392,16 @@ __global__ void __launch_bounds__(256) dilate_assign_kernel(const int *__restric
 }
 
 __global__ void __launch_bounds__(256) dilate_link_kernel(const int *__restrict__ qslot,
-                                                          const int *__restrict__ hvals, int n_q,
+                                                          const int *__restrict__ hvals,
+                                                          const int *__restrict__ n_g_dev,
                                                           int *__restrict__ neighbor)
 {
     pdl_wait();
     pdl_launch_dependents();
     const int q = blockIdx.x * blockDim.x + threadIdx.x;
-    if (q >= n_q) return;
+    if (q >= *n_g_dev * 27) return;
     const int slot = qslot[q];
     neighbor[q] = slot >= 0 ? hvals[slot] : -1;
-}
-
-__global__ void __launch_bounds__(256) gblock_codes_kernel(const long long *__restrict__ gcodes,
-                                                           int n_g, long long *__restrict__ codes)
-{
-    pdl_wait();
-    pdl_launch_dependents();
-    const int g = blockIdx.x * blockDim.x + threadIdx.x;
-    if (g < n_g) codes[g] = gcodes[g];
 }
 
 __global__ void __launch_bounds__(256) block_origin_kernel(const long long *__restrict__ codes,
@@ -399,6 +415,77 @@ __global__ void __launch_bounds__(256) block_origin_kernel(const long long *__re
     const unsigned long long code = (unsigned long long)codes[b];
     origin[b] = make_int4(4 * (int)compact1by2(code), 4 * (int)compact1by2(code >> 1),
                           4 * (int)compact1by2(code >> 2), 0);
+}
+
+// Scalars of one rebuild (device words S[16], mpm_rebuild): 0 n_live, 1 n_total, 2 bad particle,
+// 3 n_gblocks, 4 hash overflow, 5 pblock count, 6 bad block, 7 n_groups, 8 abort mask,
+// 9..12 the counts an aborted rebuild needs room for (gblocks, table entries, groups, nodes).
+__global__ void rebuild_init_kernel(int *S, int *large_list, int *guard_word)
+{
+    pdl_wait();
+    pdl_launch_dependents();
+    const int i = threadIdx.x;
+    if (i < 16) S[i] = (i == 2 || i == 6) ? MPM_INT_MAX : 0;
+    if (i == 16 && large_list) large_list[0] = 0;
+    if (i == 17 && guard_word) *guard_word = MPM_INT_MAX;
+}
+
+// A count that outgrew the caller's buffers (or a particle / block outside the domain) aborts the
+// rebuild WITHOUT a host round trip: the counts the later kernels read are zeroed, so every one of
+// them -- and the rest of the rebuild step issued behind them -- is a no-op, and the guard of the
+// steps enqueued behind the rebuild is lowered below `guard_step`.  The host finds the abort mask
+// and the sizes needed when it reads the scalars (mpm_rebuild_wait), grows the buffers and calls again.
+__device__ __forceinline__ void rebuild_abort(int *S, int why, int *guard_word, int guard_step)
+{
+    S[8] |= why;
+    S[1] = 0; S[3] = 0; S[5] = 0; S[7] = 0;
+    if (guard_word) atomicMin(guard_word, guard_step - 1);
+}
+__global__ void rebuild_check_blocks_kernel(int *S, int gblocks_bound, int hash_cap, int table_cap,
+                                            int *guard_word, int guard_step)
+{
+    pdl_wait();
+    pdl_launch_dependents();
+    const int n_g = S[3];
+    int why = 0;
+    if (S[2] != MPM_INT_MAX) why |= 8;                                   // particle outside the domain
+    if (S[4] || 8ll * n_g > hash_cap) why |= 1;                          // hash table too small
+    if (n_g > gblocks_bound) { why |= 2; S[9] = n_g; }
+    if (27ll * n_g > table_cap) { why |= 2; S[10] = 27 * n_g; }          // worst case of the dilation
+    if (why) rebuild_abort(S, why, guard_word, guard_step);
+}
+__global__ void rebuild_check_groups_kernel(int *S, int groups_cap, int nodes_cap, int *guard_word, int guard_step)
+{
+    pdl_wait();
+    pdl_launch_dependents();
+    if (S[8]) return;
+    int why = 0;
+    if (S[6] != MPM_INT_MAX) why |= 16;                                  // block on the domain boundary
+    if (S[4] == 1) why |= 1;                                             // the halo did not fit the hash table
+    if (S[7] > groups_cap) { why |= 4; S[11] = S[7]; }
+    if (S[5] > nodes_cap) { why |= 4; S[12] = S[5]; }
+    if (why) {
+        const int count = S[5], n_groups = S[7], n_g = S[3], n = S[1];
+        rebuild_abort(S, why, guard_word, guard_step);
+        S[13] = n; S[14] = n_g; S[15] = count; (void)n_groups;
+    }
+}
+
+// zero the first *count rows (64 float4 nodes each) of a nodal buffer: the reset of vel at a rebuild
+__global__ void __launch_bounds__(256) zero_rows_kernel(float4 *rows, const int *__restrict__ count_dev, int bound)
+{
+    pdl_wait();
+    pdl_launch_dependents();
+    const int b = blockIdx.x * 4 + (threadIdx.x >> 6);
+    if (b >= bound || b >= *count_dev) return;
+    rows[(size_t)b * 64 + (threadIdx.x & 63)] = make_float4(0.f, 0.f, 0.f, 0.f);
+}
+
+__global__ void add_dev_kernel(int *dst, const int *a, const int *b)
+{
+    pdl_wait();
+    pdl_launch_dependents();
+    *dst = *a + *b;
 }
 
 __global__ void add_scalar_kernel(int *dst, const int *a, int b)
@@ -525,12 +612,15 @@ __global__ void __launch_bounds__(1024) large_bin_rank_kernel(const int *__restr
     }
 }
 
-__global__ void __launch_bounds__(256) block_groups_kernel(const int *__restrict__ bin_start, int n_g,
+__global__ void __launch_bounds__(256) block_groups_kernel(const int *__restrict__ bin_start,
+                                                           const int *__restrict__ n_g_dev,
                                                            int *__restrict__ ngroups)
 {
     pdl_wait();
     pdl_launch_dependents();
     const int b = blockIdx.x * blockDim.x + threadIdx.x;
+    const int n_g = *n_g_dev;
+    if (b == n_g) ngroups[b] = 0;      // n_g + 1 entries so that the scan leaves ngroups[n_g] = n_groups
     if (b >= n_g) return;
     const int c = bin_start[(b + 1) * 64] - bin_start[b * 64];
     ngroups[b] = (c + 31) >> 5;
@@ -551,16 +641,18 @@ __global__ void __launch_bounds__(256) scatter_sorted_kernel(
     const int *__restrict__ src_slot, const int *__restrict__ n_live_dev,
     const float *__restrict__ staged, const long long *__restrict__ staged_ids,
     const int *__restrict__ perm, const int *__restrict__ bin_start,
-    const int *__restrict__ block_group_first, int n_g, const int4 *__restrict__ table_origin,
+    const int *__restrict__ block_group_first, const int *__restrict__ n_g_dev,
+    const int4 *__restrict__ table_origin,
     double inv_dx, float *__restrict__ new_data, long long *__restrict__ new_ids,
     uint16_t *__restrict__ new_meta, int *__restrict__ group_len, int *__restrict__ group_block,
-    int *__restrict__ group_start, int n_groups)
+    int *__restrict__ group_start, const int *__restrict__ n_groups_dev, int n_groups_bound)
 {
     pdl_wait();
     pdl_launch_dependents();
     const int g = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
     const int lane = threadIdx.x & 31;
-    if (g >= n_groups) return;
+    if (g >= n_groups_bound || g >= *n_groups_dev) return;
+    const int n_g = *n_g_dev;
     // block of this group: last b with block_group_first[b] <= g
     int lo = 0, hi = n_g;   // invariant: bgf[lo] <= g < bgf[hi]
     while (hi - lo > 1) {
@@ -685,6 +777,7 @@ __global__ void fill_i32_kernel(int *p, int n, int v)
 // group's block as node indices, the block origin, the group length and the block index.
 __global__ void __launch_bounds__(256) group_ctx_kernel(const int *__restrict__ group_len,
                                                         const int *__restrict__ group_block, int n_groups,
+                                                        const int *__restrict__ n_groups_dev,
                                                         const int4 *__restrict__ origin,
                                                         const int *__restrict__ neighbor,
                                                         int *__restrict__ ctx)
@@ -693,7 +786,7 @@ __global__ void __launch_bounds__(256) group_ctx_kernel(const int *__restrict__ 
     pdl_launch_dependents();
     const int g = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
     const int lane = threadIdx.x & 31;
-    if (g >= n_groups) return;
+    if (g >= n_groups || (n_groups_dev && g >= *n_groups_dev)) return;
     const int b = group_block[g];
     int v;
     if (lane < 27) v = neighbor[b * 27 + lane] * 64;
@@ -774,13 +867,15 @@ int mpm_compact_live(const mpm_store_view *store, int drop_quarantined, int32_t 
     return check_launch("mpm_compact_live", 5);
 }
 
-int mpm_particle_codes(const mpm_store_view *store, const int32_t *src_slot, const int32_t *n_live_dev,
-                       const float *staged, int32_t n_staged, int32_t n_upper, double dx,
-                       int64_t *codes, int32_t *n_total, int32_t *bad_index, void *stream_)
+// `chained` = called from mpm_rebuild: the outputs (bad_index, overflow, bad_block, large_list[0])
+// were initialised by rebuild_init_kernel, so the per-call fills are skipped.
+static int particle_codes_impl(const mpm_store_view *store, const int32_t *src_slot, const int32_t *n_live_dev,
+                               const float *staged, int32_t n_staged, int32_t n_upper, double dx,
+                               int64_t *codes, int32_t *n_total, int32_t *bad_index, cudaStream_t stream,
+                               bool chained)
 {
-    cudaStream_t stream = (cudaStream_t)stream_;
     if (!(dx > 0.0)) return MPM_ERR_REJECTED_INPUT;
-    launch_chained(fill_i32_kernel, 1, 32, stream, bad_index, 1, MPM_INT_MAX);
+    if (!chained) launch_chained(fill_i32_kernel, 1, 32, stream, bad_index, 1, MPM_INT_MAX);
     if (n_live_dev) launch_chained(add_scalar_kernel, 1, 1, stream, n_total, n_live_dev, n_staged);
     else launch_chained(fill_i32_kernel, 1, 32, stream, n_total, 1, n_staged);
     if (n_upper > 0)
@@ -790,17 +885,24 @@ int mpm_particle_codes(const mpm_store_view *store, const int32_t *src_slot, con
     return check_launch("mpm_particle_codes", 3);
 }
 
-int mpm_hash_insert_blocks(const int64_t *codes, const int32_t *n_dev, int32_t n_upper,
-                           int64_t *hkeys, int32_t *hvals, int32_t *hfirst, int32_t hash_cap,
-                           int32_t *pslot, int32_t *flag_scratch, int32_t *scan_scratch,
-                           int32_t *gidx, int64_t *gcodes, int32_t *n_gblocks, int32_t *overflow,
-                           void *stream_)
+int mpm_particle_codes(const mpm_store_view *store, const int32_t *src_slot, const int32_t *n_live_dev,
+                       const float *staged, int32_t n_staged, int32_t n_upper, double dx,
+                       int64_t *codes, int32_t *n_total, int32_t *bad_index, void *stream_)
 {
-    cudaStream_t stream = (cudaStream_t)stream_;
+    return particle_codes_impl(store, src_slot, n_live_dev, staged, n_staged, n_upper, dx, codes, n_total,
+                               bad_index, (cudaStream_t)stream_, false);
+}
+
+static int hash_insert_blocks_impl(const int64_t *codes, const int32_t *n_dev, int32_t n_upper,
+                                   int64_t *hkeys, int32_t *hvals, int32_t *hfirst, int32_t hash_cap,
+                                   int32_t *pslot, int32_t *flag_scratch, int32_t *scan_scratch,
+                                   int32_t *gidx, int64_t *gcodes, int32_t *n_gblocks, int32_t *overflow,
+                                   cudaStream_t stream, bool chained)
+{
     if (hash_cap <= 0 || (hash_cap & (hash_cap - 1))) return MPM_ERR_REJECTED_INPUT;
     const int shift = hash_shift_for(hash_cap), mask = hash_cap - 1;
     launch_chained(hash_clear_kernel, nblk(hash_cap, 256), 256, stream, (long long *)hkeys, hvals, hfirst, hash_cap);
-    cudaMemsetAsync(overflow, 0, sizeof(int32_t), stream);
+    if (!chained) cudaMemsetAsync(overflow, 0, sizeof(int32_t), stream);
     if (n_upper <= 0) {
         cudaMemsetAsync(n_gblocks, 0, sizeof(int32_t), stream);
         return check_launch("mpm_hash_insert_blocks", 8);
@@ -808,7 +910,8 @@ int mpm_hash_insert_blocks(const int64_t *codes, const int32_t *n_dev, int32_t n
     const int nb = nblk(n_upper, 256);
     launch_chained(block_insert_kernel, nb, 256, stream, (const long long *)codes, n_dev, n_upper,
                                                 (long long *)hkeys, hfirst, shift, mask, pslot, overflow);
-    launch_chained(first_flag_kernel, nb, 256, stream, pslot, hfirst, hvals, n_upper, 0, flag_scratch);
+    launch_chained(first_flag_kernel, nb, 256, stream, pslot, hfirst, hvals, n_upper, (const int *)nullptr, 1, 0,
+                   flag_scratch);
     exclusive_scan_i32(flag_scratch, flag_scratch, n_upper, scan_scratch, n_gblocks, stream);
     launch_chained(block_assign_kernel, nb, 256, stream, (const long long *)codes, pslot, hfirst, flag_scratch,
                                                 n_upper, hvals, (long long *)gcodes);
@@ -816,63 +919,83 @@ int mpm_hash_insert_blocks(const int64_t *codes, const int32_t *n_dev, int32_t n
     return check_launch("mpm_hash_insert_blocks", 8);
 }
 
-int mpm_dilate_and_link(const int64_t *gcodes, int32_t n_g, int64_t *hkeys, int32_t *hvals,
-                        int32_t *hfirst, int32_t hash_cap, int32_t *qslot, int32_t *flag_scratch,
-                        int32_t *scan_scratch, int64_t *codes, int32_t *origin, int32_t *neighbor,
-                        int32_t pblock_cap, int32_t *count, int32_t *bad_block, int32_t *overflow,
-                        void *stream_)
+int mpm_hash_insert_blocks(const int64_t *codes, const int32_t *n_dev, int32_t n_upper,
+                           int64_t *hkeys, int32_t *hvals, int32_t *hfirst, int32_t hash_cap,
+                           int32_t *pslot, int32_t *flag_scratch, int32_t *scan_scratch,
+                           int32_t *gidx, int64_t *gcodes, int32_t *n_gblocks, int32_t *overflow,
+                           void *stream_)
 {
-    cudaStream_t stream = (cudaStream_t)stream_;
+    return hash_insert_blocks_impl(codes, n_dev, n_upper, hkeys, hvals, hfirst, hash_cap, pslot, flag_scratch,
+                                   scan_scratch, gidx, gcodes, n_gblocks, overflow, (cudaStream_t)stream_, false);
+}
+
+// n_g lives on the device (*n_gblocks_dev, at most gblocks_bound): the launches are sized by the bound,
+// so the host never waits for the block count in the middle of a rebuild.
+static int dilate_and_link_impl(const int64_t *gcodes, const int32_t *n_g_dev, int32_t gblocks_bound,
+                                int64_t *hkeys, int32_t *hvals, int32_t *hfirst, int32_t hash_cap,
+                                int32_t *qslot, int32_t *flag_scratch, int32_t *scan_scratch, int64_t *codes,
+                                int32_t *origin, int32_t *neighbor, int32_t pblock_cap, int32_t *count,
+                                int32_t *bad_block, int32_t *overflow, cudaStream_t stream, bool chained)
+{
     if (hash_cap <= 0 || (hash_cap & (hash_cap - 1))) return MPM_ERR_REJECTED_INPUT;
     const int shift = hash_shift_for(hash_cap), mask = hash_cap - 1;
-    launch_chained(fill_i32_kernel, 1, 32, stream, bad_block, 1, MPM_INT_MAX);
-    if (n_g <= 0) {
+    if (!chained) launch_chained(fill_i32_kernel, 1, 32, stream, bad_block, 1, MPM_INT_MAX);
+    if (gblocks_bound <= 0) {
         cudaMemsetAsync(count, 0, sizeof(int32_t), stream);
-        return check_launch("mpm_dilate_and_link", 11);
+        return check_launch("mpm_dilate_and_link", 9);
     }
-    if (n_g > pblock_cap) return MPM_ERR_RESOURCE;
-    const int n_q = n_g * 27;
+    const int n_q = gblocks_bound * 27;
     const int nb = nblk(n_q, 256);
     // hfirst of the halo slots must start at INT_MAX: gblock slots already hold particle indices,
     // but those are never compared again (their hvals >= 0).
-    launch_chained(dilate_insert_kernel, nb, 256, stream, (const long long *)gcodes, n_g, (long long *)hkeys,
+    launch_chained(dilate_insert_kernel, nb, 256, stream, (const long long *)gcodes, n_g_dev, (long long *)hkeys,
                                                  hvals, hfirst, shift, mask, qslot, bad_block, overflow);
-    launch_chained(first_flag_kernel, nb, 256, stream, qslot, hfirst, hvals, n_q, 1, flag_scratch);
+    launch_chained(first_flag_kernel, nb, 256, stream, qslot, hfirst, hvals, n_q, n_g_dev, 27, 1, flag_scratch);
     // keep the flags: the scan result goes to a second array (flag_scratch + n_q)
     int32_t *rank = flag_scratch + n_q;
-    exclusive_scan_i32(flag_scratch, rank, n_q, scan_scratch, count, stream);
-    launch_chained(gblock_codes_kernel, nblk(n_g, 256), 256, stream, (const long long *)gcodes, n_g,
-                                                            (long long *)codes);
-    launch_chained(dilate_assign_kernel, nb, 256, stream, qslot, flag_scratch, rank, n_q, n_g, pblock_cap,
-                                                 (const long long *)hkeys, hvals, (long long *)codes,
-                                                 overflow);
-    launch_chained(dilate_link_kernel, nb, 256, stream, qslot, hvals, n_q, neighbor);
-    launch_chained(add_scalar_kernel, 1, 1, stream, count, count, n_g);
+    exclusive_scan_i32(flag_scratch, rank, n_q, scan_scratch, count, stream, n_g_dev, 27, 0);
+    launch_chained(dilate_assign_kernel, nb, 256, stream, qslot, flag_scratch, rank, n_g_dev, pblock_cap,
+                                                 (const long long *)hkeys, (const long long *)gcodes, hvals,
+                                                 (long long *)codes, overflow);
+    launch_chained(dilate_link_kernel, nb, 256, stream, qslot, hvals, n_g_dev, neighbor);
+    launch_chained(add_dev_kernel, 1, 1, stream, count, (const int *)count, n_g_dev);
     launch_chained(block_origin_kernel, nblk(pblock_cap, 256), 256, stream, (const long long *)codes, count,
                                                                    pblock_cap, (int4 *)origin);
-    return check_launch("mpm_dilate_and_link", 11);
+    return check_launch("mpm_dilate_and_link", 9);
 }
 
-int mpm_sort_and_group(const int64_t *codes, const int32_t *gidx, const int32_t *n_dev, int32_t n_upper,
-                       int32_t n_g, int32_t *bin_start, int32_t *tmp_perm, int32_t *perm,
-                       int32_t *block_group_first, int32_t *scan_scratch, int32_t *n_groups,
-                       int32_t *large_scratch, int32_t *large_list, void *stream_)
+int mpm_dilate_and_link(const int64_t *gcodes, const int32_t *n_gblocks_dev, int32_t gblocks_bound,
+                        int64_t *hkeys, int32_t *hvals, int32_t *hfirst, int32_t hash_cap, int32_t *qslot,
+                        int32_t *flag_scratch, int32_t *scan_scratch, int64_t *codes, int32_t *origin,
+                        int32_t *neighbor, int32_t pblock_cap, int32_t *count, int32_t *bad_block,
+                        int32_t *overflow, void *stream_)
 {
-    cudaStream_t stream = (cudaStream_t)stream_;
-    if (n_g <= 0 || n_upper <= 0) {
+    if (!n_gblocks_dev) return MPM_ERR_REJECTED_INPUT;
+    return dilate_and_link_impl(gcodes, n_gblocks_dev, gblocks_bound, hkeys, hvals, hfirst, hash_cap, qslot,
+                                flag_scratch, scan_scratch, codes, origin, neighbor, pblock_cap, count, bad_block,
+                                overflow, (cudaStream_t)stream_, false);
+}
+
+static int sort_and_group_impl(const int64_t *codes, const int32_t *gidx, const int32_t *n_dev, int32_t n_upper,
+                               const int32_t *n_g_dev, int32_t gblocks_bound, int32_t *bin_start,
+                               int32_t *tmp_perm, int32_t *perm, int32_t *block_group_first,
+                               int32_t *scan_scratch, int32_t *n_groups, int32_t *large_scratch,
+                               int32_t *large_list, cudaStream_t stream, bool chained)
+{
+    if (gblocks_bound <= 0 || n_upper <= 0) {
         cudaMemsetAsync(n_groups, 0, sizeof(int32_t), stream);
-        return check_launch("mpm_sort_and_group", 14);
+        return check_launch("mpm_sort_and_group", 12);
     }
-    const int n_bins = n_g * 64;
+    if (!large_scratch || !large_list) return MPM_ERR_REJECTED_INPUT;
+    const int n_bins = gblocks_bound * 64;
     const int nb = nblk(n_upper, 256);
     // tickets live in `perm` until the final ranking overwrites it
     cudaMemsetAsync(bin_start, 0, sizeof(int32_t) * (size_t)(n_bins + 1), stream);
     launch_chained(hist_kernel, nb, 256, stream, (const long long *)codes, gidx, n_dev, n_upper, bin_start, perm);
-    exclusive_scan_i32(bin_start, bin_start, n_bins + 1, scan_scratch, nullptr, stream);
+    exclusive_scan_i32(bin_start, bin_start, n_bins + 1, scan_scratch, nullptr, stream, n_g_dev, 64, 1);
     launch_chained(place_kernel, nb, 256, stream, (const long long *)codes, gidx, n_dev, n_upper, bin_start,
                                          perm, tmp_perm);
-    if (!large_scratch || !large_list) return MPM_ERR_REJECTED_INPUT;
-    cudaMemsetAsync(large_list, 0, sizeof(int32_t), stream);
+    if (!chained) cudaMemsetAsync(large_list, 0, sizeof(int32_t), stream);
     launch_chained(stable_rank_kernel, nb, 256, stream, (const long long *)codes, gidx, n_dev, n_upper,
                                                bin_start, tmp_perm, perm, large_list);
     // bins above MPM_LARGE_BIN members (none in an ordinary scene: the kernel returns at once);
@@ -880,30 +1003,42 @@ int mpm_sort_and_group(const int64_t *codes, const int32_t *gidx, const int32_t 
     if (n_upper > MPM_LARGE_BIN)
         launch_chained(large_bin_rank_kernel, LARGE_BIN_CTAS, 1024, stream, bin_start, tmp_perm, perm, large_list,
                        (unsigned *)large_scratch, (n_upper + 31) / 32);
-    launch_chained(block_groups_kernel, nblk(n_g, 256), 256, stream, bin_start, n_g, block_group_first);
-    // n_g+1 entries so that block_group_first[n_g] = n_groups
-    cudaMemsetAsync(block_group_first + n_g, 0, sizeof(int32_t), stream);
-    exclusive_scan_i32(block_group_first, block_group_first, n_g + 1, scan_scratch, n_groups, stream);
-    return check_launch("mpm_sort_and_group", 14);
+    // n_g + 1 entries so that block_group_first[n_g] = n_groups after the scan
+    launch_chained(block_groups_kernel, nblk(gblocks_bound + 1, 256), 256, stream, bin_start, n_g_dev,
+                   block_group_first);
+    exclusive_scan_i32(block_group_first, block_group_first, gblocks_bound + 1, scan_scratch, n_groups, stream,
+                       n_g_dev, 1, 1);
+    return check_launch("mpm_sort_and_group", 12);
 }
 
-int mpm_scatter_sorted(const mpm_store_view *old_store, const int32_t *src_slot, const int32_t *n_live_dev,
-                       const float *staged, const int64_t *staged_ids, const int32_t *perm,
-                       const int32_t *bin_start, const int32_t *block_group_first, int32_t n_g,
-                       const int32_t *table_origin, double dx, const mpm_store_view *new_store,
-                       void *stream_)
+int mpm_sort_and_group(const int64_t *codes, const int32_t *gidx, const int32_t *n_dev, int32_t n_upper,
+                       const int32_t *n_gblocks_dev, int32_t gblocks_bound, int32_t *bin_start, int32_t *tmp_perm,
+                       int32_t *perm, int32_t *block_group_first, int32_t *scan_scratch, int32_t *n_groups,
+                       int32_t *large_scratch, int32_t *large_list, void *stream_)
 {
-    cudaStream_t stream = (cudaStream_t)stream_;
+    if (!n_gblocks_dev) return MPM_ERR_REJECTED_INPUT;
+    return sort_and_group_impl(codes, gidx, n_dev, n_upper, n_gblocks_dev, gblocks_bound, bin_start, tmp_perm,
+                               perm, block_group_first, scan_scratch, n_groups, large_scratch, large_list,
+                               (cudaStream_t)stream_, false);
+}
+
+// n_groups / n_g from the device (new_store->n_groups is the launch bound when n_groups_dev is given)
+static int scatter_sorted_impl(const mpm_store_view *old_store, const int32_t *src_slot, const int32_t *n_live_dev,
+                               const float *staged, const int64_t *staged_ids, const int32_t *perm,
+                               const int32_t *bin_start, const int32_t *block_group_first, const int32_t *n_g_dev,
+                               const int32_t *table_origin, double dx, const mpm_store_view *new_store,
+                               const int32_t *n_groups_dev, cudaStream_t stream)
+{
     const int G = new_store->n_groups;
     if (G <= 0) return MPM_OK;
     const double inv_dx = 1.0 / dx;
 #define MPM_SCATTER_SORTED(NCH)                                                                              \
     launch_chained(scatter_sorted_kernel<NCH>, nblk((int64_t)G * 32, 256), 256, stream, old_store->data,    \
                    (const long long *)old_store->orig_id, src_slot, n_live_dev, staged,                     \
-                   (const long long *)staged_ids, perm, bin_start, block_group_first, n_g,                  \
+                   (const long long *)staged_ids, perm, bin_start, block_group_first, n_g_dev,              \
                    (const int4 *)table_origin, inv_dx, new_store->data, (long long *)new_store->orig_id,    \
                    new_store->lane_meta, new_store->group_len, new_store->group_block,                      \
-                   new_store->group_start, G)
+                   new_store->group_start, n_groups_dev, G)
     switch (new_store->nch) {
     case 17: MPM_SCATTER_SORTED(17); break;
     case 25: MPM_SCATTER_SORTED(25); break;
@@ -914,14 +1049,81 @@ int mpm_scatter_sorted(const mpm_store_view *old_store, const int32_t *src_slot,
     return check_launch("mpm_scatter_sorted", 1);
 }
 
+int mpm_scatter_sorted(const mpm_store_view *old_store, const int32_t *src_slot, const int32_t *n_live_dev,
+                       const float *staged, const int64_t *staged_ids, const int32_t *perm,
+                       const int32_t *bin_start, const int32_t *block_group_first, const int32_t *n_gblocks_dev,
+                       const int32_t *table_origin, double dx, const mpm_store_view *new_store,
+                       const int32_t *n_groups_dev, void *stream_)
+{
+    if (!n_gblocks_dev || !n_groups_dev) return MPM_ERR_REJECTED_INPUT;
+    return scatter_sorted_impl(old_store, src_slot, n_live_dev, staged, staged_ids, perm, bin_start,
+                               block_group_first, n_gblocks_dev, table_origin, dx, new_store, n_groups_dev,
+                               (cudaStream_t)stream_);
+}
+
+}  // extern "C"
+
+namespace mpm {
+void rebuild_init(int32_t *S, int32_t *large_list, int32_t *guard_word, cudaStream_t stream)
+{
+    launch_chained(rebuild_init_kernel, 1, 32, stream, S, large_list, guard_word);
+}
+void rebuild_check_blocks(int32_t *S, int gblocks_bound, int hash_cap, int table_cap, int32_t *guard_word,
+                          int guard_step, cudaStream_t stream)
+{
+    launch_chained(rebuild_check_blocks_kernel, 1, 1, stream, S, gblocks_bound, hash_cap, table_cap, guard_word,
+                   guard_step);
+}
+void rebuild_check_groups(int32_t *S, int groups_cap, int nodes_cap, int32_t *guard_word, int guard_step,
+                          cudaStream_t stream)
+{
+    launch_chained(rebuild_check_groups_kernel, 1, 1, stream, S, groups_cap, nodes_cap, guard_word, guard_step);
+}
+void zero_rows(float *rows, const int32_t *count_dev, int bound, cudaStream_t stream)
+{
+    if (bound > 0) launch_chained(zero_rows_kernel, (bound + 3) / 4, 256, stream, (float4 *)rows, count_dev, bound);
+}
+int rebuild_chain(const mpm_rebuild_plan *p, int32_t *S, int gblocks_bound, int groups_bound, cudaStream_t stream)
+{
+    const float *staged = p->n_staged ? p->staged : nullptr;
+    const int64_t *staged_ids = p->n_staged ? p->staged_ids : nullptr;
+    int rc = mpm_compact_live(&p->old_store, 1, p->glive, p->src_slot, S + 0, p->scan, stream);
+    if (rc != MPM_OK) return rc;
+    rc = particle_codes_impl(&p->old_store, p->src_slot, S + 0, staged, p->n_staged, p->n_upper, p->dx, p->codes,
+                             S + 1, S + 2, stream, true);
+    if (rc != MPM_OK) return rc;
+    rc = hash_insert_blocks_impl(p->codes, S + 1, p->n_upper, p->hkeys, p->hvals, p->hfirst, p->hash_cap,
+                                 p->pslot, p->flag, p->scan, p->gidx, p->gcodes, S + 3, S + 4, stream, true);
+    if (rc != MPM_OK) return rc;
+    rebuild_check_blocks(S, gblocks_bound, p->hash_cap, p->cap_table, p->guard_word, p->guard_step, stream);
+    rc = dilate_and_link_impl(p->gcodes, S + 3, gblocks_bound, p->hkeys, p->hvals, p->hfirst, p->hash_cap,
+                              p->qslot, p->qflag, p->scan, p->table_codes, p->table_origin, p->table_neighbor,
+                              p->cap_table, S + 5, S + 6, S + 4, stream, true);
+    if (rc != MPM_OK) return rc;
+    // pslot / flag are free by now: scratch of the large-bin ranking (flag[0] was zeroed by rebuild_init)
+    rc = sort_and_group_impl(p->codes, p->gidx, S + 1, p->n_upper, S + 3, gblocks_bound, p->bin_start,
+                             p->tmp_perm, p->perm, p->bgf, p->scan, S + 7, p->pslot, p->large_list, stream, true);
+    if (rc != MPM_OK) return rc;
+    rebuild_check_groups(S, p->cap_groups, p->cap_nodes, p->guard_word, p->guard_step, stream);
+    mpm_store_view ns = p->new_store;
+    ns.n_groups = groups_bound;
+    ns.n_groups_dev = S + 7;
+    rc = scatter_sorted_impl(&p->old_store, p->src_slot, S + 0, staged, staged_ids, p->perm, p->bin_start, p->bgf,
+                             S + 3, p->table_origin, p->dx, &ns, S + 7, stream);
+    return rc;
+}
+}  // namespace mpm
+
+extern "C" {
+
 int mpm_build_group_ctx(const mpm_store_view *store, const mpm_table_view *table, void *stream_)
 {
     if (!store || !table || !store->group_ctx) return MPM_ERR_REJECTED_INPUT;
     const int G = store->n_groups;
     if (G <= 0) return MPM_OK;
     launch_chained(group_ctx_kernel, nblk((int64_t)G * 32, 256), 256, (cudaStream_t)stream_, 
-        store->group_len, store->group_block, G, (const int4 *)table->origin, table->neighbor,
-        store->group_ctx);
+        store->group_len, store->group_block, G, store->n_groups_dev, (const int4 *)table->origin,
+        table->neighbor, store->group_ctx);
     return check_launch("mpm_build_group_ctx", 1);
 }
 

@@ -14,6 +14,11 @@
 // step of the batch is a no-op on the device and the host re-issues from there after rebuilding.
 #include "mpm_common.cuh"
 
+namespace mpm {
+int clear_rows_dev(float *raw, uint8_t *touched, int32_t bound, const int32_t *count_dev, int full,
+                   int32_t node_bytes, const mpm_guard *guard, cudaStream_t stream);
+}
+
 extern "C" int mpm_enqueue_steps(const mpm_step_plan *p, int32_t first_step, int32_t n_steps, void *stream_)
 {
     if (!p || n_steps < 0 || n_steps > MPM_MAX_STATUS_RING) return MPM_ERR_REJECTED_INPUT;
@@ -65,13 +70,13 @@ extern "C" int mpm_enqueue_steps(const mpm_step_plan *p, int32_t first_step, int
         if (k == 0 && p->full_clear_first) {
             // first use of the parity the last rebuild left untouched: every row, not only the
             // touched ones (pipeline.py:1022-1037)
-            rc = mpm_clear(p->raw[par], p->touched[par], p->table.count, 1, gp.deterministic ? 32 : 16, &guard,
-                           stream);
+            rc = mpm::clear_rows_dev(p->raw[par], p->touched[par], p->table.count, p->table.count_dev, 1,
+                                     gp.deterministic ? 32 : 16, &guard, stream);
             if (rc != MPM_OK) return rc;
         } else if (!gp.fuse_clear) {
             // Worker._clear (pipeline.py:1022-1037): rows of this parity touched two steps ago
-            rc = mpm_clear(p->raw[par], p->touched[par], p->table.count, 0, gp.deterministic ? 32 : 16, &guard,
-                           stream);
+            rc = mpm::clear_rows_dev(p->raw[par], p->touched[par], p->table.count, p->table.count_dev, 0,
+                                     gp.deterministic ? 32 : 16, &guard, stream);
             if (rc != MPM_OK) return rc;
         }
         if (p->fused) {

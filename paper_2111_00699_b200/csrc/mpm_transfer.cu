@@ -24,6 +24,7 @@ struct TransferArgs {
     const int *group_block;
     const int *group_ctx;
     int n_groups;
+    const int *n_groups_dev;   // optional: the count on the device (n_groups is then the launch bound)
     int nch;
     const int4 *origin;
     const int *neighbor;
@@ -389,6 +390,7 @@ __global__ void __launch_bounds__(TW * 32, MPM_MINBLOCKS) transfer_kernel(const 
     const int g = blockIdx.x * TW + warp;
     const unsigned FULL = 0xffffffffu;
     if (g >= a.n_groups) return;     // warps are independent: no CTA-wide barrier below
+    if (a.n_groups_dev && g >= __ldg(a.n_groups_dev)) return;
 
     // group context: neighbour row (as node indices of slot 0), block origin, group length.  One
     // 128-byte line per group written at the rebuild (mpm_build_group_ctx) -- every load of the
@@ -677,6 +679,7 @@ static int fill_args(TransferArgs &a, const mpm_store_view *store, const mpm_tab
     a.group_block = store->group_block;
     a.group_ctx = store->group_ctx;
     a.n_groups = store->n_groups;
+    a.n_groups_dev = store->n_groups_dev;
     a.nch = store->nch;
     a.origin = (const int4 *)table->origin;
     a.neighbor = table->neighbor;

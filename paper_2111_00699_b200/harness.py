@@ -230,7 +230,7 @@ def run(cfg: RunConfig, params_override: SimParams | None = None) -> RunResult:
     workers = cluster.workers
     for w in workers:
         w.cfl_mode = cfg.cfl_enabled
-        w.time_kernels = cfg.profile_phases
+        w.time_kernels = w.profile_all_phases = cfg.profile_phases
     cluster.seed(spec.positions, spec.velocities, spec.particle_mass)
     next_id = len(spec.positions)
 

@@ -555,6 +555,8 @@ class CudaWorker:
             self._guard_word = torch.full((1,), _INT_MAX, dtype=torch.int32, device=self.device)
             self._scalars = torch.zeros(16, dtype=torch.int32, device=self.device)
             self._scalars_host = torch.zeros(16, dtype=torch.int32).pin_memory()
+            self._rebuild_event = torch.cuda.Event()
+            self._rebuild_event.record()
             # step clock of CFL-auto frames (mpm_step_clock: dt[2], t, reserved), device-resident
             self._clock = torch.zeros(4, dtype=torch.float64, device=self.device)
             self._clock_host = torch.zeros(4, dtype=torch.float64).pin_memory()
@@ -603,8 +605,13 @@ class CudaWorker:
         self._scratch_allocs = 0
         self.kernel_calls = 0
         self._tail_done = False
+        self._tail_g2p_done = False
+        self._rebuild_next = 0        # steps mpm_rebuild may enqueue behind the rebuild step (frame drivers)
+        self._rebuild_enqueued = 0    # ... and how many it did
+        self._tp_gather, self._tp_scatter, self._gp_tail = TransferParams(), TransferParams(), _capi.GridParams()
         self._time_rot = 0
         self.time_kernels = False     # bench: CUDA events around the step kernels
+        self.profile_all_phases = False   # harness CSV: every gather is issued (and timed) from Python
         self.pipelined = True         # run_frame enqueues step s+1 before reading step s's flag
         self.batch_steps = _BATCH     # fixed-dt frames: steps per mpm_enqueue_steps call (0 = off)
         self._plan = None
@@ -1009,10 +1016,16 @@ class CudaWorker:
                     self._guard = None
                     self._defer, self._unconsumed = True, None
                     step = self._global_step
+                    # a rebuild step may enqueue the batch that follows it from C (mpm_rebuild), so that
+                    # the device has work while the host books the new tables
+                    left = self.batch_steps if cfl else min(self.batch_steps, spf - self._frame_steps - 1)
+                    self._rebuild_next = max(left, 0) if self.flags.rebuild_needed else 0
+                    self._rebuild_enqueued = 0
                     try:
                         self.run_step(step)
                     finally:
                         self._defer = False
+                        self._rebuild_next = 0
                     if self._unconsumed is not None:
                         self._consume(*self._unconsumed)
                         self._unconsumed = None
@@ -1025,6 +1038,23 @@ class CudaWorker:
                     self.frame_dts.append(self.dt)
                     enq = self._frame_steps
                     next_step = self._global_step
+                    if self._rebuild_enqueued:
+                        n = self._rebuild_enqueued
+                        self._rebuild_enqueued = 0
+                        self._pending_full_clear_parity = -1      # that batch cleared the other parity
+                        if self.flags.rebuild_needed or frame_done:
+                            # the rebuild step itself asked for another rebuild / ended the frame: its
+                            # gather raised the guard, the batch behind it ran as no-ops
+                            self.speculative_discards += n
+                            self._pending_full_clear_parity = (step + 1) & 1
+                            if self.flags.rebuild_needed and self._rebuild_tail_ok_static():
+                                self._guard_reset_in_rebuild = True
+                            else:
+                                self._call("mpm_fill_i32", self._guard_word.data_ptr(), 1, _INT_MAX, _stream_ptr())
+                        else:
+                            pending.append((next_step, n, None))
+                            next_step += n
+                            enq += n
                     continue
                 first, n, tev = pending.pop(0)
                 for k in range(n):
@@ -1111,6 +1141,16 @@ class CudaWorker:
         self._reduce_and_update(par, step)
         if self._fused_now:
             self._pending_gather = True
+        elif self._tail_g2p_done:
+            # issued (and its status block published) by mpm_rebuild behind the grid update
+            self._tail_g2p_done = False
+            slot = step % _RING
+            self._slot_clean[slot] = False
+            if self._defer:
+                self._unconsumed = (slot, step)
+            else:
+                self._consume(slot, step)
+            self._pending_gather = False
         else:
             self._run_g2p(step)
             self._pending_gather = False
@@ -1163,11 +1203,15 @@ class CudaWorker:
         return self._guard is None and self._rebuild_tail_ok_static()
 
     def _rebuild(self, step, par, flushed=None, tail=False):
-        """Worker._rebuild (pipeline.py:958-1015) on the device: one call (mpm_rebuild) that issues
-        every rebuild kernel and takes the two host syncs of the paper's rebuild (block count,
-        then pblock + group counts) in C.  Buffers stay Python's: they are sized
-        here from the counts of the previous rebuild (4x growth rule, so a steady state never
-        reallocates) and the call reports what it needs when a count outgrew one."""
+        """Worker._rebuild (pipeline.py:958-1015) on the device: one call (mpm_rebuild) that enqueues
+        every rebuild kernel WITHOUT a host round trip in between (the counts stay on the device,
+        launches are sized by the capacities given here), then -- for a single worker (`tail`) --
+        the rest of the rebuild step and the first batch of steady steps.  The host waits only
+        for the scalars (mpm_rebuild_wait), while those kernels run, and does its bookkeeping
+        of the new tables under their cover.  Buffers stay Python's: they are sized here from
+        the counts of the previous rebuild (4x growth rule, so a steady state never
+        reallocates); a count that outgrew one aborts the chain on the device and the call
+        reports what it needs."""
         lib, st, tb, gr = self.lib, self.store, self.table, self.grid
         stream = _stream_ptr()
         t_rebuild = time.perf_counter()
@@ -1186,6 +1230,7 @@ class CudaWorker:
         cap = max(tb.hash_cap, _pow2_at_least(8 * max(tb.count, 1)), 1 << 12)
         if tb.count == 0:
             cap = max(cap, _pow2_at_least(max(n_upper // 2, 1)))
+        tight = True
         plan, res = _capi.RebuildPlan(), _capi.RebuildResult()
         plan.old_store = st.view()
         plan.n_staged, plan.n_upper = n_staged, n_upper
@@ -1196,22 +1241,54 @@ class CudaWorker:
         for tag in ("src_slot", "pslot", "flag", "gidx", "tmp_perm", "perm"):
             setattr(plan, tag, S(tag, n_upper).ptr)
         plan.codes, plan.gcodes = S64("codes", n_upper).ptr, S64("gcodes", n_upper).ptr
-        plan.scan = S("scan", n_upper // 16 + 1024).ptr      # block sums of the largest scan
+        scan = S("scan", n_upper // 8 + 1024)                # block sums of the largest scan
+        plan.scan = scan.ptr
         plan.node_bytes = self._node_bytes
         plan.scalars_dev, plan.scalars_host = self._scalars.data_ptr(), self._scalars_host.data_ptr()
-        if self._guard_reset_in_rebuild:
+        plan.large_list = S("large_list", n_upper // 1024 + 2).ptr
+        if self._guard_reset_in_rebuild or tail:
+            # tail: nothing guarded is in flight (_rebuild_tail_ok), the word is reset by the call and
+            # then guards the rest of the step and the next batch, so that an aborted rebuild (a
+            # buffer too small) voids them without the host
             plan.guard_word = self._guard_word.data_ptr()
+            plan.guard_step = int(step)
             self._guard_reset_in_rebuild = False
+        next_n = 0
         if tail:
             # rest of the step (step_pre_barrier / step_post_barrier): P2G into status slot `step`,
             # grid update that also zeroes the status block of the gather following it
-            tp, gp = self._params(step=step), self._grid_params(step)
+            fused = self._fused_active()
+            # private copies: _step_plan() below refills the cached structs for the next batch
+            tp, gp = self._tp_scatter, self._gp_tail
+            C.memmove(C.byref(tp), C.byref(self._params(step=step)), C.sizeof(TransferParams))
+            C.memmove(C.byref(gp), C.byref(self._grid_params(step)), C.sizeof(_capi.GridParams))
             gp.fuse_clear = int(self.fuse_clear)
-            reset_slot = (step + 1 if self._fused_active() else step) % _RING
+            reset_slot = (step + 1 if fused else step) % _RING
             plan.p2g_params, plan.grid_params = C.addressof(tp), C.addressof(gp)
             plan.p2g_status = self._status_ptr(step % _RING)
             plan.grid_reset_status = self._status_ptr(reset_slot)
             self._tail_reset_slot = reset_slot
+            plan.async_ = 1
+            plan.done_event = self._rebuild_event.cuda_event
+            if not fused and self._status_alias and not self.profile_all_phases:
+                # split transfer: the step's gather and the publication of its status block too
+                slot = step % _RING
+                g2 = self._tp_gather
+                C.memmove(C.byref(g2), C.byref(tp), C.sizeof(TransferParams))
+                g2.dt_gather = float(self.dt)          # the update of this very step (pipeline.py:1230)
+                g2.clock_gather_step = int(step)
+                plan.g2p_params = C.addressof(g2)
+                plan.g2p_status = self._status_ptr(slot)
+                plan.status_publish_dst = (self._status_alias + slot * _capi.STATUS_BYTES) \
+                    if self._status_alias else None
+                plan.status_event = self._status_events[slot].cuda_event
+            next_n = int(self._rebuild_next or 0)
+            if next_n > 0 and (plan.g2p_params or fused):
+                # the first batch of steady steps, enqueued by the call itself behind the rebuild step
+                # (its store / table views are filled in C from this rebuild)
+                self._plan_stale = True
+            else:
+                next_n = 0
         while True:
             # block-indexed scratch and tables; codes/origin/touched sized for the worst case of the
             # dilation, 27 n_g (they are small)
@@ -1228,9 +1305,15 @@ class CudaWorker:
                 buf.ensure_capacity(want_groups, keep=False)
             gr._vel.ensure_capacity(want_nodes, keep=False)
             gr._raw[par].ensure_capacity(want_nodes, keep=False)
+            gr._raw[1 - par].ensure_capacity(want_nodes, keep=False)   # next step's parity: cleared in full there
             plan.qslot, plan.qflag, plan.bin_start, plan.bgf = qslot.ptr, qflag.ptr, bin_start.ptr, bgf.ptr
+            # Capacities double as launch bounds (the counts are read on the device).  The 4x growth
+            # rule leaves them up to 4x the real counts; twice the last counts is what a first attempt
+            # launches over, the full capacity only after a count outgrew that.
             plan.cap_gblocks = min(tb._neighbor.capacity, qslot.capacity // 27, qflag.capacity // 54,
-                                   (bin_start.capacity - 1) // 64, bgf.capacity - 1)
+                                   (bin_start.capacity - 1) // 64, bgf.capacity - 1,
+                                   (scan.capacity - 2) * 16,     # 64 bins per block, 1024 per scan tile
+                                   max(2 * want_g, 64) if tight else _INT_MAX)
             plan.hkeys, plan.hvals, plan.hfirst = tb._hkeys.ptr, tb._hvals.ptr, tb._hfirst.ptr
             plan.hash_cap = cap
             plan.cap_table = min(tb._codes.capacity, tb._origin.capacity, tb._touched[0].capacity,
@@ -1241,18 +1324,31 @@ class CudaWorker:
             plan.cap_groups = min(b.capacity for b in new_bufs)
             plan.vel, plan.raw_par = gr._vel.ptr, gr._raw[par].ptr
             plan.touched_par = tb._touched[par].ptr
-            plan.cap_nodes = min(gr._vel.capacity, gr._raw[par].capacity)
+            plan.cap_nodes = min(gr._vel.capacity, gr._raw[par].capacity, gr._raw[1 - par].capacity,
+                                 max(2 * want_nodes, 256) if tight else _INT_MAX)
+            if next_n > 0:
+                self._plan_stale = True              # buffers may just have been grown
+                sp = self._step_plan()
+                sp.full_clear_first = 1              # step + 1 is the first use of the other parity
+                sp.transfer.dt_gather = float(self.dt)
+                for k in range(2 * next_n):
+                    sp.time_events[k] = None
+                plan.next_steps = C.addressof(sp)
+                plan.next_first_step, plan.next_n_steps = int(step) + 1, next_n
             self.kernel_calls += 1
             rc = lib.mpm_rebuild(C.byref(plan), C.byref(res), stream)
             if flushed is not None:
                 self._consume(*flushed)      # the gather flushed just before this rebuild
                 flushed = None
+            if rc == 0 and plan.async_:
+                rc = lib.mpm_rebuild_wait(C.byref(plan), C.byref(res))
             if rc == _capi.NEED_CAPACITY:
                 if res.need_hash:
                     cap *= 4
                 want_g = max(want_g, res.need_gblocks, (res.need_table + 26) // 27)
                 want_groups = max(want_groups, res.need_groups)
                 want_nodes = max(want_nodes, res.need_nodes)
+                tight = False
                 continue
             if rc == -2 and res.bad_particle != _INT_MAX:
                 raise SpatialDomainError(
@@ -1285,6 +1381,8 @@ class CudaWorker:
         for k in (0, 1):
             tb._touched[k].len = count
         self._tail_done = bool(res.tail_done)
+        self._tail_g2p_done = bool(res.g2p_done)
+        self._rebuild_enqueued = int(res.next_done)
         self._pending_full_clear_parity = 1 - par
         self._plan_stale = True       # buffers may have moved: the batched-step plan refreshes its views
         self._published_codes = (tb._codes, count)
