@@ -187,7 +187,16 @@ __device__ __forceinline__ int corotated_tau(const float *f, float mu, float lam
 #pragma unroll
         for (int k = 0; k < 9; ++k) { w[k] = f[k]; dm[k] = f[k] - dm[k]; }
     } else {
-        clamped = corotated_parts_svd(f, w, dm, &J);
+        // The out-of-line route takes addresses: it works on private copies so that f, w, dm and J
+        // of the regular route stay in registers (arrays whose address escapes to a call live on
+        // the stack for the whole kernel, ~20 local stores per warp on the hot path before).
+        float ft[9], wt[9], dt[9], Jt = J;
+#pragma unroll
+        for (int k = 0; k < 9; ++k) ft[k] = f[k];
+        clamped = corotated_parts_svd(ft, wt, dt, &Jt);
+#pragma unroll
+        for (int k = 0; k < 9; ++k) { w[k] = wt[k]; dm[k] = dt[k]; }
+        J = Jt;
     }
     const float two_mu = 2.0f * mu;
     const float diag = lam * (J - 1.0f) * J;
@@ -294,11 +303,11 @@ __device__ __forceinline__ void plastic_return(const float *s, float &plastic, c
 // General route: Jacobi SVD of F itself (reflections, near-singular states).  Out of line: only
 // states the Newton polar iteration refuses (J <= 0.02) come here.
 template <int MAT>
-__device__ __noinline__ void plastic_project_svd(float *f, float &plastic, const PlasticParams &p, float *tau)
+__device__ __noinline__ void plastic_project_svd(float *f, float *plastic, PlasticParams p, float *tau)
 {
     float u[9], s[3], v[9], sc[3], d[3];
     svd3(f, u, s, v);
-    plastic_return<MAT>(s, plastic, p, sc, d);
+    plastic_return<MAT>(s, *plastic, p, sc, d);
     rebuild_from_svd(u, sc, v, f);
     tau_from_principal(u, d, tau);
 }
@@ -357,7 +366,15 @@ __device__ __forceinline__ void plastic_project(float *f, float &plastic, const 
     float r[9];
     const float J = det3(f);
     if (!polar_rotation(f, J, r)) {
-        plastic_project_svd<MAT>(f, plastic, p, tau);
+        // private copies for the out-of-line route (see corotated_tau): f, tau, the plastic scalar
+        // and the parameters of the regular route never have their address taken
+        float ft[9], tt[9], pl = plastic;
+#pragma unroll
+        for (int k = 0; k < 9; ++k) ft[k] = f[k];
+        plastic_project_svd<MAT>(ft, &pl, p, tt);
+#pragma unroll
+        for (int k = 0; k < 9; ++k) { f[k] = ft[k]; tau[k] = tt[k]; }
+        plastic = pl;
         return;
     }
     const float s00 = r[0] * f[0] + r[3] * f[3] + r[6] * f[6];

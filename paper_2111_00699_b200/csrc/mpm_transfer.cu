@@ -70,11 +70,38 @@ struct TransferArgs {
 #ifndef MPM_RUNCAP
 #define MPM_RUNCAP 4      // power of two; 32 = one reduction per (subgroup, node) whatever the run length
 #endif
+#ifndef MPM_MASSFOLD
+#define MPM_MASSFOLD 1    // scatter: particle mass folded into the x weight, Q carried per unit mass
+#endif
+#ifndef MPM_ROWLDS
+#define MPM_ROWLDS 1      // neighbour-row lookups as explicit ld.shared on a byte address (one IADD each)
+#endif
+#ifndef MPM_GATHER_PREFETCH
+#define MPM_GATHER_PREFETCH 0   // the eight node lines of a lane's stencil asked of L1 in the prologue
+#endif
 constexpr int TW = MPM_TW;   // warps (groups) per CTA
 
 __device__ __forceinline__ void prefetch_l1(const void *p)
 {
     asm volatile("prefetch.global.L1 [%0];" ::"l"(p));
+}
+
+// Neighbour-row lookup.  The row table of the warp sits in shared memory; `rowb` is the shared-space
+// byte address of entry rx + 3 ry + 9 rz.  Written as an explicit ld.shared so that the address is
+// one integer add per node (the compiler otherwise re-derives index * 4 + base with IMAD + LEA per
+// node); the volatile form of the scatter keeps the load where it is written -- ahead of the
+// shuffles whose latency it overlaps -- instead of being sunk into the run leader's branch.
+__device__ __forceinline__ int row_lds(unsigned rowb)
+{
+    int v;
+    asm("ld.shared.b32 %0, [%1];" : "=r"(v) : "r"(rowb));
+    return v;
+}
+__device__ __forceinline__ int row_lds_pinned(unsigned rowb)
+{
+    int v;
+    asm volatile("ld.shared.b32 %0, [%1];" : "=r"(v) : "r"(rowb));
+    return v;
 }
 
 __device__ __forceinline__ void red_add_v4(float4 *addr, float a, float b, float c, float d)
@@ -188,15 +215,28 @@ __device__ __forceinline__ void gather27(const float4 *__restrict__ vel, const i
     float wy[3], wz[3];
     quad_weights(fy, wy); quad_weights(fz, wz);
     int ry[3], rz[3], sy[3], sz[3];
+#if MPM_ROWLDS
+    const int nb = (int)__cvta_generic_to_shared(nrow);   // rows addressed in bytes (row_lds)
+#pragma unroll
+    for (int q = 0; q < 3; ++q) {
+        ry[q] = ((ky + q) >> 2) * 12; sy[q] = slot_bits<1>(ky + q);
+        rz[q] = ((kz + q) >> 2) * 36 + nb; sz[q] = slot_bits<2>(kz + q);
+    }
+#else
 #pragma unroll
     for (int q = 0; q < 3; ++q) {
         ry[q] = ((ky + q) >> 2) * 3; sy[q] = slot_bits<1>(ky + q);
         rz[q] = ((kz + q) >> 2) * 9; sz[q] = slot_bits<2>(kz + q);
     }
+#endif
     float V[3] = {0.f, 0.f, 0.f}, Mx[3] = {0.f, 0.f, 0.f}, My[3] = {0.f, 0.f, 0.f}, Mz[3] = {0.f, 0.f, 0.f};
 #pragma unroll 1
     for (int i = 0; i < 3; ++i) {
+#if MPM_ROWLDS
+        const int rx = ((kx + i) >> 2) * 4, sx = slot_bits<0>(kx + i);
+#else
         const int rx = (kx + i) >> 2, sx = slot_bits<0>(kx + i);
+#endif
         const float wxi = quad_weight_at(fx, i);
         const float cmi = (float)(i - 1) * wxi;
         float S[3] = {0.f, 0.f, 0.f}, Ty[3] = {0.f, 0.f, 0.f}, Tz[3] = {0.f, 0.f, 0.f};
@@ -205,8 +245,13 @@ __device__ __forceinline__ void gather27(const float4 *__restrict__ vel, const i
             const int rxy = rx + ry[j];
             const int sxy = sx + sy[j];
             float4 n[3];
+#if MPM_ROWLDS
+#pragma unroll
+            for (int k = 0; k < 3; ++k) n[k] = __ldg(&vel[row_lds((unsigned)(rxy + rz[k])) + sxy + sz[k]]);
+#else
 #pragma unroll
             for (int k = 0; k < 3; ++k) n[k] = __ldg(&vel[nrow[rxy + rz[k]] + sxy + sz[k]]);
+#endif
             // along z: s = sum_k wz_k v_k, t = wz_2 v_2 - wz_0 v_0
             const float s0 = wz[0] * n[0].y + wz[1] * n[1].y + wz[2] * n[2].y;
             const float s1 = wz[0] * n[0].z + wz[1] * n[1].z + wz[2] * n[2].z;
@@ -286,11 +331,20 @@ __device__ __forceinline__ void scatter27(float4 *__restrict__ raw, const int *n
     float wy[3], wz[3];
     quad_weights(fy, wy); quad_weights(fz, wz);
     int ry[3], rz[3], sy[3], sz[3];
+#if MPM_ROWLDS
+    const int nb = (int)__cvta_generic_to_shared(nrow);   // rows addressed in bytes (row_lds)
+#pragma unroll
+    for (int q = 0; q < 3; ++q) {
+        ry[q] = ((ky + q) >> 2) * 12; sy[q] = slot_bits<1>(ky + q);
+        rz[q] = ((kz + q) >> 2) * 36 + nb; sz[q] = slot_bits<2>(kz + q);
+    }
+#else
 #pragma unroll
     for (int q = 0; q < 3; ++q) {
         ry[q] = ((ky + q) >> 2) * 3; sy[q] = slot_bits<1>(ky + q);
         rz[q] = ((kz + q) >> 2) * 9; sz[q] = slot_bits<2>(kz + q);
     }
+#endif
     float QZ[3][3];
 #pragma unroll
     for (int k = 0; k < 3; ++k) {
@@ -301,10 +355,21 @@ __device__ __forceinline__ void scatter27(float4 *__restrict__ raw, const int *n
                 f8 = reach >= 8 ? 1.0f : 0.0f, f16 = reach >= 16 ? 1.0f : 0.0f;
 #pragma unroll 1
     for (int i = 0; i < 3; ++i) {
+#if MPM_ROWLDS
+        const int rx = ((kx + i) >> 2) * 4, sx = slot_bits<0>(kx + i);
+#else
         const int rx = (kx + i) >> 2, sx = slot_bits<0>(kx + i);
-        const float wxi = mm > 0.0f ? quad_weight_at(fx, i) : 0.0f;   // inactive lanes contribute zeros
+#endif
         const float dpx = ((float)i - fx) * dx;
+#if MPM_MASSFOLD
+        // Q is per unit mass here and the mass rides on the x weight: the node's mass share IS the
+        // weight product, momentum = w (v + Q dpos); inactive lanes (mm = 0) contribute exact zeros
+        const float wxi = mm * quad_weight_at(fx, i);
+        const float X0 = vx + Q[0] * dpx, X1 = vy + Q[3] * dpx, X2 = vz + Q[6] * dpx;
+#else
+        const float wxi = mm > 0.0f ? quad_weight_at(fx, i) : 0.0f;   // inactive lanes contribute zeros
         const float X0 = mm * vx + Q[0] * dpx, X1 = mm * vy + Q[3] * dpx, X2 = mm * vz + Q[6] * dpx;
+#endif
 #if MPM_ROLL_J
 #pragma unroll 1
 #else
@@ -326,15 +391,24 @@ __device__ __forceinline__ void scatter27(float4 *__restrict__ raw, const int *n
             for (int k = 0; k < 3; ++k) {
                 const float w = wxy * wz[k];
                 // issued before the shuffles so that its shared-memory latency overlaps them
+#if MPM_ROWLDS
+                const int node = row_lds_pinned((unsigned)(rxy + rz[k])) + sxy + sz[k];
+#else
                 const int node = nrow[rxy + rz[k]] + sxy + sz[k];
+#endif
+#if MPM_MASSFOLD
+                const float wm = w;
+#else
+                const float wm = w * mm;
+#endif
                 acc_t c0, c1, c2, c3;
                 if (DET) {
-                    c0 = (acc_t)__float2ll_rn((w * mm) * MPM_MASS_SCALE);
+                    c0 = (acc_t)__float2ll_rn(wm * MPM_MASS_SCALE);
                     c1 = (acc_t)__float2ll_rn((w * (XY0 + QZ[k][0])) * MPM_MOM_SCALE);
                     c2 = (acc_t)__float2ll_rn((w * (XY1 + QZ[k][1])) * MPM_MOM_SCALE);
                     c3 = (acc_t)__float2ll_rn((w * (XY2 + QZ[k][2])) * MPM_MOM_SCALE);
                 } else {
-                    c0 = (acc_t)(w * mm);
+                    c0 = (acc_t)wm;
                     c1 = (acc_t)(w * (XY0 + QZ[k][0]));
                     c2 = (acc_t)(w * (XY1 + QZ[k][1]));
                     c3 = (acc_t)(w * (XY2 + QZ[k][2]));
@@ -456,6 +530,17 @@ __global__ void __launch_bounds__(TW * 32, MPM_MINBLOCKS) transfer_kernel(const 
             // must lie in [0.5, 1.5) cells.  If it does not, the particle has left the
             // neighbourhood its key can express (the digits were clamped).
             const int kx = key % 10, ky = (key / 10) % 10, kz = key / 100;
+#if MPM_GATHER_PREFETCH
+            // A stencil of three cells per axis covers two 2-cell pairs per axis: eight 128-byte node
+            // lines.  Asking L1 for them now turns the nine dependent load batches of the node
+            // gather into hits (they otherwise each expose an L2 round trip).
+#pragma unroll
+            for (int q = 0; q < 8; ++q) {
+                const int tx = kx + ((q & 1) << 1), ty = ky + (q & 2), tz = kz + ((q & 4) >> 1);
+                const int row = nrow[(tx >> 2) + (ty >> 2) * 3 + (tz >> 2) * 9];
+                prefetch_l1(&a.vel[row + (slot_bits<0>(tx) | slot_bits<1>(ty) | slot_bits<2>(tz))]);
+            }
+#endif
             const float fx = px * a.inv_dx - (float)(org.x - 4 + kx - MPM_CELL_BIAS);
             const float fy = py * a.inv_dx - (float)(org.y - 4 + ky - MPM_CELL_BIAS);
             const float fz = pz * a.inv_dx - (float)(org.z - 4 + kz - MPM_CELL_BIAS);
@@ -583,8 +668,11 @@ __global__ void __launch_bounds__(TW * 32, MPM_MINBLOCKS) transfer_kernel(const 
             }
         }
         if (active) {
-            const float coeff = (a.clock ? a.coeff_per_dt * (float)__ldcg(&a.clock->dt[a.clock_step & 1])
-                                         : a.coeff_base) * m;
+            // Q = m C - 4 dt / (rho dx^2) m tau (pipeline.py:226-238); MPM_MASSFOLD carries it per unit
+            // mass (qm = 1) and scatter27 puts the mass on the weights
+            const float cb = a.clock ? a.coeff_per_dt * (float)__ldcg(&a.clock->dt[a.clock_step & 1]) : a.coeff_base;
+            const float qm = MPM_MASSFOLD ? 1.0f : m;
+            const float coeff = cb * qm;
             if (MAT == MPM_MAT_FLUID) {
                 float tau;
                 if (F[0] <= 0.0f) {
@@ -592,18 +680,18 @@ __global__ void __launch_bounds__(TW * 32, MPM_MINBLOCKS) transfer_kernel(const 
                     tau = 0.0f;
                 } else tau = fluid_tau(F[0], a.kappa, a.gamma, a.clamp_tension);
 #pragma unroll
-                for (int r = 0; r < 9; ++r) Q[r] = m * C[r];
+                for (int r = 0; r < 9; ++r) Q[r] = qm * C[r];
                 Q[0] += coeff * tau; Q[4] += coeff * tau; Q[8] += coeff * tau;
             } else if (MAT == MPM_MAT_FIXED_COROTATED) {
                 float t[9];
                 if (corotated_tau(F, a.mu, a.lam, t))
                     atomicAdd(&a.status->counters[MPM_C_SVD_CLAMP], 1ull);
 #pragma unroll
-                for (int r = 0; r < 9; ++r) Q[r] = m * C[r] + coeff * t[r];
+                for (int r = 0; r < 9; ++r) Q[r] = qm * C[r] + coeff * t[r];
             } else {
                 if (!GATHER) plastic_tau<MAT>(F, plastic, pp, tau);
 #pragma unroll
-                for (int r = 0; r < 9; ++r) Q[r] = m * C[r] + coeff * tau[r];
+                for (int r = 0; r < 9; ++r) Q[r] = qm * C[r] + coeff * tau[r];
             }
         } else {
             // lanes outside any run still take part in the shuffles: their payload must be exact

@@ -386,6 +386,19 @@ class CudaParticleStore:
         return float(self._aggregates()[4])
 
 
+class _Ms:
+    """A kernel duration already read from its CUDA events.  The events of batched steps are a
+    small ring that later batches record again, so their elapsed time is taken when the step is
+    consumed; `kernel_events` entries keep the (name, a, b) shape with a.elapsed_time(b)."""
+    __slots__ = ("ms",)
+
+    def __init__(self, ms):
+        self.ms = float(ms)
+
+    def elapsed_time(self, _other=None):
+        return self.ms
+
+
 class PendingReadback:
     """A snapshot on its way to pinned host memory (CudaParticleStore.positions_with_ids_async)."""
 
@@ -1066,8 +1079,10 @@ class CudaWorker:
                         frame_done = self._last_frame_end
                     if tev is not None and k == tev[1]:
                         name = "mpm_g2p2g" if self.options.transfer == "g2p2g" else "mpm_p2g"
-                        self.kernel_events.append((name, self._time_events[2 * tev[0]],
-                                                   self._time_events[2 * tev[0] + 1]))
+                        # read now: the ring's events are recorded again by the batch after next (the
+                        # step's status arrived, so its transfer kernel and both events are complete)
+                        ms = self._time_events[2 * tev[0]].elapsed_time(self._time_events[2 * tev[0] + 1])
+                        self.kernel_events.append((name, _Ms(ms), None))
                     # step `step` itself ran to completion (the guard only stops LATER steps)
                     self._global_step = step + 1
                     self._vel_dt = self.dt
