@@ -390,10 +390,11 @@ class _Ms:
     """A kernel duration already read from its CUDA events.  The events of batched steps are a
     small ring that later batches record again, so their elapsed time is taken when the step is
     consumed; `kernel_events` entries keep the (name, a, b) shape with a.elapsed_time(b)."""
-    __slots__ = ("ms",)
+    __slots__ = ("ms", "age")
 
-    def __init__(self, ms):
+    def __init__(self, ms, age=-1):
         self.ms = float(ms)
+        self.age = int(age)       # steps since the last rebuild when the kernel ran
 
     def elapsed_time(self, _other=None):
         return self.ms
@@ -1082,7 +1083,7 @@ class CudaWorker:
                         # read now: the ring's events are recorded again by the batch after next (the
                         # step's status arrived, so its transfer kernel and both events are complete)
                         ms = self._time_events[2 * tev[0]].elapsed_time(self._time_events[2 * tev[0] + 1])
-                        self.kernel_events.append((name, _Ms(ms), None))
+                        self.kernel_events.append((name, _Ms(ms, self.flags.steps_since_rebuild), None))
                     # step `step` itself ran to completion (the guard only stops LATER steps)
                     self._global_step = step + 1
                     self._vel_dt = self.dt
