@@ -65,3 +65,16 @@ for d, p, q in gaps:
     agg[(p, q)] += d; agc[(p, q)] += 1
 for (p, q), d in agg.most_common(16):
     print("   %8.1f us  x%-4d mean %6.1f us   %s -> %s" % (d, agc[(p, q)], d / agc[(p, q)], p, q))
+# raw intervals of a stretch of steady steps (RAW=<n> kernels): start / end relative to the first
+if os.environ.get("RAW"):
+    nraw = int(os.environ["RAW"])
+    mid = len(ks) // 2
+    # start at a fused transfer kernel
+    while mid < len(ks) and "transfer_kernel" not in ks[mid][2]:
+        mid += 1
+    base = ks[mid][0]
+    prev_end = None
+    for a, b, nme in ks[mid:mid + nraw]:
+        print("   start %9.1f  end %9.1f  dur %7.1f  gap-from-prev-end %7.1f   %s"
+              % (a - base, b - base, b - a, (a - prev_end) if prev_end is not None else 0.0, nme.split("(")[0][-48:]))
+        prev_end = b
