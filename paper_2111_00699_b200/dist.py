@@ -54,6 +54,24 @@ def build_halo_lists(peer_map: torch.Tensor):
     return send_idx, recv_pos
 
 
+def plan_slabs(hist, n: int):
+    """Slab boundaries of a re-partition from the GLOBAL histogram of the particle coordinate along
+    the partition axis: bin b goes to the worker whose share of the running count it falls in, so
+    every worker gets total / n particles up to the population of one bin (the reference cuts the
+    stable argsort into equal ranges, multiworker.py:114-137; with the particles spread over
+    processes the cut is made on the histogram instead).  Returns dest[bin] (int64, non-decreasing)."""
+    hist = np.asarray(hist, dtype=np.int64)
+    total = int(hist.sum())
+    if n < 1:
+        raise ValueError(f"worker count must be >= 1, got {n}")
+    if total == 0:
+        return np.zeros(len(hist), dtype=np.int64)
+    before = np.cumsum(hist) - hist                     # particles in the bins below
+    mid = before + hist // 2                            # a bin goes where its middle particle goes
+    dest = (mid * n) // total
+    return np.minimum(dest, n - 1).astype(np.int64)
+
+
 class DistRuntime:
     """SharedRuntime (multiworker.py:73-107) across processes."""
 
@@ -245,6 +263,10 @@ class DistWorker(CudaWorker):
             if self._pending_gather:
                 self._flush_gather()
 
+    def repartition(self, tol: float = 0.10, force: bool = False):
+        """Collective, between frames: see dist.repartition."""
+        return repartition(self, tol=tol, force=force)
+
     def _publish(self, par, rebuilt):
         self._rebuilt_this_step = rebuilt
 
@@ -328,6 +350,131 @@ class DistWorker(CudaWorker):
         if tb.count:
             self._slot_clean[nxt] = True
         self._vel_dt = self.dt
+
+
+# --------------------------------------------------------------------------------------
+# dynamic re-partitioning (the paper's future work)
+# --------------------------------------------------------------------------------------
+REPARTITION_BINS = 4096
+
+
+def _state_on_device(w: CudaWorker):
+    """Every stored lane in (group, lane) order as device tensors: rows [n, nch] fp32, ids [n],
+    and the flat (group * 32 + lane) position of each row in the store."""
+    st = w.store
+    n, G = st.count, st.n_groups
+    flat = torch.zeros((max(n, 1), st.nch), dtype=torch.float32, device=w.device)
+    ids = torch.zeros(max(n, 1), dtype=torch.int64, device=w.device)
+    where = torch.zeros(max(n, 1), dtype=torch.int64, device=w.device)
+    if n:
+        v = st.view()
+        _capi.check(_capi.lib().mpm_gather_state(C.byref(v), flat.data_ptr(), ids.data_ptr(), _stream_ptr()),
+                    "mpm_gather_state")
+        glen = st._group_len[st.cur].data[:G].to(torch.int64)
+        gstart = torch.cumsum(glen, 0) - glen
+        grp = torch.repeat_interleave(torch.arange(G, device=w.device), glen)
+        where = grp * 32 + (torch.arange(n, device=w.device) - gstart[grp])
+    return flat[:n], ids[:n], where[:n]
+
+
+def repartition(w: "DistWorker", tol: float = 0.10, force: bool = False, bins: int = REPARTITION_BINS):
+    """Collective, between frames.  Re-cut the slabs along the longest axis of the CURRENT particle
+    positions and migrate the particles whose slab now belongs to another rank.
+
+    The reference partitions once (bench.py:434-439, multiworker.py:114-137) and a worker keeps its
+    particles for good: as the material moves, the slabs interleave, the shared blocks (halo rows)
+    grow, and sources / sinks unbalance the counts.  Here every rank histograms its particles
+    along the axis, the global histogram is cut into equal shares (plan_slabs), and each particle
+    whose share is another rank's travels there with its whole state (x, v, C, m, F | J, plastic
+    scalar, id): it is removed here the way a sink removes it (mass 0, lane flagged, id -1, dropped
+    by the next rebuild's compaction) and staged there like an appended particle with state.  Ids
+    are preserved, the total mass is unchanged, and the step sequence continues with a rebuild
+    on every rank.  Nothing moves unless `force` or some rank's count is more than `tol` away
+    from the mean.  Returns a dict of counts (before, after, sent, received) or None."""
+    rt = w.runtime
+    n_ranks = rt.n_workers
+    with torch.cuda.device(w.device):
+        if w._pending_gather:
+            w._flush_gather()
+        flat, ids, where = _state_on_device(w)
+        meta = w.store._lane_meta[w.store.cur].data.view(-1)
+        alive = torch.ones(len(ids), dtype=torch.bool, device=w.device)
+        if len(ids):
+            alive = (meta[where].to(torch.int32) & 0x8000) == 0      # quarantined / sunk lanes stay put
+        pos = flat[:, 0:3].to(torch.float64)
+        big = 1e300
+        lo = pos[alive].min(dim=0).values.cpu().numpy() if bool(alive.any()) else np.full(3, big)
+        hi = pos[alive].max(dim=0).values.cpu().numpy() if bool(alive.any()) else np.full(3, -big)
+        n_alive = int(alive.sum().item())
+        # bounding box and counts of everybody (float64 bit patterns through the int64 exchange)
+        info = rt.all_gather_i64([int(np.float64(x).view(np.int64)) for x in list(lo) + list(hi)]
+                                 + [n_alive, w.store.nch])
+        los = info[:, 0:3].copy().view(np.float64)
+        his = info[:, 3:6].copy().view(np.float64)
+        counts = info[:, 6].astype(np.int64)
+        if not (info[:, 7] == w.store.nch).all():
+            from .errors import ConfigError
+            raise ConfigError("re-partitioning moves particles between ranks of ONE material population")
+        total = int(counts.sum())
+        if total == 0:
+            return None
+        mean = total / n_ranks
+        if not force and float(np.abs(counts - mean).max()) <= tol * mean:
+            return None
+        glo, ghi = los.min(axis=0), his.max(axis=0)
+        axis = int(np.argmax(ghi - glo))
+        width = max(float(ghi[axis] - glo[axis]), 1e-300)
+        # histogram of my particles, cut of the global one
+        b = torch.clamp(((pos[:, axis] - glo[axis]) * (bins / width)).to(torch.int64), 0, bins - 1)
+        hist = torch.bincount(b[alive], minlength=bins).cpu().numpy() if n_alive else np.zeros(bins, np.int64)
+        ghist = rt._all_gather_i64_dist(hist.tolist()).sum(axis=0)
+        dest_of_bin = torch.from_numpy(plan_slabs(ghist, n_ranks)).to(w.device)
+        dest = dest_of_bin[b]
+        dest[~alive] = rt.wid
+        leaving = dest != rt.wid
+        # who sends how many to whom
+        out_counts = torch.bincount(dest[leaving], minlength=n_ranks).cpu().numpy()
+        table = rt.all_gather_i64(out_counts.tolist()) if n_ranks <= _capi.SHM_MAX_VALUES else \
+            rt._all_gather_i64_dist(out_counts.tolist())
+        send_rows, send_ids, recv_rows, recv_ids = {}, {}, {}, {}
+        for q in range(n_ranks):
+            if q == rt.wid:
+                continue
+            if out_counts[q]:
+                sel = dest == q
+                send_rows[q] = flat[sel].contiguous()
+                send_ids[q] = ids[sel].contiguous()
+            k = int(table[q, rt.wid])
+            if k:
+                recv_rows[q] = torch.empty((k, w.store.nch), dtype=torch.float32, device=w.device)
+                recv_ids[q] = torch.empty(k, dtype=torch.int64, device=w.device)
+        torch.cuda.current_stream().synchronize()
+        rt.exchange_rows(send_rows, recv_rows)
+        rt.exchange_rows(send_ids, recv_ids)
+        n_out, n_in = int(leaving.sum().item()), int(sum(len(t) for t in recv_ids.values()))
+        if n_out:
+            # leave like a sunk particle: flagged, massless, id -1 (dropped by the next compaction)
+            st = w.store
+            gone = where[leaving]
+            flag = torch.tensor(-32768 | 0x4000, dtype=torch.int16, device=w.device)   # QUARANTINED | SUNK
+            meta[gone] = meta[gone] | flag
+            data = st._data[st.cur].data                      # [G, nch, 32]
+            data[gone // 32, 15, gone % 32] = 0.0             # CH_MASS
+            st._orig_id[st.cur].data.view(-1)[gone] = -1
+            st.has_sink = True
+        if n_in:
+            rows = torch.cat([recv_rows[q] for q in sorted(recv_rows)]).cpu().numpy()
+            rid = torch.cat([recv_ids[q] for q in sorted(recv_ids)]).cpu().numpy()
+            w.store.stage_append(rows[:, 0:3], rows[:, 3:6], rows[:, 15].copy(), deformation=rows[:, 16:],
+                                 affine=rows[:, 6:15], ids=rid)
+        # every rank rebuilds on the next step (SPMD), whether or not its own population changed
+        w.flags.rebuild_needed = True
+        w.flags.fused_mode = False
+        w._clock_valid = False
+        if hasattr(w, "_need_collective"):
+            w._need_collective = True
+        after = counts - table.sum(axis=1) + table.sum(axis=0)
+        return {"axis": axis, "before": counts.tolist(), "after": after.tolist(), "sent": n_out, "received": n_in}
 
 
 def seed_rank(worker: DistWorker, positions, velocities, mass):

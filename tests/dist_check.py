@@ -32,6 +32,8 @@ def main():
     torch.cuda.set_device(dev)
     if os.environ.get("MPM_SCENE", "") == "snow":
         return snow_slabs(rank, world, dev)
+    if os.environ.get("MPM_SCENE", "") == "repartition":
+        return repartition_check(rank, world, dev)
     g = golden("two_worker.npz")
     material, params, boundary = elastic_setup()
     transfer = os.environ.get("MPM_TRANSFER", "split")
@@ -64,6 +66,60 @@ def main():
     for s in range(1, 24):
         w.run_step(s)
     finish(w, g, rank, world, transfer, halo, frames)
+
+
+def repartition_check(rank, world, dev):
+    """Dynamic re-partitioning (dist.repartition): the two-worker scene seeded with a deliberately bad
+    partition -- 70 % of the particles on rank 0, the slabs interleaved -- runs 12 steps, re-cuts the
+    slabs (particles migrate with their whole state), runs 12 more.  The union must match the
+    reference's 24-step state at the short-run bars (the result does not depend on who owns a
+    particle), ids and total mass must be preserved and the counts balanced."""
+    import dataclasses
+    g = golden("two_worker.npz")
+    material, params, boundary = elastic_setup()
+    params = dataclasses.replace(params, steps_per_frame=12, frame_dt=12 * params.dt)
+    halo = os.environ.get("MPM_HALO", "sendrecv")
+    transfer = os.environ.get("MPM_TRANSFER", "split")
+    vmax0 = float(np.linalg.norm(g["vel"], axis=1).max())
+    if halo == "peer":
+        w = PeerDistWorker(PeerRuntime(dev, initial_vmax=vmax0), params, material, boundary,
+                           PipelineOptions(transfer=transfer), device=dev, wait_timeout_ms=20000)
+    else:
+        w = DistWorker(DistRuntime(dev, initial_vmax=vmax0), params, material, boundary,
+                       PipelineOptions(transfer=transfer), device=dev)
+    n = len(g["pos"])
+    rng = np.random.default_rng(5)
+    owner = (rng.random(n) > 0.7).astype(np.int64) if world == 2 else rng.integers(0, world, n)
+    mine = np.flatnonzero(owner == rank)
+    w.seed_particles(g["pos"][mine], g["vel"][mine], float(g["mass"]), ids=mine)
+    w.run_frame()
+    assert w.repartition(tol=10.0) is None           # within tolerance: nothing moves (still collective)
+    rep = w.repartition(force=True)
+    assert rep is not None and sum(rep["before"]) == n and sum(rep["after"]) == n, rep
+    assert max(rep["after"]) - min(rep["after"]) <= max(0.10 * n, 8), rep   # up to one histogram bin (a lattice plane)
+    w.run_frame()
+    if w._pending_gather:
+        w._flush_gather()
+    flat, ids = w.store.state_with_ids()
+    parts = [None] * world
+    dist.all_gather_object(parts, (flat, ids, list(w.rebuild_steps), rep))
+    if rank == 0:
+        flat = np.concatenate([p[0] for p in parts])
+        ids = np.concatenate([p[1] for p in parts])
+        assert np.array_equal(np.sort(ids), np.arange(n)), "ids lost or duplicated by the migration"
+        state = flat[np.argsort(ids, kind="stable")]
+        assert abs(state[:, 15].sum() - n * float(g["mass"])) <= 1e-6 * n * float(g["mass"])
+        edge = float(g["pos"].max() - g["pos"].min())
+        ex, ev, ef, ec = U.particle_errors(state, g["state_24"], edge, 9)
+        print(f"dist_check repartition world={world} halo={halo} transfer={transfer}: {rep['before']} -> "
+              f"{[len(p[1]) for p in parts]} (sent {[p[3]['sent'] for p in parts]}), "
+              f"x {ex:.2e} v {ev:.2e} F {ef:.2e} rebuilds {[p[2] for p in parts]}")
+        assert [len(p[1]) for p in parts] == rep["after"]
+        tolx = 1 if transfer == "split" else 10
+        assert ex <= tolx * U.X_RTOL_RUN and ev <= tolx * U.V_RTOL_RUN and ef <= tolx * U.F_ATOL_RUN, (ex, ev, ef)
+        print("DIST_CHECK_OK")
+    dist.barrier()
+    dist.destroy_process_group()
 
 
 def snow_slabs(rank, world, dev):

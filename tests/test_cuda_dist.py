@@ -79,3 +79,12 @@ def test_headline_scene_as_peer_mapped_slabs(world):
     device-paced frame, union of the slabs vs a single worker at the short-run bars; the grid
     update's barrier-wait / halo-byte counters are on and reported."""
     _run(world, "g2p2g", halo="peer", mode="frames", scene="snow")
+
+
+# ---- dynamic re-partitioning (dist.repartition; SURVEY 8f row 4) -----------------------------------
+@pytest.mark.parametrize("world,halo,transfer", [(2, "sendrecv", "split"), (2, "peer", "g2p2g"), (3, "peer", "split")])
+def test_repartition_migrates_particles_and_keeps_the_result(world, halo, transfer):
+    """A bad partition (70/30, slabs interleaved) is re-cut between two frames: particles migrate with
+    their whole state, ids and mass are preserved, counts end balanced, and the 24-step state still
+    matches the reference dump."""
+    _run(world, transfer, halo=halo, scene="repartition")

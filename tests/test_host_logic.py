@@ -256,3 +256,21 @@ def test_run_config_accepts_the_reference_fields():
         RunConfig(lane_width=0)
     with pytest.raises(ConfigError):
         RunConfig.from_dict({"no_such_field": 1})
+
+
+def test_plan_slabs_cuts_the_global_histogram_into_equal_shares():
+    """dist.plan_slabs (dynamic re-partitioning): non-decreasing destinations, every worker within one
+    bin's population of total / n, empty and degenerate histograms handled."""
+    from paper_2111_00699_b200.dist import plan_slabs
+    rng = np.random.default_rng(3)
+    for n in (1, 2, 3, 8):
+        hist = rng.integers(0, 50, size=512)
+        dest = plan_slabs(hist, n)
+        assert dest.min() >= 0 and dest.max() <= n - 1 and np.all(np.diff(dest) >= 0)
+        got = np.bincount(dest, weights=hist, minlength=n)
+        assert np.abs(got - hist.sum() / n).max() <= hist.max()
+    assert plan_slabs(np.zeros(16, dtype=np.int64), 4).tolist() == [0] * 16
+    one = np.zeros(16, dtype=np.int64); one[5] = 100          # everything in one bin: it cannot be split
+    assert len(set(plan_slabs(one, 4)[5:6].tolist())) == 1
+    with pytest.raises(ValueError):
+        plan_slabs(np.ones(4), 0)
