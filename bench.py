@@ -657,6 +657,73 @@ def run_mixed(args):
     print(json.dumps(line), flush=True)
 
 
+def run_mixed_ranks(args):
+    """configs[4] over N ranks: 2 material populations x N/2 slabs, one peer-mapped rank per (population,
+    slab) -- dist.population_layout.  On the 8-GPU box that is 4 slabs per population; several ranks
+    may share a device (MPM_DIST_BACKEND=gloo: functional check on one GPU)."""
+    import torch
+    import torch.distributed as dist
+    from paper_2111_00699_b200 import PipelineOptions, _capi, scenes
+    from paper_2111_00699_b200.dist import population_layout, seed_population_rank
+    from paper_2111_00699_b200.peer import PeerDistWorker, PeerRuntime
+    rank, world = int(os.environ.get("RANK", "0")), int(os.environ.get("WORLD_SIZE", "1"))
+    local = int(os.environ.get("LOCAL_RANK", "0")) % max(torch.cuda.device_count(), 1)
+    backend = os.environ.get("MPM_DIST_BACKEND", "nccl")
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    dist.init_process_group(backend, device_id=dev) if backend == "nccl" else dist.init_process_group(backend)
+    W = scenes.mixed_sparse(l=50, pairs_side=4) if args.scene == "mixed32m" else scenes.mixed_sparse(l=40, pairs_side=2)
+    pop, slab, n_slabs = population_layout(rank, world, len(W.populations))
+    w = PeerDistWorker(PeerRuntime(dev, initial_vmax=150.0), W.params, W.populations[pop].material, W.boundary,
+                       PipelineOptions(transfer=args.transfer, fused_threshold=1 << 62), device=dev,
+                       count_stats=False, lazy_flush=True)
+    mine = seed_population_rank(w, W.populations)
+    sampler = ClockSampler(local)
+    if rank == 0:
+        sampler.start()
+    for _ in range(args.warmup):
+        w.run_frame()
+
+    def barrier():
+        dist.barrier()
+        torch.cuda.synchronize()
+    barrier()
+    l0 = _capi.lib().mpm_launch_count()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    sampler.mark_begin()
+    e0.record()
+    for _ in range(args.steps):
+        w.run_frame()
+    e1.record()
+    barrier()
+    sampler.mark_end()
+    t = torch.tensor([e0.elapsed_time(e1)], dtype=torch.float64, device=dev if backend == "nccl" else "cpu")
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    ms = float(t.item())
+    info = [None] * world
+    dist.all_gather_object(info, (pop, slab, len(mine), int(w.table.count), w.collective_steps,
+                                  w.device_paced_steps, len(w.rebuild_steps)))
+    if rank == 0:
+        n, spf = W.n_particles, W.params.steps_per_frame
+        line = {"metric": METRIC, "value": round(n * spf * args.steps / (ms * 1e-3) / 1e6, 2), "unit": UNIT,
+                "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
+                "ms_per_step": round(ms / args.steps, 4), "higher_is_better": True, "scaling": "strong",
+                "vs_baseline": None, "dtype": "f32", "data": "synthetic",
+                "config": {"workload": W.name, "particles": n, "substeps_per_step": spf, "step": "one frame",
+                           "transfer": args.transfer, "material": "SNOW + SAND populations",
+                           "parallelism": f"{world} peer-mapped ranks = 2 populations x {n_slabs} slabs",
+                           "ranks": [{"population": a, "slab": b, "particles": c, "pblocks": d,
+                                      "collective_steps": e, "device_paced_steps": f, "rebuilds": g}
+                                     for a, b, c, d, e, f, g in info],
+                           "l2_policy": "inputs larger than L2 per rank unless the ranks share one device"},
+                "ms_per_frame": round(ms / args.steps, 4),
+                "gpu_launches": int(_capi.lib().mpm_launch_count() - l0), "e2e": None, "roofline": None,
+                "cpu_baseline": None, "clocks": sampler.stop()}
+        print(json.dumps(line), flush=True)
+    dist.barrier()
+    dist.destroy_process_group()
+
+
 def cpu_baseline(W, substeps, threads, warm=True):
     """The CPU oracle (C restatement of the reference, oracle/) timed on the host cores on a
     bounded sample: the full scene, rebuild + `substeps` substeps."""
@@ -733,6 +800,6 @@ if __name__ == "__main__":
     elif a.scene == "fountain":
         run_fountain(a)
     elif a.scene.startswith("mixed"):
-        run_mixed(a)
+        run_mixed_ranks(a) if int(os.environ.get("WORLD_SIZE", "1")) > 1 else run_mixed(a)
     else:
         run_ours(a)

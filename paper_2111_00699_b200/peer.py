@@ -504,7 +504,7 @@ class PeerDistWorker(DistWorker):
 
     def _run_frame_collective_cfl(self):
         from .domain import cfl_dt
-        c_sound = self.material.sound_speed()
+        c_sound = self.global_sound_speed()
         t = 0.0
         while t < self.params.frame_dt - 1e-12:
             vmax = self.runtime.global_vmax((self._global_step - 2) % 3)

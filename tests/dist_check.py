@@ -34,6 +34,8 @@ def main():
         return snow_slabs(rank, world, dev)
     if os.environ.get("MPM_SCENE", "") == "repartition":
         return repartition_check(rank, world, dev)
+    if os.environ.get("MPM_SCENE", "") == "mixed":
+        return mixed_populations(rank, world, dev)
     g = golden("two_worker.npz")
     material, params, boundary = elastic_setup()
     transfer = os.environ.get("MPM_TRANSFER", "split")
@@ -117,6 +119,54 @@ def repartition_check(rank, world, dev):
         assert [len(p[1]) for p in parts] == rep["after"]
         tolx = 1 if transfer == "split" else 10
         assert ex <= tolx * U.X_RTOL_RUN and ev <= tolx * U.V_RTOL_RUN and ef <= tolx * U.F_ATOL_RUN, (ex, ev, ef)
+        print("DIST_CHECK_OK")
+    dist.barrier()
+    dist.destroy_process_group()
+
+
+def mixed_populations(rank, world, dev):
+    """Material populations over ranks (configs[4]): a small snow + sand scene (sand boxes dropped onto
+    snow boxes) as `world` peer-mapped ranks = 2 populations x world/2 slabs, each rank with the
+    material of its population; one frame of 30 substeps.  The union is compared with the same
+    frame run as two logical workers of ONE process (CudaCluster, one per population)."""
+    from paper_2111_00699_b200 import CudaCluster, scenes
+    from paper_2111_00699_b200.dist import population_layout, seed_population_rank
+    W = scenes.mixed_sparse(l=8, pairs_side=2, domain_cells=64, gap_cells=1)
+    f32r = lambda a: np.asarray(a, dtype=np.float64).astype(np.float32).astype(np.float64)
+    for p in W.populations:
+        p.positions, p.velocities = f32r(p.positions), f32r(p.velocities)
+    transfer = os.environ.get("MPM_TRANSFER", "g2p2g")
+    opts = PipelineOptions(transfer=transfer, fused_threshold=1 << 62)
+    pop, slab, n_slabs = population_layout(rank, world, len(W.populations))
+    w = PeerDistWorker(PeerRuntime(dev, initial_vmax=150.0), W.params, W.populations[pop].material, W.boundary,
+                       opts, device=dev, wait_timeout_ms=60000, count_stats=False)
+    mine = seed_population_rank(w, W.populations)
+    w.run_frame()
+    flat, ids = w.store.state_with_ids()
+    parts = [None] * world
+    dist.all_gather_object(parts, (flat, ids, pop, slab, (w.collective_steps, w.device_paced_steps,
+                                                           len(w.rebuild_steps))))
+    if rank == 0:
+        n = W.n_particles
+        flat = np.concatenate([p[0] for p in parts])
+        ids = np.concatenate([p[1] for p in parts])
+        assert np.array_equal(np.sort(ids), np.arange(n))
+        state = flat[np.argsort(ids, kind="stable")]
+        cl = CudaCluster(2, W.params, [p.material for p in W.populations], W.boundary, opts, initial_vmax=150.0,
+                         device=dev, count_stats=False)
+        cl.seed_populations([(p.positions, p.velocities, p.particle_mass) for p in W.populations])
+        cl.run_frame()
+        ref = cl.state_sorted_by_id()
+        shared = len(np.intersect1d(cl.workers[0].table.codes, cl.workers[1].table.codes))
+        edge = float(max(p.positions.max() for p in W.populations) - min(p.positions.min() for p in W.populations))
+        ex, ev, ef, _ = U.particle_errors(state, ref, edge, 9)
+        ej = np.abs(state[:, 25] - ref[:, 25]).max()
+        print(f"dist_check mixed world={world} ({n_slabs} slab(s) x 2 populations, {n} particles, {shared} pblocks "
+              f"shared by the populations): x {ex:.2e} v {ev:.2e} F {ef:.2e} plastic {ej:.2e} vs one process; "
+              f"rank -> (population, slab, collective/device-paced/rebuilds): {[(p[2], p[3], p[4]) for p in parts]}")
+        assert shared > 0
+        assert ex <= 10 * U.X_RTOL_RUN and ev <= 10 * U.V_RTOL_RUN and ef <= 10 * U.F_ATOL_RUN and \
+            ej <= 10 * U.F_ATOL_RUN, (ex, ev, ef, ej)
         print("DIST_CHECK_OK")
     dist.barrier()
     dist.destroy_process_group()

@@ -88,3 +88,11 @@ def test_repartition_migrates_particles_and_keeps_the_result(world, halo, transf
     their whole state, ids and mass are preserved, counts end balanced, and the 24-step state still
     matches the reference dump."""
     _run(world, transfer, halo=halo, scene="repartition")
+
+
+# ---- material populations over ranks (configs[4]) ---------------------------------------------------
+@pytest.mark.parametrize("world", [2, 4])
+def test_material_populations_over_peer_mapped_ranks(world):
+    """Snow + sand populations as 2 / 4 peer-mapped ranks (2 populations x 1 / 2 slabs, each rank with
+    its population's material) against the two-population run of one process."""
+    _run(world, "g2p2g", halo="peer", scene="mixed")
