@@ -453,8 +453,8 @@ def run_ours(args):
 # committed `ncu --set full` capture of the fused kernel on the 1.37 M scene
 # (profiles/r1_l_fused_snow_final_metrics.csv: 96.5 MB read + 52.7 MB write; r1_l_fused_snow_fc_final: 89.8 + 40.8);
 # only quoted for those scenes
-TRAFFIC_NCU = {"snow": (149.2e6, "profiles/r1_l_fused_snow_final_metrics.csv (ncu --set full, one launch; not measured in this run)"),
-               "snow_fc": (130.5e6, "profiles/r1_l_fused_snow_fc_final_metrics.csv (ncu --set full, one launch; not measured in this run)")}
+TRAFFIC_NCU = {"snow": (136.9e6, "profiles/r2f_fused_snow_metrics.csv (ncu --set full, one launch; not measured in this run)"),
+               "snow_fc": (124.9e6, "profiles/r2f_fused_snow_fc_metrics.csv (ncu --set full, one launch; not measured in this run)")}
 
 
 FOUNTAIN_CAP = 143_500      # the paper's interactive fountain holds at most 143.5 K particles

@@ -423,6 +423,27 @@ __device__ __forceinline__ void plastic_project(float *f, float &plastic, const 
 template <int MAT>
 __device__ __forceinline__ void plastic_tau(const float *f, float plastic, const PlasticParams &p, float *tau)
 {
+    if (MAT == MPM_MAT_SNOW) {
+        // The stored F_E is already projected, so its stress is the fixed-corotated form with
+        // hardened moduli, tau = 2 mu_h (F - R) F^T + lam_h (J - 1) J I (= U (2 mu_h (S - I) S + ...) U^T):
+        // the polar factor is all it takes.  States the Newton iteration refuses go through the SVD.
+        float r[9];
+        const float J = det3(f);
+        if (polar_rotation(f, J, r)) {
+            const float h = expf(p.hardening * (1.0f - plastic));
+            const float two_mu = 2.0f * p.mu * h, diag = p.lam * h * (J - 1.0f) * J;
+#pragma unroll
+            for (int a = 0; a < 3; ++a)
+#pragma unroll
+                for (int b = 0; b < 3; ++b) {
+                    const float acc = two_mu * ((f[3 * a] - r[3 * a]) * f[3 * b] +
+                                                (f[3 * a + 1] - r[3 * a + 1]) * f[3 * b + 1] +
+                                                (f[3 * a + 2] - r[3 * a + 2]) * f[3 * b + 2]);
+                    tau[3 * a + b] = (a == b) ? acc + diag : acc;
+                }
+            return;
+        }
+    }
     float u[9], s[3], v[9], d[3];
     svd3(f, u, s, v);
     if (MAT == MPM_MAT_SNOW) {
