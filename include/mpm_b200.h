@@ -350,6 +350,14 @@ typedef struct mpm_rebuild_plan {
      * table views are taken from this rebuild (counts on the device); next_steps NULL = none. */
     const struct mpm_step_plan *next_steps;
     int32_t next_first_step, next_n_steps;
+    /* Optional: device word that receives the group count of the new store.  With it the NEXT rebuild
+     * can describe this store as old_store {n_groups = capacity of its buffers, n_groups_dev = this
+     * word}: nothing in the kernel chain then depends on a host-side count of the previous rebuild,
+     * and a rebuild whose buffers, capacities and particle count equal an earlier one's is replayed
+     * as a CUDA graph (one launch instead of ~35; use_graph). */
+    int32_t *n_groups_out;
+    int32_t use_graph;                 /* 1: capture / replay the rebuild kernels as a CUDA graph (n_staged == 0) */
+    int32_t reserved1;
 } mpm_rebuild_plan;
 typedef struct mpm_rebuild_result {
     int32_t n, n_gblocks, count, n_groups;
@@ -358,6 +366,7 @@ typedef struct mpm_rebuild_result {
     int32_t tail_done;                 /* 1: the P2G and the grid update of the step were issued */
     int32_t g2p_done;                  /* 1: ... and the split gather + its status publication */
     int32_t next_done;                 /* steps of next_steps that were enqueued */
+    int32_t graph;                     /* 0 launched kernel by kernel, 1 graph captured by this call, 2 replayed */
 } mpm_rebuild_result;
 int mpm_rebuild(const mpm_rebuild_plan *plan, mpm_rebuild_result *result, void *stream);
 /* Blocks until the scalars of an async mpm_rebuild are on the host, then fills `result` and returns

@@ -123,13 +123,14 @@ class RebuildPlan(C.Structure):
         ("guard_step", i32), ("async_", i32), ("large_list", p_void), ("done_event", p_void),
         ("g2p_params", p_void), ("g2p_status", p_void), ("status_publish_dst", p_void),
         ("status_event", p_void), ("next_steps", p_void), ("next_first_step", i32), ("next_n_steps", i32),
+        ("n_groups_out", p_void), ("use_graph", i32), ("reserved1", i32),
     ]
 
 
 class RebuildResult(C.Structure):
     _fields_ = [(k, i32) for k in ("n", "n_gblocks", "count", "n_groups", "bad_particle", "bad_block",
                                    "need_hash", "need_gblocks", "need_table", "need_groups",
-                                   "need_nodes", "tail_done", "g2p_done", "next_done")]
+                                   "need_nodes", "tail_done", "g2p_done", "next_done", "graph")]
 
 
 NEED_CAPACITY = 1

@@ -19,6 +19,13 @@ void set_last_error(const char *what, cudaError_t e)
 // asynchronous.  Execution errors surface at the host's next synchronisation.
 static std::atomic<unsigned long long> g_launches{0};
 
+thread_local bool g_plain_launch = false;
+
+unsigned long long launch_counter_add(unsigned long long n)
+{
+    return g_launches.fetch_add(n, std::memory_order_relaxed) + n;
+}
+
 int check_launch(const char *what, int n_kernels)
 {
     g_launches.fetch_add((unsigned long long)n_kernels, std::memory_order_relaxed);

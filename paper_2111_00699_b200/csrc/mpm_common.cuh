@@ -142,10 +142,20 @@ __device__ __forceinline__ void pdl_launch_dependents()
     asm volatile("griddepcontrol.launch_dependents;");
 #endif
 }
+// Set while a kernel chain is being captured into a CUDA graph (mpm_rebuild): the nodes of a graph are
+// launched the plain way (a programmatic edge behind a memset / memcpy node is not capturable, and
+// inside a graph the launch latency the attribute hides is not there).
+extern thread_local bool g_plain_launch;
+unsigned long long launch_counter_add(unsigned long long n);
+
 template <typename... KArgs, typename... Args>
 inline void launch_chained(void (*kernel)(KArgs...), int grid, int block, cudaStream_t stream, Args &&...args)
 {
 #if MPM_PDL
+    if (g_plain_launch) {
+        kernel<<<grid, block, 0, stream>>>(static_cast<KArgs>(args)...);
+        return;
+    }
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = dim3((unsigned)grid);
     cfg.blockDim = dim3((unsigned)block);

@@ -148,15 +148,16 @@ void exclusive_scan_i32(const int32_t *in, int32_t *out, int32_t n, int32_t *blo
 // ===================================================================================
 __global__ void __launch_bounds__(256) live_count_kernel(const uint16_t *__restrict__ lane_meta,
                                                          const int *__restrict__ group_len,
-                                                         int n_groups, int drop_q,
-                                                         int *__restrict__ group_live)
+                                                         int n_groups, const int *__restrict__ n_groups_dev,
+                                                         int drop_q, int *__restrict__ group_live)
 {
     pdl_wait();
     pdl_launch_dependents();
     const int g = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
     const int lane = threadIdx.x & 31;
     if (g >= n_groups) return;
-    const int len = group_len[g];
+    // the count on the device (n_groups is then the launch bound): groups beyond it hold nothing
+    const int len = (n_groups_dev && g >= *n_groups_dev) ? 0 : group_len[g];
     bool live = lane < len;
     if (live && drop_q) live = !(lane_meta[g * 32 + lane] & MPM_LANE_QUARANTINED);
     unsigned m = __ballot_sync(0xffffffffu, live);
@@ -165,8 +166,8 @@ __global__ void __launch_bounds__(256) live_count_kernel(const uint16_t *__restr
 
 __global__ void __launch_bounds__(256) live_write_kernel(const uint16_t *__restrict__ lane_meta,
                                                          const int *__restrict__ group_len,
-                                                         int n_groups, int drop_q,
-                                                         const int *__restrict__ group_base,
+                                                         int n_groups, const int *__restrict__ n_groups_dev,
+                                                         int drop_q, const int *__restrict__ group_base,
                                                          int *__restrict__ src_slot)
 {
     pdl_wait();
@@ -174,7 +175,7 @@ __global__ void __launch_bounds__(256) live_write_kernel(const uint16_t *__restr
     const int g = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
     const int lane = threadIdx.x & 31;
     if (g >= n_groups) return;
-    const int len = group_len[g];
+    const int len = (n_groups_dev && g >= *n_groups_dev) ? 0 : group_len[g];
     bool live = lane < len;
     if (live && drop_q) live = !(lane_meta[g * 32 + lane] & MPM_LANE_QUARANTINED);
     unsigned m = __ballot_sync(0xffffffffu, live);
@@ -433,13 +434,15 @@ __global__ void rebuild_init_kernel(int *S, int *large_list, int *guard_word)
 // A count that outgrew the caller's buffers (or a particle / block outside the domain) aborts the
 // rebuild WITHOUT a host round trip: the counts the later kernels read are zeroed, so every one of
 // them -- and the rest of the rebuild step issued behind them -- is a no-op, and the guard of the
-// steps enqueued behind the rebuild is lowered below `guard_step`.  The host finds the abort mask
+// steps enqueued behind the rebuild is lowered below every step (-1: the chain does not depend on the
+// step number, so it can be replayed as a CUDA graph).  The host finds the abort mask
 // and the sizes needed when it reads the scalars (mpm_rebuild_wait), grows the buffers and calls again.
 __device__ __forceinline__ void rebuild_abort(int *S, int why, int *guard_word, int guard_step)
 {
+    (void)guard_step;
     S[8] |= why;
     S[1] = 0; S[3] = 0; S[5] = 0; S[7] = 0;
-    if (guard_word) atomicMin(guard_word, guard_step - 1);
+    if (guard_word) atomicMin(guard_word, -1);
 }
 __global__ void rebuild_check_blocks_kernel(int *S, int gblocks_bound, int hash_cap, int table_cap,
                                             int *guard_word, int guard_step)
@@ -454,10 +457,13 @@ __global__ void rebuild_check_blocks_kernel(int *S, int gblocks_bound, int hash_
     if (27ll * n_g > table_cap) { why |= 2; S[10] = 27 * n_g; }          // worst case of the dilation
     if (why) rebuild_abort(S, why, guard_word, guard_step);
 }
-__global__ void rebuild_check_groups_kernel(int *S, int groups_cap, int nodes_cap, int *guard_word, int guard_step)
+__global__ void rebuild_check_groups_kernel(int *S, int groups_cap, int nodes_cap, int *guard_word, int guard_step,
+                                            int *n_groups_out)
 {
     pdl_wait();
     pdl_launch_dependents();
+    // the new store's group count, kept on the device for the NEXT rebuild (it is then the old store)
+    if (n_groups_out) *n_groups_out = (S[8] || S[7] > groups_cap) ? 0 : S[7];
     if (S[8]) return;
     int why = 0;
     if (S[6] != MPM_INT_MAX) why |= 16;                                  // block on the domain boundary
@@ -860,10 +866,10 @@ int mpm_compact_live(const mpm_store_view *store, int drop_quarantined, int32_t 
         return check_launch("mpm_compact_live", 5);
     }
     launch_chained(live_count_kernel, nblk((int64_t)G * 32, 256), 256, stream, 
-        store->lane_meta, store->group_len, G, drop_quarantined, group_live_scratch);
+        store->lane_meta, store->group_len, G, store->n_groups_dev, drop_quarantined, group_live_scratch);
     exclusive_scan_i32(group_live_scratch, group_live_scratch, G, scan_scratch, n_live, stream);
     launch_chained(live_write_kernel, nblk((int64_t)G * 32, 256), 256, stream, 
-        store->lane_meta, store->group_len, G, drop_quarantined, group_live_scratch, src_slot);
+        store->lane_meta, store->group_len, G, store->n_groups_dev, drop_quarantined, group_live_scratch, src_slot);
     return check_launch("mpm_compact_live", 5);
 }
 
@@ -1075,9 +1081,10 @@ void rebuild_check_blocks(int32_t *S, int gblocks_bound, int hash_cap, int table
                    guard_step);
 }
 void rebuild_check_groups(int32_t *S, int groups_cap, int nodes_cap, int32_t *guard_word, int guard_step,
-                          cudaStream_t stream)
+                          int32_t *n_groups_out, cudaStream_t stream)
 {
-    launch_chained(rebuild_check_groups_kernel, 1, 1, stream, S, groups_cap, nodes_cap, guard_word, guard_step);
+    launch_chained(rebuild_check_groups_kernel, 1, 1, stream, S, groups_cap, nodes_cap, guard_word, guard_step,
+                   n_groups_out);
 }
 void zero_rows(float *rows, const int32_t *count_dev, int bound, cudaStream_t stream)
 {
@@ -1104,7 +1111,7 @@ int rebuild_chain(const mpm_rebuild_plan *p, int32_t *S, int gblocks_bound, int 
     rc = sort_and_group_impl(p->codes, p->gidx, S + 1, p->n_upper, S + 3, gblocks_bound, p->bin_start,
                              p->tmp_perm, p->perm, p->bgf, p->scan, S + 7, p->pslot, p->large_list, stream, true);
     if (rc != MPM_OK) return rc;
-    rebuild_check_groups(S, p->cap_groups, p->cap_nodes, p->guard_word, p->guard_step, stream);
+    rebuild_check_groups(S, p->cap_groups, p->cap_nodes, p->guard_word, p->guard_step, p->n_groups_out, stream);
     mpm_store_view ns = p->new_store;
     ns.n_groups = groups_bound;
     ns.n_groups_dev = S + 7;

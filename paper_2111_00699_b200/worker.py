@@ -571,6 +571,10 @@ class CudaWorker:
             self._scalars_host = torch.zeros(16, dtype=torch.int32).pin_memory()
             self._rebuild_event = torch.cuda.Event()
             self._rebuild_event.record()
+            # group count of either half of the particle store, kept on the device by the rebuild
+            # that filled it (mpm_rebuild_plan.n_groups_out): the next rebuild reads it there
+            self._ngroups_dev = torch.zeros(2, dtype=torch.int32, device=self.device)
+            self._ngroups_dev_valid = [False, False]
             # step clock of CFL-auto frames (mpm_step_clock: dt[2], t, reserved), device-resident
             self._clock = torch.zeros(4, dtype=torch.float64, device=self.device)
             self._clock_host = torch.zeros(4, dtype=torch.float64).pin_memory()
@@ -620,6 +624,11 @@ class CudaWorker:
         self.kernel_calls = 0
         self._tail_done = False
         self._tail_g2p_done = False
+        self.rebuild_graph = True     # replay the rebuild kernels as a CUDA graph when nothing changed shape
+        self.rebuild_graph_max = 600_000   # ... up to this many particles (beyond, the chain is device-bound)
+        self.rebuild_graph_replays = 0
+        self._rb_cache = {}           # store half -> (key, plan, result) of the last rebuild out of it
+        self._rebuild_next_n = 0
         self._rebuild_next = 0        # steps mpm_rebuild may enqueue behind the rebuild step (frame drivers)
         self._rebuild_enqueued = 0    # ... and how many it did
         self._tp_gather, self._tp_scatter, self._gp_tail = TransferParams(), TransferParams(), _capi.GridParams()
@@ -1247,13 +1256,93 @@ class CudaWorker:
         if tb.count == 0:
             cap = max(cap, _pow2_at_least(max(n_upper // 2, 1)))
         tight = True
-        plan, res = _capi.RebuildPlan(), _capi.RebuildResult()
+        # The plan of the last rebuild out of this half of the store is reused as it stands when
+        # nothing it describes can have changed: no staged particles, the same particle count, no
+        # buffer reallocated since (only the step-dependent fields below are refreshed).  Its launch
+        # bounds may then be older than the counts; a count that outgrew one aborts on the device and
+        # comes back through the sizing below, like any other.
+        ck = (st.cur, n_upper, self.realloc_count) \
+            if (n_staged == 0 and st.n_groups > 0 and self._ngroups_dev_valid[st.cur]) else None
+        cached = self._rb_cache.get(st.cur) if ck is not None else None
+        fast = cached is not None and cached[0] == ck
+        if fast:
+            plan, res = cached[1], cached[2]
+        else:
+            plan, res = _capi.RebuildPlan(), _capi.RebuildResult()
+            self._rebuild_static_fields(plan, st, nxt, n_upper, n_staged, staged, staged_ids)
+        cur_before = st.cur
+        self._rebuild_step_fields(plan, step, par, tail)
+        next_n = self._rebuild_next_n
+        while True:
+            if fast:
+                plan.raw_par = gr._raw[par].ptr
+                plan.touched_par = tb._touched[par].ptr
+            else:
+                self._rebuild_size(plan, par, want_g, want_groups, want_nodes, cap, tight, new_bufs, n_upper)
+            if next_n > 0:
+                self._plan_stale = True              # buffers may just have been grown
+                sp = self._step_plan()
+                sp.full_clear_first = 1              # step + 1 is the first use of the other parity
+                sp.transfer.dt_gather = float(self.dt)
+                for k in range(2 * next_n):
+                    sp.time_events[k] = None
+                plan.next_steps = C.addressof(sp)
+                plan.next_first_step, plan.next_n_steps = int(step) + 1, next_n
+            else:
+                plan.next_steps = None
+                plan.next_first_step = plan.next_n_steps = 0
+            self.kernel_calls += 1
+            rc = lib.mpm_rebuild(C.byref(plan), C.byref(res), stream)
+            if flushed is not None:
+                self._consume(*flushed)      # the gather flushed just before this rebuild
+                flushed = None
+            if rc == 0 and plan.async_:
+                rc = lib.mpm_rebuild_wait(C.byref(plan), C.byref(res))
+            if rc == _capi.NEED_CAPACITY:
+                if res.need_hash:
+                    cap *= 4
+                want_g = max(want_g, res.need_gblocks, (res.need_table + 26) // 27)
+                want_groups = max(want_groups, res.need_groups)
+                want_nodes = max(want_nodes, res.need_nodes)
+                tight = False
+                fast = False
+                continue
+            if rc == -2 and res.bad_particle != _INT_MAX:
+                raise SpatialDomainError(
+                    f"worker {self.wid}: particle {res.bad_particle} of the rebuild input lies outside "
+                    f"the encodable domain [0, 2^21) cells")
+            if rc == -2 and res.bad_block != _INT_MAX:
+                code = int(self._scratch["gcodes"].data[res.bad_block].item())
+                x, y, z = _decode(code)
+                raise SpatialDomainError(
+                    f"block ({x - CELL_BIAS // 4}, {y - CELL_BIAS // 4}, {z - CELL_BIAS // 4}) "
+                    f"touches the domain boundary; scenes must leave a one-block margin")
+            check(rc, "mpm_rebuild")
+            break
+        self._rebuild_adopt(res, nxt, new_bufs, step, par, t_rebuild)
+        if n_staged == 0:
+            self._rb_cache[cur_before] = ((cur_before, n_upper, self.realloc_count), plan, res)
+
+    def _rebuild_static_fields(self, plan, st, nxt, n_upper, n_staged, staged, staged_ids):
+        """Fields of a rebuild plan that only change with the buffers, the particle count or staging."""
+        S, S64 = self._scratch_i32, self._scratch_i64
         plan.old_store = st.view()
+        old_bufs = [b[st.cur] for b in (st._data, st._orig_id, st._lane_meta, st._group_len, st._group_block,
+                                        st._group_start, st._group_ctx)]
+        old_bound = st.n_groups
+        if st.n_groups > 0 and self._ngroups_dev_valid[st.cur]:
+            # the old store by its CAPACITY, its count read on the device: the chain then looks the
+            # same from one rebuild to the next (mpm_rebuild replays it as a graph)
+            old_bound = min(b.capacity for b in old_bufs)
+            plan.old_store.n_groups = old_bound
+            plan.old_store.n_groups_dev = self._ngroups_dev.data_ptr() + 4 * st.cur
+        plan.n_groups_out = self._ngroups_dev.data_ptr() + 4 * nxt
+        plan.use_graph = int(self.rebuild_graph and n_staged == 0 and n_upper <= self.rebuild_graph_max)
         plan.n_staged, plan.n_upper = n_staged, n_upper
         plan.staged = staged.data_ptr() if n_staged else None
         plan.staged_ids = staged_ids.data_ptr() if n_staged else None
         plan.dx = float(self.params.dx)
-        plan.glive = S("glive", st.n_groups + 1).ptr
+        plan.glive = S("glive", old_bound + 1).ptr
         for tag in ("src_slot", "pslot", "flag", "gidx", "tmp_perm", "perm"):
             setattr(plan, tag, S(tag, n_upper).ptr)
         plan.codes, plan.gcodes = S64("codes", n_upper).ptr, S64("gcodes", n_upper).ptr
@@ -1262,6 +1351,14 @@ class CudaWorker:
         plan.node_bytes = self._node_bytes
         plan.scalars_dev, plan.scalars_host = self._scalars.data_ptr(), self._scalars_host.data_ptr()
         plan.large_list = S("large_list", n_upper // 1024 + 2).ptr
+
+    def _rebuild_step_fields(self, plan, step, par, tail):
+        """Fields of a rebuild plan that depend on the step: the guard, the rest of the rebuild step and
+        the batch behind it (every one of them is assigned, a reused plan keeps nothing)."""
+        plan.guard_word, plan.guard_step = None, 0
+        plan.p2g_params = plan.grid_params = plan.p2g_status = plan.grid_reset_status = None
+        plan.g2p_params = plan.g2p_status = plan.status_publish_dst = plan.status_event = None
+        plan.async_, plan.done_event = 0, None
         if self._guard_reset_in_rebuild or tail:
             # tail: nothing guarded is in flight (_rebuild_tail_ok), the word is reset by the call and
             # then guards the rest of the step and the next batch, so that an aborted rebuild (a
@@ -1305,7 +1402,14 @@ class CudaWorker:
                 self._plan_stale = True
             else:
                 next_n = 0
-        while True:
+        self._rebuild_next_n = next_n
+
+    def _rebuild_size(self, plan, par, want_g, want_groups, want_nodes, cap, tight, new_bufs, n_upper):
+        """Size the caller-owned buffers of a rebuild (4x growth rule) and describe them to the plan."""
+        st, tb, gr = self.store, self.table, self.grid
+        S = self._scratch_i32
+        scan = self._scratch["scan"]
+        if True:
             # block-indexed scratch and tables; codes/origin/touched sized for the worst case of the
             # dilation, 27 n_g (they are small)
             qslot, qflag = S("qslot", 27 * want_g), S("qflag", 2 * 27 * want_g)
@@ -1329,7 +1433,7 @@ class CudaWorker:
             plan.cap_gblocks = min(tb._neighbor.capacity, qslot.capacity // 27, qflag.capacity // 54,
                                    (bin_start.capacity - 1) // 64, bgf.capacity - 1,
                                    (scan.capacity - 2) * 16,     # 64 bins per block, 1024 per scan tile
-                                   max(2 * want_g, 64) if tight else _INT_MAX)
+                                   _pow2_at_least(max(2 * want_g, 64)) if tight else _INT_MAX)
             plan.hkeys, plan.hvals, plan.hfirst = tb._hkeys.ptr, tb._hvals.ptr, tb._hfirst.ptr
             plan.hash_cap = cap
             plan.cap_table = min(tb._codes.capacity, tb._origin.capacity, tb._touched[0].capacity,
@@ -1341,44 +1445,14 @@ class CudaWorker:
             plan.vel, plan.raw_par = gr._vel.ptr, gr._raw[par].ptr
             plan.touched_par = tb._touched[par].ptr
             plan.cap_nodes = min(gr._vel.capacity, gr._raw[par].capacity, gr._raw[1 - par].capacity,
-                                 max(2 * want_nodes, 256) if tight else _INT_MAX)
-            if next_n > 0:
-                self._plan_stale = True              # buffers may just have been grown
-                sp = self._step_plan()
-                sp.full_clear_first = 1              # step + 1 is the first use of the other parity
-                sp.transfer.dt_gather = float(self.dt)
-                for k in range(2 * next_n):
-                    sp.time_events[k] = None
-                plan.next_steps = C.addressof(sp)
-                plan.next_first_step, plan.next_n_steps = int(step) + 1, next_n
-            self.kernel_calls += 1
-            rc = lib.mpm_rebuild(C.byref(plan), C.byref(res), stream)
-            if flushed is not None:
-                self._consume(*flushed)      # the gather flushed just before this rebuild
-                flushed = None
-            if rc == 0 and plan.async_:
-                rc = lib.mpm_rebuild_wait(C.byref(plan), C.byref(res))
-            if rc == _capi.NEED_CAPACITY:
-                if res.need_hash:
-                    cap *= 4
-                want_g = max(want_g, res.need_gblocks, (res.need_table + 26) // 27)
-                want_groups = max(want_groups, res.need_groups)
-                want_nodes = max(want_nodes, res.need_nodes)
-                tight = False
-                continue
-            if rc == -2 and res.bad_particle != _INT_MAX:
-                raise SpatialDomainError(
-                    f"worker {self.wid}: particle {res.bad_particle} of the rebuild input lies outside "
-                    f"the encodable domain [0, 2^21) cells")
-            if rc == -2 and res.bad_block != _INT_MAX:
-                code = int(self._scratch["gcodes"].data[res.bad_block].item())
-                x, y, z = _decode(code)
-                raise SpatialDomainError(
-                    f"block ({x - CELL_BIAS // 4}, {y - CELL_BIAS // 4}, {z - CELL_BIAS // 4}) "
-                    f"touches the domain boundary; scenes must leave a one-block margin")
-            check(rc, "mpm_rebuild")
-            break
+                                 _pow2_at_least(max(2 * want_nodes, 256)) if tight else _INT_MAX)
+
+    def _rebuild_adopt(self, res, nxt, new_bufs, step, par, t_rebuild):
+        """Host bookkeeping of the tables a rebuild produced."""
+        st, tb, gr = self.store, self.table, self.grid
         n, n_g, count, G = res.n, res.n_gblocks, res.count, res.n_groups
+        self._ngroups_dev_valid[nxt] = True
+        self.rebuild_graph_replays += int(res.graph == 2)
         tb.n_gblocks, tb.count = n_g, count
         tb._codes.len = tb._origin.len = count
         tb._neighbor.len = n_g
