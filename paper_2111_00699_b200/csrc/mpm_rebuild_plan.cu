@@ -86,10 +86,10 @@ static int enqueue_rebuild_kernels(const mpm_rebuild_plan *p, int32_t *S, int gb
     if (rc != MPM_OK) return rc;
     // the counts, to the host: everything below keeps the device busy while the host waits for them
     cudaMemcpyAsync(p->scalars_host, S, 16 * sizeof(int32_t), cudaMemcpyDeviceToHost, stream);
-    if (p->done_event) {
-        if (capturing) cudaEventRecordWithFlags((cudaEvent_t)p->done_event, stream, cudaEventRecordExternal);
-        else cudaEventRecord((cudaEvent_t)p->done_event, stream);
-    }
+    // (a graph records the event behind its launch instead: an event-record NODE only turns the event
+    // pending when it executes, so a host that waits right after cudaGraphLaunch would find the
+    // previous rebuild's recording complete and read stale counts)
+    if (p->done_event && !capturing) cudaEventRecord((cudaEvent_t)p->done_event, stream);
     mpm_store_view ns = p->new_store;
     ns.n_groups = groups_bound;
     ns.n_groups_dev = S + 7;
@@ -187,6 +187,7 @@ static int rebuild_by_graph(const mpm_rebuild_plan *p, int32_t *S, int gblocks_b
         return MPM_ERR_RESOURCE;
     }
     launch_counter_add(hit->kernels);
+    if (p->done_event) cudaEventRecord((cudaEvent_t)p->done_event, stream);
     return MPM_OK;
 }
 }  // namespace mpm

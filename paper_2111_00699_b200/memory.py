@@ -24,6 +24,8 @@ def grown_capacity(capacity: int, requested: int) -> int:
 class DeviceBuffer:
     """Typed device array, `data[:len]` live; contents up to len survive a reallocation."""
 
+    generation = 0      # bumped by every (re)allocation of any buffer of the process: "has a pointer moved?" in O(1)
+
     def __init__(self, dtype, element_shape=(), device="cuda", capacity: int = 0):
         self.dtype = dtype
         self.element_shape = tuple(element_shape)
@@ -50,6 +52,7 @@ class DeviceBuffer:
             self.data = fresh
             self.capacity = new_cap
             self.realloc_count += 1
+            DeviceBuffer.generation += 1
         return self
 
     def resize(self, new_len: int, keep: bool = True) -> torch.Tensor:

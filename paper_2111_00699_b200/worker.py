@@ -442,6 +442,7 @@ class CudaBlockTable:
                 b.data = torch.empty(cap, dtype=b.dtype, device=self.device)
                 b.capacity = cap
                 b.realloc_count += 1
+                DeviceBuffer.generation += 1
         self.hash_cap = cap
 
     def view(self) -> TableView:
@@ -624,10 +625,16 @@ class CudaWorker:
         self.kernel_calls = 0
         self._tail_done = False
         self._tail_g2p_done = False
-        self.rebuild_graph = True     # replay the rebuild kernels as a CUDA graph when nothing changed shape
-        self.rebuild_graph_max = 600_000   # ... up to this many particles (beyond, the chain is device-bound)
+        # Opt-in: replay the rebuild kernels as a CUDA graph once the scene is in steady state (same
+        # particle count, no buffer moved for four rebuilds).  Measured (profiles/experiments/README.md):
+        # the host's part of a rebuild at 64 K particles falls from ~130 to ~40 us, the frame by 0-7 %;
+        # nothing at 171 K and above (the chain is device-bound there), and a scene whose count keeps
+        # changing (fountain: emitter + sink) pays for captures it never reuses.  Off by default.
+        self.rebuild_graph = False
+        self.rebuild_graph_max = 200_000   # ... up to this many particles
         self.rebuild_graph_replays = 0
         self._rb_cache = {}           # store half -> (key, plan, result) of the last rebuild out of it
+        self._rb_shape, self._rb_stable = None, 0
         self._rebuild_next_n = 0
         self._rebuild_next = 0        # steps mpm_rebuild may enqueue behind the rebuild step (frame drivers)
         self._rebuild_enqueued = 0    # ... and how many it did
@@ -1261,16 +1268,28 @@ class CudaWorker:
         # buffer reallocated since (only the step-dependent fields below are refreshed).  Its launch
         # bounds may then be older than the counts; a count that outgrew one aborts on the device and
         # comes back through the sizing below, like any other.
-        ck = (st.cur, n_upper, self.realloc_count) \
-            if (n_staged == 0 and st.n_groups > 0 and self._ngroups_dev_valid[st.cur]) else None
+        # graph replay only for a scene in steady state (same particle count, no buffer moved over the
+        # last rebuilds): a scene whose count changes all the time (emitter, sink) would capture a
+        # graph per shape and never reuse it.  `by_capacity`: the old store described by the capacity
+        # of its buffers and its count on the device (what makes the chain replayable) -- only then,
+        # since it also launches the compaction over the whole capacity.
+        shape = (n_upper, n_staged, DeviceBuffer.generation)
+        self._rb_stable = self._rb_stable + 1 if shape == self._rb_shape else 0
+        self._rb_shape = shape
+        by_capacity = bool(self.rebuild_graph and n_staged == 0 and n_upper <= self.rebuild_graph_max
+                           and self._rb_stable >= 3 and st.n_groups > 0 and self._ngroups_dev_valid[st.cur])
+        use_graph = by_capacity and self._rb_stable >= 4
+        # (a plan that states the old store's group count by value is good for that rebuild only)
+        ck = (st.cur, n_upper, DeviceBuffer.generation, tb.hash_cap) if by_capacity else None
         cached = self._rb_cache.get(st.cur) if ck is not None else None
         fast = cached is not None and cached[0] == ck
         if fast:
             plan, res = cached[1], cached[2]
         else:
             plan, res = _capi.RebuildPlan(), _capi.RebuildResult()
-            self._rebuild_static_fields(plan, st, nxt, n_upper, n_staged, staged, staged_ids)
+            self._rebuild_static_fields(plan, st, nxt, n_upper, n_staged, staged, staged_ids, by_capacity)
         cur_before = st.cur
+        plan.use_graph = int(use_graph)
         self._rebuild_step_fields(plan, step, par, tail)
         next_n = self._rebuild_next_n
         while True:
@@ -1320,24 +1339,24 @@ class CudaWorker:
             check(rc, "mpm_rebuild")
             break
         self._rebuild_adopt(res, nxt, new_bufs, step, par, t_rebuild)
-        if n_staged == 0:
-            self._rb_cache[cur_before] = ((cur_before, n_upper, self.realloc_count), plan, res)
+        if by_capacity:
+            self._rb_cache[cur_before] = ((cur_before, n_upper, DeviceBuffer.generation, tb.hash_cap), plan, res)
 
-    def _rebuild_static_fields(self, plan, st, nxt, n_upper, n_staged, staged, staged_ids):
+    def _rebuild_static_fields(self, plan, st, nxt, n_upper, n_staged, staged, staged_ids, by_capacity):
         """Fields of a rebuild plan that only change with the buffers, the particle count or staging."""
         S, S64 = self._scratch_i32, self._scratch_i64
         plan.old_store = st.view()
         old_bufs = [b[st.cur] for b in (st._data, st._orig_id, st._lane_meta, st._group_len, st._group_block,
                                         st._group_start, st._group_ctx)]
         old_bound = st.n_groups
-        if st.n_groups > 0 and self._ngroups_dev_valid[st.cur]:
+        if by_capacity:
             # the old store by its CAPACITY, its count read on the device: the chain then looks the
             # same from one rebuild to the next (mpm_rebuild replays it as a graph)
             old_bound = min(b.capacity for b in old_bufs)
             plan.old_store.n_groups = old_bound
             plan.old_store.n_groups_dev = self._ngroups_dev.data_ptr() + 4 * st.cur
         plan.n_groups_out = self._ngroups_dev.data_ptr() + 4 * nxt
-        plan.use_graph = int(self.rebuild_graph and n_staged == 0 and n_upper <= self.rebuild_graph_max)
+        plan.use_graph = 0        # set per call (_rebuild): only once the shape has been stable for a while
         plan.n_staged, plan.n_upper = n_staged, n_upper
         plan.staged = staged.data_ptr() if n_staged else None
         plan.staged_ids = staged_ids.data_ptr() if n_staged else None

@@ -242,6 +242,35 @@ def test_whole_frame_of_the_64k_scene_against_the_oracle():
         assert wc.store.total_mass() == pytest.approx(64000 * W.particle_mass, rel=1e-6)
 
 
+def test_rebuild_chain_replayed_as_a_cuda_graph_keeps_the_result():
+    """Opt-in CudaWorker.rebuild_graph: once the 64 K scene is in steady state the rebuild kernels are
+    captured and replayed as a CUDA graph (old store described by capacity + device count, plan of the
+    last rebuild reused).  Six frames with it against six frames without: same rebuild steps, same
+    particle count at every rebuild, state within the run bars (the graph replays the same kernels on
+    the same data; only launch boundaries differ)."""
+    from paper_2111_00699_b200 import scenes
+    W = scenes.sand_blocks(l=20, boxes=1)
+    f32r = lambda a: np.asarray(a, dtype=np.float64).astype(np.float32).astype(np.float64)
+    W.positions, W.velocities = f32r(W.positions), f32r(W.velocities)
+    ws = []
+    for graph in (False, True):
+        w = _worker(W, transfer="g2p2g")
+        w.rebuild_graph = graph
+        for _ in range(6):
+            w.run_frame()
+        ws.append(w)
+    plain, graphed = ws
+    assert graphed.rebuild_graph_replays >= 1 and plain.rebuild_graph_replays == 0
+    assert graphed.rebuild_steps == plain.rebuild_steps and len(plain.rebuild_steps) >= 8
+    assert graphed.store.count == plain.store.count == 64000
+    edge = float(W.positions.max() - W.positions.min())
+    ex, ev, ef, _ = U.particle_errors(U.state_by_id(graphed), U.state_by_id(plain), edge, 9)
+    print("64 K scene, six frames, rebuild graph replays %d of %d rebuilds: x %.2e v %.2e F %.2e vs kernel-by-kernel"
+          % (graphed.rebuild_graph_replays, len(graphed.rebuild_steps), ex, ev, ef))
+    assert ex <= U.X_RTOL_RUN and ev <= U.V_RTOL_RUN and ef <= U.F_ATOL_RUN
+    assert graphed.store.total_mass() == pytest.approx(64000 * W.particle_mass, rel=1e-6)
+
+
 def test_one_substep_of_the_389k_scene_against_the_oracle():
     """configs[3] sweep point (sand_blocks l=23 boxes=4: 389 344 particles): rebuild + 2 substeps."""
     from paper_2111_00699_b200 import scenes
