@@ -1279,10 +1279,17 @@ class CudaWorker:
         by_capacity = bool(self.rebuild_graph and n_staged == 0 and n_upper <= self.rebuild_graph_max
                            and self._rb_stable >= 3 and st.n_groups > 0 and self._ngroups_dev_valid[st.cur])
         use_graph = by_capacity and self._rb_stable >= 4
-        # (a plan that states the old store's group count by value is good for that rebuild only)
-        ck = (st.cur, n_upper, DeviceBuffer.generation, tb.hash_cap) if by_capacity else None
+        ck = (st.cur, n_upper, DeviceBuffer.generation, tb.hash_cap, by_capacity) \
+            if (n_staged == 0 and st.n_groups > 0) else None
         cached = self._rb_cache.get(st.cur) if ck is not None else None
         fast = cached is not None and cached[0] == ck
+        if fast and not by_capacity:
+            # the reused plan states the old store's group count by value: refresh it (and make sure
+            # the compaction scratch, sized for the count of the rebuild the plan was made for, holds it)
+            if self._scratch["glive"].capacity < st.n_groups + 1:
+                fast = False
+            else:
+                cached[1].old_store.n_groups = st.n_groups
         if fast:
             plan, res = cached[1], cached[2]
         else:
@@ -1339,8 +1346,9 @@ class CudaWorker:
             check(rc, "mpm_rebuild")
             break
         self._rebuild_adopt(res, nxt, new_bufs, step, par, t_rebuild)
-        if by_capacity:
-            self._rb_cache[cur_before] = ((cur_before, n_upper, DeviceBuffer.generation, tb.hash_cap), plan, res)
+        if n_staged == 0:
+            self._rb_cache[cur_before] = ((cur_before, n_upper, DeviceBuffer.generation, tb.hash_cap, by_capacity),
+                                          plan, res)
 
     def _rebuild_static_fields(self, plan, st, nxt, n_upper, n_staged, staged, staged_ids, by_capacity):
         """Fields of a rebuild plan that only change with the buffers, the particle count or staging."""
@@ -1428,43 +1436,42 @@ class CudaWorker:
         st, tb, gr = self.store, self.table, self.grid
         S = self._scratch_i32
         scan = self._scratch["scan"]
-        if True:
-            # block-indexed scratch and tables; codes/origin/touched sized for the worst case of the
-            # dilation, 27 n_g (they are small)
-            qslot, qflag = S("qslot", 27 * want_g), S("qflag", 2 * 27 * want_g)
-            bin_start, bgf = S("bin_start", want_g * 64 + 1), S("bgf", want_g + 1)
-            tb.ensure_hash(cap)
-            tb._codes.ensure_capacity(27 * want_g, keep=False)
-            tb._origin.ensure_capacity(27 * want_g, keep=False)
-            tb._neighbor.ensure_capacity(want_g, keep=False)
-            for k in (0, 1):
-                tb._touched[k].len = min(tb._touched[k].len, tb.count)
-                tb._touched[k].ensure_capacity(27 * want_g, keep=True)
-            for buf in new_bufs:
-                buf.ensure_capacity(want_groups, keep=False)
-            gr._vel.ensure_capacity(want_nodes, keep=False)
-            gr._raw[par].ensure_capacity(want_nodes, keep=False)
-            gr._raw[1 - par].ensure_capacity(want_nodes, keep=False)   # next step's parity: cleared in full there
-            plan.qslot, plan.qflag, plan.bin_start, plan.bgf = qslot.ptr, qflag.ptr, bin_start.ptr, bgf.ptr
-            # Capacities double as launch bounds (the counts are read on the device).  The 4x growth
-            # rule leaves them up to 4x the real counts; twice the last counts is what a first attempt
-            # launches over, the full capacity only after a count outgrew that.
-            plan.cap_gblocks = min(tb._neighbor.capacity, qslot.capacity // 27, qflag.capacity // 54,
-                                   (bin_start.capacity - 1) // 64, bgf.capacity - 1,
-                                   (scan.capacity - 2) * 16,     # 64 bins per block, 1024 per scan tile
-                                   _pow2_at_least(max(2 * want_g, 64)) if tight else _INT_MAX)
-            plan.hkeys, plan.hvals, plan.hfirst = tb._hkeys.ptr, tb._hvals.ptr, tb._hfirst.ptr
-            plan.hash_cap = cap
-            plan.cap_table = min(tb._codes.capacity, tb._origin.capacity, tb._touched[0].capacity,
-                                 tb._touched[1].capacity)
-            plan.table_codes, plan.table_origin = tb._codes.ptr, tb._origin.ptr
-            plan.table_neighbor = tb._neighbor.ptr
-            plan.new_store = StoreView(*(b.ptr for b in new_bufs[:6]), 0, st.nch, new_bufs[6].ptr)
-            plan.cap_groups = min(b.capacity for b in new_bufs)
-            plan.vel, plan.raw_par = gr._vel.ptr, gr._raw[par].ptr
-            plan.touched_par = tb._touched[par].ptr
-            plan.cap_nodes = min(gr._vel.capacity, gr._raw[par].capacity, gr._raw[1 - par].capacity,
-                                 _pow2_at_least(max(2 * want_nodes, 256)) if tight else _INT_MAX)
+        # block-indexed scratch and tables; codes/origin/touched sized for the worst case of the
+        # dilation, 27 n_g (they are small)
+        qslot, qflag = S("qslot", 27 * want_g), S("qflag", 2 * 27 * want_g)
+        bin_start, bgf = S("bin_start", want_g * 64 + 1), S("bgf", want_g + 1)
+        tb.ensure_hash(cap)
+        tb._codes.ensure_capacity(27 * want_g, keep=False)
+        tb._origin.ensure_capacity(27 * want_g, keep=False)
+        tb._neighbor.ensure_capacity(want_g, keep=False)
+        for k in (0, 1):
+            tb._touched[k].len = min(tb._touched[k].len, tb.count)
+            tb._touched[k].ensure_capacity(27 * want_g, keep=True)
+        for buf in new_bufs:
+            buf.ensure_capacity(want_groups, keep=False)
+        gr._vel.ensure_capacity(want_nodes, keep=False)
+        gr._raw[par].ensure_capacity(want_nodes, keep=False)
+        gr._raw[1 - par].ensure_capacity(want_nodes, keep=False)   # next step's parity: cleared in full there
+        plan.qslot, plan.qflag, plan.bin_start, plan.bgf = qslot.ptr, qflag.ptr, bin_start.ptr, bgf.ptr
+        # Capacities double as launch bounds (the counts are read on the device).  The 4x growth
+        # rule leaves them up to 4x the real counts; twice the last counts is what a first attempt
+        # launches over, the full capacity only after a count outgrew that.
+        plan.cap_gblocks = min(tb._neighbor.capacity, qslot.capacity // 27, qflag.capacity // 54,
+                               (bin_start.capacity - 1) // 64, bgf.capacity - 1,
+                               (scan.capacity - 2) * 16,     # 64 bins per block, 1024 per scan tile
+                               _pow2_at_least(max(2 * want_g, 64)) if tight else _INT_MAX)
+        plan.hkeys, plan.hvals, plan.hfirst = tb._hkeys.ptr, tb._hvals.ptr, tb._hfirst.ptr
+        plan.hash_cap = cap
+        plan.cap_table = min(tb._codes.capacity, tb._origin.capacity, tb._touched[0].capacity,
+                             tb._touched[1].capacity)
+        plan.table_codes, plan.table_origin = tb._codes.ptr, tb._origin.ptr
+        plan.table_neighbor = tb._neighbor.ptr
+        plan.new_store = StoreView(*(b.ptr for b in new_bufs[:6]), 0, st.nch, new_bufs[6].ptr)
+        plan.cap_groups = min(b.capacity for b in new_bufs)
+        plan.vel, plan.raw_par = gr._vel.ptr, gr._raw[par].ptr
+        plan.touched_par = tb._touched[par].ptr
+        plan.cap_nodes = min(gr._vel.capacity, gr._raw[par].capacity, gr._raw[1 - par].capacity,
+                             _pow2_at_least(max(2 * want_nodes, 256)) if tight else _INT_MAX)
 
     def _rebuild_adopt(self, res, nxt, new_bufs, step, par, t_rebuild):
         """Host bookkeeping of the tables a rebuild produced."""
