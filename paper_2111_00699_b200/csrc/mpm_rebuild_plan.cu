@@ -19,6 +19,8 @@
 #include <stdlib.h>
 #include <string.h>
 
+#include <mutex>
+
 #include "mpm_common.cuh"
 
 namespace mpm {
@@ -115,6 +117,9 @@ static int rebuild_by_graph(const mpm_rebuild_plan *p, int32_t *S, int gblocks_b
                             int nodes_bound, cudaStream_t stream, int *how)
 {
     *how = 0;
+    // worker handles may be driven from different host threads: the cache and the capture stream are shared
+    static std::mutex lock;
+    std::lock_guard<std::mutex> hold(lock);
     if (!graphs_enabled() || p->n_staged != 0) return MPM_OK;
     mpm_rebuild_plan key;
     graph_key(p, &key);
