@@ -387,6 +387,75 @@ def _state_on_device(w: CudaWorker):
     return flat[:n], ids[:n], where[:n]
 
 
+def migrate_rows(rt: DistRuntime, flat: torch.Tensor, ids: torch.Tensor, alive: torch.Tensor, nch: int,
+                 tol: float = 0.10, force: bool = False, bins: int = REPARTITION_BINS):
+    """The collective part of a re-partition, on whatever device the tensors live (CUDA per rank, or CPU
+    tensors under gloo in the tests): agree on the longest axis of the global bounding box, histogram,
+    cut (plan_slabs), tell every rank how many rows it gets from whom, and exchange rows + ids.
+
+    flat [n, nch] float32 particle rows (positions in columns 0:3), ids [n] int64, alive [n] bool (rows
+    that may move).  Returns None when nothing has to move, else a dict:
+      leaving [n] bool, rows / row_ids (what arrived here, concatenated in rank order), before / after
+      (per-rank counts), axis."""
+    n_ranks = rt.n_workers
+    dev = flat.device
+    pos = flat[:, 0:3].to(torch.float64)
+    big = 1e300
+    any_alive = bool(alive.any()) if len(ids) else False
+    lo = pos[alive].min(dim=0).values.cpu().numpy() if any_alive else np.full(3, big)
+    hi = pos[alive].max(dim=0).values.cpu().numpy() if any_alive else np.full(3, -big)
+    n_alive = int(alive.sum().item()) if len(ids) else 0
+    # bounding box and counts of everybody (float64 bit patterns through the int64 exchange)
+    info = rt.all_gather_i64([int(np.float64(x).view(np.int64)) for x in list(lo) + list(hi)] + [n_alive, nch])
+    los = info[:, 0:3].copy().view(np.float64)
+    his = info[:, 3:6].copy().view(np.float64)
+    counts = info[:, 6].astype(np.int64)
+    if not (info[:, 7] == nch).all():
+        from .errors import ConfigError
+        raise ConfigError("re-partitioning moves particles between ranks of ONE material population")
+    total = int(counts.sum())
+    if total == 0:
+        return None
+    mean = total / n_ranks
+    if not force and float(np.abs(counts - mean).max()) <= tol * mean:
+        return None
+    glo, ghi = los.min(axis=0), his.max(axis=0)
+    axis = int(np.argmax(ghi - glo))
+    width = max(float(ghi[axis] - glo[axis]), 1e-300)
+    # histogram of my particles, cut of the global one
+    b = torch.clamp(((pos[:, axis] - glo[axis]) * (bins / width)).to(torch.int64), 0, bins - 1)
+    hist = torch.bincount(b[alive], minlength=bins).cpu().numpy() if n_alive else np.zeros(bins, np.int64)
+    ghist = rt._all_gather_i64_dist(hist.tolist()).sum(axis=0)
+    dest = torch.from_numpy(plan_slabs(ghist, n_ranks)).to(dev)[b]
+    dest[~alive] = rt.wid
+    leaving = dest != rt.wid
+    # who sends how many to whom
+    out_counts = torch.bincount(dest[leaving], minlength=n_ranks).cpu().numpy()
+    table = rt.all_gather_i64(out_counts.tolist()) if n_ranks <= _capi.SHM_MAX_VALUES else \
+        rt._all_gather_i64_dist(out_counts.tolist())
+    send_rows, send_ids, recv_rows, recv_ids = {}, {}, {}, {}
+    for q in range(n_ranks):
+        if q == rt.wid:
+            continue
+        if out_counts[q]:
+            sel = dest == q
+            send_rows[q] = flat[sel].contiguous()
+            send_ids[q] = ids[sel].contiguous()
+        k = int(table[q, rt.wid])
+        if k:
+            recv_rows[q] = torch.empty((k, nch), dtype=torch.float32, device=dev)
+            recv_ids[q] = torch.empty(k, dtype=torch.int64, device=dev)
+    if dev.type == "cuda":
+        torch.cuda.current_stream().synchronize()
+    rt.exchange_rows(send_rows, recv_rows)
+    rt.exchange_rows(send_ids, recv_ids)
+    rows = torch.cat([recv_rows[q] for q in sorted(recv_rows)]) if recv_rows else flat[:0]
+    row_ids = torch.cat([recv_ids[q] for q in sorted(recv_ids)]) if recv_ids else ids[:0]
+    after = counts - table.sum(axis=1) + table.sum(axis=0)
+    return {"leaving": leaving, "rows": rows, "row_ids": row_ids, "axis": axis,
+            "before": counts.tolist(), "after": after.tolist()}
+
+
 def repartition(w: "DistWorker", tol: float = 0.10, force: bool = False, bins: int = REPARTITION_BINS):
     """Collective, between frames.  Re-cut the slabs along the longest axis of the CURRENT particle
     positions and migrate the particles whose slab now belongs to another rank.
@@ -401,8 +470,6 @@ def repartition(w: "DistWorker", tol: float = 0.10, force: bool = False, bins: i
     are preserved, the total mass is unchanged, and the step sequence continues with a rebuild
     on every rank.  Nothing moves unless `force` or some rank's count is more than `tol` away
     from the mean.  Returns a dict of counts (before, after, sent, received) or None."""
-    rt = w.runtime
-    n_ranks = rt.n_workers
     with torch.cuda.device(w.device):
         if w._pending_gather:
             w._flush_gather()
@@ -411,57 +478,11 @@ def repartition(w: "DistWorker", tol: float = 0.10, force: bool = False, bins: i
         alive = torch.ones(len(ids), dtype=torch.bool, device=w.device)
         if len(ids):
             alive = (meta[where].to(torch.int32) & 0x8000) == 0      # quarantined / sunk lanes stay put
-        pos = flat[:, 0:3].to(torch.float64)
-        big = 1e300
-        lo = pos[alive].min(dim=0).values.cpu().numpy() if bool(alive.any()) else np.full(3, big)
-        hi = pos[alive].max(dim=0).values.cpu().numpy() if bool(alive.any()) else np.full(3, -big)
-        n_alive = int(alive.sum().item())
-        # bounding box and counts of everybody (float64 bit patterns through the int64 exchange)
-        info = rt.all_gather_i64([int(np.float64(x).view(np.int64)) for x in list(lo) + list(hi)]
-                                 + [n_alive, w.store.nch])
-        los = info[:, 0:3].copy().view(np.float64)
-        his = info[:, 3:6].copy().view(np.float64)
-        counts = info[:, 6].astype(np.int64)
-        if not (info[:, 7] == w.store.nch).all():
-            from .errors import ConfigError
-            raise ConfigError("re-partitioning moves particles between ranks of ONE material population")
-        total = int(counts.sum())
-        if total == 0:
+        mig = migrate_rows(w.runtime, flat, ids, alive, w.store.nch, tol=tol, force=force, bins=bins)
+        if mig is None:
             return None
-        mean = total / n_ranks
-        if not force and float(np.abs(counts - mean).max()) <= tol * mean:
-            return None
-        glo, ghi = los.min(axis=0), his.max(axis=0)
-        axis = int(np.argmax(ghi - glo))
-        width = max(float(ghi[axis] - glo[axis]), 1e-300)
-        # histogram of my particles, cut of the global one
-        b = torch.clamp(((pos[:, axis] - glo[axis]) * (bins / width)).to(torch.int64), 0, bins - 1)
-        hist = torch.bincount(b[alive], minlength=bins).cpu().numpy() if n_alive else np.zeros(bins, np.int64)
-        ghist = rt._all_gather_i64_dist(hist.tolist()).sum(axis=0)
-        dest_of_bin = torch.from_numpy(plan_slabs(ghist, n_ranks)).to(w.device)
-        dest = dest_of_bin[b]
-        dest[~alive] = rt.wid
-        leaving = dest != rt.wid
-        # who sends how many to whom
-        out_counts = torch.bincount(dest[leaving], minlength=n_ranks).cpu().numpy()
-        table = rt.all_gather_i64(out_counts.tolist()) if n_ranks <= _capi.SHM_MAX_VALUES else \
-            rt._all_gather_i64_dist(out_counts.tolist())
-        send_rows, send_ids, recv_rows, recv_ids = {}, {}, {}, {}
-        for q in range(n_ranks):
-            if q == rt.wid:
-                continue
-            if out_counts[q]:
-                sel = dest == q
-                send_rows[q] = flat[sel].contiguous()
-                send_ids[q] = ids[sel].contiguous()
-            k = int(table[q, rt.wid])
-            if k:
-                recv_rows[q] = torch.empty((k, w.store.nch), dtype=torch.float32, device=w.device)
-                recv_ids[q] = torch.empty(k, dtype=torch.int64, device=w.device)
-        torch.cuda.current_stream().synchronize()
-        rt.exchange_rows(send_rows, recv_rows)
-        rt.exchange_rows(send_ids, recv_ids)
-        n_out, n_in = int(leaving.sum().item()), int(sum(len(t) for t in recv_ids.values()))
+        leaving = mig["leaving"]
+        n_out, n_in = int(leaving.sum().item()), int(len(mig["row_ids"]))
         if n_out:
             # leave like a sunk particle: flagged, massless, id -1 (dropped by the next compaction)
             st = w.store
@@ -473,8 +494,7 @@ def repartition(w: "DistWorker", tol: float = 0.10, force: bool = False, bins: i
             st._orig_id[st.cur].data.view(-1)[gone] = -1
             st.has_sink = True
         if n_in:
-            rows = torch.cat([recv_rows[q] for q in sorted(recv_rows)]).cpu().numpy()
-            rid = torch.cat([recv_ids[q] for q in sorted(recv_ids)]).cpu().numpy()
+            rows, rid = mig["rows"].cpu().numpy(), mig["row_ids"].cpu().numpy()
             w.store.stage_append(rows[:, 0:3], rows[:, 3:6], rows[:, 15].copy(), deformation=rows[:, 16:],
                                  affine=rows[:, 6:15], ids=rid)
         # every rank rebuilds on the next step (SPMD), whether or not its own population changed
@@ -483,40 +503,8 @@ def repartition(w: "DistWorker", tol: float = 0.10, force: bool = False, bins: i
         w._clock_valid = False
         if hasattr(w, "_need_collective"):
             w._need_collective = True
-        after = counts - table.sum(axis=1) + table.sum(axis=0)
-        return {"axis": axis, "before": counts.tolist(), "after": after.tolist(), "sent": n_out, "received": n_in}
-
-
-# --------------------------------------------------------------------------------------
-# material populations over ranks (BASELINE.json configs[4]: mixed snow / sand on 8 GPUs)
-# --------------------------------------------------------------------------------------
-def population_layout(rank: int, world: int, n_populations: int):
-    """Which (population, slab, n_slabs) a rank holds when `n_populations` material populations
-    are spread over `world` ranks: ranks p, p + n_populations, ... hold the slabs of population p.
-    One logical worker (one material, one block table) per process, as everywhere else; a GPU
-    that is to carry several populations runs one process per population (the peer-mapped
-    transport maps the tables of processes on one device like those of another device), and
-    the populations meet on the grid through the same halo reduction as the slabs do
-    (pipeline.py:1172-1188)."""
-    if n_populations < 1 or world % n_populations:
-        from .errors import ConfigError
-        raise ConfigError(f"{world} ranks cannot hold {n_populations} populations in equal numbers of slabs")
-    return rank % n_populations, rank // n_populations, world // n_populations
-
-
-def seed_population_rank(worker: "DistWorker", populations):
-    """Seed this rank's slab of its population.  `populations`: sequence of objects with
-    .positions / .velocities / .particle_mass (scenes.Population); ids are consecutive ranges in
-    population order, as CudaCluster.seed_populations numbers them.  Returns the global ids."""
-    rt = worker.runtime
-    p, slab, n_slabs = population_layout(rt.wid, rt.n_workers, len(populations))
-    pop = populations[p]
-    base = int(sum(len(q.positions) for q in populations[:p]))
-    part = partition_particles(pop.positions, n_slabs)[slab]
-    if len(part):
-        worker.seed_particles(np.asarray(pop.positions)[part], np.asarray(pop.velocities)[part],
-                              pop.particle_mass, ids=part + base)
-    return part + base
+        return {"axis": mig["axis"], "before": mig["before"], "after": mig["after"], "sent": n_out,
+                "received": n_in}
 
 
 def seed_rank(worker: DistWorker, positions, velocities, mass):

@@ -124,3 +124,67 @@ def test_build_halo_lists_orders_by_receiver_index():
     send_idx, recv_pos = build_halo_lists(pm)
     assert send_idx.tolist() == [2, 4, 1]              # peer indices 2, 5, 7 ascending
     assert recv_pos.tolist() == [-1, 0, 1, -1, 2]      # rows arrive in OUR ascending order
+
+
+# ---- dynamic re-partitioning: the collective part on CPU tensors ------------------------------------
+def _migrate_worker(rank, world, port, q):
+    try:
+        sys.path.insert(0, ROOT)
+        os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port), RANK=str(rank), WORLD_SIZE=str(world))
+        dist.init_process_group("gloo", rank=rank, world_size=world)
+        from paper_2111_00699_b200.dist import DistRuntime, migrate_rows
+        rt = DistRuntime("cpu")
+        nch, n = 25, 3000
+        rng = np.random.default_rng(11)                       # every rank draws the SAME global scene
+        pos = rng.random((n, 3)) * np.array([10.0, 3.0, 2.0])  # longest axis: x
+        owner = np.minimum((rng.random(n) ** 2 * world).astype(np.int64), world - 1)   # skewed, interleaved
+        mine = np.flatnonzero(owner == rank)
+        flat = torch.zeros((len(mine), nch), dtype=torch.float32)
+        flat[:, 0:3] = torch.from_numpy(pos[mine]).float()
+        flat[:, 15] = 1.0 + torch.from_numpy(mine % 7).float()                 # "mass": travels with the row
+        ids = torch.from_numpy(mine)
+        alive = torch.ones(len(mine), dtype=torch.bool)
+        if len(mine):
+            alive[0] = False                                   # a quarantined lane never moves
+        assert migrate_rows(rt, flat, ids, alive, nch, tol=10.0) is None      # inside the tolerance: nothing moves
+        mig = migrate_rows(rt, flat, ids, alive, nch, force=True, bins=1024)
+        assert mig is not None and mig["axis"] == 0 and sum(mig["before"]) == sum(mig["after"])
+        assert not bool(mig["leaving"][0]) if len(mine) else True
+        keep = ~mig["leaving"]
+        new_ids = torch.cat([ids[keep], mig["row_ids"]]).numpy()
+        new_rows = torch.cat([flat[keep], mig["rows"]]).numpy()
+        assert len(new_ids) == mig["after"][rank] + int((~alive).sum())     # counts are of the movable rows
+        # every row still carries the state of its id
+        assert np.allclose(new_rows[:, 0:3], pos[new_ids].astype(np.float32))
+        assert np.array_equal(new_rows[:, 15], (1.0 + new_ids % 7).astype(np.float32))
+        q.put((rank, "ok", (new_ids.tolist(), float(new_rows[1:, 0].min()) if len(new_rows) > 1 else 0.0,
+                            float(new_rows[1:, 0].max()) if len(new_rows) > 1 else 0.0, mig["after"])))
+        dist.barrier()
+        dist.destroy_process_group()
+    except Exception:  # noqa
+        import traceback
+        q.put((rank, "fail", traceback.format_exc()))
+
+
+@pytest.mark.parametrize("world", [2, 3])
+def test_repartition_exchange_on_cpu(world):
+    """dist.migrate_rows under gloo: ids preserved (each exactly once), counts balanced to a histogram
+    bin, slabs ordered along the longest axis, rows keep their state, stuck rows stay."""
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_migrate_worker, args=(r, world, port, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    results = sorted(q.get(timeout=180) for _ in procs)
+    for p in procs:
+        p.join(timeout=60)
+    for rank, status, info in results:
+        assert status == "ok", info
+    all_ids = sorted(i for _, _, info in results for i in info[0])
+    assert all_ids == list(range(3000))
+    after = results[0][2][3]
+    assert max(after) - min(after) <= 0.05 * 3000 + world      # a bin of 1/1024 of the range + the stuck rows
+    # slabs do not interleave (the one stuck row per rank aside): rank r's range ends where r + 1's begins
+    for (_, _, a), (_, _, b) in zip(results[:-1], results[1:]):
+        assert a[2] <= b[1] + 10.0 / 1024 + 1e-6
