@@ -507,6 +507,38 @@ def repartition(w: "DistWorker", tol: float = 0.10, force: bool = False, bins: i
                 "received": n_in}
 
 
+# --------------------------------------------------------------------------------------
+# material populations over ranks (BASELINE.json configs[4]: mixed snow / sand on 8 GPUs)
+# --------------------------------------------------------------------------------------
+def population_layout(rank: int, world: int, n_populations: int):
+    """Which (population, slab, n_slabs) a rank holds when `n_populations` material populations
+    are spread over `world` ranks: ranks p, p + n_populations, ... hold the slabs of population p.
+    One logical worker (one material, one block table) per process, as everywhere else; a GPU
+    that is to carry several populations runs one process per population (the peer-mapped
+    transport maps the tables of processes on one device like those of another device), and
+    the populations meet on the grid through the same halo reduction as the slabs do
+    (pipeline.py:1172-1188)."""
+    if n_populations < 1 or world % n_populations:
+        from .errors import ConfigError
+        raise ConfigError(f"{world} ranks cannot hold {n_populations} populations in equal numbers of slabs")
+    return rank % n_populations, rank // n_populations, world // n_populations
+
+
+def seed_population_rank(worker: "DistWorker", populations):
+    """Seed this rank's slab of its population.  `populations`: sequence of objects with
+    .positions / .velocities / .particle_mass (scenes.Population); ids are consecutive ranges in
+    population order, as CudaCluster.seed_populations numbers them.  Returns the global ids."""
+    rt = worker.runtime
+    p, slab, n_slabs = population_layout(rt.wid, rt.n_workers, len(populations))
+    pop = populations[p]
+    base = int(sum(len(q.positions) for q in populations[:p]))
+    part = partition_particles(pop.positions, n_slabs)[slab]
+    if len(part):
+        worker.seed_particles(np.asarray(pop.positions)[part], np.asarray(pop.velocities)[part],
+                              pop.particle_mass, ids=part + base)
+    return part + base
+
+
 def seed_rank(worker: DistWorker, positions, velocities, mass):
     """bench.py:434-439 of the reference: rank r takes the r-th slab of the partition; ids are
     the indices into the global arrays."""

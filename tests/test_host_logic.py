@@ -274,3 +274,17 @@ def test_plan_slabs_cuts_the_global_histogram_into_equal_shares():
     assert len(set(plan_slabs(one, 4)[5:6].tolist())) == 1
     with pytest.raises(ValueError):
         plan_slabs(np.ones(4), 0)
+
+
+def test_population_layout_and_dist_surface():
+    """The multi-rank helpers the GPU tests and bench.py import exist (a refactor once dropped two of
+    them), and populations are dealt to ranks round-robin: rank r holds slab r // P of population r % P."""
+    from paper_2111_00699_b200 import dist as D
+    for name in ("DistRuntime", "DistWorker", "seed_rank", "plan_slabs", "migrate_rows", "repartition",
+                 "population_layout", "seed_population_rank", "build_halo_lists"):
+        assert callable(getattr(D, name)), name
+    assert [D.population_layout(r, 4, 2) for r in range(4)] == [(0, 0, 2), (1, 0, 2), (0, 1, 2), (1, 1, 2)]
+    assert D.population_layout(5, 8, 1) == (0, 5, 8)
+    from paper_2111_00699_b200.errors import ConfigError
+    with pytest.raises(ConfigError):
+        D.population_layout(0, 3, 2)
