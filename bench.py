@@ -334,9 +334,11 @@ def run_ours(args):
                   # particle store (the reference flushes at every frame end, pipeline.py:877-880)
                   "lazy_flush": bool(getattr(w, "lazy_flush", False)),
                   "fuse_clear": world == 1,
-                  "l2_policy": "inputs larger than L2: "
-                               f"{n_local * w.store.nch * 4 / 1e6:.0f} MB particle state per GPU "
-                               "streamed every substep (L2 126 MB)"}
+                  "l2_policy": (("inputs larger than L2: " if n_local * w.store.nch * 4 > 126e6 else
+                                 "per-GPU working set SMALLER than L2 at this rank count (strong scaling of a "
+                                 "fixed scene); no flush between steps, every substep rewrites the whole state: ")
+                                + f"{n_local * w.store.nch * 4 / 1e6:.0f} MB particle state per GPU "
+                                "streamed every substep (L2 126 MB)")}
         return {"value": round(value, 2), "ms_per_step": round(ms_per_step, 4), "roofline": roofline,
                 "config": config, "launches": launches, "window": (t_begin, t_end)}
 
