@@ -17,6 +17,7 @@ from __future__ import annotations
 import ctypes as C
 import logging
 import math
+import os
 import time
 
 import numpy as np
@@ -630,7 +631,7 @@ class CudaWorker:
         # the host's part of a rebuild at 64 K particles falls from ~130 to ~40 us, the frame by 0-7 %;
         # nothing at 171 K and above (the chain is device-bound there), and a scene whose count keeps
         # changing (fountain: emitter + sink) pays for captures it never reuses.  Off by default.
-        self.rebuild_graph = False
+        self.rebuild_graph = os.environ.get("MPM_REBUILD_GRAPH", "0") == "1"
         self.rebuild_graph_max = 200_000   # ... up to this many particles
         self.rebuild_graph_replays = 0
         self._rb_cache = {}           # store half -> (key, plan, result) of the last rebuild out of it

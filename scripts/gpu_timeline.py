@@ -26,7 +26,7 @@ w = CudaWorker(0, SharedRuntime(1, 150.0), W.params, W.material, W.boundary,
                fuse_clear=True, lazy_flush=True)
 w.seed_particles(W.positions.astype(np.float32), W.velocities.astype(np.float32), W.particle_mass,
                  ids=np.arange(n))
-for _ in range(4):
+for _ in range(int(os.environ.get("WARM", "4"))):
     w.run_frame()
 torch.cuda.synchronize()
 from torch.profiler import profile, ProfilerActivity
@@ -69,9 +69,14 @@ for (p, q), d in agg.most_common(16):
 if os.environ.get("RAW"):
     nraw = int(os.environ["RAW"])
     mid = len(ks) // 2
-    # start at a fused transfer kernel
-    while mid < len(ks) and "transfer_kernel" not in ks[mid][2]:
-        mid += 1
+    # start at a fused transfer kernel (RAW_AT=rebuild: a few kernels before a rebuild instead)
+    if os.environ.get("RAW_AT") == "rebuild":
+        while mid < len(ks) and "rebuild_init" not in ks[mid][2]:
+            mid += 1
+        mid = max(mid - 12, 0)
+    else:
+        while mid < len(ks) and "transfer_kernel" not in ks[mid][2]:
+            mid += 1
     base = ks[mid][0]
     prev_end = None
     for a, b, nme in ks[mid:mid + nraw]:
