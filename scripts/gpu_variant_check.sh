@@ -8,7 +8,6 @@ bash scripts/build_variant.sh $name "$@" > gpurun_out/ab_build_$name.log 2>&1
 export MPM_B200_LIB=$PWD/paper_2111_00699_b200/variants/libmpm_$name.so
 ls -la $MPM_B200_LIB
 python -m pytest tests/test_cuda_parity.py tests/test_cuda_pipeline.py tests/test_cuda_fullsize.py -m gpu -x -q 2>&1 | tail -8 | tee gpurun_out/var_${name}_pytest.log
-NOTREE=1 bash scripts/gpu_ab.sh >/dev/null   # (defines nothing; keeps the output dir)
 for scene in ${SCENES:-snow_fc snow}; do
   python bench.py --scene $scene --steps 10 --warmup 3 --no-cpu-baseline --no-e2e --no-pinned-variant > gpurun_out/ab_${name}_$scene.log 2> gpurun_out/ab_${name}_$scene.err
   python - $name $scene <<'PY'
