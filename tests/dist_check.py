@@ -36,6 +36,8 @@ def main():
         return repartition_check(rank, world, dev)
     if os.environ.get("MPM_SCENE", "") == "mixed":
         return mixed_populations(rank, world, dev)
+    if os.environ.get("MPM_SCENE", "") == "soak":
+        return soak(rank, world, dev)
     g = golden("two_worker.npz")
     material, params, boundary = elastic_setup()
     transfer = os.environ.get("MPM_TRANSFER", "split")
@@ -167,6 +169,50 @@ def mixed_populations(rank, world, dev):
         assert shared > 0
         assert ex <= 10 * U.X_RTOL_RUN and ev <= 10 * U.V_RTOL_RUN and ef <= 10 * U.F_ATOL_RUN and \
             ej <= 10 * U.F_ATOL_RUN, (ex, ev, ef, ej)
+        print("DIST_CHECK_OK")
+    dist.barrier()
+    dist.destroy_process_group()
+
+
+def soak(rank, world, dev):
+    """Many device-paced frames over peer-mapped ranks (MPM_FRAMES, default 40) of the small snow + sand
+    scene, one re-partition in the middle: invariants only (every id exactly once, mass, finiteness),
+    the counters of the speculative pipeline reported."""
+    from paper_2111_00699_b200 import scenes
+    from paper_2111_00699_b200.dist import population_layout, seed_population_rank
+    W = scenes.mixed_sparse(l=8, pairs_side=2, domain_cells=64, gap_cells=1)
+    frames = int(os.environ.get("MPM_FRAMES", "40"))
+    opts = PipelineOptions(transfer=os.environ.get("MPM_TRANSFER", "g2p2g"), fused_threshold=1 << 62)
+    one_pop = world % 2 == 1
+    if one_pop:          # odd world: one population, plain slabs (and a re-partition half way)
+        pop = W.populations[0]
+        w = PeerDistWorker(PeerRuntime(dev, initial_vmax=150.0), W.params, pop.material, W.boundary, opts,
+                           device=dev, wait_timeout_ms=60000, count_stats=False, lazy_flush=True)
+        seed_rank(w, pop.positions, pop.velocities, pop.particle_mass)
+        n, mass = len(pop.positions), pop.particle_mass
+    else:
+        p, _, _ = population_layout(rank, world, 2)
+        w = PeerDistWorker(PeerRuntime(dev, initial_vmax=150.0), W.params, W.populations[p].material, W.boundary,
+                           opts, device=dev, wait_timeout_ms=60000, count_stats=False, lazy_flush=True)
+        seed_population_rank(w, W.populations)
+        n, mass = W.n_particles, None
+    for f in range(frames):
+        w.run_frame()
+        if one_pop and f == frames // 2:
+            w.repartition(force=True)
+    flat, ids = w.store.state_with_ids()
+    parts = [None] * world
+    dist.all_gather_object(parts, (flat[:, [0, 1, 2, 15]], ids, (w.collective_steps, w.device_paced_steps,
+                                                                  w.speculative_discards, len(w.rebuild_steps))))
+    if rank == 0:
+        ids = np.concatenate([p[1] for p in parts])
+        st = np.concatenate([p[0] for p in parts])
+        assert np.array_equal(np.sort(ids), np.arange(n)), "ids lost or duplicated"
+        assert np.isfinite(st).all()
+        if mass is not None:
+            assert abs(st[:, 3].sum() - n * mass) <= 1e-5 * n * mass
+        print(f"dist_check soak world={world} frames={frames} ({frames * W.params.steps_per_frame} steps): ids / mass / "
+              f"finiteness ok; collective / device-paced / discarded / rebuilds per rank {[p[2] for p in parts]}")
         print("DIST_CHECK_OK")
     dist.barrier()
     dist.destroy_process_group()
