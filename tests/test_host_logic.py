@@ -288,3 +288,32 @@ def test_population_layout_and_dist_surface():
     from paper_2111_00699_b200.errors import ConfigError
     with pytest.raises(ConfigError):
         D.population_layout(0, 3, 2)
+
+
+def test_committed_bench_lines_keep_the_contract():
+    """Every bench line committed under profiles/ (one per scene + the default run) carries the keys the
+    driver and the judge read: metric / value / unit / timing fields, a workload name, the clocks record,
+    and -- where a dominant kernel was timed -- a roofline block whose fraction is achieved / peak and
+    cannot exceed 1 (a fraction above 1 was how a timing bug showed up in round 2)."""
+    import json
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    lines = [json.loads(l) for l in open(os.path.join(root, "profiles", "r2f_scenes.jsonl")) if l.strip()]
+    lines.append(json.load(open(os.path.join(root, "profiles", "r2f_bench_default.json"))))
+    assert len(lines) >= 10
+    for d in lines:
+        for k in ("metric", "value", "unit", "n_gpus", "steps", "warmup", "ms_per_step", "higher_is_better",
+                  "scaling", "vs_baseline", "dtype", "data", "config", "gpu_launches", "clocks"):
+            assert k in d, (k, d.get("config", {}).get("workload"))
+        assert d["metric"] == "particle_substeps_per_s" and d["higher_is_better"] is True and d["vs_baseline"] is None
+        assert d["config"]["workload"] and "model" not in d["config"]
+        assert d["gpu_launches"] > 0 and d["value"] > 0
+        c = d["clocks"]
+        assert c and c["sm_mhz"] > 0.9 * c["sm_max_mhz"] and not set(c["reasons"]) & {
+            "hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown"}
+        r = d.get("roofline")
+        if r:
+            assert r["bound"] == "hbm" and 0.0 < r["frac"] < 1.0
+            assert r["frac"] == pytest.approx(r["achieved"] / r["peak"], rel=2e-3)
+    default = lines[-1]
+    assert default["e2e"]["h2d_bytes_per_step"] > 0 and default["e2e"]["d2h_bytes_per_step"] > 0
+    assert default["cpu_baseline"]["kind"] in ("port", "reference") and default["cpu_baseline"]["cores"] >= 1
